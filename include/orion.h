@@ -1,0 +1,252 @@
+/*
+ * orion.h — C ABI of the B200-native hot path of Orion's content parallel expansion
+ * (Gao et al., arXiv 2510.24390, "Improving LLM Reasoning via Dependency-Aware Query
+ * Decomposition and Logic-Parallel Content Expansion").
+ *
+ * The library implements ONE expansion decode step (Alg. 1 l.16 "LLM processes
+ * the running node set R"; §3.3 PAPER.md:387 yellow "LLM Decoding" bars) for every point
+ * ("branch") of every in-flight query at once, plus the host-side DAG work that feeds it:
+ *
+ *   orion_dag_waves      Alg. 1 l.1-8 + Eq. (1)-(3): validate a point DAG, split points into
+ *                        Prefill/Decode stages, compute expansion levels and per-branch
+ *                        segment lists (which KV spans each branch attends to).
+ *   orion_bind_segments  map symbolic segment lists to token ranges of a paged KV cache.
+ *   orion_expand_plan    cut the bound segments into shared pieces (maximal token ranges with
+ *                        a fixed reader set) and emit the device work plan.
+ *   orion_kv_append      write each branch's new-token K/V into its own pages (device).
+ *   orion_expand_attn    dependency-masked batched GQA decode attention over the paged bf16
+ *                        cache; each shared piece is read from HBM once per (query, kv head)
+ *                        group (device; split kernel + combine kernel).
+ *
+ * Conventions (all functions):
+ *  - Every buffer is caller-owned.  The library keeps no pointer after a call returns, has no
+ *    global state (except a thread-local error string), never allocates device memory and never
+ *    synchronises a stream.  Device functions only enqueue work on `stream`.
+ *  - Errors are returned as orion_status codes; nothing is thrown, aborted or exited.  On a
+ *    non-OK status, orion_last_error() returns a thread-local human-readable message.
+ *  - Two-call sizing: when an output buffer is too small the function returns
+ *    ORION_ERR_CAPACITY and writes the required size to the *_needed argument.
+ *  - Host functions are pure and thread-safe; a plan is immutable once built and may be used by
+ *    any number of launches.  Host functions run without a GPU.
+ *  - Point ids are 1..n_points within a query.  Branch indices are global
+ *    0..n_branches-1 over all queries of one call.
+ *  - KV cache layout, per layer: K and V each bf16 [num_pages][num_kv_heads][page_size][head_dim].
+ *    q and out: bf16 [n_branches][num_q_heads][head_dim]; lse: fp32 [n_branches][num_q_heads].
+ *    GQA mapping: q head h reads kv head h / (num_q_heads / num_kv_heads) (reading S16).
+ */
+#ifndef ORION_H_
+#define ORION_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t orion_status;
+enum {
+  ORION_OK = 0,
+  ORION_ERR_INVALID_ARG = 1,   /* bad pointer, size, kind, policy, overlap, empty context */
+  ORION_ERR_CYCLE = 2,         /* the point DAG has a cycle (SPEC.md:67 CycleDetected) */
+  ORION_ERR_UNKNOWN_POINT = 3, /* an edge names a point outside 1..n */
+  ORION_ERR_CAPACITY = 4,      /* output buffer too small; see *_needed */
+  ORION_ERR_UNSUPPORTED = 5,   /* shape not compiled in / segment pattern not supported */
+  ORION_ERR_CUDA = 6           /* a CUDA launch failed; message from cudaGetErrorString */
+};
+
+/* Edge kinds (§3.3 "Null, Contextual, and Dependent"). */
+enum { ORION_EDGE_NULL = 0, ORION_EDGE_CONTEXTUAL = 1, ORION_EDGE_DEPENDENT = 2 };
+
+/* Dependency-set policies (readings S6-S8).
+ * ANCESTORS: a branch attends to every transitive ancestor; FULL span if the ancestor's decode
+ *            happens-before the branch's prefill in the stage graph, else CONTENT span.
+ * PARENTS_EQ3: Eq. (2)/(3) literally: direct parents only, OUTPUT span for a
+ *            Dependent edge, CONTENT span for a Contextual edge. */
+enum { ORION_POLICY_ANCESTORS = 0, ORION_POLICY_PARENTS_EQ3 = 1 };
+
+/* Symbolic segment kinds.  A point k's KV segment S_k = [P_k content (Lc_k tokens) | Output_k]. */
+enum {
+  ORION_SEG_PREFIX = 0,  /* the query's shared prefix, Prompt_Pre of Eq. (2) (reading S13) */
+  ORION_SEG_CONTENT = 1, /* S_k[0, Lc_k)          f(k,j) = P_k (Eq. 3, Contextual)          */
+  ORION_SEG_FULL = 2,    /* S_k[0, T_k)           ANCESTORS span of a Dependent ancestor    */
+  ORION_SEG_OUTPUT = 3,  /* S_k[Lc_k, T_k)        f(k,j) = Output_k (Eq. 3, Dependent)      */
+  ORION_SEG_OWN = 4      /* S_j[0, T_j)           the branch's own tokens incl. the new one */
+};
+
+/* Stage phases in the wave listing (Alg. 1 l.8 "split each node into prefilling and decoding"). */
+enum { ORION_PHASE_PREFILL = 0, ORION_PHASE_DECODE = 1 };
+
+/* kv_append modes.  ADVANCE: write at own_len[b], then own_len[b] += 1 (a real decode step).
+ * REWRITE: write at own_len[b]-1, lengths unchanged (stationary steady-state benchmarking). */
+enum { ORION_APPEND_ADVANCE = 0, ORION_APPEND_REWRITE = 1 };
+
+/* from = prerequisite point k, to = dependent point j. */
+typedef struct { int32_t from, to, kind; } orion_edge;
+
+/* One symbolic list entry.  point = 0 for PREFIX, else the query-local point id. */
+typedef struct { int32_t kind, point; } orion_segref;
+
+/* One bound segment: tokens [start, start + len_eff) of the page run that starts at
+ * page_table[pt_off]; token position t lives on page page_table[pt_off + t / page_size],
+ * row t % page_size.  dyn = -1: len_eff = len (static).  dyn = b >= 0: the segment grows with
+ * branch b's decode: len_eff = clamp(own_len[b] - start, 0, len), i.e. len is a capacity bound. */
+typedef struct { int32_t pt_off, start, len, dyn; } orion_seg;
+
+typedef struct {
+  int32_t num_q_heads;   /* Hq */
+  int32_t num_kv_heads;  /* Hkv; Hq % Hkv == 0 */
+  int32_t head_dim;      /* 64 or 128 */
+  int32_t page_size;     /* power of two in [8, 256] */
+  float sm_scale;        /* softmax scale; <= 0 selects 1/sqrt(head_dim) (reading S16) */
+} orion_attn_shape;
+
+/* Per query: its points are global branches [branch0, branch0 + n_points). */
+typedef struct { int32_t n_points, branch0, prefix_pt_off, prefix_len; } orion_query_desc;
+
+/* Per global branch (= point): its page run, content length Lc and capacity in tokens. */
+typedef struct { int32_t pt_off, content_len, capacity; } orion_point_desc;
+
+typedef struct {
+  int32_t num_sms;        /* SMs to balance for; <= 0 selects 148 (B200) */
+  int32_t chunk_tokens;   /* max tokens per work item along a piece; <= 0 selects the default */
+  int32_t flags;          /* reserved, 0 */
+} orion_plan_opts;
+
+typedef struct {
+  int64_t n_items;          /* split-kernel work items */
+  int64_t n_pieces;         /* shared pieces (token range x reader set), per kv head counted once */
+  int64_t n_partials;       /* fp32 partial rows written by the split kernel */
+  int64_t n_rows;           /* n_branches * num_q_heads */
+  int64_t unique_tokens;    /* sum of piece capacities (upper bound of unique KV tokens per kv head) */
+  int64_t logical_tokens;   /* sum over branches of their context capacity (per kv head) */
+  int64_t plan_bytes;
+  int64_t workspace_bytes;
+} orion_plan_stats;
+
+/*
+ * orion_dag_waves — Alg. 1 l.1-8, Eq. (1) generalised to
+ * longest-path expansion levels (reading S10), and Eq. (2)/(3) read as KV
+ * segment lists (readings S6-S9).  Host only, no CUDA.
+ *
+ *  n_points            N >= 1; points are 1..N.
+ *  edges[n_edges]      typed edges; Null edges are dropped, duplicates merged, Dependent
+ *                      dominates Contextual on the same pair (reading S5).
+ *  policy              ORION_POLICY_*.
+ *  pre_level[N], dec_level[N]  out: level of Prefill(i) / Decode(i) (index i-1).
+ *  n_levels[1]         out: 1 + max level.
+ *  wave_offsets[2N+1]  out, nullable: CSR over levels (only n_levels+1 entries are written).
+ *  wave_stages[2N]     out, nullable: stages in wave order, each wave sorted by (point, Pre<Dec),
+ *                      encoded as point * 2 + phase.
+ *  seg_offsets[N+1]    out: CSR over points of the segment lists.
+ *  segs[segs_cap]      out: [PREFIX] + dependencies ascending by point id + [OWN(j)].
+ *  segs_needed[1]      out: total list entries (always written when validation passed).
+ *  err_info[err_cap]   out, nullable: on CYCLE the point ids of one cycle in order; on
+ *                      UNKNOWN_POINT / bad kind the offending edge index.  err_info is written up
+ *                      to err_cap entries; the first entry not written is left untouched.
+ * Errors: INVALID_ARG (N < 1, null pointer, kind outside 0..2 — checked per edge in input order
+ * before the point-range check of the same edge), UNKNOWN_POINT, CYCLE (a non-Null self-loop is a
+ * 1-cycle), CAPACITY (segs_cap < *segs_needed; levels are still written).
+ */
+orion_status orion_dag_waves(int32_t n_points, const orion_edge* edges, int32_t n_edges,
+                             int32_t policy, int32_t* pre_level, int32_t* dec_level,
+                             int32_t* n_levels, int32_t* wave_offsets, int32_t* wave_stages,
+                             int32_t* seg_offsets, orion_segref* segs, int32_t segs_cap,
+                             int32_t* segs_needed, int32_t* err_info, int32_t err_cap);
+
+/*
+ * orion_bind_segments — physical binding of symbolic lists (reading S7/S19; SURVEY.md
+ * §8(c) O2).  Host only.
+ *   PREFIX     -> {prefix_pt_off, 0, prefix_len, -1}
+ *   CONTENT(k) -> {pt_off_k, 0, Lc_k, -1}
+ *   FULL(k)    -> {pt_off_k, 0, cap_k, dyn = branch of k}
+ *   OUTPUT(k)  -> {pt_off_k, Lc_k, cap_k - Lc_k, dyn = branch of k}
+ *   OWN(j)     -> {pt_off_j, 0, cap_j, dyn = branch of j}
+ *  queries[n_queries]       query descriptors; branches of different queries must not overlap.
+ *  points[n_branches]       per-branch page runs (n_branches = max(branch0 + n_points)).
+ *  seg_offsets[n_branches+1], refs[]  global CSR: branch b's list is refs[seg_offsets[b] ..
+ *                           seg_offsets[b+1]), with query-local point ids (as produced by
+ *                           orion_dag_waves for that query).
+ *  segs_out[seg_offsets[n_branches]]  out.
+ * Errors: INVALID_ARG (null pointers, bad kind, point outside its query, Lc > capacity,
+ * negative sizes).
+ */
+orion_status orion_bind_segments(int32_t n_queries, const orion_query_desc* queries,
+                                 int32_t n_branches, const orion_point_desc* points,
+                                 const int32_t* seg_offsets, const orion_segref* refs,
+                                 orion_seg* segs_out);
+
+/*
+ * orion_expand_plan — host planner for orion_expand_attn.  Groups segments by page run (pt_off),
+ * cuts every run at all segment boundaries into pieces, attaches to each piece its reader set
+ * (the branches whose lists cover it), merges neighbours with equal reader sets, splits pieces
+ * into work items of at most opts->chunk_tokens tokens and 64 query rows, orders work items
+ * longest-first, and lays out the combine lists.  Host only; the caller uploads plan_buf to the
+ * device (any 16-byte aligned copy) and keeps the host copy for launches.
+ *  h_seg_offsets[n_branches+1], h_segs[]  bound segments (orion_bind_segments).
+ *  h_own_len[n_branches]  nullable: current lengths, used to validate that a static segment
+ *                         overlapping a growing (dyn) segment never reaches past own_len.
+ *  plan_buf[plan_cap]     out (16-byte aligned); plan_needed / workspace_needed out (bytes).
+ * Errors: INVALID_ARG (overlapping segments in one branch list; a branch with an empty
+ * capacity context; dyn out of range), UNSUPPORTED (two different dyn branches on one page run;
+ * shape not supported), CAPACITY.
+ */
+orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t n_branches,
+                               const int32_t* h_seg_offsets, const orion_seg* h_segs,
+                               const int32_t* h_own_len, const orion_plan_opts* opts,
+                               void* plan_buf, size_t plan_cap, size_t* plan_needed,
+                               size_t* workspace_needed);
+
+/* orion_plan_stats — read counters of a built (host) plan. */
+orion_status orion_plan_get_stats(const void* h_plan, orion_plan_stats* out);
+
+/*
+ * orion_kv_append — KV-cache write of each branch's new token (reading S15).
+ * Device; enqueued on `stream`.  One thread block per branch; bit-exact bf16 copy.
+ *  k_new, v_new   bf16 [n_branches][Hkv][d] (device).
+ *  k_cache, v_cache  bf16 [num_pages][Hkv][P][d] (device, one layer).
+ *  own_pt_off[n_branches], own_cap[n_branches]  device int32: branch page runs and capacities.
+ *  page_table     device int32.
+ *  own_len[n_branches]  device int32, in/out.  ADVANCE: write slot own_len, then own_len += 1.
+ *                 REWRITE: write slot own_len - 1.  A slot outside [0, own_cap) is skipped and
+ *                 own_len is left unchanged (no out-of-run write ever happens).
+ * Errors: INVALID_ARG (null/unaligned pointers, bad mode), UNSUPPORTED (shape), CUDA.
+ */
+orion_status orion_kv_append(const orion_attn_shape* shape, int32_t n_branches,
+                             const void* k_new, const void* v_new, void* k_cache, void* v_cache,
+                             const int32_t* own_pt_off, const int32_t* own_cap,
+                             const int32_t* page_table, int32_t* own_len, int32_t mode,
+                             void* stream);
+
+/*
+ * orion_expand_attn — one dependency-masked, batched GQA decode-attention step (PAPER.md:337
+ * Alg. 1 l.16; reading S21: every branch of the plan decodes one token).  For each branch b and
+ * q head h:  out[b,h] = softmax(sm_scale * q[b,h] . K_ctx(b)^T) . V_ctx(b), where ctx(b) is the
+ * concatenation of b's bound segments with their current (dyn) lengths; lse[b,h] = natural-log
+ * sum-exp of the scaled scores.  The current token's K/V must already be appended.
+ * Device; enqueues the split kernel (fp32 partials (m, l, acc) per piece chunk) and the combine
+ * kernel (LSE merge in plan order, RNE to bf16) on `stream`.
+ *  q, out        bf16 [n_branches][Hq][d] (device).   lse  fp32 [n_branches][Hq], nullable.
+ *  k_cache, v_cache, num_pages, page_table  as for orion_kv_append.
+ *  own_len       device int32 [n_branches] (dyn segment lengths).
+ *  h_plan, d_plan  the host plan and its device copy (same bytes).
+ *  workspace     device, >= workspace_needed bytes from orion_expand_plan, 16-byte aligned.
+ * Errors: INVALID_ARG (null/unaligned pointers, plan/shape mismatch, workspace too small),
+ * UNSUPPORTED (shape), CUDA.
+ */
+orion_status orion_expand_attn(const orion_attn_shape* shape, int32_t n_branches, const void* q,
+                               void* out, float* lse, const void* k_cache, const void* v_cache,
+                               int32_t num_pages, const int32_t* page_table,
+                               const int32_t* own_len, const void* h_plan, const void* d_plan,
+                               void* workspace, size_t workspace_bytes, void* stream);
+
+/* Thread-local message describing the last non-OK status returned on this thread. */
+const char* orion_last_error(void);
+
+/* Library version string (also names the compiled-in kernel variants). */
+const char* orion_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ORION_H_ */

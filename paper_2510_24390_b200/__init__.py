@@ -1,0 +1,204 @@
+"""paper_2510_24390_b200 — B200-native hot path of Orion's content parallel expansion.
+
+Python surface of the C ABI in include/orion.h (same names, argument marshalling only):
+
+    dag_waves(n_points, edges, policy)           -> levels, waves, segment lists     (host)
+    bind_segments(queries, points, offs, refs)   -> bound segments                   (host)
+    expand_plan(shape, offs, segs, own_len)      -> device work plan                 (host)
+    kv_append(...)                               -> K1 on the current CUDA stream    (device)
+    expand_attn(...)                             -> K2 + K3 on the current stream    (device)
+
+`ExpansionBatch` strings them together for a set of in-flight queries: it builds the plan once
+per in-flight-set change (Alg. 1 readiness loop) and then runs decode steps
+(Alg. 1 l.16) with no host work and no host<->device traffic.
+"""
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import (OrionError, POLICY_ANCESTORS, POLICY_PARENTS_EQ3, APPEND_ADVANCE,
+                   APPEND_REWRITE, SEG_PREFIX, SEG_CONTENT, SEG_FULL, SEG_OUTPUT, SEG_OWN,
+                   EDGE_NULL, EDGE_CONTEXTUAL, EDGE_DEPENDENT, SEG_DTYPE, SEGREF_DTYPE, lib)
+
+__all__ = ["dag_waves", "bind_segments", "expand_plan", "plan_stats", "kv_append", "expand_attn",
+           "ExpansionBatch", "OrionError", "version", "POLICY_ANCESTORS", "POLICY_PARENTS_EQ3",
+           "APPEND_ADVANCE", "APPEND_REWRITE"]
+
+
+def version():
+    return lib().orion_version().decode()
+
+
+def _shape(hq, hkv, d, page, sm_scale=0.0):
+    return _lib.AttnShape(hq, hkv, d, page, float(sm_scale))
+
+
+def dag_waves(n_points, edges, policy=POLICY_ANCESTORS):
+    """orion_dag_waves.  edges: iterable of (from, to, kind).  Returns a dict with
+    pre_level, dec_level (np.int32 [n]), n_levels, waves (list of lists of (point, phase)),
+    seg_offsets (np.int32 [n+1]) and segs (structured np array of (kind, point))."""
+    e = np.array(list(edges), dtype=np.int32).reshape(-1, 3)
+    e = np.ascontiguousarray(e)
+    n = int(n_points)
+    nn = max(n, 1)
+    pre = np.zeros(nn, np.int32)
+    dec = np.zeros(nn, np.int32)
+    nl = np.zeros(1, np.int32)
+    woff = np.zeros(2 * nn + 1, np.int32)
+    wst = np.zeros(2 * nn, np.int32)
+    soff = np.zeros(nn + 1, np.int32)
+    need = np.zeros(1, np.int32)
+    err = np.full(max(nn, 1), -1, np.int32)
+    cap = 4 * nn + 4
+    for _ in range(2):
+        segs = np.zeros(cap, SEGREF_DTYPE)
+        code = lib().orion_dag_waves(n, _lib.ptr(e) if len(e) else None, len(e), int(policy),
+                                     _lib.ptr(pre), _lib.ptr(dec), _lib.ptr(nl), _lib.ptr(woff),
+                                     _lib.ptr(wst), _lib.ptr(soff), _lib.ptr(segs), cap,
+                                     _lib.ptr(need), _lib.ptr(err), len(err))
+        if code == _lib.ERR_CAPACITY:
+            cap = int(need[0])
+            continue
+        if code != _lib.OK:
+            info = [int(x) for x in err if x >= 0]
+            _lib.check(code, info)
+        break
+    L = int(nl[0])
+    waves = [[(int(s) // 2, int(s) % 2) for s in wst[woff[w]:woff[w + 1]]] for w in range(L)]
+    return {"pre_level": pre[:n], "dec_level": dec[:n], "n_levels": L, "waves": waves,
+            "seg_offsets": soff[:n + 1], "segs": segs[:int(need[0])]}
+
+
+def bind_segments(queries, points, seg_offsets, refs):
+    """orion_bind_segments.  queries: [(n_points, branch0, prefix_pt_off, prefix_len)],
+    points: [(pt_off, content_len, capacity)] per global branch; seg_offsets/refs: global CSR."""
+    qd = np.ascontiguousarray(np.array(queries, dtype=np.int32).reshape(-1, 4))
+    pd = np.ascontiguousarray(np.array(points, dtype=np.int32).reshape(-1, 3))
+    so = np.ascontiguousarray(seg_offsets, dtype=np.int32)
+    rf = np.ascontiguousarray(refs).astype(SEGREF_DTYPE)
+    out = np.zeros(int(so[-1]), SEG_DTYPE)
+    _lib.check(lib().orion_bind_segments(len(qd), _lib.ptr(qd), len(pd), _lib.ptr(pd),
+                                         _lib.ptr(so), _lib.ptr(rf), _lib.ptr(out)))
+    return out
+
+
+def expand_plan(hq, hkv, d, page, seg_offsets, segs, own_len=None, chunk_tokens=0, num_sms=0,
+                sm_scale=0.0):
+    """orion_expand_plan -> (plan: np.uint8 16-byte aligned host buffer, workspace_bytes)."""
+    shape = _shape(hq, hkv, d, page, sm_scale)
+    so = np.ascontiguousarray(seg_offsets, dtype=np.int32)
+    sg = np.ascontiguousarray(segs).astype(SEG_DTYPE)
+    ol = None if own_len is None else np.ascontiguousarray(own_len, dtype=np.int32)
+    opts = _lib.PlanOpts(int(num_sms), int(chunk_tokens), 0)
+    need = ctypes.c_size_t(0)
+    ws = ctypes.c_size_t(0)
+    nb = len(so) - 1
+    code = lib().orion_expand_plan(ctypes.byref(shape), nb, _lib.ptr(so), _lib.ptr(sg), _lib.ptr(ol),
+                                   ctypes.byref(opts), None, 0, ctypes.byref(need), ctypes.byref(ws))
+    if code != _lib.ERR_CAPACITY:
+        _lib.check(code)
+    plan = _lib.aligned_empty(need.value)
+    _lib.check(lib().orion_expand_plan(ctypes.byref(shape), nb, _lib.ptr(so), _lib.ptr(sg),
+                                       _lib.ptr(ol), ctypes.byref(opts), _lib.ptr(plan), need.value,
+                                       ctypes.byref(need), ctypes.byref(ws)))
+    return plan, int(ws.value)
+
+
+def plan_stats(plan):
+    st = _lib.PlanStats()
+    _lib.check(lib().orion_plan_get_stats(_lib.ptr(plan), ctypes.byref(st)))
+    return {n: int(getattr(st, n)) for n, _ in _lib.PlanStats._fields_}
+
+
+def _stream_ptr(stream):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise OrionError(_lib.ERR_INVALID_ARG, "device argument is not a CUDA tensor")
+
+
+def kv_append(hq, hkv, d, page, k_new, v_new, k_cache, v_cache, own_pt_off, own_cap, page_table,
+              own_len, mode=APPEND_ADVANCE, stream=None):
+    """orion_kv_append on `stream` (default: torch's current stream).  All tensors on the GPU."""
+    _require_cuda(k_new, v_new, k_cache, v_cache, own_pt_off, own_cap, page_table, own_len)
+    shape = _shape(hq, hkv, d, page)
+    _lib.check(lib().orion_kv_append(ctypes.byref(shape), int(own_len.shape[0]), k_new.data_ptr(),
+                                     v_new.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(),
+                                     own_pt_off.data_ptr(), own_cap.data_ptr(),
+                                     page_table.data_ptr(), own_len.data_ptr(), int(mode),
+                                     _stream_ptr(stream)))
+
+
+def expand_attn(hq, hkv, d, page, q, out, lse, k_cache, v_cache, page_table, own_len, h_plan,
+                d_plan, workspace, stream=None, sm_scale=0.0):
+    """orion_expand_attn on `stream` (default: torch's current stream)."""
+    _require_cuda(q, out, lse, k_cache, v_cache, page_table, own_len, d_plan, workspace)
+    shape = _shape(hq, hkv, d, page, sm_scale)
+    _lib.check(lib().orion_expand_attn(
+        ctypes.byref(shape), int(q.shape[0]), q.data_ptr(), out.data_ptr(),
+        None if lse is None else lse.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(),
+        int(k_cache.shape[0]), page_table.data_ptr(), own_len.data_ptr(), _lib.ptr(h_plan),
+        d_plan.data_ptr(), workspace.data_ptr(), workspace.numel() * workspace.element_size(),
+        _stream_ptr(stream)))
+
+
+class ExpansionBatch:
+    """The in-flight set of one GPU: several queries, each a point DAG whose points all decode.
+
+    queries: list of dicts {n_points, edges, prefix_pt_off, prefix_len}; points of query i are
+             global branches branch0_i .. branch0_i + n_points - 1 in order.
+    points:  per global branch (pt_off, content_len, capacity).
+    page_table: int32 array of physical page ids; own_len: int32 [n_branches] current lengths.
+    """
+
+    def __init__(self, hq, hkv, d, page, queries, points, page_table, own_len,
+                 policy=POLICY_ANCESTORS, device="cuda", chunk_tokens=0, sm_scale=0.0):
+        import torch
+        self.hq, self.hkv, self.d, self.page = hq, hkv, d, page
+        self.sm_scale = sm_scale
+        qdesc, offs, refs, b0 = [], [0], [], 0
+        for q in queries:
+            w = dag_waves(q["n_points"], q["edges"], policy)
+            so = w["seg_offsets"]
+            for j in range(q["n_points"]):
+                refs.append(w["segs"][so[j]:so[j + 1]])
+                offs.append(offs[-1] + int(so[j + 1] - so[j]))
+            qdesc.append((q["n_points"], b0, q["prefix_pt_off"], q["prefix_len"]))
+            b0 += q["n_points"]
+        self.n_branches = b0
+        self.seg_offsets = np.array(offs, np.int32)
+        self.refs = np.concatenate(refs) if refs else np.zeros(0, SEGREF_DTYPE)
+        pts = np.array(points, np.int32).reshape(-1, 3)
+        self.segs = bind_segments(qdesc, pts, self.seg_offsets, self.refs)
+        own = np.ascontiguousarray(own_len, dtype=np.int32)
+        self.h_plan, ws = expand_plan(hq, hkv, d, page, self.seg_offsets, self.segs, own,
+                                      chunk_tokens=chunk_tokens, sm_scale=sm_scale)
+        self.stats = plan_stats(self.h_plan)
+        dev = torch.device(device)
+        self.d_plan = torch.from_numpy(self.h_plan.copy()).to(dev)
+        self.workspace = torch.empty((ws + 15) // 16 * 4, dtype=torch.float32, device=dev)
+        self.page_table = torch.from_numpy(np.ascontiguousarray(page_table, np.int32)).to(dev)
+        self.own_pt_off = torch.from_numpy(np.ascontiguousarray(pts[:, 0])).to(dev)
+        self.own_cap = torch.from_numpy(np.ascontiguousarray(pts[:, 2])).to(dev)
+        self.own_len = torch.from_numpy(own.copy()).to(dev)
+
+    def append(self, k_new, v_new, k_cache, v_cache, mode=APPEND_ADVANCE, stream=None):
+        kv_append(self.hq, self.hkv, self.d, self.page, k_new, v_new, k_cache, v_cache,
+                  self.own_pt_off, self.own_cap, self.page_table, self.own_len, mode, stream)
+
+    def attend(self, q, out, k_cache, v_cache, lse=None, stream=None):
+        expand_attn(self.hq, self.hkv, self.d, self.page, q, out, lse, k_cache, v_cache,
+                    self.page_table, self.own_len, self.h_plan, self.d_plan, self.workspace,
+                    stream, self.sm_scale)
+
+    def step(self, q, k_new, v_new, k_cache, v_cache, out, lse=None, mode=APPEND_ADVANCE,
+             stream=None):
+        """One expansion decode step for one layer: K1 append, then K2 split + K3 combine."""
+        self.append(k_new, v_new, k_cache, v_cache, mode, stream)
+        self.attend(q, out, k_cache, v_cache, lse, stream)

@@ -1,0 +1,481 @@
+// host.cpp — host side of the Orion expansion hot path: DAG -> stage levels -> segment lists
+// (orion_dag_waves), symbolic -> physical binding (orion_bind_segments), and the sharing-aware
+// work planner (orion_expand_plan).  Pure C++17, no CUDA calls: runs on the GPU-less dev box.
+//
+// Paper anchors: Alg. 1 l.1-8 (322-329), §3.3 edge kinds (359), Eq. (1) (362-366),
+// Eq. (2)/(3) (369-384), Fig. 4 walkthrough (387).  Readings S1-S23 are listed in DESIGN.md.
+#include <algorithm>
+#include <cstdarg>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/orion.h"
+#include "plan_format.h"
+
+namespace orion {
+
+thread_local std::string g_last_error;
+
+orion_status fail(orion_status code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+orion_status fail(orion_status code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+namespace {
+
+constexpr int32_t kMaxPoints = 8192;  // stage-reachability bitsets are (2N)^2 bits
+
+struct Bits {
+  std::vector<uint64_t> w;
+  explicit Bits(int n = 0) : w((n + 63) / 64, 0) {}
+  void set(int i) { w[i >> 6] |= uint64_t(1) << (i & 63); }
+  bool get(int i) const { return (w[i >> 6] >> (i & 63)) & 1; }
+  void merge(const Bits& o) {
+    for (size_t i = 0; i < w.size(); ++i) w[i] |= o.w[i];
+  }
+};
+
+// Validated point graph: materialised edges with their kind bitmask (bit0 Ctx, bit1 Dep).
+struct PointGraph {
+  int n = 0;
+  std::vector<std::vector<int>> succ;             // point -> successors (0-based)
+  std::vector<std::vector<std::pair<int, int>>> par;  // point -> (parent, kindmask), sorted
+};
+
+orion_status build_point_graph(int32_t n, const orion_edge* edges, int32_t n_edges,
+                               PointGraph& g, int32_t* err_info, int32_t err_cap) {
+  if (n < 1 || n > kMaxPoints)
+    return fail(ORION_ERR_INVALID_ARG, "n_points=%d outside [1, %d]", n, kMaxPoints);
+  if (n_edges < 0 || (n_edges > 0 && !edges))
+    return fail(ORION_ERR_INVALID_ARG, "bad edge array");
+  std::map<std::pair<int, int>, int> kinds;
+  for (int32_t i = 0; i < n_edges; ++i) {
+    const orion_edge& e = edges[i];
+    if (e.kind < ORION_EDGE_NULL || e.kind > ORION_EDGE_DEPENDENT) {
+      if (err_info && err_cap > 0) err_info[0] = i;
+      return fail(ORION_ERR_INVALID_ARG, "edge %d: kind %d not in {0,1,2}", i, e.kind);
+    }
+    if (e.from < 1 || e.from > n || e.to < 1 || e.to > n) {
+      if (err_info && err_cap > 0) err_info[0] = i;
+      return fail(ORION_ERR_UNKNOWN_POINT, "edge %d: (%d -> %d) names a point outside 1..%d", i,
+                  e.from, e.to, n);
+    }
+    if (e.kind == ORION_EDGE_NULL) continue;  // Null = absence of an edge
+    kinds[{e.from - 1, e.to - 1}] |= (e.kind == ORION_EDGE_CONTEXTUAL ? 1 : 2);
+  }
+  g.n = n;
+  g.succ.assign(n, {});
+  g.par.assign(n, {});
+  for (auto& kv : kinds) {
+    g.succ[kv.first.first].push_back(kv.first.second);
+    g.par[kv.first.second].push_back({kv.first.first, kv.second});
+  }
+  // Kahn over the point graph; whatever remains lies on or behind a cycle.
+  std::vector<int> indeg(n, 0), order;
+  for (int u = 0; u < n; ++u)
+    for (int v : g.succ[u]) indeg[v]++;
+  for (int u = 0; u < n; ++u)
+    if (!indeg[u]) order.push_back(u);
+  for (size_t i = 0; i < order.size(); ++i)
+    for (int v : g.succ[order[i]])
+      if (--indeg[v] == 0) order.push_back(v);
+  if ((int)order.size() == n) return ORION_OK;
+  // Extract one cycle: walk predecessors inside the remaining set until a node repeats.
+  std::vector<char> rem(n, 0);
+  for (int u = 0; u < n; ++u) rem[u] = indeg[u] > 0;
+  int u = 0;
+  while (!rem[u]) ++u;
+  std::vector<int> pos(n, -1), walk;
+  while (pos[u] < 0) {
+    pos[u] = (int)walk.size();
+    walk.push_back(u);
+    int nxt = -1;
+    for (auto& pk : g.par[u])
+      if (rem[pk.first]) { nxt = pk.first; break; }
+    u = nxt;  // every remaining node has a remaining predecessor
+  }
+  std::vector<int> cyc(walk.begin() + pos[u], walk.end());
+  std::reverse(cyc.begin(), cyc.end());  // predecessor walk -> forward edge order
+  if (err_info)
+    for (int i = 0; i < (int)cyc.size() && i < err_cap; ++i) err_info[i] = cyc[i] + 1;
+  return fail(ORION_ERR_CYCLE, "point DAG has a cycle of length %zu through point %d", cyc.size(),
+              cyc[0] + 1);
+}
+
+}  // namespace
+}  // namespace orion
+
+using namespace orion;
+
+extern "C" const char* orion_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" orion_status orion_dag_waves(int32_t n, const orion_edge* edges, int32_t n_edges,
+                                        int32_t policy, int32_t* pre_level, int32_t* dec_level,
+                                        int32_t* n_levels, int32_t* wave_offsets,
+                                        int32_t* wave_stages, int32_t* seg_offsets,
+                                        orion_segref* segs, int32_t segs_cap,
+                                        int32_t* segs_needed, int32_t* err_info,
+                                        int32_t err_cap) {
+  if (!pre_level || !dec_level || !n_levels || !seg_offsets || !segs_needed)
+    return fail(ORION_ERR_INVALID_ARG, "null output pointer");
+  if (policy != ORION_POLICY_ANCESTORS && policy != ORION_POLICY_PARENTS_EQ3)
+    return fail(ORION_ERR_INVALID_ARG, "unknown policy %d", policy);
+  PointGraph g;
+  orion_status st = build_point_graph(n, edges, n_edges, g, err_info, err_cap);
+  if (st != ORION_OK) return st;
+
+  // Stage graph (Alg. 1 l.8): stage s = 2*i + phase.
+  //   Pre(i) -> Dec(i);  Ctx k->j: Pre(k) -> Pre(j);  Dep k->j: Dec(k) -> Pre(j).
+  const int S = 2 * n;
+  std::vector<std::vector<int>> ssucc(S);
+  std::vector<int> sindeg(S, 0);
+  auto add = [&](int a, int b) { ssucc[a].push_back(b); sindeg[b]++; };
+  for (int i = 0; i < n; ++i) add(2 * i, 2 * i + 1);
+  for (int j = 0; j < n; ++j)
+    for (auto& pk : g.par[j]) {
+      if (pk.second & 1) add(2 * pk.first, 2 * j);
+      if (pk.second & 2) add(2 * pk.first + 1, 2 * j);
+    }
+  // Kahn order with longest-path levels (Eq. (1) generalised; reading S10).
+  std::vector<int> level(S, 0), order;
+  order.reserve(S);
+  for (int s = 0; s < S; ++s)
+    if (!sindeg[s]) order.push_back(s);
+  for (size_t i = 0; i < order.size(); ++i) {
+    int s = order[i];
+    for (int t : ssucc[s]) {
+      level[t] = std::max(level[t], level[s] + 1);
+      if (--sindeg[t] == 0) order.push_back(t);
+    }
+  }
+  int nl = 0;
+  for (int s = 0; s < S; ++s) nl = std::max(nl, level[s] + 1);
+  for (int i = 0; i < n; ++i) {
+    pre_level[i] = level[2 * i];
+    dec_level[i] = level[2 * i + 1];
+  }
+  *n_levels = nl;
+  if (wave_offsets || wave_stages) {
+    std::vector<int> cnt(nl + 1, 0);
+    for (int s = 0; s < S; ++s) cnt[level[s] + 1]++;
+    for (int w = 0; w < nl; ++w) cnt[w + 1] += cnt[w];
+    if (wave_offsets)
+      for (int w = 0; w <= nl; ++w) wave_offsets[w] = cnt[w];
+    if (wave_stages) {
+      std::vector<int> fill(cnt.begin(), cnt.end() - 1);
+      for (int s = 0; s < S; ++s)  // ascending s == ascending (point, Pre<Dec)
+        wave_stages[fill[level[s]]++] = (s / 2 + 1) * 2 + (s & 1);
+    }
+  }
+
+  // Segment lists: [PREFIX] + deps ascending by point id + [OWN(j)].
+  std::vector<std::vector<orion_segref>> lists(n);
+  if (policy == ORION_POLICY_ANCESTORS) {
+    // anc[s] = stages with a path to s, propagated in topological order.
+    std::vector<Bits> anc(S, Bits(S));
+    for (int s : order)
+      for (int t : ssucc[s]) {
+        anc[t].set(s);
+        anc[t].merge(anc[s]);
+      }
+    for (int j = 0; j < n; ++j) {
+      const Bits& a = anc[2 * j];
+      for (int k = 0; k < n; ++k) {
+        if (k == j || !a.get(2 * k)) continue;  // point ancestor <=> Pre(k) ~> Pre(j)
+        lists[j].push_back({a.get(2 * k + 1) ? ORION_SEG_FULL : ORION_SEG_CONTENT, k + 1});
+      }
+    }
+  } else {
+    for (int j = 0; j < n; ++j)
+      for (auto& pk : g.par[j])
+        lists[j].push_back({(pk.second & 2) ? ORION_SEG_OUTPUT : ORION_SEG_CONTENT, pk.first + 1});
+  }
+  int32_t total = 0;
+  for (int j = 0; j < n; ++j) total += 2 + (int32_t)lists[j].size();
+  *segs_needed = total;
+  if (segs_cap < total || !segs)
+    return fail(ORION_ERR_CAPACITY, "segs_cap=%d < needed %d", segs_cap, total);
+  int32_t o = 0;
+  for (int j = 0; j < n; ++j) {
+    seg_offsets[j] = o;
+    segs[o++] = {ORION_SEG_PREFIX, 0};
+    for (auto& r : lists[j]) segs[o++] = r;
+    segs[o++] = {ORION_SEG_OWN, j + 1};
+  }
+  seg_offsets[n] = o;
+  return ORION_OK;
+}
+
+extern "C" orion_status orion_bind_segments(int32_t n_queries, const orion_query_desc* queries,
+                                            int32_t n_branches, const orion_point_desc* points,
+                                            const int32_t* seg_offsets, const orion_segref* refs,
+                                            orion_seg* out) {
+  if (n_queries < 0 || n_branches < 0 || (n_queries && !queries) || (n_branches && !points) ||
+      !seg_offsets || (n_branches && (!refs || !out)))
+    return fail(ORION_ERR_INVALID_ARG, "null or negative argument");
+  std::vector<int32_t> qof(n_branches, -1);
+  for (int32_t q = 0; q < n_queries; ++q) {
+    const orion_query_desc& Q = queries[q];
+    if (Q.n_points < 1 || Q.branch0 < 0 || Q.branch0 + Q.n_points > n_branches ||
+        Q.prefix_len < 0 || Q.prefix_pt_off < 0)
+      return fail(ORION_ERR_INVALID_ARG, "query %d: bad descriptor", q);
+    for (int32_t b = Q.branch0; b < Q.branch0 + Q.n_points; ++b) {
+      if (qof[b] >= 0) return fail(ORION_ERR_INVALID_ARG, "branch %d in two queries", b);
+      qof[b] = q;
+    }
+  }
+  for (int32_t b = 0; b < n_branches; ++b) {
+    const orion_point_desc& p = points[b];
+    if (p.pt_off < 0 || p.content_len < 0 || p.capacity < p.content_len)
+      return fail(ORION_ERR_INVALID_ARG, "branch %d: bad point descriptor", b);
+    if (qof[b] < 0) return fail(ORION_ERR_INVALID_ARG, "branch %d belongs to no query", b);
+    if (seg_offsets[b] > seg_offsets[b + 1] || seg_offsets[b] < 0)
+      return fail(ORION_ERR_INVALID_ARG, "seg_offsets not monotone at %d", b);
+  }
+  for (int32_t b = 0; b < n_branches; ++b) {
+    const orion_query_desc& Q = queries[qof[b]];
+    for (int32_t i = seg_offsets[b]; i < seg_offsets[b + 1]; ++i) {
+      const orion_segref r = refs[i];
+      if (r.kind == ORION_SEG_PREFIX) {
+        out[i] = {Q.prefix_pt_off, 0, Q.prefix_len, -1};
+        continue;
+      }
+      if (r.point < 1 || r.point > Q.n_points)
+        return fail(ORION_ERR_INVALID_ARG, "branch %d entry %d: point %d outside its query", b,
+                    i - seg_offsets[b], r.point);
+      const int32_t kb = Q.branch0 + r.point - 1;
+      const orion_point_desc& P = points[kb];
+      switch (r.kind) {
+        case ORION_SEG_CONTENT: out[i] = {P.pt_off, 0, P.content_len, -1}; break;
+        case ORION_SEG_FULL: out[i] = {P.pt_off, 0, P.capacity, kb}; break;
+        case ORION_SEG_OUTPUT: out[i] = {P.pt_off, P.content_len, P.capacity - P.content_len, kb}; break;
+        case ORION_SEG_OWN: out[i] = {P.pt_off, 0, P.capacity, kb}; break;
+        default: return fail(ORION_ERR_INVALID_ARG, "branch %d: segment kind %d", b, r.kind);
+      }
+    }
+  }
+  return ORION_OK;
+}
+
+namespace {
+
+struct Interval {
+  int32_t start, end, dyn, branch;
+};
+
+struct Piece {
+  int32_t pt_off, t0, t1, dyn;
+  std::vector<int32_t> readers;  // ascending branch ids
+};
+
+orion_status check_shape(const orion_attn_shape* s) {
+  if (!s) return fail(ORION_ERR_INVALID_ARG, "null shape");
+  if (s->num_q_heads < 1 || s->num_kv_heads < 1 || s->num_q_heads % s->num_kv_heads)
+    return fail(ORION_ERR_INVALID_ARG, "heads %d/%d", s->num_q_heads, s->num_kv_heads);
+  if (s->head_dim != 64 && s->head_dim != 128)
+    return fail(ORION_ERR_UNSUPPORTED, "head_dim %d not in {64,128}", s->head_dim);
+  if (s->page_size < 8 || s->page_size > 256 || (s->page_size & (s->page_size - 1)))
+    return fail(ORION_ERR_UNSUPPORTED, "page_size %d not a power of two in [8,256]", s->page_size);
+  return ORION_OK;
+}
+
+inline int64_t align16(int64_t x) { return (x + 15) & ~int64_t(15); }
+
+}  // namespace
+
+namespace orion {
+orion_status check_shape_public(const orion_attn_shape* s) { return check_shape(s); }
+}  // namespace orion
+
+extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t n_branches,
+                                          const int32_t* h_seg_offsets, const orion_seg* h_segs,
+                                          const int32_t* h_own_len, const orion_plan_opts* opts,
+                                          void* plan_buf, size_t plan_cap, size_t* plan_needed,
+                                          size_t* workspace_needed) {
+  orion_status st = check_shape(shape);
+  if (st != ORION_OK) return st;
+  if (n_branches < 1 || !h_seg_offsets || !h_segs || !plan_needed || !workspace_needed)
+    return fail(ORION_ERR_INVALID_ARG, "bad plan arguments");
+  const int32_t Hq = shape->num_q_heads, Hkv = shape->num_kv_heads, G = Hq / Hkv;
+  int32_t chunk = (opts && opts->chunk_tokens > 0) ? opts->chunk_tokens : 512;
+  chunk = std::max(kTileTokens, (chunk + kTileTokens - 1) / kTileTokens * kTileTokens);
+
+  // 1. Group bound segments by page run.
+  std::map<int32_t, std::vector<Interval>> groups;
+  std::vector<int64_t> logical(n_branches, 0);
+  int64_t logical_total = 0;
+  for (int32_t b = 0; b < n_branches; ++b) {
+    if (h_seg_offsets[b] > h_seg_offsets[b + 1] || h_seg_offsets[b] < 0)
+      return fail(ORION_ERR_INVALID_ARG, "seg_offsets not monotone at %d", b);
+    for (int32_t i = h_seg_offsets[b]; i < h_seg_offsets[b + 1]; ++i) {
+      const orion_seg& s = h_segs[i];
+      if (s.pt_off < 0 || s.start < 0 || s.len < 0 || s.dyn < -1 || s.dyn >= n_branches)
+        return fail(ORION_ERR_INVALID_ARG, "branch %d segment %d: bad fields", b, i);
+      if (s.len == 0) continue;  // zero-length segments are skipped (reading S22)
+      groups[s.pt_off].push_back({s.start, s.start + s.len, s.dyn, b});
+      logical[b] += s.len;
+    }
+    if (logical[b] == 0) return fail(ORION_ERR_INVALID_ARG, "branch %d has an empty context", b);
+    logical_total += logical[b];
+  }
+
+  // 2. Cut each run at every boundary; attach reader sets; merge equal neighbours.
+  std::vector<Piece> pieces;
+  for (auto& gkv : groups) {
+    std::vector<Interval>& iv = gkv.second;
+    int32_t dyn = -1;
+    for (auto& x : iv)
+      if (x.dyn >= 0) {
+        if (dyn >= 0 && dyn != x.dyn)
+          return fail(ORION_ERR_UNSUPPORTED,
+                      "page run %d grows with two branches (%d, %d)", gkv.first, dyn, x.dyn);
+        dyn = x.dyn;
+      }
+    std::vector<int32_t> cuts;
+    for (auto& x : iv) { cuts.push_back(x.start); cuts.push_back(x.end); }
+    std::sort(cuts.begin(), cuts.end());
+    cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
+    for (size_t c = 0; c + 1 < cuts.size(); ++c) {
+      const int32_t a = cuts[c], z = cuts[c + 1];
+      Piece p{gkv.first, a, z, -1, {}};
+      bool any_static = false;
+      int32_t static_end = 0;
+      for (auto& x : iv)
+        if (x.start <= a && x.end >= z) {
+          p.readers.push_back(x.branch);
+          if (x.dyn >= 0) p.dyn = x.dyn;
+          else { any_static = true; static_end = std::max(static_end, x.end); }
+        }
+      if (p.readers.empty()) continue;
+      std::sort(p.readers.begin(), p.readers.end());
+      for (size_t r = 1; r < p.readers.size(); ++r)
+        if (p.readers[r] == p.readers[r - 1])
+          return fail(ORION_ERR_INVALID_ARG,
+                      "branch %d covers tokens [%d,%d) of run %d twice", p.readers[r], a, z,
+                      gkv.first);
+      if (p.dyn >= 0 && any_static && h_own_len && static_end > h_own_len[p.dyn])
+        return fail(ORION_ERR_INVALID_ARG,
+                    "static segment of run %d ends at %d past own_len[%d]=%d", gkv.first,
+                    static_end, p.dyn, h_own_len[p.dyn]);
+      if (!pieces.empty()) {
+        Piece& q = pieces.back();
+        if (q.pt_off == p.pt_off && q.t1 == p.t0 && q.dyn == p.dyn && q.readers == p.readers) {
+          q.t1 = p.t1;
+          continue;
+        }
+      }
+      pieces.push_back(std::move(p));
+    }
+  }
+
+  // 3. Work items: piece x kv head x chunk x 64-row block.  Chunk length grows with the row
+  //    count so the fp32 partial traffic stays a small fraction of the KV bytes.
+  std::vector<WorkItem> items;
+  std::vector<int32_t> readers;
+  std::vector<int64_t> cost;
+  int64_t unique_tokens = 0;
+  int32_t n_slots = 0;
+  std::vector<std::vector<int32_t>> row_slots((size_t)n_branches * Hq);
+  for (size_t pi = 0; pi < pieces.size(); ++pi) {
+    const Piece& p = pieces[pi];
+    unique_tokens += p.t1 - p.t0;
+    const int32_t roff = (int32_t)readers.size();
+    readers.insert(readers.end(), p.readers.begin(), p.readers.end());
+    const int32_t rows = (int32_t)p.readers.size() * G;
+    const int32_t rows_blk = std::min(rows, kRowsPerItem);
+    int32_t ch = std::max(chunk, 32 * rows_blk);
+    ch = (ch + kTileTokens - 1) / kTileTokens * kTileTokens;
+    for (int32_t g = 0; g < Hkv; ++g)
+      for (int32_t t = p.t0; t < p.t1; t += ch)
+        for (int32_t r0 = 0; r0 < rows; r0 += kRowsPerItem) {
+          WorkItem w{};
+          w.pt_off = p.pt_off; w.t0 = t; w.t1 = std::min(p.t1, t + ch); w.dyn = p.dyn;
+          w.kv_head = g; w.readers_off = roff; w.row_begin = r0;
+          w.n_rows = std::min(kRowsPerItem, rows - r0); w.slot0 = n_slots; w.piece = (int32_t)pi;
+          for (int32_t r = r0; r < r0 + w.n_rows; ++r) {
+            const int32_t b = p.readers[r / G], h = g * G + r % G;
+            row_slots[(size_t)b * Hq + h].push_back(n_slots + (r - r0));
+          }
+          n_slots += w.n_rows;
+          items.push_back(w);
+          // ~ cycles: stream the tokens, plus the row tiles' MMA work, plus a fixed start-up.
+          cost.push_back((int64_t)(w.t1 - w.t0) * (2 + (w.n_rows + 15) / 16) + 256);
+        }
+  }
+  for (size_t r = 0; r < row_slots.size(); ++r)
+    if (row_slots[r].empty())
+      return fail(ORION_ERR_INVALID_ARG, "row %zu (branch %zu) has no context", r, r / Hq);
+
+  // Longest first; row blocks of one chunk stay adjacent (same cost, stable sort) so they run
+  // together and share the chunk through L2.
+  std::vector<int32_t> perm(items.size());
+  for (size_t i = 0; i < perm.size(); ++i) perm[i] = (int32_t)i;
+  std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) { return cost[a] > cost[b]; });
+
+  // 4. Serialise.
+  const int64_t n_rows = (int64_t)n_branches * Hq;
+  PlanHeader h{};
+  h.magic = kPlanMagic; h.version = kPlanVersion;
+  h.n_branches = n_branches; h.num_q_heads = Hq; h.num_kv_heads = Hkv;
+  h.head_dim = shape->head_dim; h.page_size = shape->page_size; h.group = G;
+  h.n_items = (int32_t)items.size(); h.n_partials = n_slots; h.n_rows = (int32_t)n_rows;
+  h.n_reader_entries = (int32_t)readers.size();
+  h.items_off = align16(sizeof(PlanHeader));
+  h.readers_off = align16(h.items_off + (int64_t)items.size() * sizeof(WorkItem));
+  h.comb_off_off = align16(h.readers_off + (int64_t)readers.size() * 4);
+  h.comb_slot_off = align16(h.comb_off_off + (n_rows + 1) * 4);
+  h.plan_bytes = align16(h.comb_slot_off + (int64_t)n_slots * 4);
+  h.acc_bytes = align16((int64_t)n_slots * shape->head_dim * 4);
+  h.workspace_bytes = h.acc_bytes + align16((int64_t)n_slots * 8);
+  h.n_pieces = (int64_t)pieces.size();
+  h.unique_tokens = unique_tokens;
+  h.logical_tokens = logical_total;
+  h.sm_scale = shape->sm_scale > 0.f ? shape->sm_scale : 1.0f / std::sqrt((float)shape->head_dim);
+  *plan_needed = (size_t)h.plan_bytes;
+  *workspace_needed = (size_t)h.workspace_bytes;
+  if (!plan_buf || plan_cap < (size_t)h.plan_bytes)
+    return fail(ORION_ERR_CAPACITY, "plan_cap=%zu < needed %lld", plan_cap, (long long)h.plan_bytes);
+  if (reinterpret_cast<uintptr_t>(plan_buf) & 15)
+    return fail(ORION_ERR_INVALID_ARG, "plan_buf must be 16-byte aligned");
+  char* base = static_cast<char*>(plan_buf);
+  std::memset(base, 0, (size_t)h.plan_bytes);
+  std::memcpy(base, &h, sizeof h);
+  WorkItem* wi = reinterpret_cast<WorkItem*>(base + h.items_off);
+  for (size_t i = 0; i < perm.size(); ++i) wi[i] = items[perm[i]];
+  std::memcpy(base + h.readers_off, readers.data(), readers.size() * 4);
+  int32_t* coff = reinterpret_cast<int32_t*>(base + h.comb_off_off);
+  int32_t* cslot = reinterpret_cast<int32_t*>(base + h.comb_slot_off);
+  int32_t o = 0;
+  for (int64_t r = 0; r < n_rows; ++r) {
+    coff[r] = o;
+    for (int32_t s : row_slots[r]) cslot[o++] = s;
+  }
+  coff[n_rows] = o;
+  return ORION_OK;
+}
+
+extern "C" orion_status orion_plan_get_stats(const void* h_plan, orion_plan_stats* out) {
+  if (!h_plan || !out) return fail(ORION_ERR_INVALID_ARG, "null argument");
+  const PlanHeader* h = static_cast<const PlanHeader*>(h_plan);
+  if (h->magic != kPlanMagic || h->version != kPlanVersion)
+    return fail(ORION_ERR_INVALID_ARG, "not an orion plan");
+  out->n_items = h->n_items;
+  out->n_pieces = h->n_pieces;
+  out->n_partials = h->n_partials;
+  out->n_rows = h->n_rows;
+  out->unique_tokens = h->unique_tokens;
+  out->logical_tokens = h->logical_tokens;
+  out->plan_bytes = h->plan_bytes;
+  out->workspace_bytes = h->workspace_bytes;
+  return ORION_OK;
+}

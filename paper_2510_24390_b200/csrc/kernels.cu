@@ -1,0 +1,506 @@
+// kernels.cu — device side of the Orion expansion decode step for sm_100a.
+//
+//   K1 kv_append_kernel   one block per branch; 128-bit bit-exact copy of the new token's K/V
+//                         into slot own_len of the branch's own page run.
+//   K2 split_kernel       one work item = (shared piece, kv head, token chunk, <=64 query rows).
+//                         The chunk's K/V tokens are gathered page-by-page with 16-byte cp.async
+//                         into an XOR-swizzled 3-stage shared-memory ring, so every token of a
+//                         shared prefix/ancestor piece is read from HBM once for all the rows
+//                         (branches x GQA heads) that attend to it.  Q.K^T and P.V run on the
+//                         tensor cores (mma.sync m16n8k16 bf16 -> fp32), with an fp32 online
+//                         softmax in the log2 domain (row max / sum by warp shuffles).  Each
+//                         row's partial (m, l, acc) goes to the fp32 workspace.
+//   K3 combine_kernel     one warp per (branch, q head): LSE-merge of its partials in plan order,
+//                         out = acc / l rounded to bf16 (RNE), lse = ln-sum-exp.
+//
+// Semantics: include/orion.h.  Design and rooflines: DESIGN.md §"Kernels".
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <mutex>
+
+#include "../../include/orion.h"
+#include "plan_format.h"
+
+namespace orion {
+orion_status fail(orion_status code, const char* fmt, ...);
+orion_status check_shape_public(const orion_attn_shape* s);
+}  // namespace orion
+
+using namespace orion;
+
+namespace {
+
+constexpr int kStages = 3;
+constexpr int kThreads = 128;   // 4 warps, 16 query rows each
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+// ------------------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async_16(uint32_t dst, const void* src, bool valid) {
+  const int n = valid ? 16 : 0;  // n == 0: zero-fill, nothing read
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                        uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                          uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ float2 unpack_bf16(uint32_t v) {
+  return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&v));
+}
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Byte offset of 16-byte chunk `c` of row `r` in a [rows][D] bf16 tile; XOR swizzle on the low
+// three chunk bits makes the 8 rows of every ldmatrix phase hit 8 distinct bank groups.
+template <int D>
+__device__ __forceinline__ uint32_t swz(int r, int c) {
+  return static_cast<uint32_t>(r * (D * 2) + ((c ^ (r & 7)) << 4));
+}
+
+struct SplitArgs {
+  const WorkItem* items;
+  const int32_t* readers;
+  const __nv_bfloat16* q;
+  const __nv_bfloat16* k;
+  const __nv_bfloat16* v;
+  const int32_t* page_table;
+  const int32_t* own_len;
+  float* part_acc;
+  float2* part_ml;
+  int32_t hq, hkv, group, page_shift;
+  float scale_log2;
+};
+
+// ------------------------------------------------------------------------------ K2 split
+template <int D>
+__global__ void __launch_bounds__(kThreads, 2) split_kernel(const SplitArgs a) {
+  constexpr int CH = D / 8;                 // 16-byte chunks per token row
+  constexpr int TILE_BYTES = kTileTokens * D * 2;
+  constexpr int NB_S = kTileTokens / 8;     // n-blocks of S per tile (8 tokens each)
+  constexpr int NB_O = D / 8;               // n-blocks of the output accumulator
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* sQ = smem;
+  uint8_t* sK = smem + kRowsPerItem * D * 2;
+  uint8_t* sV = sK + kStages * TILE_BYTES;
+
+  const WorkItem w = a.items[blockIdx.x];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  int end = w.t1;
+  if (w.dyn >= 0) end = min(end, __ldg(a.own_len + w.dyn));
+  const int ntok = max(0, end - w.t0);
+  const int ntiles = (ntok + kTileTokens - 1) / kTileTokens;
+  const int pmask = (1 << a.page_shift) - 1;
+  const size_t head_stride = static_cast<size_t>(D) << a.page_shift;  // one (page, kv head) block
+
+  // Q rows of this item -> sQ (zero rows past n_rows).
+  for (int i = tid; i < kRowsPerItem * CH; i += kThreads) {
+    const int r = i / CH, c = i % CH;
+    const bool ok = r < w.n_rows;
+    const __nv_bfloat16* src = a.q;
+    if (ok) {
+      const int rr = w.row_begin + r;
+      const int b = __ldg(a.readers + w.readers_off + rr / a.group);
+      const int h = w.kv_head * a.group + rr % a.group;
+      src = a.q + (static_cast<size_t>(b) * a.hq + h) * D + c * 8;
+    }
+    cp_async_16(smem_addr(sQ + swz<D>(r, c)), src, ok);
+  }
+  cp_async_commit();
+
+  auto load_tile = [&](int tile, int stage) {
+    const int tbase = w.t0 + tile * kTileTokens;
+    uint8_t* dk = sK + stage * TILE_BYTES;
+    uint8_t* dv = sV + stage * TILE_BYTES;
+#pragma unroll 4
+    for (int i = tid; i < kTileTokens * CH; i += kThreads) {
+      const int tt = i / CH, c = i % CH;
+      const int pos = tbase + tt;
+      const bool ok = pos < end;
+      size_t off = 0;
+      if (ok) {
+        const int page = __ldg(a.page_table + w.pt_off + (pos >> a.page_shift));
+        off = (static_cast<size_t>(page) * a.hkv + w.kv_head) * head_stride +
+              static_cast<size_t>(pos & pmask) * D + c * 8;
+      }
+      cp_async_16(smem_addr(dk + swz<D>(tt, c)), a.k + off, ok);
+      cp_async_16(smem_addr(dv + swz<D>(tt, c)), a.v + off, ok);
+    }
+  };
+
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (s < ntiles) load_tile(s, s);
+    cp_async_commit();
+  }
+
+  const int wr0 = warp * 16;
+  const bool active = wr0 < w.n_rows;
+  uint32_t qf[D / 16][4];
+  float acc[NB_O][4];
+#pragma unroll
+  for (int n = 0; n < NB_O; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+
+  for (int it = 0; it < ntiles; ++it) {
+    cp_async_wait<kStages - 2>();
+    __syncthreads();
+    {
+      const int nt = it + kStages - 1;
+      if (nt < ntiles) load_tile(nt, nt % kStages);
+      cp_async_commit();
+    }
+    if (!active) continue;
+    if (it == 0) {
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const int m = lane >> 3;
+        const int r = wr0 + (m & 1) * 8 + (lane & 7);
+        ldsm_x4(smem_addr(sQ + swz<D>(r, kk * 2 + (m >> 1))), qf[kk][0], qf[kk][1], qf[kk][2],
+                qf[kk][3]);
+      }
+    }
+    const uint8_t* tk = sK + (it % kStages) * TILE_BYTES;
+    const uint8_t* tv = sV + (it % kStages) * TILE_BYTES;
+
+    // S = Q K^T for this warp's 16 rows x 64 tokens.
+    float s[NB_S][4];
+#pragma unroll
+    for (int n = 0; n < NB_S; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+#pragma unroll
+      for (int np = 0; np < NB_S / 2; ++np) {
+        const int m = lane >> 3;
+        const int tok = np * 16 + (m >> 1) * 8 + (lane & 7);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(smem_addr(tk + swz<D>(tok, kk * 2 + (m & 1))), b0, b1, b2, b3);
+        mma_bf16(s[2 * np], qf[kk], b0, b1);
+        mma_bf16(s[2 * np + 1], qf[kk], b2, b3);
+      }
+    }
+    // Scale into the log2 domain and mask tokens past the end.
+    const int tbase = w.t0 + it * kTileTokens;
+    const bool tail = tbase + kTileTokens > end;
+#pragma unroll
+    for (int n = 0; n < NB_S; ++n)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float x = s[n][e] * a.scale_log2;
+        if (tail && tbase + n * 8 + 2 * (lane & 3) + (e & 1) >= end) x = -INFINITY;
+        s[n][e] = x;
+      }
+    float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+    for (int n = 0; n < NB_S; ++n) {
+      mx0 = fmaxf(mx0, fmaxf(s[n][0], s[n][1]));
+      mx1 = fmaxf(mx1, fmaxf(s[n][2], s[n][3]));
+    }
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+    const float nm0 = fmaxf(m0, mx0), nm1 = fmaxf(m1, mx1);
+    const float base0 = nm0 == -INFINITY ? 0.f : nm0;
+    const float base1 = nm1 == -INFINITY ? 0.f : nm1;
+    const float al0 = fast_exp2(m0 - base0), al1 = fast_exp2(m1 - base1);
+    m0 = nm0;
+    m1 = nm1;
+    // P = exp2(S - m), rounded to bf16 for the PV MMA; l sums the SAME rounded values.
+    uint32_t p[NB_S][2];
+    float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+    for (int n = 0; n < NB_S; ++n) {
+      p[n][0] = pack_bf16(fast_exp2(s[n][0] - base0), fast_exp2(s[n][1] - base0));
+      p[n][1] = pack_bf16(fast_exp2(s[n][2] - base1), fast_exp2(s[n][3] - base1));
+      const float2 u = unpack_bf16(p[n][0]), v = unpack_bf16(p[n][1]);
+      rs0 += u.x + u.y;
+      rs1 += v.x + v.y;
+    }
+    l0 = l0 * al0 + rs0;
+    l1 = l1 * al1 + rs1;
+#pragma unroll
+    for (int n = 0; n < NB_O; ++n) {
+      acc[n][0] *= al0; acc[n][1] *= al0;
+      acc[n][2] *= al1; acc[n][3] *= al1;
+    }
+    // O += P V.
+#pragma unroll
+    for (int kt = 0; kt < kTileTokens / 16; ++kt) {
+      const uint32_t pa[4] = {p[2 * kt][0], p[2 * kt][1], p[2 * kt + 1][0], p[2 * kt + 1][1]};
+#pragma unroll
+      for (int np = 0; np < NB_O / 2; ++np) {
+        const int m = lane >> 3;
+        const int tok = kt * 16 + (m & 1) * 8 + (lane & 7);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(smem_addr(tv + swz<D>(tok, np * 2 + (m >> 1))), b0, b1, b2, b3);
+        mma_bf16(acc[2 * np], pa, b0, b1);
+        mma_bf16(acc[2 * np + 1], pa, b2, b3);
+      }
+    }
+  }
+  cp_async_wait<0>();
+  if (!active) return;
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  const int r0 = wr0 + (lane >> 2), r1 = r0 + 8;
+  const int c0 = 2 * (lane & 3);
+  if (r0 < w.n_rows) {
+    float* dst = a.part_acc + static_cast<size_t>(w.slot0 + r0) * D;
+#pragma unroll
+    for (int n = 0; n < NB_O; ++n)
+      *reinterpret_cast<float2*>(dst + n * 8 + c0) = make_float2(acc[n][0], acc[n][1]);
+    if ((lane & 3) == 0) a.part_ml[w.slot0 + r0] = make_float2(m0, l0);
+  }
+  if (r1 < w.n_rows) {
+    float* dst = a.part_acc + static_cast<size_t>(w.slot0 + r1) * D;
+#pragma unroll
+    for (int n = 0; n < NB_O; ++n)
+      *reinterpret_cast<float2*>(dst + n * 8 + c0) = make_float2(acc[n][2], acc[n][3]);
+    if ((lane & 3) == 0) a.part_ml[w.slot0 + r1] = make_float2(m1, l1);
+  }
+}
+
+// ------------------------------------------------------------------------------ K3 combine
+template <int D>
+__global__ void __launch_bounds__(256) combine_kernel(const int32_t* __restrict__ comb_off,
+                                                      const int32_t* __restrict__ comb_slot,
+                                                      const float* __restrict__ part_acc,
+                                                      const float2* __restrict__ part_ml,
+                                                      __nv_bfloat16* __restrict__ out,
+                                                      float* __restrict__ lse, int n_rows) {
+  constexpr int V = D / 32;  // floats per lane
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n_rows) return;
+  const int e0 = __ldg(comb_off + row), e1 = __ldg(comb_off + row + 1);
+  float M = -INFINITY;
+  for (int e = e0 + lane; e < e1; e += 32) M = fmaxf(M, part_ml[__ldg(comb_slot + e)].x);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  const float base = M == -INFINITY ? 0.f : M;
+  float acc[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) acc[i] = 0.f;
+  float L = 0.f;
+  for (int e = e0; e < e1; ++e) {  // fixed plan order -> deterministic
+    const int slot = __ldg(comb_slot + e);
+    const float2 ml = part_ml[slot];
+    const float wgt = fast_exp2(ml.x - base);
+    L += wgt * ml.y;
+    const float* src = part_acc + static_cast<size_t>(slot) * D + lane * V;
+    if constexpr (V == 4) {
+      const float4 x = *reinterpret_cast<const float4*>(src);
+      acc[0] += wgt * x.x; acc[1] += wgt * x.y; acc[2] += wgt * x.z; acc[3] += wgt * x.w;
+    } else {
+      const float2 x = *reinterpret_cast<const float2*>(src);
+      acc[0] += wgt * x.x; acc[1] += wgt * x.y;
+    }
+  }
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  __nv_bfloat16* o = out + static_cast<size_t>(row) * D + lane * V;
+  if constexpr (V == 4) {
+    uint2 pk;
+    pk.x = pack_bf16(acc[0] * inv, acc[1] * inv);
+    pk.y = pack_bf16(acc[2] * inv, acc[3] * inv);
+    *reinterpret_cast<uint2*>(o) = pk;
+  } else {
+    *reinterpret_cast<uint32_t*>(o) = pack_bf16(acc[0] * inv, acc[1] * inv);
+  }
+  if (lse && lane == 0) lse[row] = L > 0.f ? (M + log2f(L)) * kLn2 : -INFINITY;
+}
+
+// ------------------------------------------------------------------------------ K1 append
+template <int D>
+__global__ void __launch_bounds__(128) kv_append_kernel(
+    const __nv_bfloat16* __restrict__ k_new, const __nv_bfloat16* __restrict__ v_new,
+    __nv_bfloat16* __restrict__ k_cache, __nv_bfloat16* __restrict__ v_cache,
+    const int32_t* __restrict__ own_pt_off, const int32_t* __restrict__ own_cap,
+    const int32_t* __restrict__ page_table, int32_t* __restrict__ own_len, int hkv,
+    int page_shift, int mode) {
+  constexpr int CH = D / 8;
+  __shared__ int s_pos, s_page, s_len;
+  const int b = blockIdx.x;
+  if (threadIdx.x == 0) {
+    const int len = own_len[b];
+    const int pos = mode == ORION_APPEND_REWRITE ? len - 1 : len;
+    const bool ok = pos >= 0 && pos < own_cap[b];
+    s_len = len;
+    s_pos = pos;
+    s_page = ok ? page_table[own_pt_off[b] + (pos >> page_shift)] : -1;
+  }
+  __syncthreads();
+  const int page = s_page, pos = s_pos;
+  if (page < 0) return;
+  const size_t row = static_cast<size_t>(pos & ((1 << page_shift) - 1)) * D;
+  for (int i = threadIdx.x; i < hkv * CH; i += blockDim.x) {
+    const int g = i / CH, c = i % CH;
+    const size_t dst = ((static_cast<size_t>(page) * hkv + g) << page_shift) * D + row + c * 8;
+    const size_t src = (static_cast<size_t>(b) * hkv + g) * D + c * 8;
+    *reinterpret_cast<uint4*>(k_cache + dst) = *reinterpret_cast<const uint4*>(k_new + src);
+    *reinterpret_cast<uint4*>(v_cache + dst) = *reinterpret_cast<const uint4*>(v_new + src);
+  }
+  if (threadIdx.x == 0 && mode == ORION_APPEND_ADVANCE) own_len[b] = s_len + 1;
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int log2i(int x) {
+  int s = 0;
+  while ((1 << s) < x) ++s;
+  return s;
+}
+
+template <int D>
+size_t split_smem_bytes() {
+  return static_cast<size_t>(kRowsPerItem) * D * 2 + 2ull * kStages * kTileTokens * D * 2;
+}
+
+template <int D>
+orion_status launch_attn(const PlanHeader* h, const char* dplan, const void* q, void* out,
+                         float* lse, const void* k, const void* v, const int32_t* page_table,
+                         const int32_t* own_len, void* ws, cudaStream_t st) {
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(split_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)split_smem_bytes<D>());
+  });
+  if (attr_err != cudaSuccess)
+    return fail(ORION_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
+  SplitArgs a;
+  a.items = reinterpret_cast<const WorkItem*>(dplan + h->items_off);
+  a.readers = reinterpret_cast<const int32_t*>(dplan + h->readers_off);
+  a.q = static_cast<const __nv_bfloat16*>(q);
+  a.k = static_cast<const __nv_bfloat16*>(k);
+  a.v = static_cast<const __nv_bfloat16*>(v);
+  a.page_table = page_table;
+  a.own_len = own_len;
+  a.part_acc = static_cast<float*>(ws);
+  a.part_ml = reinterpret_cast<float2*>(static_cast<char*>(ws) + h->acc_bytes);
+  a.hq = h->num_q_heads;
+  a.hkv = h->num_kv_heads;
+  a.group = h->group;
+  a.page_shift = log2i(h->page_size);
+  a.scale_log2 = h->sm_scale * kLog2e;
+  split_kernel<D><<<h->n_items, kThreads, split_smem_bytes<D>(), st>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ORION_ERR_CUDA, "split_kernel: %s", cudaGetErrorString(e));
+  const int nb = (h->n_rows + 7) / 8;
+  combine_kernel<D><<<nb, 256, 0, st>>>(
+      reinterpret_cast<const int32_t*>(dplan + h->comb_off_off),
+      reinterpret_cast<const int32_t*>(dplan + h->comb_slot_off), a.part_acc, a.part_ml,
+      static_cast<__nv_bfloat16*>(out), lse, h->n_rows);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ORION_ERR_CUDA, "combine_kernel: %s", cudaGetErrorString(e));
+  return ORION_OK;
+}
+
+}  // namespace
+
+extern "C" orion_status orion_kv_append(const orion_attn_shape* shape, int32_t n_branches,
+                                        const void* k_new, const void* v_new, void* k_cache,
+                                        void* v_cache, const int32_t* own_pt_off,
+                                        const int32_t* own_cap, const int32_t* page_table,
+                                        int32_t* own_len, int32_t mode, void* stream) {
+  orion_status st = check_shape_public(shape);
+  if (st != ORION_OK) return st;
+  if (n_branches < 0) return fail(ORION_ERR_INVALID_ARG, "n_branches < 0");
+  if (mode != ORION_APPEND_ADVANCE && mode != ORION_APPEND_REWRITE)
+    return fail(ORION_ERR_INVALID_ARG, "bad append mode %d", mode);
+  if (!k_new || !v_new || !k_cache || !v_cache || !own_pt_off || !own_cap || !page_table ||
+      !own_len)
+    return fail(ORION_ERR_INVALID_ARG, "null device pointer");
+  if (!aligned16(k_new) || !aligned16(v_new) || !aligned16(k_cache) || !aligned16(v_cache))
+    return fail(ORION_ERR_INVALID_ARG, "K/V pointers must be 16-byte aligned");
+  if (n_branches == 0) return ORION_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int shift = log2i(shape->page_size);
+  if (shape->head_dim == 128)
+    kv_append_kernel<128><<<n_branches, 128, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(k_new), static_cast<const __nv_bfloat16*>(v_new),
+        static_cast<__nv_bfloat16*>(k_cache), static_cast<__nv_bfloat16*>(v_cache), own_pt_off,
+        own_cap, page_table, own_len, shape->num_kv_heads, shift, mode);
+  else
+    kv_append_kernel<64><<<n_branches, 128, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(k_new), static_cast<const __nv_bfloat16*>(v_new),
+        static_cast<__nv_bfloat16*>(k_cache), static_cast<__nv_bfloat16*>(v_cache), own_pt_off,
+        own_cap, page_table, own_len, shape->num_kv_heads, shift, mode);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ORION_ERR_CUDA, "kv_append_kernel: %s", cudaGetErrorString(e));
+  return ORION_OK;
+}
+
+extern "C" orion_status orion_expand_attn(const orion_attn_shape* shape, int32_t n_branches,
+                                          const void* q, void* out, float* lse,
+                                          const void* k_cache, const void* v_cache,
+                                          int32_t num_pages, const int32_t* page_table,
+                                          const int32_t* own_len, const void* h_plan,
+                                          const void* d_plan, void* workspace,
+                                          size_t workspace_bytes, void* stream) {
+  orion_status st = check_shape_public(shape);
+  if (st != ORION_OK) return st;
+  if (!q || !out || !k_cache || !v_cache || !page_table || !own_len || !h_plan || !d_plan ||
+      !workspace)
+    return fail(ORION_ERR_INVALID_ARG, "null pointer");
+  if (!aligned16(q) || !aligned16(out) || !aligned16(k_cache) || !aligned16(v_cache) ||
+      !aligned16(d_plan) || !aligned16(workspace))
+    return fail(ORION_ERR_INVALID_ARG, "device pointers must be 16-byte aligned");
+  const PlanHeader* h = static_cast<const PlanHeader*>(h_plan);
+  if (h->magic != kPlanMagic || h->version != kPlanVersion)
+    return fail(ORION_ERR_INVALID_ARG, "h_plan is not an orion plan");
+  if (h->n_branches != n_branches || h->num_q_heads != shape->num_q_heads ||
+      h->num_kv_heads != shape->num_kv_heads || h->head_dim != shape->head_dim ||
+      h->page_size != shape->page_size)
+    return fail(ORION_ERR_INVALID_ARG, "plan was built for another shape / branch count");
+  if (workspace_bytes < static_cast<size_t>(h->workspace_bytes))
+    return fail(ORION_ERR_INVALID_ARG, "workspace %zu < %lld bytes", workspace_bytes,
+                (long long)h->workspace_bytes);
+  if (num_pages < 1) return fail(ORION_ERR_INVALID_ARG, "num_pages < 1");
+  if (h->n_items < 1) return fail(ORION_ERR_INVALID_ARG, "empty plan");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const char* dp = static_cast<const char*>(d_plan);
+  if (shape->head_dim == 128)
+    return launch_attn<128>(h, dp, q, out, lse, k_cache, v_cache, page_table, own_len, workspace, s);
+  return launch_attn<64>(h, dp, q, out, lse, k_cache, v_cache, page_table, own_len, workspace, s);
+}
+
+extern "C" const char* orion_version(void) {
+  return "orion-b200 0.1 (sm_100a; K1 append, K2 split mma.sync m16n8k16 bf16 + cp.async 3-stage, "
+         "K3 combine)";
+}

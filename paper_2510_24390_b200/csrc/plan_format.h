@@ -1,0 +1,42 @@
+// plan_format.h — device plan layout shared by the host planner (host.cpp) and the kernels
+// (kernels.cu).  Product-side only; the oracle never sees it.
+//
+// A plan is one contiguous byte buffer:
+//   PlanHeader | WorkItem[n_items] | readers[n_reader_entries] (int32 branch ids)
+//              | comb_off[n_rows + 1] (int32) | comb_slot[n_partials] (int32)
+// Workspace (caller-allocated, device):
+//   part_acc fp32 [n_partials][head_dim] | part_ml fp32 [n_partials][2]  (m in log2 units, l)
+#pragma once
+#include <stdint.h>
+
+namespace orion {
+
+constexpr int32_t kPlanMagic = 0x314e524f;  // "ORN1"
+constexpr int32_t kPlanVersion = 1;
+constexpr int kRowsPerItem = 64;   // query rows per split work item (4 warps x m16)
+constexpr int kTileTokens = 64;    // tokens per pipeline stage in the split kernel
+
+struct PlanHeader {
+  int32_t magic, version;
+  int32_t n_branches, num_q_heads, num_kv_heads, head_dim, page_size, group;
+  int32_t n_items, n_partials, n_rows, n_reader_entries;
+  int64_t items_off, readers_off, comb_off_off, comb_slot_off;  // byte offsets from plan start
+  int64_t plan_bytes, workspace_bytes, acc_bytes;                // acc_bytes = part_ml offset
+  int64_t n_pieces, unique_tokens, logical_tokens;
+  float sm_scale;
+  int32_t pad_[3];
+};
+static_assert(sizeof(PlanHeader) % 16 == 0, "header must keep 16-byte alignment");
+
+// One split-kernel work item: tokens [t0, min(t1, own_len[dyn])) of the page run at pt_off,
+// kv head `kv_head`, query rows [row_begin, row_begin + n_rows) of the piece's row space
+// (row r -> reader branch readers[readers_off + r / group], q head kv_head*group + r % group).
+// Row r writes partial slot slot0 + (r - row_begin).
+struct WorkItem {
+  int32_t pt_off, t0, t1, dyn;
+  int32_t kv_head, readers_off, row_begin, n_rows;
+  int32_t slot0, piece, pad0, pad1;
+};
+static_assert(sizeof(WorkItem) == 48, "WorkItem is 3 x 16 bytes");
+
+}  // namespace orion

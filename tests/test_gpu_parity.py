@@ -1,0 +1,152 @@
+"""T2 — GPU parity of the CUDA path (C ABI) against the fp64 oracle on the same seeded bytes.
+Gates (north_star): append bit-exact; out max-abs <= 2e-2 and rel-L2 <= 5e-3; lse abs <= 5e-3."""
+import random
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2510_24390_b200 as orion
+from workloads import configs as C, tensors as T, dags as W
+from tests.gpu_helpers import check_parity, run_step, u16, batch_for
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.mark.parametrize("policy", [0, 1])
+@pytest.mark.parametrize("variant", ["plain", "peaky", "sink", "contiguous", "ragged"])
+def test_c1_diamond(policy, variant):
+    cfg = C.CONFIGS["c1"]
+    lay = T.make_layout(cfg, contiguous=variant == "contiguous", ragged=variant == "ragged",
+                        extra_tokens=cfg.page)
+    ten = T.make_qkv(cfg, lay, q_scale=4.0 if variant == "peaky" else 1.0, sink=variant == "sink")
+    check_parity(cfg, lay, ten, policy)
+
+
+@pytest.mark.parametrize("page", [16, 32, 64])
+@pytest.mark.parametrize("hq,hkv,d", [(4, 2, 64), (8, 8, 128), (28, 4, 128), (32, 4, 64)])
+def test_shapes_pages_ragged(page, hq, hkv, d):
+    cfg = C.CONFIGS["c1"].with_(hq=hq, hkv=hkv, d=d, page=page, lp=300, t=150, lc=20, n_queries=2,
+                                dag="mixed8")
+    lay = T.make_layout(cfg, ragged=True, extra_tokens=page)
+    ten = T.make_qkv(cfg, lay, q_scale=2.0)
+    check_parity(cfg, lay, ten, 0, chunk_tokens=128)
+
+
+def test_c2_full_layer():
+    cfg = C.CONFIGS["c2"]
+    lay = T.make_layout(cfg, extra_tokens=cfg.page)
+    ten = T.make_qkv(cfg, lay)
+    check_parity(cfg, lay, ten, 0)
+
+
+@pytest.mark.parametrize("policy", [0, 1])
+def test_c3_full_layer(policy):
+    cfg = C.CONFIGS["c3"]
+    lay = T.make_layout(cfg, extra_tokens=cfg.page)
+    ten = T.make_qkv(cfg, lay, q_scale=2.0)
+    check_parity(cfg, lay, ten, policy)
+
+
+def _sample(lay, k, seed):
+    rng = random.Random(seed)
+    return sorted(rng.sample(range(lay.n_branches), k))
+
+
+def test_c4_full_size_sampled():
+    # The bench workload at full size (64 queries x mixed16, 4K prefix, 512 tok/point); outputs
+    # are checked on a sample of branches the oracle computes one by one.
+    cfg = C.CONFIGS["c4"]
+    lay = T.make_layout(cfg, extra_tokens=cfg.page)
+    ten = T.make_qkv(cfg, lay, device="cuda")
+    ten = {k: v.cpu() for k, v in ten.items()}
+    check_parity(cfg, lay, ten, 0, branches=_sample(lay, 24, 4) + [lay.n_branches - 1])
+
+
+@pytest.mark.parametrize("name", ["c5w", "c5c"])
+def test_c5_per_gpu_share_sampled(name):
+    cfg = C.CONFIGS[name].with_(n_queries=8)     # one GPU's share at 8 GPUs
+    lay = T.make_layout(cfg, extra_tokens=cfg.page)
+    ten = T.make_qkv(cfg, lay, device="cuda", q_scale=2.0)
+    ten = {k: v.cpu() for k, v in ten.items()}
+    check_parity(cfg, lay, ten, 0, branches=_sample(lay, 12, 5) + [63, lay.n_branches - 1])
+
+
+def test_page_permutation_bitwise_and_determinism():
+    cfg = C.CONFIGS["c2"].with_(lp=1024)
+    lay = T.make_layout(cfg, contiguous=True, extra_tokens=cfg.page)
+    ten = T.make_qkv(cfg, lay)
+    a = run_step(cfg, lay, ten)
+    b = run_step(cfg, lay, ten)
+    assert torch.equal(a["out"], b["out"]) and torch.equal(a["lse"], b["lse"])
+    perm = torch.from_numpy(np.random.default_rng(3).permutation(lay.num_pages))
+    ten2 = dict(ten)
+    for key in ("k_cache", "v_cache"):
+        x = torch.empty_like(ten[key])
+        x[:, perm] = ten[key]
+        ten2[key] = x
+    lay2 = T.make_layout(cfg, contiguous=True, extra_tokens=cfg.page)
+    lay2.page_table = perm.numpy()[lay.page_table].astype(np.int32)
+    c = run_step(cfg, lay2, ten2)
+    assert torch.equal(a["out"], c["out"]) and torch.equal(a["lse"], c["lse"])
+
+
+def test_advance_three_steps_and_rewrite():
+    cfg = C.CONFIGS["c1"].with_(lp=200, t=70, lc=8, hq=8, hkv=2, d=128)
+    lay = T.make_layout(cfg, ragged=True, extra_tokens=3 * cfg.page)
+    ten = T.make_qkv(cfg, lay, layers=3)
+    from oracle import append as OA, step as OS
+    dev = torch.device("cuda")
+    batch = batch_for(cfg, lay)
+    kc, vc = ten["k_cache"][0].to(dev), ten["v_cache"][0].to(dev)
+    k_ref, v_ref, own = u16(ten["k_cache"][0]), u16(ten["v_cache"][0]), lay.own_len.copy()
+    for step in range(3):
+        q, kn, vn = (ten[x][step].to(dev).contiguous() for x in ("q", "k_new", "v_new"))
+        out = torch.empty_like(q)
+        batch.step(q, kn, vn, kc, vc, out)
+        k_ref, own2 = OA.kv_append(k_ref, u16(ten["k_new"][step]), lay.page_table, lay.point_pt_off, own, cfg.page)
+        v_ref, _ = OA.kv_append(v_ref, u16(ten["v_new"][step]), lay.page_table, lay.point_pt_off, own, cfg.page)
+        own = own2
+        ref, _ = OS.expand_step(lay, u16(ten["q"][step]), k_ref, v_ref, own_len=own)
+        torch.cuda.synchronize()
+        assert np.array_equal(batch.own_len.cpu().numpy(), own)
+        assert np.array_equal(u16(kc), k_ref) and np.array_equal(u16(vc), v_ref)
+        o = out.float().cpu().numpy()
+        assert np.abs(o - ref).max() <= 2e-2
+        assert np.linalg.norm(o - ref) / np.linalg.norm(ref) <= 5e-3
+    # rewrite mode keeps lengths and rewrites the last slot
+    q, kn, vn = (ten[x][0].to(dev).contiguous() for x in ("q", "k_new", "v_new"))
+    batch.step(q, kn, vn, kc, vc, torch.empty_like(q), mode=orion.APPEND_REWRITE)
+    torch.cuda.synchronize()
+    assert np.array_equal(batch.own_len.cpu().numpy(), own)
+
+
+def test_append_capacity_guard():
+    cfg = C.CONFIGS["c1"]
+    lay = T.make_layout(cfg)
+    lay.point_cap[:] = lay.own_len                 # capacity == own_len: no room to append
+    ten = T.make_qkv(cfg, lay)
+    res = run_step(cfg, lay, ten)
+    assert np.array_equal(res["own_len"], lay.own_len)
+    assert torch.equal(res["k_cache"].cpu(), ten["k_cache"][0])
+
+
+def test_single_token_contexts_bitwise_v():
+    # closed form on the GPU: a one-token context returns that V row exactly (P = 1).
+    cfg = C.CONFIGS["c1"].with_(lp=0, t=1, lc=0)
+    lay = T.make_layout(cfg, dag_override=lambda: W.wide(5), extra_tokens=0)
+    lay.own_len[:] = 0
+    ten = T.make_qkv(cfg, lay)
+    lay.point_cap[:] = 64
+    res = run_step(cfg, lay, ten)
+    kc = res["v_cache"].cpu()
+    for b in range(5):
+        page = lay.page_table[lay.point_pt_off[b]]
+        for h in range(cfg.hq):
+            assert torch.equal(res["out"][b, h].cpu(), kc[page, h // cfg.g, 0])

@@ -1,0 +1,254 @@
+"""T1 — the native host library (no GPU needed): symbols, orion_dag_waves bit-exact against
+the oracle (goldens + fuzz, both policies, error taxonomy), orion_bind_segments against the
+oracle's binding, and orion_expand_plan coverage properties (every row's partial items cover
+exactly its context, once)."""
+import random
+import re
+
+import numpy as np
+import pytest
+
+import paper_2510_24390_b200 as orion
+from paper_2510_24390_b200 import _lib
+from oracle import dag as OD, step as OS
+from workloads import dags as W, configs as C, tensors as T
+
+HEADER = open(__file__.rsplit("/tests/", 1)[0] + "/include/orion.h").read()
+
+
+def test_library_exports_every_header_symbol():
+    L = _lib.lib()
+    decl = set(re.findall(r"^\s*(?:orion_status|const char\*)\s+(orion_\w+)\(", HEADER, re.M))
+    assert decl == set(_lib.EXPORTED_SYMBOLS)
+    for name in decl:
+        assert hasattr(L, name), name
+    assert "sm_100a" in orion.version()
+
+
+def _oracle_or_error(n, edges, policy):
+    try:
+        return OD.levels(n, edges), OD.waves(n, edges), OD.segment_lists(n, edges, policy), None
+    except OD.DagError as e:
+        return None, None, None, e
+
+
+def _compare(n, edges, policy):
+    lev, waves, lists, err = _oracle_or_error(n, edges, policy)
+    if err is not None:
+        with pytest.raises(orion.OrionError) as ei:
+            orion.dag_waves(n, edges, policy)
+        assert ei.value.code == err.code
+        if err.code == OD.CYCLE:
+            cyc = ei.value.info
+            es = {(a, b) for a, b, k in edges if k}
+            assert cyc and all((cyc[i], cyc[(i + 1) % len(cyc)]) in es for i in range(len(cyc)))
+        else:
+            assert ei.value.info[:1] == err.info
+        return
+    got = orion.dag_waves(n, edges, policy)
+    assert list(got["pre_level"]) == lev[0] and list(got["dec_level"]) == lev[1]
+    assert got["n_levels"] == lev[2]
+    assert got["waves"] == waves
+    so, segs = got["seg_offsets"], got["segs"]
+    for j in range(1, n + 1):
+        mine = [(int(s["kind"]), int(s["point"])) for s in segs[so[j - 1]:so[j]]]
+        assert mine == lists[j], (j, mine, lists[j])
+
+
+@pytest.mark.parametrize("name", list(W.DAGS))
+@pytest.mark.parametrize("policy", [0, 1])
+def test_dag_waves_named_families(name, policy):
+    _compare(*W.DAGS[name](), policy)
+
+
+def test_dag_waves_fuzz_bit_exact():
+    rng = random.Random(2024)
+    for i in range(1200):
+        n = rng.randint(1, 64 if i % 10 == 0 else 12)
+        n_, edges = W.random_dag(rng, n, p=rng.choice([0.05, 0.2, 0.5]), null_frac=0.15)
+        if rng.random() < 0.2 and n > 1:   # inject cycles / bad points / bad kinds
+            r = rng.random()
+            if r < 0.5:
+                a, b = rng.sample(range(1, n + 1), 2)
+                edges = edges + [(a, b, 2), (b, a, rng.choice([1, 2]))]
+            elif r < 0.75:
+                edges = edges + [(rng.randint(1, n), n + rng.randint(1, 3), 1)]
+            else:
+                edges = edges + [(1, 2, 5)]
+        _compare(n, edges, i % 2)
+
+
+def test_dag_waves_errors_and_degenerate():
+    with pytest.raises(orion.OrionError) as ei:
+        orion.dag_waves(0, [])
+    assert ei.value.code == _lib.ERR_INVALID_ARG
+    with pytest.raises(orion.OrionError) as ei:
+        orion.dag_waves(3, [], policy=7)
+    assert ei.value.code == _lib.ERR_INVALID_ARG
+    with pytest.raises(orion.OrionError) as ei:
+        orion.dag_waves(2, [(2, 2, 2)])
+    assert ei.value.code == _lib.ERR_CYCLE and ei.value.info == [2]
+    g = orion.dag_waves(1, [])
+    assert g["waves"] == [[(1, 0)], [(1, 1)]]
+
+
+def _bind_layout(cfg, layout, policy):
+    qdesc, offs, refs = [], [0], []
+    for qi in range(layout.n_queries):
+        n = int(layout.n_points[qi])
+        w = orion.dag_waves(n, layout.edges[qi], policy)
+        so = w["seg_offsets"]
+        for j in range(n):
+            refs.append(w["segs"][so[j]:so[j + 1]])
+            offs.append(offs[-1] + int(so[j + 1] - so[j]))
+        qdesc.append((n, int(layout.branch0[qi]), int(layout.prefix_pt_off[qi]), int(layout.prefix_len[qi])))
+    pts = np.stack([layout.point_pt_off, layout.content_len, layout.point_cap], 1)
+    segs = orion.bind_segments(qdesc, pts, np.array(offs, np.int32), np.concatenate(refs))
+    return np.array(offs, np.int32), segs
+
+
+@pytest.mark.parametrize("cfgname", ["c1", "c2", "c3"])
+@pytest.mark.parametrize("policy", [0, 1])
+def test_bind_matches_oracle_binding(cfgname, policy):
+    cfg = C.CONFIGS[cfgname].with_(n_queries=min(C.CONFIGS[cfgname].n_queries, 3))
+    lay = T.make_layout(cfg, ragged=True, extra_tokens=cfg.page)
+    offs, segs = _bind_layout(cfg, lay, policy)
+    bound = OS.bound_segments(lay, policy)
+    for b in range(lay.n_branches):
+        mine = segs[offs[b]:offs[b + 1]]
+        assert len(mine) == len(bound[b])
+        for s, (pages, start, length) in zip(mine, bound[b]):
+            eff = s["len"] if s["dyn"] < 0 else min(max(lay.own_len[s["dyn"]] - s["start"], 0), s["len"])
+            assert (int(s["start"]), int(eff)) == (start, length)
+            npg = -(-int(s["start"] + s["len"]) // cfg.page)
+            assert list(lay.page_table[s["pt_off"]:s["pt_off"] + npg]) == list(pages[:npg])
+
+
+# ------------------------------------------------------------------ plan parsing (test side)
+HDR = np.dtype([("magic", "<i4"), ("version", "<i4"), ("n_branches", "<i4"), ("hq", "<i4"),
+                ("hkv", "<i4"), ("d", "<i4"), ("page", "<i4"), ("group", "<i4"),
+                ("n_items", "<i4"), ("n_partials", "<i4"), ("n_rows", "<i4"), ("n_readers", "<i4"),
+                ("items_off", "<i8"), ("readers_off", "<i8"), ("comb_off_off", "<i8"),
+                ("comb_slot_off", "<i8"), ("plan_bytes", "<i8"), ("workspace_bytes", "<i8"),
+                ("acc_bytes", "<i8"), ("n_pieces", "<i8"), ("unique_tokens", "<i8"),
+                ("logical_tokens", "<i8"), ("sm_scale", "<f4"), ("pad", "<i4", 3)])
+ITEM = np.dtype([(n, "<i4") for n in ("pt_off", "t0", "t1", "dyn", "kv_head", "readers_off",
+                                      "row_begin", "n_rows", "slot0", "piece", "p0", "p1")])
+
+
+def parse_plan(plan):
+    h = np.frombuffer(plan, HDR, 1)[0]
+    items = np.frombuffer(plan, ITEM, int(h["n_items"]), int(h["items_off"]))
+    readers = np.frombuffer(plan, "<i4", int(h["n_readers"]), int(h["readers_off"]))
+    coff = np.frombuffer(plan, "<i4", int(h["n_rows"]) + 1, int(h["comb_off_off"]))
+    cslot = np.frombuffer(plan, "<i4", int(h["n_partials"]), int(h["comb_slot_off"]))
+    return h, items, readers, coff, cslot
+
+
+def _check_plan_covers(cfg, lay, offs, segs, own_len):
+    plan, ws = orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, own_len, chunk_tokens=128)
+    h, items, readers, coff, cslot = parse_plan(plan)
+    G = cfg.hq // cfg.hkv
+    assert h["magic"] == 0x314e524f and h["n_rows"] == lay.n_branches * cfg.hq
+    assert ws >= h["n_partials"] * (cfg.d * 4 + 8)
+    slot_tokens = {}
+    slot_row = {}
+    for it in items:
+        end = it["t1"] if it["dyn"] < 0 else min(it["t1"], own_len[it["dyn"]])
+        toks = [(int(it["pt_off"]), t) for t in range(it["t0"], max(it["t0"], end))]
+        for r in range(it["row_begin"], it["row_begin"] + it["n_rows"]):
+            b = readers[it["readers_off"] + r // G]
+            hh = it["kv_head"] * G + r % G
+            s = it["slot0"] + r - it["row_begin"]
+            assert s not in slot_tokens
+            slot_tokens[s] = toks
+            slot_row[s] = b * cfg.hq + hh
+    assert sorted(slot_tokens) == list(range(h["n_partials"]))
+    for row in range(h["n_rows"]):
+        b, hh = divmod(row, cfg.hq)
+        got = []
+        for s in cslot[coff[row]:coff[row + 1]]:
+            assert slot_row[s] == row
+            got += slot_tokens[s]
+        want = []
+        for s in segs[offs[b]:offs[b + 1]]:
+            eff = s["len"] if s["dyn"] < 0 else min(max(own_len[s["dyn"]] - s["start"], 0), s["len"])
+            want += [(int(s["pt_off"]), t) for t in range(s["start"], s["start"] + eff)]
+        assert len(got) == len(set(got)) and sorted(got) == sorted(want)
+    return h
+
+
+@pytest.mark.parametrize("cfgname,policy", [("c1", 0), ("c1", 1), ("c2", 0), ("c3", 1)])
+def test_plan_covers_each_context_exactly_once(cfgname, policy):
+    cfg = C.CONFIGS[cfgname].with_(n_queries=2, lp=min(C.CONFIGS[cfgname].lp, 256),
+                                   t=min(C.CONFIGS[cfgname].t, 96))
+    lay = T.make_layout(cfg, ragged=True, extra_tokens=cfg.page)
+    offs, segs = _bind_layout(cfg, lay, policy)
+    h = _check_plan_covers(cfg, lay, offs, segs, lay.own_len)
+    assert h["unique_tokens"] <= h["logical_tokens"]
+
+
+def test_plan_random_dags_cover():
+    rng = random.Random(77)
+    for trial in range(25):
+        cfg = C.CONFIGS["c1"].with_(lp=rng.choice([1, 16, 70]), t=rng.choice([9, 40, 100]),
+                                    lc=rng.choice([0, 3, 8]), page=rng.choice([16, 32]),
+                                    hq=rng.choice([2, 4, 6]), hkv=2, n_queries=2)
+        n = rng.randint(1, 9)
+        lay = T.make_layout(cfg, ragged=True, extra_tokens=rng.choice([0, 20]),
+                            dag_override=lambda: W.random_dag(random.Random(trial), n, p=0.4))
+        offs, segs = _bind_layout(cfg, lay, trial % 2)
+        _check_plan_covers(cfg, lay, offs, segs, lay.own_len)
+
+
+def test_plan_sharing_counts_c4():
+    cfg = C.CONFIGS["c4"].with_(n_queries=1)
+    lay = T.make_layout(cfg)
+    offs, segs = _bind_layout(cfg, lay, 0)
+    plan, ws = orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, lay.own_len)
+    st = orion.plan_stats(plan)
+    # unique tokens per kv head = prefix + all point segments (capacity); logical/unique ~ 7.6
+    assert st["unique_tokens"] == cfg.lp + 16 * cfg.t
+    assert 7.0 < st["logical_tokens"] / st["unique_tokens"] < 8.0
+
+
+def test_plan_errors():
+    S = _lib.SEG_DTYPE
+    # overlapping segments in one branch list
+    segs = np.array([(0, 0, 10, -1), (0, 5, 10, -1)], S)
+    with pytest.raises(orion.OrionError) as ei:
+        orion.expand_plan(4, 2, 64, 16, np.array([0, 2], np.int32), segs)
+    assert ei.value.code == _lib.ERR_INVALID_ARG
+    # one page run growing with two branches
+    segs = np.array([(0, 0, 10, 0), (0, 0, 10, 1)], S)
+    with pytest.raises(orion.OrionError) as ei:
+        orion.expand_plan(4, 2, 64, 16, np.array([0, 1, 2], np.int32), segs)
+    assert ei.value.code == _lib.ERR_UNSUPPORTED
+    # unsupported head_dim / page size
+    segs = np.array([(0, 0, 10, -1)], S)
+    for d, p in ((96, 16), (64, 24)):
+        with pytest.raises(orion.OrionError) as ei:
+            orion.expand_plan(4, 2, d, p, np.array([0, 1], np.int32), segs)
+        assert ei.value.code == _lib.ERR_UNSUPPORTED
+    # empty context
+    segs = np.array([(0, 0, 0, -1)], S)
+    with pytest.raises(orion.OrionError) as ei:
+        orion.expand_plan(4, 2, 64, 16, np.array([0, 1], np.int32), segs)
+    assert ei.value.code == _lib.ERR_INVALID_ARG
+    # zero-length segments are skipped
+    segs = np.array([(0, 0, 0, -1), (3, 0, 5, -1)], S)
+    plan, _ = orion.expand_plan(4, 2, 64, 16, np.array([0, 2], np.int32), segs)
+    assert orion.plan_stats(plan)["unique_tokens"] == 5
+
+
+def test_device_entry_points_validate_without_gpu():
+    import ctypes
+    L = _lib.lib()
+    shape = _lib.AttnShape(4, 2, 64, 16, 0.0)
+    assert L.orion_kv_append(ctypes.byref(shape), 1, None, None, None, None, None, None, None,
+                             None, 0, None) == _lib.ERR_INVALID_ARG
+    assert L.orion_expand_attn(ctypes.byref(shape), 1, None, None, None, None, None, 1, None,
+                               None, None, None, None, 0, None) == _lib.ERR_INVALID_ARG
+    bad = _lib.AttnShape(4, 2, 80, 16, 0.0)
+    assert L.orion_kv_append(ctypes.byref(bad), 1, None, None, None, None, None, None, None,
+                             None, 0, None) == _lib.ERR_UNSUPPORTED
