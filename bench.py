@@ -1,0 +1,425 @@
+#!/usr/bin/env python
+"""bench.py — expansion tokens/s of Orion's content-parallel-expansion decode step on B200.
+
+One "step" = one decode token for EVERY branch (key point) of every in-flight query, through
+all L layers: per layer K1 kv_append, K2 split attention, K3 combine (
+PAPER.md:337 Alg. 1 l.16).  Default workload = config c4 (BASELINE.json configs[3]: Llama-3-8B
+attention shape, 64 queries x mixed16 DAG, 4K prefix, 512 tokens/point, 32 layers), the
+8B-shaped config the north_star's >=70%-of-HBM target names.  Inputs are synthetic (seeded
+N(0,1) bf16), every layer has its own KV pool, so each step's working set (~113 GB) is far
+larger than L2 — no flush needed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl orion|reference]
+
+Multi-GPU: launched by torchrun, one rank per GPU; the config's queries are partitioned across
+ranks (query q -> rank floor(q*N/Q)), no collective on the data path; rank 0 prints one JSON
+line with the whole-job value (branches of all ranks / max-over-ranks step time).
+`--impl reference` times the CPU oracle (the tier's reference arm) on a bounded sample.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from workloads import configs as WC, tensors as WT  # noqa: E402
+
+METRIC = "expansion tokens/sec"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c4", choices=sorted(WC.CONFIGS))
+    ap.add_argument("--impl", default="orion", choices=["orion", "reference"])
+    ap.add_argument("--policy", type=int, default=0, help="0 ANCESTORS, 1 PARENTS_EQ3")
+    ap.add_argument("--chunk", type=int, default=0, help="plan chunk_tokens (0 = default)")
+    ap.add_argument("--layers", type=int, default=0, help="override layer count (0 = config)")
+    ap.add_argument("--queries", type=int, default=0, help="override query count (0 = config)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the config's queries are split across ranks; weak: every rank "
+                         "runs the full config")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------ helpers
+def rank_queries(cfg, rank, world, scaling):
+    if scaling == "weak" or world == 1:
+        return list(range(cfg.n_queries))
+    return [q for q in range(cfg.n_queries) if (q * world) // cfg.n_queries == rank]
+
+
+def algorithmic_bytes(cfg, lay):
+    """Per layer: unique KV (each valid token row once per (query, kv head)),
+    q read and out write.  Returns (kv_bytes, q_bytes, out_bytes)."""
+    tokens = 0
+    for qi in range(lay.n_queries):
+        b0, n = int(lay.branch0[qi]), int(lay.n_points[qi])
+        tokens += int(lay.prefix_len[qi]) + int(lay.own_len[b0:b0 + n].sum())
+    kv = tokens * cfg.hkv * cfg.d * 2 * 2
+    qb = lay.n_branches * cfg.hq * cfg.d * 2
+    return kv, qb, qb
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic(config_name):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    e = d.get(config_name)
+    return None if e is None else e.get("split_dram_bytes_per_launch")
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, gpu_index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), "--query-gpu=" + self.FIELDS,
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+        time.sleep(0.3)
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(", ") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], [], set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, r[3:7]):
+                if v.strip() == "Active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i["num_threads"] for i in threadpool_info() if i.get("user_api") == "blas"]
+        if n:
+            return max(n)
+    except Exception:
+        pass
+    return len(os.sched_getaffinity(0))
+
+
+# ------------------------------------------------------------------------------ oracle leg
+def oracle_sample(cfg, seed):
+    """One bounded sample of the workload on the CPU oracle: one query (all its points), one
+    layer — K1 append (O4) of K and V, then the attention of every branch (O3).  Returns
+    (seconds, branches)."""
+    from oracle import append as OA, step as OS
+    import torch
+    lay = WT.make_layout(cfg, queries=[0], seed=seed, extra_tokens=0)
+    ten = WT.make_qkv(cfg, lay, seed=seed)
+
+    def u16(t):
+        return t[0].contiguous().view(torch.int16).numpy().view(np.uint16)
+
+    k, v, q, kn, vn = (u16(ten[x]) for x in ("k_cache", "v_cache", "q", "k_new", "v_new"))
+    t0 = time.perf_counter()
+    k2, own = OA.kv_append(k, kn, lay.page_table, lay.point_pt_off, lay.own_len, cfg.page, rewrite=True)
+    v2, _ = OA.kv_append(v, vn, lay.page_table, lay.point_pt_off, lay.own_len, cfg.page, rewrite=True)
+    OS.expand_step(lay, q, k2, v2, own_len=own)
+    return time.perf_counter() - t0, lay.n_branches
+
+
+def cpu_baseline(cfg, layers, seconds):
+    spent, n_br, n = 0.0, 0, 0
+    while spent < seconds or n == 0:
+        dt, br = oracle_sample(cfg, cfg.seed + 17 * n)
+        spent += dt
+        n_br += br
+        n += 1
+        if n >= 64:
+            break
+    # whole-job equivalent: each sampled (query, layer) would repeat for every layer
+    value = n_br / (spent * layers)
+    return {"value": value, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+            "sample": f"{n} x (1 query of {cfg.name}: append + attention of all its branches, "
+                      f"1 layer), {spent:.1f} s CPU; scaled by {layers} layers"}
+
+
+def run_reference(args, cfg, layers):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    times, n_br = [], 0
+    for s in range(args.warmup + args.steps):
+        dt, br = oracle_sample(cfg, cfg.seed + 1000 + s)
+        if s >= args.warmup:
+            times.append(dt)
+            n_br = br
+    t_step = statistics.mean(times) * layers          # seconds per (query x all layers)
+    value = n_br / t_step
+    cores = blas_threads()
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"{cfg.name} (oracle sample: 1 query x 1 layer per step, "
+                                   f"scaled by {layers} layers)", "policy": "ancestors"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"per step 1 query of {cfg.name} (all {n_br} branches), "
+                                       f"1 layer, append + attention"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ GPU leg
+def run_orion(args, cfg, layers):
+    import torch
+    import torch.distributed as dist
+    import paper_2510_24390_b200 as orion
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    qs = rank_queries(cfg, rank, world, args.scaling)
+    lay = WT.make_layout(cfg, queries=qs, seed=cfg.seed * 101 + rank)
+    B = lay.n_branches
+    P, H, Hq, D = cfg.page, cfg.hkv, cfg.hq, cfg.d
+    kc = torch.empty((layers, lay.num_pages, H, P, D), dtype=torch.bfloat16, device=dev)
+    vc = torch.empty_like(kc)
+    q = torch.empty((layers, B, Hq, D), dtype=torch.bfloat16, device=dev)
+    kn = torch.empty((layers, B, H, D), dtype=torch.bfloat16, device=dev)
+    vn = torch.empty_like(kn)
+    out = torch.empty_like(q)
+    g = torch.Generator(device=dev)
+    g.manual_seed(cfg.seed * 7 + rank)
+    for t in (kc, vc, q, kn, vn):
+        for l in range(layers):
+            t[l].normal_(generator=g)
+    queries = [dict(n_points=int(lay.n_points[i]), edges=lay.edges[i],
+                    prefix_pt_off=int(lay.prefix_pt_off[i]), prefix_len=int(lay.prefix_len[i]))
+               for i in range(lay.n_queries)]
+    points = np.stack([lay.point_pt_off, lay.content_len, lay.point_cap], 1)
+    t0 = time.perf_counter()
+    batch = orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, lay.page_table,
+                                 lay.own_len, policy=args.policy, device=dev,
+                                 chunk_tokens=args.chunk)
+    plan_s = time.perf_counter() - t0
+    stream = torch.cuda.current_stream(dev)
+    REW = orion.APPEND_REWRITE
+
+    def step(ev=None, k=0):
+        for l in range(layers):
+            batch.append(kn[l], vn[l], kc[l], vc[l], mode=REW)
+            if ev is not None:
+                ev[k][l][0].record(stream)
+            batch.split(q[l], kc[l], vc[l])
+            if ev is not None:
+                ev[k][l][1].record(stream)
+            batch.combine(out[l])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(layers)] for _ in range(args.steps)]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local) if rank == 0 else None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for k in range(args.steps):
+        step(ev, k)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    elapsed_ms = e0.elapsed_time(e1)
+    split_ms = [ev[k][l][0].elapsed_time(ev[k][l][1]) for k in range(args.steps) for l in range(layers)]
+    # whole-job aggregation: branches of all ranks / max step time over ranks
+    t = torch.tensor([elapsed_ms, float(B)], dtype=torch.float64, device=dev)
+    if world > 1:
+        tmax = t[:1].clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tot = t[1:].clone()
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        elapsed_ms, total_b = float(tmax.item()), float(tot.item())
+    else:
+        total_b = float(B)
+    ms_step = elapsed_ms / args.steps
+    value = total_b / (ms_step / 1e3)
+
+    # ---- end to end through the public API with host buffers (pinned), copies inside timing
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, batch, layers, q, kn, vn, out, kc, vc, dev, world, total_b)
+
+    kv_b, q_b, o_b = algorithmic_bytes(cfg, lay)
+    split_bytes = kv_b + q_b                        # K2 reads: unique KV + q
+    split_avg_s = statistics.mean(split_ms) / 1e3
+    peak, peak_src = load_peaks()
+    achieved = split_bytes / split_avg_s / 1e9
+    st = batch.stats
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": args.scaling if world > 1 else "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded N(0,1) bf16 q/K/V; random page permutation)",
+        "config": {"workload": f"{cfg.name}: Hq/Hkv/d={cfg.hq}/{cfg.hkv}/{cfg.d}, "
+                               f"{cfg.n_queries} queries x {cfg.dag}, prefix {cfg.lp}, "
+                               f"{cfg.t} tok/point (Lc {cfg.lc}), page {cfg.page}, {layers} layers",
+                   "branches_per_step": int(total_b), "layers": layers,
+                   "policy": "parents_eq3" if args.policy else "ancestors",
+                   "append_mode": "rewrite (stationary snapshot)",
+                   "l2": "no flush: per-layer KV pools, step working set "
+                         f"{layers * (kv_b + q_b + o_b) / 1e9:.1f} GB >> 126 MB L2",
+                   "parallelism": f"queries partitioned over {world} GPU(s), no collective"},
+        "roofline": {"bound": "hbm", "kernel": "split_kernel (K2)", "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": load_traffic(cfg.name),
+                     "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": split_bytes,
+                     "split_ms_per_launch": split_avg_s * 1e3,
+                     "split_share_of_step": sum(split_ms) / elapsed_ms if world == 1 else None,
+                     "step_gbs_all_kernels": layers * (kv_b + q_b + o_b) / (ms_step / 1e3) / 1e9},
+        "plan": {"items": st["n_items"], "pieces": st["n_pieces"], "partials": st["n_partials"],
+                 "unique_tokens_per_kvhead": st["unique_tokens"],
+                 "logical_tokens_per_kvhead": st["logical_tokens"],
+                 "partial_bytes_per_layer": st["n_partials"] * (cfg.d * 4 + 8) * 2,
+                 "plan_build_s": plan_s},
+        "gpu_launches": args.steps * layers * 3,
+        "clocks": clocks,
+        "e2e": e2e,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, layers, args.cpu_seconds)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, batch, layers, q, kn, vn, out, kc, vc, dev, world, total_b):
+    """Same step through the public API, inputs from pinned host memory every step and the
+    result read back: per layer H2D(q, k_new, v_new) on a copy stream -> append/split/combine
+    on the compute stream -> D2H(out) on a third stream, pipelined across layers."""
+    import torch
+    import torch.distributed as dist
+    import paper_2510_24390_b200 as orion
+    hq, hkn, hvn = (t.cpu().pin_memory() for t in (q, kn, vn))
+    hout = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+    comp = torch.cuda.current_stream(dev)
+    h2d = torch.cuda.Stream(dev)
+    d2h = torch.cuda.Stream(dev)
+    in_ready = [torch.cuda.Event() for _ in range(layers)]
+    done = [torch.cuda.Event() for _ in range(layers)]
+    out_read = [torch.cuda.Event() for _ in range(layers)]
+    REW = orion.APPEND_REWRITE
+
+    def step(first):
+        for l in range(layers):
+            with torch.cuda.stream(h2d):
+                if not first:
+                    h2d.wait_event(done[l])        # previous step's compute released the inputs
+                q[l].copy_(hq[l], non_blocking=True)
+                kn[l].copy_(hkn[l], non_blocking=True)
+                vn[l].copy_(hvn[l], non_blocking=True)
+                in_ready[l].record(h2d)
+            comp.wait_event(in_ready[l])
+            if not first:
+                comp.wait_event(out_read[l])       # previous step's out[l] was read back
+            batch.step(q[l], kn[l], vn[l], kc[l], vc[l], out[l], mode=REW)
+            done[l].record(comp)
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(done[l])
+                hout[l].copy_(out[l], non_blocking=True)
+                out_read[l].record(d2h)
+
+    for i in range(max(1, args.warmup)):
+        step(i == 0)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(comp)
+    for _ in range(args.steps):
+        step(False)
+    comp.wait_stream(d2h)
+    e1.record(comp)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    bi = layers * (q[0].numel() + kn[0].numel() + vn[0].numel()) * 2
+    bo = layers * out[0].numel() * 2
+    return {"value": total_b / (ms_step / 1e3), "unit": UNIT, "h2d_bytes_per_step": bi,
+            "d2h_bytes_per_step": bo, "ms_per_step": ms_step,
+            "wall_ms_per_step": wall * 1e3 / args.steps,
+            "note": "pinned host inputs copied H2D and out copied D2H every step, pipelined per layer"}
+
+
+def main():
+    args = parse()
+    cfg = WC.CONFIGS[args.config]
+    if args.queries:
+        cfg = cfg.with_(n_queries=args.queries)
+    layers = args.layers or cfg.layers
+    if args.impl == "reference":
+        run_reference(args, cfg, layers)
+    else:
+        run_orion(args, cfg, layers)
+
+
+if __name__ == "__main__":
+    main()

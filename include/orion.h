@@ -240,6 +240,21 @@ orion_status orion_expand_attn(const orion_attn_shape* shape, int32_t n_branches
                                const int32_t* own_len, const void* h_plan, const void* d_plan,
                                void* workspace, size_t workspace_bytes, void* stream);
 
+/*
+ * orion_expand_split / orion_expand_combine — the two kernels of orion_expand_attn as separate
+ * launches (same arguments; orion_expand_attn == split then combine on one stream).  split writes
+ * only the fp32 partials in `workspace`; combine reads them and writes out / lse.  Exposed so
+ * callers can time or overlap the phases; the combine may also be re-run on kept partials.
+ */
+orion_status orion_expand_split(const orion_attn_shape* shape, int32_t n_branches, const void* q,
+                                const void* k_cache, const void* v_cache, int32_t num_pages,
+                                const int32_t* page_table, const int32_t* own_len,
+                                const void* h_plan, const void* d_plan, void* workspace,
+                                size_t workspace_bytes, void* stream);
+orion_status orion_expand_combine(const orion_attn_shape* shape, int32_t n_branches, void* out,
+                                  float* lse, const void* h_plan, const void* d_plan,
+                                  const void* workspace, size_t workspace_bytes, void* stream);
+
 /* Thread-local message describing the last non-OK status returned on this thread. */
 const char* orion_last_error(void);
 

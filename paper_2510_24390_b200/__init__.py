@@ -22,6 +22,7 @@ from ._lib import (OrionError, POLICY_ANCESTORS, POLICY_PARENTS_EQ3, APPEND_ADVA
                    EDGE_NULL, EDGE_CONTEXTUAL, EDGE_DEPENDENT, SEG_DTYPE, SEGREF_DTYPE, lib)
 
 __all__ = ["dag_waves", "bind_segments", "expand_plan", "plan_stats", "kv_append", "expand_attn",
+           "expand_split", "expand_combine",
            "ExpansionBatch", "OrionError", "version", "POLICY_ANCESTORS", "POLICY_PARENTS_EQ3",
            "APPEND_ADVANCE", "APPEND_REWRITE"]
 
@@ -148,6 +149,29 @@ def expand_attn(hq, hkv, d, page, q, out, lse, k_cache, v_cache, page_table, own
         _stream_ptr(stream)))
 
 
+def expand_split(hq, hkv, d, page, q, k_cache, v_cache, page_table, own_len, h_plan, d_plan,
+                 workspace, stream=None, sm_scale=0.0):
+    """orion_expand_split: K2 only (partials into `workspace`)."""
+    _require_cuda(q, k_cache, v_cache, page_table, own_len, d_plan, workspace)
+    shape = _shape(hq, hkv, d, page, sm_scale)
+    _lib.check(lib().orion_expand_split(
+        ctypes.byref(shape), int(q.shape[0]), q.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(),
+        int(k_cache.shape[0]), page_table.data_ptr(), own_len.data_ptr(), _lib.ptr(h_plan),
+        d_plan.data_ptr(), workspace.data_ptr(), workspace.numel() * workspace.element_size(),
+        _stream_ptr(stream)))
+
+
+def expand_combine(hq, hkv, d, page, n_branches, out, lse, h_plan, d_plan, workspace, stream=None,
+                   sm_scale=0.0):
+    """orion_expand_combine: K3 only (partials in `workspace` -> out / lse)."""
+    _require_cuda(out, lse, d_plan, workspace)
+    shape = _shape(hq, hkv, d, page, sm_scale)
+    _lib.check(lib().orion_expand_combine(
+        ctypes.byref(shape), int(n_branches), out.data_ptr(), None if lse is None else lse.data_ptr(),
+        _lib.ptr(h_plan), d_plan.data_ptr(), workspace.data_ptr(),
+        workspace.numel() * workspace.element_size(), _stream_ptr(stream)))
+
+
 class ExpansionBatch:
     """The in-flight set of one GPU: several queries, each a point DAG whose points all decode.
 
@@ -196,6 +220,14 @@ class ExpansionBatch:
         expand_attn(self.hq, self.hkv, self.d, self.page, q, out, lse, k_cache, v_cache,
                     self.page_table, self.own_len, self.h_plan, self.d_plan, self.workspace,
                     stream, self.sm_scale)
+
+    def split(self, q, k_cache, v_cache, stream=None):
+        expand_split(self.hq, self.hkv, self.d, self.page, q, k_cache, v_cache, self.page_table,
+                     self.own_len, self.h_plan, self.d_plan, self.workspace, stream, self.sm_scale)
+
+    def combine(self, out, lse=None, stream=None):
+        expand_combine(self.hq, self.hkv, self.d, self.page, self.n_branches, out, lse,
+                       self.h_plan, self.d_plan, self.workspace, stream, self.sm_scale)
 
     def step(self, q, k_new, v_new, k_cache, v_cache, out, lse=None, mode=APPEND_ADVANCE,
              stream=None):

@@ -17,7 +17,8 @@ APPEND_ADVANCE, APPEND_REWRITE = 0, 1
 
 EXPORTED_SYMBOLS = ("orion_dag_waves", "orion_bind_segments", "orion_expand_plan",
                     "orion_plan_get_stats", "orion_kv_append", "orion_expand_attn",
-                    "orion_last_error", "orion_version")
+                    "orion_expand_split", "orion_expand_combine", "orion_last_error",
+                    "orion_version")
 
 
 class Edge(ctypes.Structure):
@@ -92,7 +93,10 @@ def lib():
         L.orion_kv_append.argtypes = [P(AttnShape), i32, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp]
         L.orion_expand_attn.argtypes = [P(AttnShape), i32, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp,
                                         vp, sz, vp]
-        for f in ("orion_dag_waves", "orion_bind_segments", "orion_expand_plan",
+        L.orion_expand_split.argtypes = [P(AttnShape), i32, vp, vp, vp, i32, vp, vp, vp, vp, vp,
+                                         sz, vp]
+        L.orion_expand_combine.argtypes = [P(AttnShape), i32, vp, vp, vp, vp, vp, sz, vp]
+        for f in ("orion_expand_split", "orion_expand_combine", "orion_dag_waves", "orion_bind_segments", "orion_expand_plan",
                   "orion_plan_get_stats", "orion_kv_append", "orion_expand_attn"):
             getattr(L, f).restype = ctypes.c_int32
         L.orion_last_error.restype = ctypes.c_char_p

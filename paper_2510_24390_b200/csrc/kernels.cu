@@ -392,9 +392,9 @@ size_t split_smem_bytes() {
 }
 
 template <int D>
-orion_status launch_attn(const PlanHeader* h, const char* dplan, const void* q, void* out,
-                         float* lse, const void* k, const void* v, const int32_t* page_table,
-                         const int32_t* own_len, void* ws, cudaStream_t st) {
+orion_status launch_split(const PlanHeader* h, const char* dplan, const void* q, const void* k,
+                          const void* v, const int32_t* page_table, const int32_t* own_len,
+                          void* ws, cudaStream_t st) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
@@ -421,13 +421,44 @@ orion_status launch_attn(const PlanHeader* h, const char* dplan, const void* q, 
   split_kernel<D><<<h->n_items, kThreads, split_smem_bytes<D>(), st>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ORION_ERR_CUDA, "split_kernel: %s", cudaGetErrorString(e));
+  return ORION_OK;
+}
+
+template <int D>
+orion_status launch_combine(const PlanHeader* h, const char* dplan, void* out, float* lse,
+                            const void* ws, cudaStream_t st) {
   const int nb = (h->n_rows + 7) / 8;
-  combine_kernel<D><<<nb, 256, 0, st>>>(
-      reinterpret_cast<const int32_t*>(dplan + h->comb_off_off),
-      reinterpret_cast<const int32_t*>(dplan + h->comb_slot_off), a.part_acc, a.part_ml,
-      static_cast<__nv_bfloat16*>(out), lse, h->n_rows);
-  e = cudaGetLastError();
+  const float* acc = static_cast<const float*>(ws);
+  const float2* ml = reinterpret_cast<const float2*>(static_cast<const char*>(ws) + h->acc_bytes);
+  combine_kernel<D><<<nb, 256, 0, st>>>(reinterpret_cast<const int32_t*>(dplan + h->comb_off_off),
+                                        reinterpret_cast<const int32_t*>(dplan + h->comb_slot_off),
+                                        acc, ml, static_cast<__nv_bfloat16*>(out), lse, h->n_rows);
+  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ORION_ERR_CUDA, "combine_kernel: %s", cudaGetErrorString(e));
+  return ORION_OK;
+}
+
+// Shared validation of the attention entry points.
+orion_status check_attn(const orion_attn_shape* shape, int32_t n_branches, const void* h_plan,
+                        const void* d_plan, const void* workspace, size_t workspace_bytes,
+                        const PlanHeader** hp) {
+  orion_status st = check_shape_public(shape);
+  if (st != ORION_OK) return st;
+  if (!h_plan || !d_plan || !workspace) return fail(ORION_ERR_INVALID_ARG, "null plan/workspace");
+  if (!aligned16(d_plan) || !aligned16(workspace))
+    return fail(ORION_ERR_INVALID_ARG, "d_plan / workspace must be 16-byte aligned");
+  const PlanHeader* h = static_cast<const PlanHeader*>(h_plan);
+  if (h->magic != kPlanMagic || h->version != kPlanVersion)
+    return fail(ORION_ERR_INVALID_ARG, "h_plan is not an orion plan");
+  if (h->n_branches != n_branches || h->num_q_heads != shape->num_q_heads ||
+      h->num_kv_heads != shape->num_kv_heads || h->head_dim != shape->head_dim ||
+      h->page_size != shape->page_size)
+    return fail(ORION_ERR_INVALID_ARG, "plan was built for another shape / branch count");
+  if (workspace_bytes < static_cast<size_t>(h->workspace_bytes))
+    return fail(ORION_ERR_INVALID_ARG, "workspace %zu < %lld bytes", workspace_bytes,
+                (long long)h->workspace_bytes);
+  if (h->n_items < 1) return fail(ORION_ERR_INVALID_ARG, "empty plan");
+  *hp = h;
   return ORION_OK;
 }
 
@@ -466,6 +497,43 @@ extern "C" orion_status orion_kv_append(const orion_attn_shape* shape, int32_t n
   return ORION_OK;
 }
 
+extern "C" orion_status orion_expand_split(const orion_attn_shape* shape, int32_t n_branches,
+                                           const void* q, const void* k_cache,
+                                           const void* v_cache, int32_t num_pages,
+                                           const int32_t* page_table, const int32_t* own_len,
+                                           const void* h_plan, const void* d_plan,
+                                           void* workspace, size_t workspace_bytes,
+                                           void* stream) {
+  const PlanHeader* h = nullptr;
+  orion_status st = check_attn(shape, n_branches, h_plan, d_plan, workspace, workspace_bytes, &h);
+  if (st != ORION_OK) return st;
+  if (!q || !k_cache || !v_cache || !page_table || !own_len)
+    return fail(ORION_ERR_INVALID_ARG, "null pointer");
+  if (!aligned16(q) || !aligned16(k_cache) || !aligned16(v_cache))
+    return fail(ORION_ERR_INVALID_ARG, "device pointers must be 16-byte aligned");
+  if (num_pages < 1) return fail(ORION_ERR_INVALID_ARG, "num_pages < 1");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const char* dp = static_cast<const char*>(d_plan);
+  if (shape->head_dim == 128)
+    return launch_split<128>(h, dp, q, k_cache, v_cache, page_table, own_len, workspace, s);
+  return launch_split<64>(h, dp, q, k_cache, v_cache, page_table, own_len, workspace, s);
+}
+
+extern "C" orion_status orion_expand_combine(const orion_attn_shape* shape, int32_t n_branches,
+                                             void* out, float* lse, const void* h_plan,
+                                             const void* d_plan, const void* workspace,
+                                             size_t workspace_bytes, void* stream) {
+  const PlanHeader* h = nullptr;
+  orion_status st = check_attn(shape, n_branches, h_plan, d_plan, workspace, workspace_bytes, &h);
+  if (st != ORION_OK) return st;
+  if (!out) return fail(ORION_ERR_INVALID_ARG, "null out");
+  if (!aligned16(out)) return fail(ORION_ERR_INVALID_ARG, "out must be 16-byte aligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const char* dp = static_cast<const char*>(d_plan);
+  if (shape->head_dim == 128) return launch_combine<128>(h, dp, out, lse, workspace, s);
+  return launch_combine<64>(h, dp, out, lse, workspace, s);
+}
+
 extern "C" orion_status orion_expand_attn(const orion_attn_shape* shape, int32_t n_branches,
                                           const void* q, void* out, float* lse,
                                           const void* k_cache, const void* v_cache,
@@ -473,31 +541,13 @@ extern "C" orion_status orion_expand_attn(const orion_attn_shape* shape, int32_t
                                           const int32_t* own_len, const void* h_plan,
                                           const void* d_plan, void* workspace,
                                           size_t workspace_bytes, void* stream) {
-  orion_status st = check_shape_public(shape);
+  if (!out) return fail(ORION_ERR_INVALID_ARG, "null out");
+  orion_status st = orion_expand_split(shape, n_branches, q, k_cache, v_cache, num_pages,
+                                       page_table, own_len, h_plan, d_plan, workspace,
+                                       workspace_bytes, stream);
   if (st != ORION_OK) return st;
-  if (!q || !out || !k_cache || !v_cache || !page_table || !own_len || !h_plan || !d_plan ||
-      !workspace)
-    return fail(ORION_ERR_INVALID_ARG, "null pointer");
-  if (!aligned16(q) || !aligned16(out) || !aligned16(k_cache) || !aligned16(v_cache) ||
-      !aligned16(d_plan) || !aligned16(workspace))
-    return fail(ORION_ERR_INVALID_ARG, "device pointers must be 16-byte aligned");
-  const PlanHeader* h = static_cast<const PlanHeader*>(h_plan);
-  if (h->magic != kPlanMagic || h->version != kPlanVersion)
-    return fail(ORION_ERR_INVALID_ARG, "h_plan is not an orion plan");
-  if (h->n_branches != n_branches || h->num_q_heads != shape->num_q_heads ||
-      h->num_kv_heads != shape->num_kv_heads || h->head_dim != shape->head_dim ||
-      h->page_size != shape->page_size)
-    return fail(ORION_ERR_INVALID_ARG, "plan was built for another shape / branch count");
-  if (workspace_bytes < static_cast<size_t>(h->workspace_bytes))
-    return fail(ORION_ERR_INVALID_ARG, "workspace %zu < %lld bytes", workspace_bytes,
-                (long long)h->workspace_bytes);
-  if (num_pages < 1) return fail(ORION_ERR_INVALID_ARG, "num_pages < 1");
-  if (h->n_items < 1) return fail(ORION_ERR_INVALID_ARG, "empty plan");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const char* dp = static_cast<const char*>(d_plan);
-  if (shape->head_dim == 128)
-    return launch_attn<128>(h, dp, q, out, lse, k_cache, v_cache, page_table, own_len, workspace, s);
-  return launch_attn<64>(h, dp, q, out, lse, k_cache, v_cache, page_table, own_len, workspace, s);
+  return orion_expand_combine(shape, n_branches, out, lse, h_plan, d_plan, workspace,
+                              workspace_bytes, stream);
 }
 
 extern "C" const char* orion_version(void) {
