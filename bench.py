@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--impl", default="orion", choices=["orion", "reference"])
     ap.add_argument("--policy", type=int, default=0, help="0 ANCESTORS, 1 PARENTS_EQ3")
     ap.add_argument("--chunk", type=int, default=0, help="plan chunk_tokens (0 = default)")
+    ap.add_argument("--kernel", default="tc", choices=["tc", "mma"],
+                    help="split kernel: tcgen05/TMEM/TMA (default) or legacy mma.sync")
     ap.add_argument("--layers", type=int, default=0, help="override layer count (0 = config)")
     ap.add_argument("--queries", type=int, default=0, help="override query count (0 = config)")
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
@@ -245,7 +247,8 @@ def run_orion(args, cfg, layers):
     t0 = time.perf_counter()
     batch = orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, lay.page_table,
                                  lay.own_len, policy=args.policy, device=dev,
-                                 chunk_tokens=args.chunk)
+                                 chunk_tokens=args.chunk,
+                                 flags=orion.PLAN_MMA_SYNC if args.kernel == "mma" else 0)
     plan_s = time.perf_counter() - t0
     stream = torch.cuda.current_stream(dev)
     REW = orion.APPEND_REWRITE
@@ -322,7 +325,8 @@ def run_orion(args, cfg, layers):
                    "l2": "no flush: per-layer KV pools, step working set "
                          f"{layers * (kv_b + q_b + o_b) / 1e9:.1f} GB >> 126 MB L2",
                    "parallelism": f"queries partitioned over {world} GPU(s), no collective"},
-        "roofline": {"bound": "hbm", "kernel": "split_kernel (K2)", "achieved": achieved, "peak": peak,
+        "roofline": {"bound": "hbm",
+                     "kernel": "split_tc_kernel (K2, tcgen05)" if args.kernel == "tc" else "split_kernel (K2, mma.sync)", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": load_traffic(cfg.name),
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": split_bytes,

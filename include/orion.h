@@ -97,7 +97,7 @@ typedef struct {
   int32_t num_q_heads;   /* Hq */
   int32_t num_kv_heads;  /* Hkv; Hq % Hkv == 0 */
   int32_t head_dim;      /* 64 or 128 */
-  int32_t page_size;     /* power of two in [8, 256] */
+  int32_t page_size;     /* power of two in [16, 256] */
   float sm_scale;        /* softmax scale; <= 0 selects 1/sqrt(head_dim) (reading S16) */
 } orion_attn_shape;
 
@@ -107,10 +107,14 @@ typedef struct { int32_t n_points, branch0, prefix_pt_off, prefix_len; } orion_q
 /* Per global branch (= point): its page run, content length Lc and capacity in tokens. */
 typedef struct { int32_t pt_off, content_len, capacity; } orion_point_desc;
 
+/* Plan flags.  ORION_PLAN_MMA_SYNC selects the legacy split kernel (mma.sync m16n8k16 + cp.async,
+ * <= 64 rows per work item) instead of the default tcgen05/TMEM/TMA kernel (<= 128 rows). */
+enum { ORION_PLAN_MMA_SYNC = 1 };
+
 typedef struct {
   int32_t num_sms;        /* SMs to balance for; <= 0 selects 148 (B200) */
   int32_t chunk_tokens;   /* max tokens per work item along a piece; <= 0 selects the default */
-  int32_t flags;          /* reserved, 0 */
+  int32_t flags;          /* ORION_PLAN_* bits, 0 = defaults */
 } orion_plan_opts;
 
 typedef struct {

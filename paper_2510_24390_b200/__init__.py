@@ -84,14 +84,17 @@ def bind_segments(queries, points, seg_offsets, refs):
     return out
 
 
+PLAN_MMA_SYNC = 1   # ORION_PLAN_MMA_SYNC: legacy mma.sync split kernel
+
+
 def expand_plan(hq, hkv, d, page, seg_offsets, segs, own_len=None, chunk_tokens=0, num_sms=0,
-                sm_scale=0.0):
+                sm_scale=0.0, flags=0):
     """orion_expand_plan -> (plan: np.uint8 16-byte aligned host buffer, workspace_bytes)."""
     shape = _shape(hq, hkv, d, page, sm_scale)
     so = np.ascontiguousarray(seg_offsets, dtype=np.int32)
     sg = np.ascontiguousarray(segs).astype(SEG_DTYPE)
     ol = None if own_len is None else np.ascontiguousarray(own_len, dtype=np.int32)
-    opts = _lib.PlanOpts(int(num_sms), int(chunk_tokens), 0)
+    opts = _lib.PlanOpts(int(num_sms), int(chunk_tokens), int(flags))
     need = ctypes.c_size_t(0)
     ws = ctypes.c_size_t(0)
     nb = len(so) - 1
@@ -182,7 +185,7 @@ class ExpansionBatch:
     """
 
     def __init__(self, hq, hkv, d, page, queries, points, page_table, own_len,
-                 policy=POLICY_ANCESTORS, device="cuda", chunk_tokens=0, sm_scale=0.0):
+                 policy=POLICY_ANCESTORS, device="cuda", chunk_tokens=0, sm_scale=0.0, flags=0):
         import torch
         self.hq, self.hkv, self.d, self.page = hq, hkv, d, page
         self.sm_scale = sm_scale
@@ -202,7 +205,7 @@ class ExpansionBatch:
         self.segs = bind_segments(qdesc, pts, self.seg_offsets, self.refs)
         own = np.ascontiguousarray(own_len, dtype=np.int32)
         self.h_plan, ws = expand_plan(hq, hkv, d, page, self.seg_offsets, self.segs, own,
-                                      chunk_tokens=chunk_tokens, sm_scale=sm_scale)
+                                      chunk_tokens=chunk_tokens, sm_scale=sm_scale, flags=flags)
         self.stats = plan_stats(self.h_plan)
         dev = torch.device(device)
         self.d_plan = torch.from_numpy(self.h_plan.copy()).to(dev)

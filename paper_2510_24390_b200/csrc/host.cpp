@@ -284,8 +284,8 @@ orion_status check_shape(const orion_attn_shape* s) {
     return fail(ORION_ERR_INVALID_ARG, "heads %d/%d", s->num_q_heads, s->num_kv_heads);
   if (s->head_dim != 64 && s->head_dim != 128)
     return fail(ORION_ERR_UNSUPPORTED, "head_dim %d not in {64,128}", s->head_dim);
-  if (s->page_size < 8 || s->page_size > 256 || (s->page_size & (s->page_size - 1)))
-    return fail(ORION_ERR_UNSUPPORTED, "page_size %d not a power of two in [8,256]", s->page_size);
+  if (s->page_size < 16 || s->page_size > 256 || (s->page_size & (s->page_size - 1)))
+    return fail(ORION_ERR_UNSUPPORTED, "page_size %d not a power of two in [16,256]", s->page_size);
   return ORION_OK;
 }
 
@@ -308,6 +308,8 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
     return fail(ORION_ERR_INVALID_ARG, "bad plan arguments");
   const int32_t Hq = shape->num_q_heads, Hkv = shape->num_kv_heads, G = Hq / Hkv;
   int32_t chunk = (opts && opts->chunk_tokens > 0) ? opts->chunk_tokens : 512;
+  const int32_t variant = (opts && (opts->flags & ORION_PLAN_MMA_SYNC)) ? kVariantMmaSync : kVariantTC;
+  const int32_t rows_per_item = variant == kVariantTC ? kRowsPerItemTC : kRowsPerItemMMA;
   chunk = std::max(kTileTokens, (chunk + kTileTokens - 1) / kTileTokens * kTileTokens);
 
   // 1. Group bound segments by page run.
@@ -392,16 +394,16 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
     const int32_t roff = (int32_t)readers.size();
     readers.insert(readers.end(), p.readers.begin(), p.readers.end());
     const int32_t rows = (int32_t)p.readers.size() * G;
-    const int32_t rows_blk = std::min(rows, kRowsPerItem);
+    const int32_t rows_blk = std::min(rows, rows_per_item);
     int32_t ch = std::max(chunk, 32 * rows_blk);
     ch = (ch + kTileTokens - 1) / kTileTokens * kTileTokens;
     for (int32_t g = 0; g < Hkv; ++g)
       for (int32_t t = p.t0; t < p.t1; t += ch)
-        for (int32_t r0 = 0; r0 < rows; r0 += kRowsPerItem) {
+        for (int32_t r0 = 0; r0 < rows; r0 += rows_per_item) {
           WorkItem w{};
           w.pt_off = p.pt_off; w.t0 = t; w.t1 = std::min(p.t1, t + ch); w.dyn = p.dyn;
           w.kv_head = g; w.readers_off = roff; w.row_begin = r0;
-          w.n_rows = std::min(kRowsPerItem, rows - r0); w.slot0 = n_slots; w.piece = (int32_t)pi;
+          w.n_rows = std::min(rows_per_item, rows - r0); w.slot0 = n_slots; w.piece = (int32_t)pi;
           for (int32_t r = r0; r < r0 + w.n_rows; ++r) {
             const int32_t b = p.readers[r / G], h = g * G + r % G;
             row_slots[(size_t)b * Hq + h].push_back(n_slots + (r - r0));
@@ -440,6 +442,7 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
   h.n_pieces = (int64_t)pieces.size();
   h.unique_tokens = unique_tokens;
   h.logical_tokens = logical_total;
+  h.variant = variant;
   h.sm_scale = shape->sm_scale > 0.f ? shape->sm_scale : 1.0f / std::sqrt((float)shape->head_dim);
   *plan_needed = (size_t)h.plan_bytes;
   *workspace_needed = (size_t)h.workspace_bytes;

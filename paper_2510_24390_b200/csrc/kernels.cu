@@ -23,9 +23,9 @@
 
 #include "../../include/orion.h"
 #include "plan_format.h"
+#include "split_tc.h"
 
 namespace orion {
-orion_status fail(orion_status code, const char* fmt, ...);
 orion_status check_shape_public(const orion_attn_shape* s);
 }  // namespace orion
 
@@ -393,8 +393,25 @@ size_t split_smem_bytes() {
 
 template <int D>
 orion_status launch_split(const PlanHeader* h, const char* dplan, const void* q, const void* k,
-                          const void* v, const int32_t* page_table, const int32_t* own_len,
-                          void* ws, cudaStream_t st) {
+                          const void* v, int32_t num_pages, const int32_t* page_table,
+                          const int32_t* own_len, void* ws, cudaStream_t st) {
+  if (h->variant == kVariantTC) {
+    TcArgs t;
+    t.items = reinterpret_cast<const WorkItem*>(dplan + h->items_off);
+    t.readers = reinterpret_cast<const int32_t*>(dplan + h->readers_off);
+    t.q = static_cast<const __nv_bfloat16*>(q);
+    t.page_table = page_table;
+    t.own_len = own_len;
+    t.part_acc = static_cast<float*>(ws);
+    t.part_ml = reinterpret_cast<float2*>(static_cast<char*>(ws) + h->acc_bytes);
+    t.n_items = h->n_items;
+    t.hq = h->num_q_heads;
+    t.hkv = h->num_kv_heads;
+    t.group = h->group;
+    t.page_shift = log2i(h->page_size);
+    t.scale_log2 = h->sm_scale * kLog2e;
+    return launch_split_tc<D>(h, t, k, v, num_pages, st);
+  }
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
@@ -515,8 +532,8 @@ extern "C" orion_status orion_expand_split(const orion_attn_shape* shape, int32_
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const char* dp = static_cast<const char*>(d_plan);
   if (shape->head_dim == 128)
-    return launch_split<128>(h, dp, q, k_cache, v_cache, page_table, own_len, workspace, s);
-  return launch_split<64>(h, dp, q, k_cache, v_cache, page_table, own_len, workspace, s);
+    return launch_split<128>(h, dp, q, k_cache, v_cache, num_pages, page_table, own_len, workspace, s);
+  return launch_split<64>(h, dp, q, k_cache, v_cache, num_pages, page_table, own_len, workspace, s);
 }
 
 extern "C" orion_status orion_expand_combine(const orion_attn_shape* shape, int32_t n_branches,
@@ -551,6 +568,6 @@ extern "C" orion_status orion_expand_attn(const orion_attn_shape* shape, int32_t
 }
 
 extern "C" const char* orion_version(void) {
-  return "orion-b200 0.1 (sm_100a; K1 append, K2 split mma.sync m16n8k16 bf16 + cp.async 3-stage, "
-         "K3 combine)";
+  return "orion-b200 0.2 (sm_100a; K1 append; K2 split: tcgen05.mma + TMEM + TMA (default) | "
+         "mma.sync m16n8k16 + cp.async (ORION_PLAN_MMA_SYNC); K3 combine)";
 }

@@ -13,7 +13,10 @@ namespace orion {
 
 constexpr int32_t kPlanMagic = 0x314e524f;  // "ORN1"
 constexpr int32_t kPlanVersion = 1;
-constexpr int kRowsPerItem = 64;   // query rows per split work item (4 warps x m16)
+constexpr int kRowsPerItemTC = 128;  // query rows per work item, tcgen05 kernel (MMA M = 128)
+constexpr int kRowsPerItemMMA = 64;  // query rows per work item, mma.sync kernel (4 warps x m16)
+constexpr int kRowsPerItem = kRowsPerItemMMA;  // smem sizing of the mma.sync kernel
+enum : int32_t { kVariantTC = 0, kVariantMmaSync = 1 };
 constexpr int kTileTokens = 64;    // tokens per pipeline stage in the split kernel
 
 struct PlanHeader {
@@ -24,7 +27,8 @@ struct PlanHeader {
   int64_t plan_bytes, workspace_bytes, acc_bytes;                // acc_bytes = part_ml offset
   int64_t n_pieces, unique_tokens, logical_tokens;
   float sm_scale;
-  int32_t pad_[3];
+  int32_t variant;  // kVariantTC (tcgen05, default) or kVariantMmaSync (opts.flags & 1)
+  int32_t pad_[2];
 };
 static_assert(sizeof(PlanHeader) % 16 == 0, "header must keep 16-byte alignment");
 

@@ -1,0 +1,617 @@
+// split_tc.cu — K2 split attention on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+// One persistent CTA per SM walks the plan's work items (item = shared piece x kv head x token
+// chunk x <=128 query rows; rows = reader branches x GQA heads).  Roles:
+//   warp 0 (1 lane)  TMA producer: streams the chunk's K and V tokens page by page with
+//                    cp.async.bulk.tensor (16-token x 64-dim boxes, 128B swizzle) into a 4-stage
+//                    shared-memory ring; tokens of a shared prefix / ancestor piece are read from
+//                    HBM once for all rows of the item.  Runs ahead across item boundaries.
+//   warp 1 (1 lane)  MMA issuer: S = Q.K^T (tcgen05.mma kind::f16, A=Q smem, B=K smem, D in TMEM,
+//                    M=128 rows x N=64 tokens) into a double-buffered S; O += P.V (A=P from TMEM,
+//                    B=V smem MN-major, M=128 x N=d) into the TMEM accumulator; tcgen05.commit
+//                    releases ring stages and signals the softmax warps.
+//   warp 2           TMEM allocator (512 columns).
+//   warps 4-7        softmax + epilogue, one thread per query row (TMEM lane = row): tcgen05.ld
+//                    of the S row, masking, online max in the log2 domain with lazy rescaling
+//                    (O and l are rescaled only when the running max grows by > 2^8), P = exp2
+//                    rounded to bf16 and stored to TMEM (l summed from the same rounded values),
+//                    zeroing of V rows outside the item's token range, and at item end the fp32
+//                    partial (m, l, acc) write.  They also gather the next items' Q rows.
+//
+// Layout and numerics match the mma.sync kernel and the combine kernel (kernels.cu): partial m is
+// in log2 units relative to which acc and l are accumulated.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "../../include/orion.h"
+#include "plan_format.h"
+#include "split_tc.h"
+#include "tmem_ops.h"
+
+namespace orion {
+namespace tc {
+
+constexpr int kTok = 64;       // tokens per S tile / ring stage
+constexpr int kStagesTC = 4;   // K/V ring depth
+constexpr int kRows = 128;     // MMA M (query rows per item)
+constexpr int kBox = 16;       // token rows per TMA box
+
+// ------------------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(b))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(
+                   smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+// Bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  const uint32_t a = smem_u32(b);
+  for (uint32_t spin = 0;; ++spin) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (spin > (1u << 26)) __trap();
+  }
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n .reg .b32 rx;\n .reg .pred px;\n elect.sync rx|px, %1;\n @px mov.s32 %0, 1;\n}\n"
+      : "+r"(pred)
+      : "r"(0xFFFFFFFFu));
+  return pred != 0;
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   smem_u32(b))
+               : "memory");
+}
+__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void mma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                       uint32_t accum) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                       uint32_t accum) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0));
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// UMMA shared-memory descriptor (sm_100 format, version 1), 128-byte swizzle.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;   // descriptor version (Blackwell)
+  d |= static_cast<uint64_t>(2) << 61;   // SWIZZLE_128B
+  return d;
+}
+// Instruction descriptor, kind::f16: bf16 A/B, fp32 D.
+__host__ __device__ constexpr uint32_t idesc_bf16(int m, int n, bool b_mn_major) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn_major ? 1u : 0u) << 16) |
+         (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(m >> 4) << 24);
+}
+
+struct ItemGeom {
+  int32_t base, end, ntiles;
+};
+__device__ __forceinline__ ItemGeom geom(const WorkItem& w, const int32_t* own_len) {
+  ItemGeom g;
+  g.end = w.t1;
+  if (w.dyn >= 0) g.end = min(g.end, __ldg(own_len + w.dyn));
+  g.base = w.t0 & ~(kTok - 1);
+  g.ntiles = g.end > w.t0 ? (g.end - g.base + kTok - 1) / kTok : 0;
+  return g;
+}
+
+__device__ __forceinline__ int next_nonempty(const TcArgs& a, int it) {
+  while (it < a.n_items && geom(a.items[it], a.own_len).ntiles == 0) it += gridDim.x;
+  return it;
+}
+
+template <int D>
+struct Smem {
+  static constexpr int QB = kRows * D * 2;      // one Q buffer
+  static constexpr int KVB = kTok * D * 2;      // one K (or V) stage
+  static constexpr int HALF_Q = kRows * 128;    // 64-dim half of Q
+  static constexpr int HALF_KV = kTok * 128;    // 64-dim half of a K/V stage
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = 2 * QB;
+  static constexpr int OFF_V = OFF_K + kStagesTC * KVB;
+  static constexpr int OFF_XCH = OFF_V + kStagesTC * KVB;   // WG1 -> WG0 (m, l) per row, x2
+  static constexpr int OFF_BAR = OFF_XCH + 2 * kRows * 8;
+  static constexpr int N_BAR = 2 * kStagesTC + 2 + 2 + 2 + 2 + 1;
+  static constexpr int BYTES = OFF_BAR + N_BAR * 8 + 16;
+};
+
+// TMEM columns: S and P double-buffered by tile parity; one O accumulator per softmax warpgroup.
+__device__ __forceinline__ uint32_t colS(uint32_t p) { return p * 64; }
+__device__ __forceinline__ uint32_t colP(uint32_t p) { return 128 + p * 32; }
+__device__ __forceinline__ uint32_t colO(uint32_t p) { return 256 + p * 128; }
+constexpr int kThreadsTC = 384;   // warps 0-3: TMA / MMA / TMEM alloc / idle; 4-7: WG0; 8-11: WG1
+
+template <int D>
+__global__ void __launch_bounds__(kThreadsTC, 1)
+    split_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                    const __grid_constant__ CUtensorMap tmK16, const __grid_constant__ CUtensorMap tmV16,
+                    const TcArgs a) {
+  using L = Smem<D>;
+  constexpr int NH = D / 64;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint64_t* kv_full = bars;
+  uint64_t* kv_empty = bars + kStagesTC;
+  uint64_t* s_full = bars + 2 * kStagesTC;
+  uint64_t* p_full = s_full + 2;
+  uint64_t* pv_done = p_full + 2;
+  uint64_t* q_full = pv_done + 2;
+  uint64_t* o_free = q_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 1);
+  float2* xch = reinterpret_cast<float2*>(smem + L::OFF_XCH);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < kStagesTC; ++s) { mbar_init(kv_full + s, 1); mbar_init(kv_empty + s, 1); }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(s_full + b, 1); mbar_init(p_full + b, 128); mbar_init(pv_done + b, 1);
+      mbar_init(q_full + b, 128);
+    }
+    mbar_init(o_free, 128);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmK)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmV)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmK16)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmV16)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int n_items = a.n_items;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer
+    // Tiles sit on the 64-token grid.  A tile fully inside [t0, end) is fetched with one box of
+    // min(64, P) token rows per page (map *_big); an item's first/last partial tile with 16-row
+    // boxes (map *_16).  The warp resolves the boxes of 32 tiles at once (one lane per tile, so the
+    // page-table loads overlap); lane 0 waits for ring slots and issues the copies.
+    uint32_t j = 0;
+    const int pmask = (1 << a.page_shift) - 1;
+    const int big = min(kTok, 1 << a.page_shift);          // rows of a full-tile box
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const WorkItem w = a.items[it];
+      const ItemGeom g = geom(w, a.own_len);
+      for (int tb0 = 0; tb0 < g.ntiles; tb0 += 32) {
+        // lane l describes tile tb0 + l: up to 4 boxes (row coordinate each), kind, offsets
+        int brow[4] = {0, 0, 0, 0};
+        int nbox = 0, first_off = 0, full = 0;
+        if (tb0 + lane < g.ntiles) {
+          const int a0 = g.base + (tb0 + lane) * kTok;
+          const int lo = max(a0, w.t0), hi = min(a0 + kTok, g.end);
+          full = (lo == a0 && hi == a0 + kTok);
+          int pos0, step;
+          if (full) { nbox = kTok / big; pos0 = a0; step = big; first_off = 0; }
+          else { pos0 = lo & ~(kBox - 1); nbox = (hi - pos0 + kBox - 1) / kBox; step = kBox; first_off = pos0 - a0; }
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            if (b < nbox) {
+              const int pos = pos0 + b * step;
+              const int page = __ldg(a.page_table + w.pt_off + (pos >> a.page_shift));
+              brow[b] = ((page * a.hkv + w.kv_head) << a.page_shift) + (pos & pmask);
+            }
+          }
+        }
+        const int tend = min(g.ntiles, tb0 + 32);
+        for (int t = tb0; t < tend; ++t, ++j) {
+          const int src = t - tb0;
+          const int tn = __shfl_sync(0xffffffffu, nbox, src);
+          const int tf = __shfl_sync(0xffffffffu, full, src);
+          const int to = __shfl_sync(0xffffffffu, first_off, src);
+          int rr[4];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) rr[b] = __shfl_sync(0xffffffffu, brow[b], src);
+          const int s = j % kStagesTC;
+          const int rows_per_box = tf ? big : kBox;
+          mbar_wait(kv_empty + s, ((j / kStagesTC) & 1) ^ 1);
+          if (elect_one()) {
+            mbar_expect_tx(kv_full + s, static_cast<uint32_t>(tn * rows_per_box * 128 * NH * 2));
+            const uint32_t dk = smem_u32(smem + L::OFF_K + s * L::KVB);
+            const uint32_t dv = smem_u32(smem + L::OFF_V + s * L::KVB);
+            const CUtensorMap* mk = tf ? &tmK : &tmK16;
+            const CUtensorMap* mv = tf ? &tmV : &tmV16;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              if (b < tn) {
+                const uint32_t roff = static_cast<uint32_t>(to + b * rows_per_box) * 128;
+#pragma unroll
+                for (int h = 0; h < NH; ++h) {
+                  tma_load_2d(dk + h * L::HALF_KV + roff, mk, h * 64, rr[b], kv_full + s);
+                  tma_load_2d(dv + h * L::HALF_KV + roff, mv, h * 64, rr[b], kv_full + s);
+                }
+              }
+            }
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer
+    // Per tile j: S(j) = Q K(j)^T into S[j&1]; then O[(j-1)&1] += P(j-1) V(j-1) once softmax
+    // warpgroup (j-1)&1 has published P(j-1).  QK runs one tile ahead of PV.  The whole warp
+    // runs the control flow (warp-uniform descriptors); one elected lane issues.
+    constexpr uint32_t ID_QK = idesc_bf16(kRows, kTok, false);
+    constexpr uint32_t ID_PV = idesc_bf16(kRows, D, true);
+    const uint64_t dq0 = sw128_desc(smem_u32(smem + L::OFF_Q), 16, 1024);
+    const uint64_t dk0 = sw128_desc(smem_u32(smem + L::OFF_K), 16, 1024);
+    const uint64_t dv0 = sw128_desc(smem_u32(smem + L::OFF_V), L::HALF_KV, 1024);
+    uint32_t j = 0, k = 0;
+    for (int it = next_nonempty(a, blockIdx.x); it < n_items; it = next_nonempty(a, it + gridDim.x), ++k) {
+      const ItemGeom g = geom(a.items[it], a.own_len);
+      mbar_wait(q_full + (k & 1), (k >> 1) & 1);
+      tc_fence_after();
+      const uint64_t dq = dq0 + static_cast<uint64_t>(((k & 1) * L::QB) >> 4);
+      for (int t = 0; t <= g.ntiles; ++t) {
+        if (t < g.ntiles) {   // S(j) = Q K(j)^T
+          const int s = j % kStagesTC;
+          mbar_wait(kv_full + s, (j / kStagesTC) & 1);
+          tc_fence_after();
+          const uint64_t dk = dk0 + static_cast<uint64_t>((s * L::KVB) >> 4);
+          const uint32_t dS = tmem + colS(j & 1);
+          if (elect_one()) {
+#pragma unroll
+            for (int ks = 0; ks < D / 16; ++ks) {
+              const uint64_t off = static_cast<uint64_t>(((ks >> 2) * L::HALF_KV + (ks & 3) * 32) >> 4);
+              const uint64_t offq = static_cast<uint64_t>(((ks >> 2) * L::HALF_Q + (ks & 3) * 32) >> 4);
+              mma_ss(dS, dq + offq, dk + off, ID_QK, ks > 0);
+            }
+            tc_commit(s_full + (j & 1));
+          }
+          __syncwarp();
+        }
+        if (t > 0) {          // O[(j-1)&1] += P(j-1) V(j-1)
+          const uint32_t jp = j - 1;
+          const int s = jp % kStagesTC;
+          mbar_wait(p_full + (jp & 1), (jp >> 1) & 1);
+          if (t == 1 && k > 0) mbar_wait(o_free, (k - 1) & 1);   // previous item's O read out
+          tc_fence_after();
+          const uint64_t dv = dv0 + static_cast<uint64_t>((s * L::KVB) >> 4);
+          const uint32_t aP = tmem + colP(jp & 1);
+          const uint32_t dO = tmem + colO(jp & 1);
+          const bool first = t <= 2;      // first tile of this parity in the item
+          if (elect_one()) {
+#pragma unroll
+            for (int kt = 0; kt < kTok / 16; ++kt)
+              mma_ts(dO, aP + kt * 8, dv + static_cast<uint64_t>((kt * 16 * 128) >> 4), ID_PV,
+                     (!first || kt > 0) ? 1u : 0u);
+            tc_commit(pv_done + (jp & 1));
+            tc_commit(kv_empty + s);
+          }
+          __syncwarp();
+        }
+        if (t < g.ntiles) ++j;
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------------ softmax / epilogue
+    // Warpgroup p (p = 0: warps 4-7, p = 1: warps 8-11) owns the tiles j with j&1 == p: its own
+    // running max m_p, sum l_p and accumulator O_p.  Thread = query row = TMEM lane.  At item end
+    // WG1 hands (m_1, l_1) to WG0, which merges O_0 and O_1 and writes the partial.
+    const int p = (warp - 4) >> 2;
+    const int r = tid - 128 - p * 128;             // query row == TMEM lane
+    const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    auto load_q = [&](int k_item, int it) {        // WG0 only
+      if (it < n_items) {
+        const WorkItem w = a.items[it];
+        const bool ok = r < w.n_rows;
+        const __nv_bfloat16* src = a.q;
+        if (ok) {
+          const int rr = w.row_begin + r;
+          const int b = __ldg(a.readers + w.readers_off + rr / a.group);
+          const int h = w.kv_head * a.group + rr % a.group;
+          src = a.q + (static_cast<size_t>(b) * a.hq + h) * D;
+        }
+        uint8_t* qb = smem + L::OFF_Q + (k_item & 1) * L::QB;
+#pragma unroll
+        for (int c = 0; c < D / 8; ++c) {
+          const uint32_t dst = smem_u32(qb + (c >> 3) * L::HALF_Q + r * 128 + (((c & 7) ^ (r & 7)) << 4));
+          cp_async16(dst, ok ? static_cast<const void*>(src + c * 8) : static_cast<const void*>(a.q), ok);
+        }
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    int pf = next_nonempty(a, blockIdx.x);
+    if (p == 0) {                                   // Q of item 0 now, item 1 ahead
+      load_q(0, pf);
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      fence_proxy_async();
+      mbar_arrive(q_full + 0);
+      if (pf < n_items) pf = next_nonempty(a, pf + gridDim.x);
+      load_q(1, pf);
+    }
+    uint32_t j = 0, k = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const WorkItem w = a.items[it];
+      const ItemGeom g = geom(w, a.own_len);
+      if (g.ntiles == 0) {                         // empty (dyn end <= t0): neutral partial
+        if (p == 0 && r < w.n_rows) {
+          float* dst = a.part_acc + static_cast<size_t>(w.slot0 + r) * D;
+#pragma unroll
+          for (int c = 0; c < D; c += 4) *reinterpret_cast<float4*>(dst + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+          a.part_ml[w.slot0 + r] = make_float2(-INFINITY, 0.f);
+        }
+        continue;
+      }
+      const bool active = (warp & 3) * 32 < w.n_rows;   // warp-uniform
+      float m_used = -INFINITY, l = 0.f;
+      bool had = false;
+      uint32_t jl = 0;                              // last tile of this WG in the item
+      for (int t = 0; t < g.ntiles; ++t, ++j) {
+        if ((j & 1) != static_cast<uint32_t>(p)) continue;
+        const int tb = g.base + t * kTok;
+        mbar_wait(s_full + p, (j >> 1) & 1);
+        tc_fence_after();
+        uint32_t sr[64];
+        tmem_ld32x64(tmem + lane_base + colS(p), sr);
+        tc_wait_ld();
+        // PV(j-2) complete: P[p] is free and O_p is up to date (needed for a rescale).
+        if (j >= 2) mbar_wait(pv_done + p, ((j - 2) >> 1) & 1);
+        const bool edge = (tb < w.t0) || (tb + kTok > g.end);
+        uint32_t pk[32];
+        if (active) {
+          float mx = -INFINITY;                     // raw scores; scale > 0 commutes with max
+#pragma unroll
+          for (int c = 0; c < 64; ++c) {
+            float v = __uint_as_float(sr[c]);
+            if (edge) {
+              const int pos = tb + c;
+              if (pos < w.t0 || pos >= g.end) v = -INFINITY;
+            }
+            sr[c] = __float_as_uint(v);
+            mx = fmaxf(mx, v);
+          }
+          mx *= a.scale_log2;
+          // Lazy rescale (exact: O_p and l refer to m_used).  Warp-uniform so the aligned TMEM
+          // accesses are executed by the whole warp.
+          const bool mine = mx > m_used + 8.f;
+          if (__any_sync(0xffffffffu, mine)) {
+            const float alpha = mine ? ex2(m_used - mx) : 1.f;   // 0 when m_used == -inf
+            if (had) {
+              tc_fence_after();
+#pragma unroll 1
+              for (int cb = 0; cb < D; cb += 16) {
+                uint32_t o[16];
+                tmem_ld32x16(tmem + lane_base + colO(p) + cb, o);
+                tc_wait_ld();
+#pragma unroll
+                for (int c = 0; c < 16; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
+                tmem_st32x16(tmem + lane_base + colO(p) + cb, o);
+              }
+              tc_wait_st();
+            }
+            if (mine) { l *= alpha; m_used = mx; }
+          }
+          const float mb = m_used == -INFINITY ? 0.f : m_used;
+          float ls = 0.f;
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            pk[c] = pack_bf16(ex2(fmaf(__uint_as_float(sr[2 * c]), a.scale_log2, -mb)),
+                              ex2(fmaf(__uint_as_float(sr[2 * c + 1]), a.scale_log2, -mb)));
+            ls += __uint_as_float(pk[c] << 16) + __uint_as_float(pk[c] & 0xFFFF0000u);
+          }
+          l += ls;
+        } else {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) pk[c] = 0u;
+        }
+        tmem_st32x32(tmem + lane_base + colP(p), pk);
+        tc_wait_st();
+        if (edge && r < kTok) {                  // zero V rows outside [t0, end) of this tile
+          const int pos = tb + r;
+          if (pos < w.t0 || pos >= g.end) {
+            uint8_t* vrow = smem + L::OFF_V + (j % kStagesTC) * L::KVB + r * 128;
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+              uint4* p4 = reinterpret_cast<uint4*>(vrow + h * L::HALF_KV);
+#pragma unroll
+              for (int c = 0; c < 8; ++c) p4[c] = make_uint4(0, 0, 0, 0);
+            }
+          }
+        }
+        fence_proxy_async();
+        tc_fence_before();
+        mbar_arrive(p_full + p);
+        had = true;
+        jl = j;
+      }
+      if (p == 0) {                  // next item's Q was gathered one item ahead: publish it
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        fence_proxy_async();
+        mbar_arrive(q_full + ((k + 1) & 1));
+      }
+      // ---- epilogue
+      if (had) {
+        mbar_wait(pv_done + p, (jl >> 1) & 1);      // last PV of this WG complete
+        tc_fence_after();
+      }
+      if (p == 1) {
+        xch[(k & 1) * kRows + r] = had ? make_float2(m_used, l) : make_float2(-INFINITY, 0.f);
+        asm volatile("bar.sync 1, 256;\n" ::: "memory");
+      } else {
+        asm volatile("bar.sync 1, 256;\n" ::: "memory");
+        const float2 o1 = xch[(k & 1) * kRows + r];
+        const bool had1 = __any_sync(0xffffffffu, o1.x > -INFINITY);   // WG1 owned a tile
+        const float M = fmaxf(m_used, o1.x);
+        const float Mb = M == -INFINITY ? 0.f : M;
+        const float a0 = had ? ex2(m_used - Mb) : 0.f;
+        const float a1 = had1 ? ex2(o1.x - Mb) : 0.f;
+        float* dst = a.part_acc + static_cast<size_t>(w.slot0 + r) * D;
+        if (active) {
+#pragma unroll 1
+          for (int cb = 0; cb < D; cb += 16) {
+            uint32_t o[16], q1[16];
+            if (had) { tmem_ld32x16(tmem + lane_base + colO(0) + cb, o); }
+            if (had1) { tmem_ld32x16(tmem + lane_base + colO(1) + cb, q1); }
+            tc_wait_ld();
+            if (r < w.n_rows) {
+#pragma unroll
+              for (int c = 0; c < 16; c += 4) {
+                float4 v;
+                v.x = (had ? a0 * __uint_as_float(o[c]) : 0.f) + (had1 ? a1 * __uint_as_float(q1[c]) : 0.f);
+                v.y = (had ? a0 * __uint_as_float(o[c + 1]) : 0.f) + (had1 ? a1 * __uint_as_float(q1[c + 1]) : 0.f);
+                v.z = (had ? a0 * __uint_as_float(o[c + 2]) : 0.f) + (had1 ? a1 * __uint_as_float(q1[c + 2]) : 0.f);
+                v.w = (had ? a0 * __uint_as_float(o[c + 3]) : 0.f) + (had1 ? a1 * __uint_as_float(q1[c + 3]) : 0.f);
+                *reinterpret_cast<float4*>(dst + cb + c) = v;
+              }
+            }
+          }
+        }
+        if (r < w.n_rows) a.part_ml[w.slot0 + r] = make_float2(M, a0 * l + a1 * o1.y);
+        tc_fence_before();
+        mbar_arrive(o_free);
+        if (pf < n_items) pf = next_nonempty(a, pf + gridDim.x);
+        load_q(k, pf);               // Q buffer (k & 1) is free: every QK of item k completed
+      }
+      ++k;
+    }
+    if (p == 0) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+  }
+}
+
+}  // namespace tc
+
+// ------------------------------------------------------------------------------ host launcher
+namespace {
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+bool make_map(CUtensorMap* m, const void* base, int d, int64_t rows, int box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(d) * 2};
+  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace
+
+template <int D>
+orion_status launch_split_tc(const PlanHeader* h, const TcArgs& a, const void* k, const void* v,
+                             int32_t num_pages, cudaStream_t st) {
+  static int num_sms = 0;
+  static cudaError_t attr_err = cudaSuccess;
+  static bool init = false;
+  if (!init) {
+    init = true;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    attr_err = cudaFuncSetAttribute(tc::split_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    tc::Smem<D>::BYTES + 1024);
+  }
+  if (attr_err != cudaSuccess)
+    return fail(ORION_ERR_CUDA, "cudaFuncSetAttribute(split_tc): %s", cudaGetErrorString(attr_err));
+  CUtensorMap mk, mv, mk16, mv16;
+  const int64_t rows = static_cast<int64_t>(num_pages) * h->num_kv_heads * h->page_size;
+  const int big = std::min(tc::kTok, h->page_size);
+  if (!make_map(&mk, k, D, rows, big) || !make_map(&mv, v, D, rows, big) ||
+      !make_map(&mk16, k, D, rows, tc::kBox) || !make_map(&mv16, v, D, rows, tc::kBox))
+    return fail(ORION_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  const int grid = std::min<int>(h->n_items, num_sms > 0 ? num_sms : 148);
+  tc::split_tc_kernel<D><<<grid, tc::kThreadsTC, tc::Smem<D>::BYTES + 1024, st>>>(mk, mv, mk16, mv16, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ORION_ERR_CUDA, "split_tc_kernel: %s", cudaGetErrorString(e));
+  return ORION_OK;
+}
+
+template orion_status launch_split_tc<64>(const PlanHeader*, const TcArgs&, const void*, const void*, int32_t,
+                                          cudaStream_t);
+template orion_status launch_split_tc<128>(const PlanHeader*, const TcArgs&, const void*, const void*, int32_t,
+                                           cudaStream_t);
+
+}  // namespace orion

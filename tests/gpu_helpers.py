@@ -16,19 +16,20 @@ def u16(t):
     return t.detach().cpu().contiguous().view(torch.int16).numpy().view(np.uint16)
 
 
-def batch_for(cfg, lay, policy=0, chunk_tokens=0, device="cuda"):
+def batch_for(cfg, lay, policy=0, chunk_tokens=0, device="cuda", flags=0):
     queries = [dict(n_points=int(lay.n_points[i]), edges=lay.edges[i],
                     prefix_pt_off=int(lay.prefix_pt_off[i]), prefix_len=int(lay.prefix_len[i]))
                for i in range(lay.n_queries)]
     points = np.stack([lay.point_pt_off, lay.content_len, lay.point_cap], 1)
     return orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, lay.page_table,
-                                lay.own_len, policy=policy, device=device, chunk_tokens=chunk_tokens)
+                                lay.own_len, policy=policy, device=device, chunk_tokens=chunk_tokens,
+                                flags=flags)
 
 
-def run_step(cfg, lay, ten, policy=0, mode=orion.APPEND_ADVANCE, chunk_tokens=0, layer=0):
+def run_step(cfg, lay, ten, policy=0, mode=orion.APPEND_ADVANCE, chunk_tokens=0, layer=0, flags=0):
     """Returns dict(out, lse, k_cache, v_cache, own_len) from the GPU after one step."""
     dev = torch.device("cuda")
-    batch = batch_for(cfg, lay, policy, chunk_tokens)
+    batch = batch_for(cfg, lay, policy, chunk_tokens, flags=flags)
     kc = ten["k_cache"][layer].to(dev).contiguous()
     vc = ten["v_cache"][layer].to(dev).contiguous()
     q = ten["q"][layer].to(dev).contiguous()
@@ -60,9 +61,10 @@ def errors(out_gpu, ref):
     return max_abs, rel, float(per_branch.max())
 
 
-def check_parity(cfg, lay, ten, policy=0, branches=None, mode=orion.APPEND_ADVANCE, chunk_tokens=0):
+def check_parity(cfg, lay, ten, policy=0, branches=None, mode=orion.APPEND_ADVANCE, chunk_tokens=0,
+                 flags=0):
     """Full GPU step vs oracle on `branches` (default all).  Asserts the gates; returns errors."""
-    res = run_step(cfg, lay, ten, policy, mode, chunk_tokens)
+    res = run_step(cfg, lay, ten, policy, mode, chunk_tokens, flags=flags)
     rewrite = mode == orion.APPEND_REWRITE
     k2, v2, own = oracle_after_append(cfg, lay, ten, rewrite=rewrite)
     assert np.array_equal(res["own_len"], own)

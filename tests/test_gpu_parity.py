@@ -19,31 +19,37 @@ def _cuda():
         pytest.skip("no CUDA device")
 
 
+KERNELS = [0, orion.PLAN_MMA_SYNC]     # tcgen05 (default) and the legacy mma.sync split kernel
+
+
+@pytest.mark.parametrize("flags", KERNELS)
 @pytest.mark.parametrize("policy", [0, 1])
 @pytest.mark.parametrize("variant", ["plain", "peaky", "sink", "contiguous", "ragged"])
-def test_c1_diamond(policy, variant):
+def test_c1_diamond(policy, variant, flags):
     cfg = C.CONFIGS["c1"]
     lay = T.make_layout(cfg, contiguous=variant == "contiguous", ragged=variant == "ragged",
                         extra_tokens=cfg.page)
     ten = T.make_qkv(cfg, lay, q_scale=4.0 if variant == "peaky" else 1.0, sink=variant == "sink")
-    check_parity(cfg, lay, ten, policy)
+    check_parity(cfg, lay, ten, policy, flags=flags)
 
 
+@pytest.mark.parametrize("flags", KERNELS)
 @pytest.mark.parametrize("page", [16, 32, 64])
 @pytest.mark.parametrize("hq,hkv,d", [(4, 2, 64), (8, 8, 128), (28, 4, 128), (32, 4, 64)])
-def test_shapes_pages_ragged(page, hq, hkv, d):
+def test_shapes_pages_ragged(page, hq, hkv, d, flags):
     cfg = C.CONFIGS["c1"].with_(hq=hq, hkv=hkv, d=d, page=page, lp=300, t=150, lc=20, n_queries=2,
                                 dag="mixed8")
     lay = T.make_layout(cfg, ragged=True, extra_tokens=page)
     ten = T.make_qkv(cfg, lay, q_scale=2.0)
-    check_parity(cfg, lay, ten, 0, chunk_tokens=128)
+    check_parity(cfg, lay, ten, 0, chunk_tokens=128, flags=flags)
 
 
-def test_c2_full_layer():
+@pytest.mark.parametrize("flags", KERNELS)
+def test_c2_full_layer(flags):
     cfg = C.CONFIGS["c2"]
     lay = T.make_layout(cfg, extra_tokens=cfg.page)
     ten = T.make_qkv(cfg, lay)
-    check_parity(cfg, lay, ten, 0)
+    check_parity(cfg, lay, ten, 0, flags=flags)
 
 
 @pytest.mark.parametrize("policy", [0, 1])
@@ -59,23 +65,25 @@ def _sample(lay, k, seed):
     return sorted(rng.sample(range(lay.n_branches), k))
 
 
-def test_c4_full_size_sampled():
+@pytest.mark.parametrize("flags", KERNELS)
+def test_c4_full_size_sampled(flags):
     # The bench workload at full size (64 queries x mixed16, 4K prefix, 512 tok/point); outputs
     # are checked on a sample of branches the oracle computes one by one.
     cfg = C.CONFIGS["c4"]
     lay = T.make_layout(cfg, extra_tokens=cfg.page)
     ten = T.make_qkv(cfg, lay, device="cuda")
     ten = {k: v.cpu() for k, v in ten.items()}
-    check_parity(cfg, lay, ten, 0, branches=_sample(lay, 24, 4) + [lay.n_branches - 1])
+    check_parity(cfg, lay, ten, 0, branches=_sample(lay, 24, 4) + [lay.n_branches - 1], flags=flags)
 
 
+@pytest.mark.parametrize("flags", KERNELS)
 @pytest.mark.parametrize("name", ["c5w", "c5c"])
-def test_c5_per_gpu_share_sampled(name):
+def test_c5_per_gpu_share_sampled(name, flags):
     cfg = C.CONFIGS[name].with_(n_queries=8)     # one GPU's share at 8 GPUs
     lay = T.make_layout(cfg, extra_tokens=cfg.page)
     ten = T.make_qkv(cfg, lay, device="cuda", q_scale=2.0)
     ten = {k: v.cpu() for k, v in ten.items()}
-    check_parity(cfg, lay, ten, 0, branches=_sample(lay, 12, 5) + [63, lay.n_branches - 1])
+    check_parity(cfg, lay, ten, 0, branches=_sample(lay, 12, 5) + [63, lay.n_branches - 1], flags=flags)
 
 
 def test_page_permutation_bitwise_and_determinism():
