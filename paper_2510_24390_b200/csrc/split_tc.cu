@@ -175,7 +175,8 @@ struct Smem {
   static constexpr int OFF_K = 2 * QB;
   static constexpr int OFF_V = OFF_K + kStagesTC * KVB;
   static constexpr int OFF_XCH = OFF_V + kStagesTC * KVB;   // WG1 -> WG0 (m, l) per row, x2
-  static constexpr int OFF_BAR = OFF_XCH + 2 * kRows * 8;
+  static constexpr int OFF_ONES = OFF_XCH + 2 * kRows * 8;  // [16][64] bf16 ones: l = P . 1 on the MMA
+  static constexpr int OFF_BAR = OFF_ONES + 16 * kTok * 2;
   static constexpr int N_BAR = 2 * kStagesTC + 2 + 2 + 2 + 2 + 1;
   static constexpr int BYTES = OFF_BAR + N_BAR * 8 + 16;
 };
@@ -184,6 +185,7 @@ struct Smem {
 __device__ __forceinline__ uint32_t colS(uint32_t p) { return p * 64; }
 __device__ __forceinline__ uint32_t colP(uint32_t p) { return 128 + p * 32; }
 __device__ __forceinline__ uint32_t colO(uint32_t p) { return 256 + p * 128; }
+__device__ __forceinline__ uint32_t colL(uint32_t p) { return 192 + p * 16; }   // row sums l
 constexpr int kThreadsTC = 384;   // warps 0-3: TMA / MMA / TMEM alloc / idle; 4-7: WG0; 8-11: WG1
 
 template <int D>
@@ -194,7 +196,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   using L = Smem<D>;
   constexpr int NH = D / 64;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps the smem space
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   uint64_t* kv_full = bars;
   uint64_t* kv_empty = bars + kStagesTC;
@@ -220,6 +222,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmK16)) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmV16)) : "memory");
   }
+  for (int i = tid; i < 16 * kTok * 2 / 16; i += blockDim.x)       // bf16 1.0 = 0x3F80
+    reinterpret_cast<uint4*>(smem + L::OFF_ONES)[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+  fence_proxy_async();
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
@@ -306,6 +311,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const uint64_t dq0 = sw128_desc(smem_u32(smem + L::OFF_Q), 16, 1024);
     const uint64_t dk0 = sw128_desc(smem_u32(smem + L::OFF_K), 16, 1024);
     const uint64_t dv0 = sw128_desc(smem_u32(smem + L::OFF_V), L::HALF_KV, 1024);
+    const uint64_t d1 = sw128_desc(smem_u32(smem + L::OFF_ONES), 16, 1024);
+    constexpr uint32_t ID_L = idesc_bf16(kRows, 16, false);
     uint32_t j = 0, k = 0;
     for (int it = next_nonempty(a, blockIdx.x); it < n_items; it = next_nonempty(a, it + gridDim.x), ++k) {
       const ItemGeom g = geom(a.items[it], a.own_len);
@@ -342,9 +349,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           const bool first = t <= 2;      // first tile of this parity in the item
           if (elect_one()) {
 #pragma unroll
-            for (int kt = 0; kt < kTok / 16; ++kt)
+            for (int kt = 0; kt < kTok / 16; ++kt) {
               mma_ts(dO, aP + kt * 8, dv + static_cast<uint64_t>((kt * 16 * 128) >> 4), ID_PV,
                      (!first || kt > 0) ? 1u : 0u);
+              // l += P . 1: the row sums of exactly the bf16 P that enters P.V (reading S17)
+              mma_ts(tmem + colL(jp & 1), aP + kt * 8, d1 + static_cast<uint64_t>((kt * 32) >> 4), ID_L,
+                     (!first || kt > 0) ? 1u : 0u);
+            }
             tc_commit(pv_done + (jp & 1));
             tc_commit(kv_empty + s);
           }
@@ -404,7 +415,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         continue;
       }
       const bool active = (warp & 3) * 32 < w.n_rows;   // warp-uniform
-      float m_used = -INFINITY, l = 0.f;
+      float m_used = -INFINITY;
       bool had = false;
       uint32_t jl = 0;                              // last tile of this WG in the item
       for (int t = 0; t < g.ntiles; ++t, ++j) {
@@ -421,18 +432,20 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         uint32_t pk[32];
         if (active) {
           float mx = -INFINITY;                     // raw scores; scale > 0 commutes with max
+          if (!edge) {
 #pragma unroll
-          for (int c = 0; c < 64; ++c) {
-            float v = __uint_as_float(sr[c]);
-            if (edge) {
-              const int pos = tb + c;
-              if (pos < w.t0 || pos >= g.end) v = -INFINITY;
+            for (int c = 0; c < 64; ++c) mx = fmaxf(mx, __uint_as_float(sr[c]));
+          } else {
+            const int lo_c = w.t0 - tb, hi_c = g.end - tb;   // valid columns [lo_c, hi_c)
+#pragma unroll
+            for (int c = 0; c < 64; ++c) {
+              const float v = (c >= lo_c && c < hi_c) ? __uint_as_float(sr[c]) : -INFINITY;
+              sr[c] = __float_as_uint(v);
+              mx = fmaxf(mx, v);
             }
-            sr[c] = __float_as_uint(v);
-            mx = fmaxf(mx, v);
           }
           mx *= a.scale_log2;
-          // Lazy rescale (exact: O_p and l refer to m_used).  Warp-uniform so the aligned TMEM
+          // Lazy rescale (exact: O_p and l_p refer to m_used).  Warp-uniform so the aligned TMEM
           // accesses are executed by the whole warp.
           const bool mine = mx > m_used + 8.f;
           if (__any_sync(0xffffffffu, mine)) {
@@ -448,19 +461,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 for (int c = 0; c < 16; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
                 tmem_st32x16(tmem + lane_base + colO(p) + cb, o);
               }
+              const uint32_t lv = tmem_ld32x1(tmem + lane_base + colL(p));
+              tc_wait_ld();
+              tmem_st32x1(tmem + lane_base + colL(p), __float_as_uint(__uint_as_float(lv) * alpha));
               tc_wait_st();
             }
-            if (mine) { l *= alpha; m_used = mx; }
+            if (mine) m_used = mx;
           }
           const float mb = m_used == -INFINITY ? 0.f : m_used;
-          float ls = 0.f;
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {
+          for (int c = 0; c < 32; ++c)
             pk[c] = pack_bf16(ex2(fmaf(__uint_as_float(sr[2 * c]), a.scale_log2, -mb)),
                               ex2(fmaf(__uint_as_float(sr[2 * c + 1]), a.scale_log2, -mb)));
-            ls += __uint_as_float(pk[c] << 16) + __uint_as_float(pk[c] & 0xFFFF0000u);
-          }
-          l += ls;
         } else {
 #pragma unroll
           for (int c = 0; c < 32; ++c) pk[c] = 0u;
@@ -496,7 +508,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         tc_fence_after();
       }
       if (p == 1) {
-        xch[(k & 1) * kRows + r] = had ? make_float2(m_used, l) : make_float2(-INFINITY, 0.f);
+        xch[(k & 1) * kRows + r] = make_float2(had ? m_used : -INFINITY, 0.f);
         asm volatile("bar.sync 1, 256;\n" ::: "memory");
       } else {
         asm volatile("bar.sync 1, 256;\n" ::: "memory");
@@ -506,6 +518,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         const float Mb = M == -INFINITY ? 0.f : M;
         const float a0 = had ? ex2(m_used - Mb) : 0.f;
         const float a1 = had1 ? ex2(o1.x - Mb) : 0.f;
+        float l0 = 0.f, l1 = 0.f;
+        if (active) {
+          if (had) l0 = __uint_as_float(tmem_ld32x1(tmem + lane_base + colL(0)));
+          if (had1) l1 = __uint_as_float(tmem_ld32x1(tmem + lane_base + colL(1)));
+          tc_wait_ld();
+        }
         float* dst = a.part_acc + static_cast<size_t>(w.slot0 + r) * D;
         if (active) {
 #pragma unroll 1
@@ -527,7 +545,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             }
           }
         }
-        if (r < w.n_rows) a.part_ml[w.slot0 + r] = make_float2(M, a0 * l + a1 * o1.y);
+        if (r < w.n_rows) a.part_ml[w.slot0 + r] = make_float2(M, a0 * l0 + a1 * l1);
         tc_fence_before();
         mbar_arrive(o_free);
         if (pf < n_items) pf = next_nonempty(a, pf + gridDim.x);
