@@ -7,7 +7,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liborion.so")
+# ORION_LIB overrides the library path (development only, e.g. the ORION_TC_TRACE build
+# liborion_trace.so used by tools/trace_tc.sh); the default is the in-tree build.
+LIB_PATH = os.environ.get("ORION_LIB") or os.path.join(_HERE, "liborion.so")
 
 OK, ERR_INVALID_ARG, ERR_CYCLE, ERR_UNKNOWN_POINT, ERR_CAPACITY, ERR_UNSUPPORTED, ERR_CUDA = range(7)
 EDGE_NULL, EDGE_CONTEXTUAL, EDGE_DEPENDENT = 0, 1, 2

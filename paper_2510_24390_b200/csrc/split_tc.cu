@@ -26,6 +26,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdio>
 
 #include "../../include/orion.h"
 #include "plan_format.h"
@@ -36,7 +37,12 @@ namespace orion {
 namespace tc {
 
 constexpr int kTok = 64;       // tokens per S tile / ring stage
-constexpr int kStagesTC = 4;   // K/V ring depth
+// Separate K and V rings: a K stage is released as soon as its QK completes, a V stage only after
+// its PV, so the producer can run ~3 tiles ahead of the QK cursor (enough bytes in flight to cover
+// HBM latency at the per-SM share of the bandwidth).
+template <int D> struct Rings;
+template <> struct Rings<128> { static constexpr int K = 3, V = 6; };
+template <> struct Rings<64> { static constexpr int K = 4, V = 8; };
 constexpr int kRows = 128;     // MMA M (query rows per item)
 constexpr int kBox = 16;       // token rows per TMA box
 
@@ -68,9 +74,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         : "r"(a), "r"(parity)
         : "memory");
     if (ok) return;
-    if (spin > (1u << 26)) __trap();
+    if (spin > (1u << 22)) __trap();
   }
 }
+#ifdef ORION_TC_TRACE
+#define TRACE_DECL unsigned long long tr_[12] = {0}; const unsigned long long tr_t0 = clock64();
+#define TW(slot, stmt) do { const unsigned long long t_ = clock64(); stmt; tr_[slot] += clock64() - t_; } while (0)
+#define TRACE_DUMP(role) do { if (blockIdx.x < 2 && (threadIdx.x & 31) == 0) printf( \
+    "TRACE blk %d warp %2d %-8s tot %llu | %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu\n", blockIdx.x, \
+    threadIdx.x >> 5, role, clock64() - tr_t0, tr_[0], tr_[1], tr_[2], tr_[3], tr_[4], tr_[5], tr_[6], tr_[7], \
+    tr_[8], tr_[9]); } while (0)
+#else
+#define TRACE_DECL
+#define TW(slot, stmt) stmt
+#define TRACE_DUMP(role) do {} while (0)
+#endif
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile(
@@ -172,12 +191,13 @@ struct Smem {
   static constexpr int HALF_Q = kRows * 128;    // 64-dim half of Q
   static constexpr int HALF_KV = kTok * 128;    // 64-dim half of a K/V stage
   static constexpr int OFF_Q = 0;
+  static constexpr int SK = Rings<D>::K, SV = Rings<D>::V;
   static constexpr int OFF_K = 2 * QB;
-  static constexpr int OFF_V = OFF_K + kStagesTC * KVB;
-  static constexpr int OFF_XCH = OFF_V + kStagesTC * KVB;   // WG1 -> WG0 (m, l) per row, x2
+  static constexpr int OFF_V = OFF_K + SK * KVB;
+  static constexpr int OFF_XCH = OFF_V + SV * KVB;   // WG1 -> WG0 (m, l) per row, x2
   static constexpr int OFF_ONES = OFF_XCH + 2 * kRows * 8;  // [16][64] bf16 ones: l = P . 1 on the MMA
   static constexpr int OFF_BAR = OFF_ONES + 16 * kTok * 2;
-  static constexpr int N_BAR = 2 * kStagesTC + 2 + 2 + 2 + 2 + 1;
+  static constexpr int N_BAR = 2 * SK + 2 * SV + 2 + 2 + 2 + 2 + 1 + 2;
   static constexpr int BYTES = OFF_BAR + N_BAR * 8 + 16;
 };
 
@@ -186,7 +206,11 @@ __device__ __forceinline__ uint32_t colS(uint32_t p) { return p * 64; }
 __device__ __forceinline__ uint32_t colP(uint32_t p) { return 128 + p * 32; }
 __device__ __forceinline__ uint32_t colO(uint32_t p) { return 256 + p * 128; }
 __device__ __forceinline__ uint32_t colL(uint32_t p) { return 192 + p * 16; }   // row sums l
-constexpr int kThreadsTC = 384;   // warps 0-3: TMA / MMA / TMEM alloc / idle; 4-7: WG0; 8-11: WG1
+constexpr int kThreadsTC = 384;   // warps 0-3: TMEM alloc / idle / TMA / MMA; 4-7: WG0; 8-11: WG1
+// The TMA and MMA warps sit on SM sub-partitions 2 and 3 so that their barrier polling does not
+// steal issue slots from the softmax warps of items with <= 64 rows (TMEM lanes 0-63 are only
+// reachable from warps 4k and 4k+1, i.e. sub-partitions 0 and 1).
+constexpr int kWarpAlloc = 0, kWarpTMA = 2, kWarpMMA = 3;
 
 template <int D>
 __global__ void __launch_bounds__(kThreadsTC, 1)
@@ -198,24 +222,31 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps the smem space
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
-  uint64_t* kv_full = bars;
-  uint64_t* kv_empty = bars + kStagesTC;
-  uint64_t* s_full = bars + 2 * kStagesTC;
+  constexpr int SK = L::SK, SV = L::SV;
+  uint64_t* k_full = bars;
+  uint64_t* k_empty = k_full + SK;
+  uint64_t* v_full = k_empty + SK;
+  uint64_t* v_empty = v_full + SV;
+  uint64_t* s_full = v_empty + SV;
   uint64_t* p_full = s_full + 2;
   uint64_t* pv_done = p_full + 2;
   uint64_t* q_full = pv_done + 2;
   uint64_t* o_free = q_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 1);
+  uint64_t* s_free = o_free + 1;                  // softmax WG has read S[b] into registers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_free + 2);
   float2* xch = reinterpret_cast<float2*>(smem + L::OFF_XCH);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int s = 0; s < kStagesTC; ++s) { mbar_init(kv_full + s, 1); mbar_init(kv_empty + s, 1); }
+    for (int s = 0; s < SK; ++s) { mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1); }
+    for (int s = 0; s < SV; ++s) { mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1); }
     for (int b = 0; b < 2; ++b) {
       mbar_init(s_full + b, 1); mbar_init(p_full + b, 128); mbar_init(pv_done + b, 1);
       mbar_init(q_full + b, 128);
     }
     mbar_init(o_free, 128);
+    mbar_init(s_free + 0, 128);
+    mbar_init(s_free + 1, 128);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmK)) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmV)) : "memory");
@@ -225,7 +256,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   for (int i = tid; i < 16 * kTok * 2 / 16; i += blockDim.x)       // bf16 1.0 = 0x3F80
     reinterpret_cast<uint4*>(smem + L::OFF_ONES)[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
   fence_proxy_async();
-  if (warp == 2) {
+  if (warp == kWarpAlloc) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
@@ -235,7 +266,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   const uint32_t tmem = *tmem_slot;
   const int n_items = a.n_items;
 
-  if (warp == 0) {
+  TRACE_DECL
+  if (warp == kWarpTMA) {
     // ------------------------------------------------------------------ TMA producer
     // Tiles sit on the 64-token grid.  A tile fully inside [t0, end) is fetched with one box of
     // min(64, P) token rows per page (map *_big); an item's first/last partial tile with 16-row
@@ -276,94 +308,131 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           int rr[4];
 #pragma unroll
           for (int b = 0; b < 4; ++b) rr[b] = __shfl_sync(0xffffffffu, brow[b], src);
-          const int s = j % kStagesTC;
+          const int sk = j % SK, sv = j % SV;
           const int rows_per_box = tf ? big : kBox;
-          mbar_wait(kv_empty + s, ((j / kStagesTC) & 1) ^ 1);
+          const uint32_t bytes = static_cast<uint32_t>(tn * rows_per_box * 128 * NH);
+          const CUtensorMap* mk = tf ? &tmK : &tmK16;
+          const CUtensorMap* mv = tf ? &tmV : &tmV16;
+          TW(0, mbar_wait(k_empty + sk, ((j / SK) & 1) ^ 1));
           if (elect_one()) {
-            mbar_expect_tx(kv_full + s, static_cast<uint32_t>(tn * rows_per_box * 128 * NH * 2));
-            const uint32_t dk = smem_u32(smem + L::OFF_K + s * L::KVB);
-            const uint32_t dv = smem_u32(smem + L::OFF_V + s * L::KVB);
-            const CUtensorMap* mk = tf ? &tmK : &tmK16;
-            const CUtensorMap* mv = tf ? &tmV : &tmV16;
+            mbar_expect_tx(k_full + sk, bytes);
+            const uint32_t dk = smem_u32(smem + L::OFF_K + sk * L::KVB);
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
+            for (int b = 0; b < 4; ++b)
               if (b < tn) {
                 const uint32_t roff = static_cast<uint32_t>(to + b * rows_per_box) * 128;
 #pragma unroll
-                for (int h = 0; h < NH; ++h) {
-                  tma_load_2d(dk + h * L::HALF_KV + roff, mk, h * 64, rr[b], kv_full + s);
-                  tma_load_2d(dv + h * L::HALF_KV + roff, mv, h * 64, rr[b], kv_full + s);
-                }
+                for (int h = 0; h < NH; ++h) tma_load_2d(dk + h * L::HALF_KV + roff, mk, h * 64, rr[b], k_full + sk);
               }
-            }
+          }
+          __syncwarp();
+          TW(1, mbar_wait(v_empty + sv, ((j / SV) & 1) ^ 1));
+          if (elect_one()) {
+            mbar_expect_tx(v_full + sv, bytes);
+            const uint32_t dv = smem_u32(smem + L::OFF_V + sv * L::KVB);
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+              if (b < tn) {
+                const uint32_t roff = static_cast<uint32_t>(to + b * rows_per_box) * 128;
+#pragma unroll
+                for (int h = 0; h < NH; ++h) tma_load_2d(dv + h * L::HALF_KV + roff, mv, h * 64, rr[b], v_full + sv);
+              }
           }
           __syncwarp();
         }
       }
     }
-  } else if (warp == 1) {
+    TRACE_DUMP("producer");
+  } else if (warp == kWarpMMA) {
     // ------------------------------------------------------------------ MMA issuer
-    // Per tile j: S(j) = Q K(j)^T into S[j&1]; then O[(j-1)&1] += P(j-1) V(j-1) once softmax
-    // warpgroup (j-1)&1 has published P(j-1).  QK runs one tile ahead of PV.  The whole warp
-    // runs the control flow (warp-uniform descriptors); one elected lane issues.
+    // Two cursors walk the flattened (item, tile) sequence: QK runs two tiles ahead of PV, so
+    // S(j+2) = Q K(j+2)^T is issued as soon as softmax warpgroup j&1 has read S(j) into registers
+    // (s_free), and O[j&1] += P(j) V(j) (plus l += P(j).1) as soon as it has published P(j).
+    // The whole warp runs the control flow (warp-uniform descriptors); one elected lane issues.
     constexpr uint32_t ID_QK = idesc_bf16(kRows, kTok, false);
     constexpr uint32_t ID_PV = idesc_bf16(kRows, D, true);
+    constexpr uint32_t ID_L = idesc_bf16(kRows, 16, false);
     const uint64_t dq0 = sw128_desc(smem_u32(smem + L::OFF_Q), 16, 1024);
     const uint64_t dk0 = sw128_desc(smem_u32(smem + L::OFF_K), 16, 1024);
     const uint64_t dv0 = sw128_desc(smem_u32(smem + L::OFF_V), L::HALF_KV, 1024);
     const uint64_t d1 = sw128_desc(smem_u32(smem + L::OFF_ONES), 16, 1024);
-    constexpr uint32_t ID_L = idesc_bf16(kRows, 16, false);
-    uint32_t j = 0, k = 0;
-    for (int it = next_nonempty(a, blockIdx.x); it < n_items; it = next_nonempty(a, it + gridDim.x), ++k) {
-      const ItemGeom g = geom(a.items[it], a.own_len);
-      mbar_wait(q_full + (k & 1), (k >> 1) & 1);
-      tc_fence_after();
-      const uint64_t dq = dq0 + static_cast<uint64_t>(((k & 1) * L::QB) >> 4);
-      for (int t = 0; t <= g.ntiles; ++t) {
-        if (t < g.ntiles) {   // S(j) = Q K(j)^T
-          const int s = j % kStagesTC;
-          mbar_wait(kv_full + s, (j / kStagesTC) & 1);
-          tc_fence_after();
-          const uint64_t dk = dk0 + static_cast<uint64_t>((s * L::KVB) >> 4);
-          const uint32_t dS = tmem + colS(j & 1);
-          if (elect_one()) {
-#pragma unroll
-            for (int ks = 0; ks < D / 16; ++ks) {
-              const uint64_t off = static_cast<uint64_t>(((ks >> 2) * L::HALF_KV + (ks & 3) * 32) >> 4);
-              const uint64_t offq = static_cast<uint64_t>(((ks >> 2) * L::HALF_Q + (ks & 3) * 32) >> 4);
-              mma_ss(dS, dq + offq, dk + off, ID_QK, ks > 0);
-            }
-            tc_commit(s_full + (j & 1));
-          }
-          __syncwarp();
-        }
-        if (t > 0) {          // O[(j-1)&1] += P(j-1) V(j-1)
-          const uint32_t jp = j - 1;
-          const int s = jp % kStagesTC;
-          mbar_wait(p_full + (jp & 1), (jp >> 1) & 1);
-          if (t == 1 && k > 0) mbar_wait(o_free, (k - 1) & 1);   // previous item's O read out
-          tc_fence_after();
-          const uint64_t dv = dv0 + static_cast<uint64_t>((s * L::KVB) >> 4);
-          const uint32_t aP = tmem + colP(jp & 1);
-          const uint32_t dO = tmem + colO(jp & 1);
-          const bool first = t <= 2;      // first tile of this parity in the item
-          if (elect_one()) {
-#pragma unroll
-            for (int kt = 0; kt < kTok / 16; ++kt) {
-              mma_ts(dO, aP + kt * 8, dv + static_cast<uint64_t>((kt * 16 * 128) >> 4), ID_PV,
-                     (!first || kt > 0) ? 1u : 0u);
-              // l += P . 1: the row sums of exactly the bf16 P that enters P.V (reading S17)
-              mma_ts(tmem + colL(jp & 1), aP + kt * 8, d1 + static_cast<uint64_t>((kt * 32) >> 4), ID_L,
-                     (!first || kt > 0) ? 1u : 0u);
-            }
-            tc_commit(pv_done + (jp & 1));
-            tc_commit(kv_empty + s);
-          }
-          __syncwarp();
-        }
-        if (t < g.ntiles) ++j;
+    struct Cur {
+      int it, t, nt;
+      uint32_t k, j;
+    };
+    auto start = [&](Cur& c) {
+      c.it = next_nonempty(a, blockIdx.x);
+      c.t = 0; c.k = 0; c.j = 0;
+      c.nt = c.it < n_items ? geom(a.items[c.it], a.own_len).ntiles : 0;
+    };
+    auto advance = [&](Cur& c) {
+      ++c.j;
+      if (++c.t == c.nt) {
+        c.it = next_nonempty(a, c.it + gridDim.x);
+        c.t = 0; ++c.k;
+        c.nt = c.it < n_items ? geom(a.items[c.it], a.own_len).ntiles : 0;
       }
+    };
+    auto issue_qk = [&](const Cur& c) {
+      const uint32_t j = c.j;
+      if (c.t == 0) {
+        TW(1, mbar_wait(q_full + (c.k & 1), (c.k >> 1) & 1));
+      }
+      const int s = j % SK;
+      TW(2, mbar_wait(k_full + s, (j / SK) & 1));
+      if (j >= 2) TW(3, mbar_wait(s_free + (j & 1), ((j - 2) >> 1) & 1));   // S[j&1] read out
+      tc_fence_after();
+      const uint64_t dq = dq0 + static_cast<uint64_t>(((c.k & 1) * L::QB) >> 4);
+      const uint64_t dk = dk0 + static_cast<uint64_t>((s * L::KVB) >> 4);
+      const uint32_t dS = tmem + colS(j & 1);
+      if (elect_one()) {
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint64_t off = static_cast<uint64_t>(((ks >> 2) * L::HALF_KV + (ks & 3) * 32) >> 4);
+          const uint64_t offq = static_cast<uint64_t>(((ks >> 2) * L::HALF_Q + (ks & 3) * 32) >> 4);
+          mma_ss(dS, dq + offq, dk + off, ID_QK, ks > 0);
+        }
+        tc_commit(s_full + (j & 1));
+        tc_commit(k_empty + s);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](const Cur& c) {
+      const uint32_t j = c.j;
+      const int s = j % SV;
+      TW(6, mbar_wait(v_full + s, (j / SV) & 1));
+      TW(4, mbar_wait(p_full + (j & 1), (j >> 1) & 1));
+      if (c.t == 0 && c.k > 0) TW(5, mbar_wait(o_free, (c.k - 1) & 1));   // previous item's O read
+      tc_fence_after();
+      const uint64_t dv = dv0 + static_cast<uint64_t>((s * L::KVB) >> 4);
+      const uint32_t aP = tmem + colP(j & 1);
+      const uint32_t dO = tmem + colO(j & 1);
+      const bool first = c.t < 2;        // first tile of this parity in the item
+      if (elect_one()) {
+#pragma unroll
+        for (int kt = 0; kt < kTok / 16; ++kt) {
+          mma_ts(dO, aP + kt * 8, dv + static_cast<uint64_t>((kt * 16 * 128) >> 4), ID_PV,
+                 (!first || kt > 0) ? 1u : 0u);
+          // l += P . 1: the row sums of exactly the bf16 P that enters P.V (reading S17)
+          mma_ts(tmem + colL(j & 1), aP + kt * 8, d1 + static_cast<uint64_t>((kt * 32) >> 4), ID_L,
+                 (!first || kt > 0) ? 1u : 0u);
+        }
+        tc_commit(pv_done + (j & 1));
+        tc_commit(v_empty + s);
+      }
+      __syncwarp();
+    };
+    // QK stays <= 2 tiles ahead of PV and never enters item k+2 before every PV of item k is
+    // issued: item k+2's Q reuses item k's buffer, which is refilled only after item k's epilogue.
+    Cur cq, cv;
+    start(cq);
+    start(cv);
+    while (cv.it < n_items) {
+      while (cq.it < n_items && cq.j <= cv.j + 2 && cq.k <= cv.k + 1) { issue_qk(cq); advance(cq); }
+      issue_pv(cv);
+      advance(cv);
     }
+    TRACE_DUMP("mma");
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ softmax / epilogue
     // Warpgroup p (p = 0: warps 4-7, p = 1: warps 8-11) owns the tiles j with j&1 == p: its own
@@ -421,13 +490,21 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       for (int t = 0; t < g.ntiles; ++t, ++j) {
         if ((j & 1) != static_cast<uint32_t>(p)) continue;
         const int tb = g.base + t * kTok;
-        mbar_wait(s_full + p, (j >> 1) & 1);
+        TW(6, mbar_wait(s_full + p, (j >> 1) & 1));
         tc_fence_after();
         uint32_t sr[64];
+#ifdef ORION_TC_TRACE
+        unsigned long long ts0 = clock64();
+#endif
         tmem_ld32x64(tmem + lane_base + colS(p), sr);
         tc_wait_ld();
+#ifdef ORION_TC_TRACE
+        tr_[0] += clock64() - ts0; ts0 = clock64();
+#endif
+        tc_fence_before();
+        mbar_arrive(s_free + p);                  // QK(j+2) may overwrite S[p] now
         // PV(j-2) complete: P[p] is free and O_p is up to date (needed for a rescale).
-        if (j >= 2) mbar_wait(pv_done + p, ((j - 2) >> 1) & 1);
+        if (j >= 2) TW(7, mbar_wait(pv_done + p, ((j - 2) >> 1) & 1));
         const bool edge = (tb < w.t0) || (tb + kTok > g.end);
         uint32_t pk[32];
         if (active) {
@@ -477,12 +554,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #pragma unroll
           for (int c = 0; c < 32; ++c) pk[c] = 0u;
         }
+#ifdef ORION_TC_TRACE
+        tr_[1] += clock64() - ts0; ts0 = clock64();
+#endif
         tmem_st32x32(tmem + lane_base + colP(p), pk);
         tc_wait_st();
+#ifdef ORION_TC_TRACE
+        tr_[2] += clock64() - ts0; ts0 = clock64();
+#endif
         if (edge && r < kTok) {                  // zero V rows outside [t0, end) of this tile
           const int pos = tb + r;
           if (pos < w.t0 || pos >= g.end) {
-            uint8_t* vrow = smem + L::OFF_V + (j % kStagesTC) * L::KVB + r * 128;
+            uint8_t* vrow = smem + L::OFF_V + (j % SV) * L::KVB + r * 128;
 #pragma unroll
             for (int h = 0; h < NH; ++h) {
               uint4* p4 = reinterpret_cast<uint4*>(vrow + h * L::HALF_KV);
@@ -494,6 +577,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         fence_proxy_async();
         tc_fence_before();
         mbar_arrive(p_full + p);
+#ifdef ORION_TC_TRACE
+        tr_[3] += clock64() - ts0;
+#endif
         had = true;
         jl = j;
       }
@@ -504,14 +590,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       }
       // ---- epilogue
       if (had) {
-        mbar_wait(pv_done + p, (jl >> 1) & 1);      // last PV of this WG complete
+        TW(8, mbar_wait(pv_done + p, (jl >> 1) & 1));      // last PV of this WG complete
         tc_fence_after();
       }
       if (p == 1) {
         xch[(k & 1) * kRows + r] = make_float2(had ? m_used : -INFINITY, 0.f);
-        asm volatile("bar.sync 1, 256;\n" ::: "memory");
+        TW(9, asm volatile("bar.sync 1, 256;\n" ::: "memory"));
       } else {
-        asm volatile("bar.sync 1, 256;\n" ::: "memory");
+        TW(9, asm volatile("bar.sync 1, 256;\n" ::: "memory"));
         const float2 o1 = xch[(k & 1) * kRows + r];
         const bool had1 = __any_sync(0xffffffffu, o1.x > -INFINITY);   // WG1 owned a tile
         const float M = fmaxf(m_used, o1.x);
@@ -554,10 +640,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       ++k;
     }
     if (p == 0) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    if ((warp & 3) < 2) TRACE_DUMP("softmax");
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == kWarpAlloc) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
   }
