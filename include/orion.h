@@ -107,9 +107,12 @@ typedef struct { int32_t n_points, branch0, prefix_pt_off, prefix_len; } orion_q
 /* Per global branch (= point): its page run, content length Lc and capacity in tokens. */
 typedef struct { int32_t pt_off, content_len, capacity; } orion_point_desc;
 
-/* Plan flags.  ORION_PLAN_MMA_SYNC selects the legacy split kernel (mma.sync m16n8k16 + cp.async,
- * <= 64 rows per work item) instead of the default tcgen05/TMEM/TMA kernel (<= 128 rows). */
-enum { ORION_PLAN_MMA_SYNC = 1 };
+/* Plan flags (split-kernel variant).  Default: the transposed tcgen05/TMEM/TMA kernel (tokens on
+ * the MMA M dimension, <= 64 query rows per work item; head_dim 128) — head_dim 64 uses the
+ * rows-on-lanes tcgen05 kernel.  ORION_PLAN_ROWS_ON_LANES forces the rows-on-lanes tcgen05 kernel
+ * (<= 128 rows per item); ORION_PLAN_MMA_SYNC the legacy mma.sync m16n8k16 + cp.async kernel
+ * (<= 64 rows per item).  All variants compute the same result (same plan semantics). */
+enum { ORION_PLAN_MMA_SYNC = 1, ORION_PLAN_ROWS_ON_LANES = 2 };
 
 typedef struct {
   int32_t num_sms;        /* SMs to balance for; <= 0 selects 148 (B200) */

@@ -84,7 +84,8 @@ def bind_segments(queries, points, seg_offsets, refs):
     return out
 
 
-PLAN_MMA_SYNC = 1   # ORION_PLAN_MMA_SYNC: legacy mma.sync split kernel
+PLAN_MMA_SYNC = 1        # ORION_PLAN_MMA_SYNC: legacy mma.sync split kernel
+PLAN_ROWS_ON_LANES = 2   # ORION_PLAN_ROWS_ON_LANES: rows-on-lanes tcgen05 split kernel
 
 
 def expand_plan(hq, hkv, d, page, seg_offsets, segs, own_len=None, chunk_tokens=0, num_sms=0,

@@ -308,8 +308,13 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
     return fail(ORION_ERR_INVALID_ARG, "bad plan arguments");
   const int32_t Hq = shape->num_q_heads, Hkv = shape->num_kv_heads, G = Hq / Hkv;
   int32_t chunk = (opts && opts->chunk_tokens > 0) ? opts->chunk_tokens : 512;
-  const int32_t variant = (opts && (opts->flags & ORION_PLAN_MMA_SYNC)) ? kVariantMmaSync : kVariantTC;
-  const int32_t rows_per_item = variant == kVariantTC ? kRowsPerItemTC : kRowsPerItemMMA;
+  const int32_t flags = opts ? opts->flags : 0;
+  const int32_t variant = (flags & ORION_PLAN_MMA_SYNC) ? kVariantMmaSync
+                          : ((flags & ORION_PLAN_ROWS_ON_LANES) || shape->head_dim != 128) ? kVariantTC
+                                                                                         : kVariantTCT;
+  const int32_t rows_per_item = variant == kVariantTC    ? kRowsPerItemTC
+                                : variant == kVariantTCT ? kRowsPerItemTCT
+                                                         : kRowsPerItemMMA;
   chunk = std::max(kTileTokens, (chunk + kTileTokens - 1) / kTileTokens * kTileTokens);
 
   // 1. Group bound segments by page run.

@@ -395,7 +395,7 @@ template <int D>
 orion_status launch_split(const PlanHeader* h, const char* dplan, const void* q, const void* k,
                           const void* v, int32_t num_pages, const int32_t* page_table,
                           const int32_t* own_len, void* ws, cudaStream_t st) {
-  if (h->variant == kVariantTC) {
+  if (h->variant == kVariantTC || h->variant == kVariantTCT) {
     TcArgs t;
     t.items = reinterpret_cast<const WorkItem*>(dplan + h->items_off);
     t.readers = reinterpret_cast<const int32_t*>(dplan + h->readers_off);
@@ -410,6 +410,10 @@ orion_status launch_split(const PlanHeader* h, const char* dplan, const void* q,
     t.group = h->group;
     t.page_shift = log2i(h->page_size);
     t.scale_log2 = h->sm_scale * kLog2e;
+    if (h->variant == kVariantTCT) {
+      if (D != 128) return fail(ORION_ERR_UNSUPPORTED, "transposed split kernel needs head_dim 128");
+      return launch_split_tct(h, t, k, v, num_pages, st);
+    }
     return launch_split_tc<D>(h, t, k, v, num_pages, st);
   }
   static std::once_flag once;

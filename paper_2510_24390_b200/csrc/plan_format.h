@@ -16,7 +16,8 @@ constexpr int32_t kPlanVersion = 1;
 constexpr int kRowsPerItemTC = 128;  // query rows per work item, tcgen05 kernel (MMA M = 128)
 constexpr int kRowsPerItemMMA = 64;  // query rows per work item, mma.sync kernel (4 warps x m16)
 constexpr int kRowsPerItem = kRowsPerItemMMA;  // smem sizing of the mma.sync kernel
-enum : int32_t { kVariantTC = 0, kVariantMmaSync = 1 };
+constexpr int kRowsPerItemTCT = 64;  // query rows per work item, transposed tcgen05 kernel (MMA N)
+enum : int32_t { kVariantTC = 0, kVariantMmaSync = 1, kVariantTCT = 2 };
 constexpr int kTileTokens = 64;    // tokens per pipeline stage in the split kernel
 
 struct PlanHeader {
@@ -27,7 +28,8 @@ struct PlanHeader {
   int64_t plan_bytes, workspace_bytes, acc_bytes;                // acc_bytes = part_ml offset
   int64_t n_pieces, unique_tokens, logical_tokens;
   float sm_scale;
-  int32_t variant;  // kVariantTC (tcgen05, default) or kVariantMmaSync (opts.flags & 1)
+  int32_t variant;  // kVariantTCT (default, d = 128), kVariantTC (d = 64 or ORION_PLAN_ROWS_ON_LANES),
+                    // kVariantMmaSync (ORION_PLAN_MMA_SYNC)
   int32_t pad_[2];
 };
 static_assert(sizeof(PlanHeader) % 16 == 0, "header must keep 16-byte alignment");

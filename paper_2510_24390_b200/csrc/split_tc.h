@@ -28,4 +28,7 @@ template <int D>
 orion_status launch_split_tc(const PlanHeader* h, const TcArgs& a, const void* k, const void* v,
                              int32_t num_pages, cudaStream_t st);
 
+orion_status launch_split_tct(const PlanHeader* h, const TcArgs& a, const void* k, const void* v,
+                              int32_t num_pages, cudaStream_t st);
+
 }  // namespace orion

@@ -1,0 +1,751 @@
+// split_tct.cu — K2 split attention, transposed ("swap-AB") tcgen05 formulation (default, d=128).
+//
+// Decode attention has few query rows per shared piece (G heads x the piece's readers: 4..64 in
+// the paper's workloads) but long token runs.  Putting query rows on the MMA M dimension (the
+// classic orientation, split_tc.cu) leaves most TMEM lanes / softmax threads idle and funnels the
+// exponentials of a small item through one SM sub-partition.  Here tokens are the M dimension:
+//
+//   S^T[128 tok x N]  = K_tile[128 x d] . Q^T            (A = K smem K-major, B = Q smem K-major)
+//   O^T[d x N]       += V_tile^T[d x 128] . P^T[128 x N] (A = V smem MN-major, B = P^T smem MN-major)
+//   L^T[128 x N]     += 1[128 x 128] . P^T               (A = ones in TMEM): every lane gets the
+//                                                         row sums l of exactly the bf16 P used
+// with N = 16/32/64 (query rows, padded).  One softmax thread per token: its N scores, a
+// block-wide "did any running max grow by > 2^8" vote (bar.red.or), and only on that rare path a
+// column max (redux.sync.max.f32 + smem).  The exponentials of a 128-token tile are spread over
+// all four sub-partitions whatever the row count.
+//
+// Roles (384 threads, one persistent CTA per SM): warp 0 TMEM alloc; warp 2 TMA producer (K ring
+// 2 x 32 KB released at QK completion, V ring 3 x 32 KB released at PV completion); warp 3 MMA
+// issuer (QK two tiles ahead of PV); warps 4-7 / 8-11 softmax warpgroups 0/1 owning even / odd
+// tiles with their own O^T / L^T accumulators, merged by warpgroup 0 at item end into one fp32
+// partial (m in log2 units, l, acc) per query row, the format combine_kernel consumes.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "../../include/orion.h"
+#include "plan_format.h"
+#include "split_tc.h"
+#include "tmem_ops.h"
+
+namespace orion {
+namespace tct {
+
+constexpr int D = 128;
+constexpr int kTok = 128;                 // tokens per tile = MMA M of S^T
+constexpr int kBox = 16;                  // token rows of a partial-tile TMA box
+constexpr int kSK = 2, kSV = 3;           // K / V ring depth (32 KB stages)
+constexpr int kThreads = 384;
+constexpr int kWarpAlloc = 0, kWarpSched = 1, kWarpTMA = 2, kWarpMMA = 3;
+// TMEM columns
+__device__ __forceinline__ uint32_t colS(uint32_t p) { return p * 64; }
+__device__ __forceinline__ uint32_t colO(uint32_t p) { return 128 + p * 64; }
+__device__ __forceinline__ uint32_t colL(uint32_t p) { return 256 + p * 64; }
+constexpr uint32_t kColOnes = 384;        // 64 columns: 128 x 128 bf16 ones (A operand of L)
+
+struct L {
+  static constexpr int QB = 64 * D * 2;          // 16 KB: [2 halves][64 rows][128 B]
+  static constexpr int HALF_Q = 64 * 128;
+  static constexpr int KVB = kTok * D * 2;       // 32 KB: [2 halves][128 tokens][128 B]
+  static constexpr int HALF_KV = kTok * 128;
+  static constexpr int PB = kTok * 128;          // 16 KB: P^T [128 tokens][64 rows] bf16, MN-major
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = 2 * QB;
+  static constexpr int OFF_V = OFF_K + kSK * KVB;
+  static constexpr int OFF_P = OFF_V + kSV * KVB;
+  static constexpr int OFF_M = OFF_P + 2 * PB;   // running max m per column: [wg 2][item parity 2][64]
+  static constexpr int OFF_SH = OFF_M + 2 * 2 * 64 * 4;   // growth-path shifts: [wg 2][64]
+  static constexpr int OFF_SCHED = OFF_SH + 2 * 64 * 4;   // item schedule ring: 8 x 64 B
+  static constexpr int OFF_BAR = OFF_SCHED + 8 * 64;
+  static constexpr int N_BAR = 2 * kSK + 2 * kSV + 2 + 2 + 2 + 2 + 2 + 2 + 1 + 2 * 8;
+  static constexpr int BYTES = OFF_BAR + N_BAR * 8 + 16;
+};
+static_assert(L::BYTES <= 232448, "shared memory budget");
+
+// ------------------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(c));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  const uint32_t a = smem_u32(b);
+  for (uint32_t spin = 0;; ++spin) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (spin > (1u << 22)) __trap();   // protocol bug: fail loudly instead of hanging
+  }
+}
+#ifdef ORION_TC_TRACE
+#define TRACE_DECL unsigned long long tr_[12] = {0}; const unsigned long long tr_t0 = clock64();
+#define TW(slot, stmt) do { const unsigned long long t_ = clock64(); stmt; tr_[slot] += clock64() - t_; } while (0)
+#define TRACE_DUMP(role) do { if (blockIdx.x < 2 && (threadIdx.x & 31) == 0) printf( \
+    "TRACE blk %d warp %2d %-8s tot %llu | %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu\n", blockIdx.x, \
+    threadIdx.x >> 5, role, clock64() - tr_t0, tr_[0], tr_[1], tr_[2], tr_[3], tr_[4], tr_[5], tr_[6], tr_[7], \
+    tr_[8], tr_[9]); } while (0)
+#else
+#define TRACE_DECL
+#define TW(slot, stmt) stmt
+#define TRACE_DUMP(role) do {} while (0)
+#endif
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n .reg .b32 rx;\n .reg .pred px;\n elect.sync rx|px, %1;\n @px mov.s32 %0, 1;\n}\n"
+               : "+r"(pred)
+               : "r"(0xFFFFFFFFu));
+  return pred != 0;
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(b))
+               : "memory");
+}
+__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+               "l"(a), "l"(b), "r"(id), "r"(acc)
+               : "memory");
+}
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+               "r"(a), "l"(b), "r"(id), "r"(acc)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0));
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ float warp_max(float v) {
+  float r;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;\n" : "=f"(r) : "f"(v));
+  return r;
+}
+// Block-level OR over the 128 threads of one softmax warpgroup (named barrier `id`).
+__device__ __forceinline__ bool wg_any(bool v, int id) {
+  int r;
+  asm volatile("{\n .reg .pred a, b;\n setp.ne.s32 a, %1, 0;\n barrier.red.or.pred b, %2, 128, a;\n selp.s32 %0, 1, 0, b;\n}\n"
+               : "=r"(r)
+               : "r"(v ? 1 : 0), "r"(id)
+               : "memory");
+  return r != 0;
+}
+__device__ __forceinline__ void wg_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
+
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(2) << 61;
+  return d;
+}
+__device__ __forceinline__ uint32_t idesc(int n, bool a_mn, bool b_mn) {   // M = 128, bf16 -> fp32
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
+}
+
+struct Geom {
+  int32_t base, end, ntiles, npad;
+};
+__device__ __forceinline__ Geom geom(const WorkItem& w, const int32_t* own_len) {
+  Geom g;
+  g.end = w.t1;
+  if (w.dyn >= 0) g.end = min(g.end, __ldg(own_len + w.dyn));
+  g.base = w.t0 & ~(kTok - 1);
+  g.ntiles = g.end > w.t0 ? (g.end - g.base + kTok - 1) / kTok : 0;
+  g.npad = w.n_rows <= 16 ? 16 : (w.n_rows <= 32 ? 32 : 64);
+  return g;
+}
+__device__ __forceinline__ int next_nonempty(const TcArgs& a, int it) {
+  while (it < a.n_items && geom(a.items[it], a.own_len).ntiles == 0) it += gridDim.x;
+  return it;
+}
+
+// One softmax tile for a warpgroup: thread t owns token row t of S^T (N = padded query rows).
+// Writes P^T row t; on the rare growth path (first tile of an item, or a running max grown by more
+// than 2^8) it moves the per-column reference m (smem) and rescales O^T / L^T of this warpgroup.
+template <int N>
+__device__ __forceinline__ void softmax_tile(uint8_t* smem, uint32_t tmem, uint32_t lane_base, int p, int t,
+                                             int tb, const WorkItem& w, const Geom& g, float* mrow,
+                                             float* shs, bool had, float scale_log2, uint32_t vstage,
+                                             uint64_t* s_free) {
+  uint32_t s[N];
+  if constexpr (N == 16) tmem_ld32x16(tmem + lane_base + colS(p), s);
+  if constexpr (N == 32) tmem_ld32x32(tmem + lane_base + colS(p), s);
+  if constexpr (N == 64) tmem_ld32x64(tmem + lane_base + colS(p), s);
+  tc_wait_ld();
+  tc_fence_before();
+  mbar_arrive(s_free + p);                           // QK(j+2) may overwrite S^T[p]
+  const int pos = tb + t;
+  const bool valid = pos >= w.t0 && pos < g.end;
+  // d = s * scale - mb (log2 domain, relative to the running reference; mb = 0 while unset)
+  bool exceed = false;
+#pragma unroll
+  for (int c4 = 0; c4 < N; c4 += 4) {
+    const float4 m4 = *reinterpret_cast<const float4*>(mrow + c4);
+    const float mm[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float mb = mm[e] == -INFINITY ? 0.f : mm[e];
+      const float d = valid ? fmaf(__uint_as_float(s[c4 + e]), scale_log2, -mb) : -INFINITY;
+      s[c4 + e] = __float_as_uint(d);
+      exceed |= valid && (mm[e] == -INFINITY || d > 8.f);
+    }
+  }
+  uint8_t* pbuf = smem + L::OFF_P + p * L::PB;      // free: PV(j-2) is complete
+  const bool grow = wg_any(exceed, 2 + p);
+  if (grow) {
+    // column max of d over the 128 tokens: warp redux, then across the 4 warps via smem (the
+    // P^T buffer is scratch until P^T is written below)
+    float* red = reinterpret_cast<float*>(pbuf);
+    const int wq = t >> 5, ln = t & 31;
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      const float wm = warp_max(__uint_as_float(s[c]));
+      if (ln == (c & 31)) red[wq * 64 + c] = wm;
+    }
+    wg_sync(2 + p, 128);
+    if (t < N) {                                     // column owner: new reference and shift
+      const float cm = fmaxf(fmaxf(red[t], red[64 + t]), fmaxf(red[128 + t], red[192 + t]));
+      const float mo = mrow[t];
+      const bool gc = cm > -INFINITY && (mo == -INFINITY || cm > 8.f);
+      const float mb = mo == -INFINITY ? 0.f : mo;
+      shs[t] = gc ? cm : 0.f;
+      if (gc) mrow[t] = mb + cm;
+    }
+    wg_sync(2 + p, 128);
+    if (had) {   // O^T and L^T columns of this warpgroup follow the new reference: * 2^-shift
+      tc_fence_after();
+#pragma unroll
+      for (int cb = 0; cb < N; cb += 16) {
+        uint32_t o[16], l16[16];
+        tmem_ld32x16(tmem + lane_base + colO(p) + cb, o);
+        tmem_ld32x16(tmem + lane_base + colL(p) + cb, l16);
+        tc_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const float al = ex2(-shs[cb + c]);
+          o[c] = __float_as_uint(__uint_as_float(o[c]) * al);
+          l16[c] = __float_as_uint(__uint_as_float(l16[c]) * al);
+        }
+        tmem_st32x16(tmem + lane_base + colO(p) + cb, o);
+        tmem_st32x16(tmem + lane_base + colL(p) + cb, l16);
+      }
+      tc_wait_st();
+    }
+  }
+  // P^T row t (MN-major, 128B swizzle): p = 2^(d - shift), rounded to bf16
+#pragma unroll
+  for (int cc = 0; cc < N / 8; ++cc) {
+    float sh[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) sh[e] = grow ? shs[cc * 8 + e] : 0.f;
+    uint4 v;
+    v.x = pack_bf16(ex2(__uint_as_float(s[cc * 8 + 0]) - sh[0]), ex2(__uint_as_float(s[cc * 8 + 1]) - sh[1]));
+    v.y = pack_bf16(ex2(__uint_as_float(s[cc * 8 + 2]) - sh[2]), ex2(__uint_as_float(s[cc * 8 + 3]) - sh[3]));
+    v.z = pack_bf16(ex2(__uint_as_float(s[cc * 8 + 4]) - sh[4]), ex2(__uint_as_float(s[cc * 8 + 5]) - sh[5]));
+    v.w = pack_bf16(ex2(__uint_as_float(s[cc * 8 + 6]) - sh[6]), ex2(__uint_as_float(s[cc * 8 + 7]) - sh[7]));
+    if (cc == 0 && grow) wg_sync(2 + p, 128);       // all red reads done before P^T overwrites them
+    *reinterpret_cast<uint4*>(pbuf + t * 128 + ((cc ^ (t & 7)) << 4)) = v;
+  }
+  if (!valid) {                                      // V rows outside [t0, end): exact zeros
+    uint8_t* vrow = smem + L::OFF_V + vstage * L::KVB + t * 128;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint4* p4 = reinterpret_cast<uint4*>(vrow + h * L::HALF_KV);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) p4[c] = make_uint4(0, 0, 0, 0);
+    }
+  }
+}
+
+// Per-CTA item schedule entry, produced by the scheduler warp (warp 1) and consumed in order by
+// the TMA, MMA and both softmax warpgroups (removes the dependent global loads of the item
+// descriptors from every role's critical path).
+struct Sched {
+  int32_t valid, it, pt_off, t0, end, base, ntiles, npad, kv_head, n_rows, slot0, pad[5];
+};
+constexpr int kSched = 8;
+constexpr uint32_t kSchedConsumers = 1 + 1 + 128 + 128;   // TMA lane, MMA lane, WG0, WG1 threads
+
+__device__ __forceinline__ Sched read_sched(const Sched* ring, uint64_t* full, uint64_t* empty, uint32_t k,
+                                            bool arrive) {
+  mbar_wait(full + (k % kSched), (k / kSched) & 1);
+  const Sched e = ring[k % kSched];
+  if (arrive) mbar_arrive(empty + (k % kSched));
+  return e;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    split_tct_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                     const __grid_constant__ CUtensorMap tmK16, const __grid_constant__ CUtensorMap tmV16,
+                     const TcArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if (smem_u32(smem) & 1023) __trap();               // 128B-swizzle atoms need 1 KB alignment
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint64_t* k_full = bars;
+  uint64_t* k_empty = k_full + kSK;
+  uint64_t* v_full = k_empty + kSK;
+  uint64_t* v_empty = v_full + kSV;
+  uint64_t* s_full = v_empty + kSV;
+  uint64_t* s_free = s_full + 2;
+  uint64_t* p_full = s_free + 2;
+  uint64_t* pv_done = p_full + 2;
+  uint64_t* q_full = pv_done + 2;
+  uint64_t* q_empty = q_full + 2;
+  uint64_t* o_free = q_empty + 2;
+  uint64_t* sch_full = o_free + 1;
+  uint64_t* sch_empty = sch_full + kSched;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sch_empty + kSched);
+  float* mall = reinterpret_cast<float*>(smem + L::OFF_M);
+  Sched* ring = reinterpret_cast<Sched*>(smem + L::OFF_SCHED);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < kSK; ++s) { mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1); }
+    for (int s = 0; s < kSV; ++s) { mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1); }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(s_full + b, 1); mbar_init(s_free + b, 128); mbar_init(p_full + b, 128);
+      mbar_init(pv_done + b, 1); mbar_init(q_full + b, 1); mbar_init(q_empty + b, 1);
+    }
+    mbar_init(o_free, 256);
+    for (int b = 0; b < kSched; ++b) { mbar_init(sch_full + b, 1); mbar_init(sch_empty + b, kSchedConsumers); }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmK)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmV)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmK16)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmV16)) : "memory");
+  }
+  if (warp == kWarpAlloc) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int n_items = a.n_items;
+  if (warp >= 4 && warp < 8) {                      // ones (bf16 pairs) for the l MMA: 64 columns
+    uint32_t one[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) one[c] = 0x3F803F80u;
+    const uint32_t lb = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    tmem_st32x32(tmem + lb + kColOnes, one);
+    tmem_st32x32(tmem + lb + kColOnes + 32, one);
+    tc_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  TRACE_DECL
+  if (warp == kWarpSched) {
+    // ------------------------------------------------------------------ scheduler + Q gather
+    uint32_t k = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const WorkItem w = a.items[it];
+      const Geom g = geom(w, a.own_len);
+      if (g.ntiles == 0) {                           // empty (dyn end <= t0): neutral partial
+        for (int i = lane; i < w.n_rows * D / 4; i += 32)
+          reinterpret_cast<float4*>(a.part_acc + static_cast<size_t>(w.slot0) * D)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int r = lane; r < w.n_rows; r += 32) a.part_ml[w.slot0 + r] = make_float2(-INFINITY, 0.f);
+        continue;
+      }
+      TW(0, mbar_wait(sch_empty + (k % kSched), ((k / kSched) & 1) ^ 1));
+      if (lane == 0) {
+        Sched e;
+        e.valid = 1; e.it = it; e.pt_off = w.pt_off; e.t0 = w.t0; e.end = g.end; e.base = g.base;
+        e.ntiles = g.ntiles; e.npad = g.npad; e.kv_head = w.kv_head; e.n_rows = w.n_rows; e.slot0 = w.slot0;
+        ring[k % kSched] = e;
+        mbar_arrive(sch_full + (k % kSched));
+      }
+      // Q rows of item k -> Q buffer k & 1, once item k-2's QKs have completed
+      if (k >= 2) TW(1, mbar_wait(q_empty + (k & 1), ((k >> 1) - 1) & 1));
+      uint8_t* qb = smem + L::OFF_Q + (k & 1) * L::QB;
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {
+        const int r = lane + rr * 32;
+        const bool ok = r < w.n_rows;
+        const __nv_bfloat16* src = a.q;
+        if (ok) {
+          const int row = w.row_begin + r;
+          const int b = __ldg(a.readers + w.readers_off + row / a.group);
+          const int hq = w.kv_head * a.group + row % a.group;
+          src = a.q + (static_cast<size_t>(b) * a.hq + hq) * D;
+        }
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          cp_async16(smem_u32(qb + (c >> 3) * L::HALF_Q + r * 128 + (((c & 7) ^ (r & 7)) << 4)),
+                     ok ? static_cast<const void*>(src + c * 8) : static_cast<const void*>(a.q), ok);
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(q_full + (k & 1));
+      ++k;
+    }
+    TW(0, mbar_wait(sch_empty + (k % kSched), ((k / kSched) & 1) ^ 1));
+    if (lane == 0) {                                 // terminator
+      ring[k % kSched].valid = 0;
+      mbar_arrive(sch_full + (k % kSched));
+    }
+  } else if (warp == kWarpTMA) {
+    // ------------------------------------------------------------------ TMA producer
+    uint32_t j = 0;
+    const int pmask = (1 << a.page_shift) - 1;
+    const int big = min(64, 1 << a.page_shift);     // rows of a full-tile box (<= one page)
+    for (uint32_t k = 0;; ++k) {
+      const Sched e = read_sched(ring, sch_full, sch_empty, k, lane == 0);
+      if (!e.valid) break;
+      for (int tb0 = 0; tb0 < e.ntiles; tb0 += 32) {
+        int brow[8];
+        int nbox = 0, first_off = 0, full = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) brow[b] = 0;
+        if (tb0 + lane < e.ntiles) {
+          const int a0 = e.base + (tb0 + lane) * kTok;
+          const int lo = max(a0, e.t0), hi = min(a0 + kTok, e.end);
+          full = (lo == a0 && hi == a0 + kTok);
+          int pos0, step;
+          if (full) { nbox = kTok / big; pos0 = a0; step = big; }
+          else { pos0 = lo & ~(kBox - 1); nbox = (hi - pos0 + kBox - 1) / kBox; step = kBox; first_off = pos0 - a0; }
+#pragma unroll
+          for (int b = 0; b < 8; ++b)
+            if (b < nbox) {
+              const int pos = pos0 + b * step;
+              const int page = __ldg(a.page_table + e.pt_off + (pos >> a.page_shift));
+              brow[b] = ((page * a.hkv + e.kv_head) << a.page_shift) + (pos & pmask);
+            }
+        }
+        const int tend = min(e.ntiles, tb0 + 32);
+        for (int t = tb0; t < tend; ++t, ++j) {
+          const int src = t - tb0;
+          const int tn = __shfl_sync(0xffffffffu, nbox, src);
+          const int tf = __shfl_sync(0xffffffffu, full, src);
+          const int to = __shfl_sync(0xffffffffu, first_off, src);
+          int rr[8];
+#pragma unroll
+          for (int b = 0; b < 8; ++b) rr[b] = __shfl_sync(0xffffffffu, brow[b], src);
+          const int sk = j % kSK, sv = j % kSV;
+          const int rpb = tf ? big : kBox;
+          const uint32_t bytes = static_cast<uint32_t>(tn * rpb * 128 * 2);
+          const CUtensorMap* mk = tf ? &tmK : &tmK16;
+          const CUtensorMap* mv = tf ? &tmV : &tmV16;
+          TW(0, mbar_wait(k_empty + sk, ((j / kSK) & 1) ^ 1));
+          if (elect_one()) {
+            mbar_expect_tx(k_full + sk, bytes);
+            const uint32_t dk = smem_u32(smem + L::OFF_K + sk * L::KVB);
+#pragma unroll
+            for (int b = 0; b < 8; ++b)
+              if (b < tn) {
+                const uint32_t roff = static_cast<uint32_t>(to + b * rpb) * 128;
+                tma_load_2d(dk + roff, mk, 0, rr[b], k_full + sk);
+                tma_load_2d(dk + L::HALF_KV + roff, mk, 64, rr[b], k_full + sk);
+              }
+          }
+          __syncwarp();
+          TW(1, mbar_wait(v_empty + sv, ((j / kSV) & 1) ^ 1));
+          if (elect_one()) {
+            mbar_expect_tx(v_full + sv, bytes);
+            const uint32_t dv = smem_u32(smem + L::OFF_V + sv * L::KVB);
+#pragma unroll
+            for (int b = 0; b < 8; ++b)
+              if (b < tn) {
+                const uint32_t roff = static_cast<uint32_t>(to + b * rpb) * 128;
+                tma_load_2d(dv + roff, mv, 0, rr[b], v_full + sv);
+                tma_load_2d(dv + L::HALF_KV + roff, mv, 64, rr[b], v_full + sv);
+              }
+          }
+          __syncwarp();
+        }
+      }
+    }
+    TRACE_DUMP("producer");
+  } else if (warp == kWarpMMA) {
+    // ------------------------------------------------------------------ MMA issuer
+    // Two cursors over the flattened (item, tile) sequence: QK two tiles ahead of PV, never into
+    // item k+2 before every PV of item k is issued (item k+2's Q reuses item k's buffer).
+    const uint64_t dq0 = sw128_desc(smem_u32(smem + L::OFF_Q), 16, 1024);
+    const uint64_t dk0 = sw128_desc(smem_u32(smem + L::OFF_K), 16, 1024);
+    const uint64_t dv0 = sw128_desc(smem_u32(smem + L::OFF_V), L::HALF_KV, 1024);   // MN-major A
+    const uint64_t dp0 = sw128_desc(smem_u32(smem + L::OFF_P), L::HALF_KV, 1024);   // MN-major B
+    // (ntiles, npad) of items k % 3: the QK cursor may have read item kv + 2's entry while the PV
+    // cursor is still on item kv.
+    int nt0 = 0, nt1 = 0, nt2 = 0, np0 = 16, np1 = 16, np2 = 16;
+    auto nt_of = [&](uint32_t k) { const uint32_t m = k % 3; return m == 0 ? nt0 : (m == 1 ? nt1 : nt2); };
+    auto np_of = [&](uint32_t k) { const uint32_t m = k % 3; return m == 0 ? np0 : (m == 1 ? np1 : np2); };
+    auto set_of = [&](uint32_t k, int nt, int np) {
+      const uint32_t m = k % 3;
+      if (m == 0) { nt0 = nt; np0 = np; } else if (m == 1) { nt1 = nt; np1 = np; } else { nt2 = nt; np2 = np; }
+    };
+    uint32_t kq = 0, tq = 0, jq = 0;                // QK cursor
+    bool q_live;
+    {
+      const Sched e = read_sched(ring, sch_full, sch_empty, 0, lane == 0);
+      q_live = e.valid;
+      set_of(0, e.ntiles, e.npad);
+    }
+    uint32_t kv = 0, tv = 0, jv = 0;                // PV cursor
+    while (true) {
+      const bool v_live = kv < kq || (kv == kq && q_live);
+      if (!v_live) break;
+      while (q_live && jq <= jv + 2 && kq <= kv + 1) {
+        // ---- S^T(jq) = K(jq) Q^T
+        const uint32_t j = jq;
+        if (tq == 0) TW(1, mbar_wait(q_full + (kq & 1), (kq >> 1) & 1));
+        const int s = j % kSK;
+        TW(2, mbar_wait(k_full + s, (j / kSK) & 1));
+        if (j >= 2) TW(3, mbar_wait(s_free + (j & 1), ((j - 2) >> 1) & 1));
+        tc_fence_after();
+        const int ntq = nt_of(kq);
+        const int npq = np_of(kq);
+        const uint64_t dq = dq0 + static_cast<uint64_t>(((kq & 1) * L::QB) >> 4);
+        const uint64_t dk = dk0 + static_cast<uint64_t>((s * L::KVB) >> 4);
+        const uint32_t id = idesc(npq, false, false);
+        if (elect_one()) {
+#pragma unroll
+          for (int ks = 0; ks < D / 16; ++ks) {
+            const uint64_t ok = static_cast<uint64_t>(((ks >> 2) * L::HALF_KV + (ks & 3) * 32) >> 4);
+            const uint64_t oq = static_cast<uint64_t>(((ks >> 2) * L::HALF_Q + (ks & 3) * 32) >> 4);
+            mma_ss(tmem + colS(j & 1), dk + ok, dq + oq, id, ks > 0);
+          }
+          tc_commit(s_full + (j & 1));
+          tc_commit(k_empty + s);
+          if (static_cast<int>(tq) + 1 == ntq) tc_commit(q_empty + (kq & 1));   // item's last QK
+        }
+        __syncwarp();
+        ++jq;
+        if (static_cast<int>(++tq) == ntq) {
+          tq = 0;
+          ++kq;
+          const Sched e = read_sched(ring, sch_full, sch_empty, kq, lane == 0);
+          q_live = e.valid;
+          set_of(kq, e.ntiles, e.npad);
+        }
+      }
+      // ---- O^T += V(jv)^T P^T(jv);  L^T += 1 P^T(jv)
+      const uint32_t j = jv;
+      const int s = j % kSV;
+      const int ntv = nt_of(kv);
+      const int npv = np_of(kv);
+      TW(6, mbar_wait(v_full + s, (j / kSV) & 1));
+      TW(4, mbar_wait(p_full + (j & 1), (j >> 1) & 1));
+      if (tv == 0 && kv > 0) TW(5, mbar_wait(o_free, (kv - 1) & 1));
+      tc_fence_after();
+      const uint64_t dv = dv0 + static_cast<uint64_t>((s * L::KVB) >> 4);
+      const uint64_t dp = dp0 + static_cast<uint64_t>(((j & 1) * L::PB) >> 4);
+      const uint32_t id_pv = idesc(npv, true, true);
+      const uint32_t id_l = idesc(npv, false, true);
+      const bool first = tv < 2;
+      if (elect_one()) {
+#pragma unroll
+        for (int kt = 0; kt < kTok / 16; ++kt) {
+          const uint64_t o = static_cast<uint64_t>((kt * 16 * 128) >> 4);
+          const uint32_t acc = (!first || kt > 0) ? 1u : 0u;
+          mma_ss(tmem + colO(j & 1), dv + o, dp + o, id_pv, acc);
+          mma_ts(tmem + colL(j & 1), tmem + kColOnes + kt * 8, dp + o, id_l, acc);
+        }
+        tc_commit(pv_done + (j & 1));
+        tc_commit(v_empty + s);
+      }
+      __syncwarp();
+      ++jv;
+      if (static_cast<int>(++tv) == ntv) { tv = 0; ++kv; }
+    }
+    TRACE_DUMP("mma");
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------------ softmax / epilogue
+    const int p = (warp - 4) >> 2;                  // warpgroup: tiles with j & 1 == p
+    const int t = tid - 128 - p * 128;              // token row of S^T / d lane of O^T
+    const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    uint32_t j = 0;
+    for (uint32_t k = 0;; ++k) {
+      const Sched e = read_sched(ring, sch_full, sch_empty, k, true);
+      if (!e.valid) break;
+      WorkItem w;
+      w.t0 = e.t0;
+      Geom g;
+      g.base = e.base; g.end = e.end; g.ntiles = e.ntiles; g.npad = e.npad;
+      float* mrow = mall + (p * 2 + (k & 1)) * 64;
+      if (t < 64) mrow[t] = -INFINITY;
+      wg_sync(2 + p, 128);
+      bool had = false;
+      uint32_t jl = 0;
+      const uint32_t j0 = j;
+      for (int tt = 0; tt < g.ntiles; ++tt, ++j) {
+        if ((j & 1) != static_cast<uint32_t>(p)) continue;
+        const int tb = g.base + tt * kTok;
+        TW(6, mbar_wait(s_full + p, (j >> 1) & 1));
+        tc_fence_after();
+        if (j >= 2) TW(7, mbar_wait(pv_done + p, ((j - 2) >> 1) & 1));   // P^T[p] free, O^T[p] current
+#ifdef ORION_TC_TRACE
+        const unsigned long long tsm = clock64();
+#endif
+        float* shs = reinterpret_cast<float*>(smem + L::OFF_SH) + p * 64;
+        if (g.npad == 16) softmax_tile<16>(smem, tmem, lane_base, p, t, tb, w, g, mrow, shs, had, a.scale_log2, j % kSV, s_free);
+        else if (g.npad == 32) softmax_tile<32>(smem, tmem, lane_base, p, t, tb, w, g, mrow, shs, had, a.scale_log2, j % kSV, s_free);
+        else softmax_tile<64>(smem, tmem, lane_base, p, t, tb, w, g, mrow, shs, had, a.scale_log2, j % kSV, s_free);
+        fence_proxy_async();
+        tc_fence_before();
+        mbar_arrive(p_full + p);
+#ifdef ORION_TC_TRACE
+        tr_[1] += clock64() - tsm;
+#endif
+        had = true;
+        jl = j;
+      }
+#ifdef ORION_TC_TRACE
+      const unsigned long long tep = clock64();
+#endif
+      if (had) {
+        TW(8, mbar_wait(pv_done + p, (jl >> 1) & 1));
+        tc_fence_after();
+      }
+      TW(9, wg_sync(1, 256));                        // both warpgroups' accumulators final
+      // ---- merge O^T_0 / O^T_1 into one partial per query row; warpgroup p takes the 8-column
+      // chunks cb with (cb / 8) % 2 == p
+      {
+        const float* mA = mall + (0 * 2 + (k & 1)) * 64;
+        const float* mB = mall + (1 * 2 + (k & 1)) * 64;
+        const bool hadA = g.ntiles > 1 || (j0 & 1) == 0;
+        const bool hadB = g.ntiles > 1 || (j0 & 1) == 1;
+        const int n = e.n_rows;
+        float* dst = a.part_acc + static_cast<size_t>(e.slot0) * D + t;
+#pragma unroll 1
+        for (int cb = p * 8; cb < g.npad; cb += 16) {
+          uint32_t oa[8], ob[8], la[8], lb[8];
+          if (hadA) { tmem_ld32x8(tmem + lane_base + colO(0) + cb, oa); tmem_ld32x8(tmem + lane_base + colL(0) + cb, la); }
+          if (hadB) { tmem_ld32x8(tmem + lane_base + colO(1) + cb, ob); tmem_ld32x8(tmem + lane_base + colL(1) + cb, lb); }
+          tc_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const int col = cb + c;
+            if (col < n) {
+              const float ma = hadA ? mA[col] : -INFINITY, mb = hadB ? mB[col] : -INFINITY;
+              const float M = fmaxf(ma, mb);
+              const float Mb = M == -INFINITY ? 0.f : M;
+              const float fa = hadA ? ex2(ma - Mb) : 0.f, fb = hadB ? ex2(mb - Mb) : 0.f;
+              const float ov = (hadA ? fa * __uint_as_float(oa[c]) : 0.f) + (hadB ? fb * __uint_as_float(ob[c]) : 0.f);
+              dst[static_cast<size_t>(col) * D] = ov;
+              if (t == col) {
+                const float lv = (hadA ? fa * __uint_as_float(la[c]) : 0.f) + (hadB ? fb * __uint_as_float(lb[c]) : 0.f);
+                a.part_ml[e.slot0 + col] = make_float2(M, lv);
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(o_free);
+#ifdef ORION_TC_TRACE
+      tr_[2] += clock64() - tep;
+#endif
+    }
+    TRACE_DUMP("softmax");
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kWarpAlloc) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+  }
+}
+
+}  // namespace tct
+
+namespace {
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn get_encode_t() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+bool make_map_t(CUtensorMap* m, const void* base, int64_t rows, int box_rows) {
+  EncodeTiledFn enc = get_encode_t();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(tct::D), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(tct::D) * 2};
+  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace
+
+orion_status launch_split_tct(const PlanHeader* h, const TcArgs& a, const void* k, const void* v,
+                              int32_t num_pages, cudaStream_t st) {
+  static int num_sms = 0;
+  static cudaError_t attr_err = cudaSuccess;
+  static bool init = false;
+  if (!init) {
+    init = true;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    attr_err = cudaFuncSetAttribute(tct::split_tct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tct::L::BYTES);
+  }
+  if (attr_err != cudaSuccess)
+    return fail(ORION_ERR_CUDA, "cudaFuncSetAttribute(split_tct): %s", cudaGetErrorString(attr_err));
+  CUtensorMap mk, mv, mk16, mv16;
+  const int64_t rows = static_cast<int64_t>(num_pages) * h->num_kv_heads * h->page_size;
+  const int big = std::min(64, h->page_size);
+  if (!make_map_t(&mk, k, rows, big) || !make_map_t(&mv, v, rows, big) || !make_map_t(&mk16, k, rows, tct::kBox) ||
+      !make_map_t(&mv16, v, rows, tct::kBox))
+    return fail(ORION_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  const int grid = std::min<int>(h->n_items, num_sms > 0 ? num_sms : 148);
+  tct::split_tct_kernel<<<grid, tct::kThreads, tct::L::BYTES, st>>>(mk, mv, mk16, mv16, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ORION_ERR_CUDA, "split_tct_kernel: %s", cudaGetErrorString(e));
+  return ORION_OK;
+}
+
+}  // namespace orion
