@@ -25,6 +25,8 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstring>
+#include <cstdlib>
 #include <cstdio>
 
 #include "../../include/orion.h"
@@ -41,11 +43,13 @@ constexpr int kBox = 16;                  // token rows of a partial-tile TMA bo
 constexpr int kSK = 2, kSV = 3;           // K / V ring depth (32 KB stages)
 constexpr int kThreads = 384;
 constexpr int kWarpAlloc = 0, kWarpSched = 1, kWarpTMA = 2, kWarpMMA = 3;
+constexpr int kWarpTMAV = 0;              // the TMEM-alloc warp streams V once allocation is done
 // TMEM columns
-__device__ __forceinline__ uint32_t colS(uint32_t p) { return p * 64; }
-__device__ __forceinline__ uint32_t colO(uint32_t p) { return 128 + p * 64; }
-__device__ __forceinline__ uint32_t colL(uint32_t p) { return 256 + p * 64; }
-constexpr uint32_t kColOnes = 384;        // 64 columns: 128 x 128 bf16 ones (A operand of L)
+constexpr int kSB = 3;                    // S^T buffers: tile j uses j % 3
+__device__ __forceinline__ uint32_t colS(uint32_t b) { return b * 64; }
+__device__ __forceinline__ uint32_t colO(uint32_t p) { return 192 + p * 64; }   // per warpgroup
+__device__ __forceinline__ uint32_t colL(uint32_t p) { return 320 + p * 64; }
+constexpr uint32_t kColOnes = 448;        // 64 columns: 128 x 128 bf16 ones (A operand of L)
 
 struct L {
   static constexpr int QB = 64 * D * 2;          // 16 KB: [2 halves][64 rows][128 B]
@@ -60,8 +64,9 @@ struct L {
   static constexpr int OFF_M = OFF_P + 2 * PB;   // running max m per column: [wg 2][item parity 2][64]
   static constexpr int OFF_SH = OFF_M + 2 * 2 * 64 * 4;   // growth-path shifts: [wg 2][64]
   static constexpr int OFF_SCHED = OFF_SH + 2 * 64 * 4;   // item schedule ring: 8 x 64 B
-  static constexpr int OFF_BAR = OFF_SCHED + 8 * 64;
-  static constexpr int N_BAR = 2 * kSK + 2 * kSV + 2 + 2 + 2 + 2 + 2 + 2 + 1 + 2 * 8;
+  static constexpr int OFF_MI = OFF_SCHED + 8 * 64;        // MMA warp's item geometry: 4 x 32 B
+  static constexpr int OFF_BAR = OFF_MI + 4 * 32;
+  static constexpr int N_BAR = 2 * kSK + 2 * kSV + 2 * 3 + 3 + 2 + 2 + 2 + 2 + 2 + 2 + 2 * 8;
   static constexpr int BYTES = OFF_BAR + N_BAR * 8 + 16;
 };
 static_assert(L::BYTES <= 232448, "shared memory budget");
@@ -81,18 +86,50 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+__device__ int g_orion_dump[1024];   // debugging: a timed-out wait asks every role of the CTA to report
+__device__ int* g_orion_hstate;   // debugging (ORION_DEBUG_HOST): host-mapped [16][12][4] progress counters
+#define DBG_STATE(w, i, v) do { if (g_orion_hstate && blockIdx.x < 16) \
+    reinterpret_cast<volatile int*>(g_orion_hstate)[(blockIdx.x * 12 + (w)) * 4 + (i)] = (v); } while (0)
+
+// Blocking wait.  try_wait carries a suspend-time hint so a waiting warp sleeps instead of
+// spinning (it resumes as soon as the phase completes); a protocol bug traps after ~2 s instead of
+// hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   const uint32_t a = smem_u32(b);
-  for (uint32_t spin = 0;; ++spin) {
-    uint32_t ok;
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(a), "r"(parity), "r"(20000u)
+      : "memory");
+  if (ok) return;
+  const long long t0 = clock64();
+  for (;;) {
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(ok)
-        : "r"(a), "r"(parity)
+        : "r"(a), "r"(parity), "r"(20000u)
         : "memory");
     if (ok) return;
-    if (spin > (1u << 22)) __trap();   // protocol bug: fail loudly instead of hanging
+    if (clock64() - t0 > (4ll << 30)) {
+      printf("ORION DEADLOCK blk %d warp %d lane %d bar_off %u parity %u\n", blockIdx.x, threadIdx.x >> 5,
+             threadIdx.x & 31, a & 0xFFFF, parity);
+      atomicExch(&g_orion_dump[blockIdx.x & 1023], 1);
+      const long long t1 = clock64();
+      while (clock64() - t1 < (1ll << 30)) {}   // give the other roles time to report
+      __trap();
+    }
   }
+}
+// Non-blocking probe of a phase (warp-uniform: lane 0 decides).
+__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return __shfl_sync(0xffffffffu, ok, 0) != 0;
 }
 #ifdef ORION_TC_TRACE
 #define TRACE_DECL unsigned long long tr_[12] = {0}; const unsigned long long tr_t0 = clock64();
@@ -203,18 +240,19 @@ __device__ __forceinline__ int next_nonempty(const TcArgs& a, int it) {
 // than 2^8) it moves the per-column reference m (smem) and rescales O^T / L^T of this warpgroup.
 template <int N>
 __device__ __forceinline__ void softmax_tile(uint8_t* smem, uint32_t tmem, uint32_t lane_base, int p, int t,
-                                             int tb, const WorkItem& w, const Geom& g, float* mrow,
-                                             float* shs, bool had, float scale_log2, uint32_t vstage,
-                                             uint64_t* s_free) {
+                                             uint32_t scol, uint32_t pslot, int tb, int lo, int hi,
+                                             float* mrow, float* shs, bool had, float scale_log2,
+                                             uint64_t* sfree, bool need_pv, uint64_t* pv_prev,
+                                             uint32_t pv_prev_par) {
   uint32_t s[N];
-  if constexpr (N == 16) tmem_ld32x16(tmem + lane_base + colS(p), s);
-  if constexpr (N == 32) tmem_ld32x32(tmem + lane_base + colS(p), s);
-  if constexpr (N == 64) tmem_ld32x64(tmem + lane_base + colS(p), s);
+  if constexpr (N == 16) tmem_ld32x16(tmem + lane_base + scol, s);
+  if constexpr (N == 32) tmem_ld32x32(tmem + lane_base + scol, s);
+  if constexpr (N == 64) tmem_ld32x64(tmem + lane_base + scol, s);
   tc_wait_ld();
   tc_fence_before();
-  mbar_arrive(s_free + p);                           // QK(j+2) may overwrite S^T[p]
+  mbar_arrive(sfree);                                // QK(j+3) may overwrite this S^T buffer
   const int pos = tb + t;
-  const bool valid = pos >= w.t0 && pos < g.end;
+  const bool valid = pos >= lo && pos < hi;
   // d = s * scale - mb (log2 domain, relative to the running reference; mb = 0 while unset)
   bool exceed = false;
 #pragma unroll
@@ -229,9 +267,15 @@ __device__ __forceinline__ void softmax_tile(uint8_t* smem, uint32_t tmem, uint3
       exceed |= valid && (mm[e] == -INFINITY || d > 8.f);
     }
   }
-  uint8_t* pbuf = smem + L::OFF_P + p * L::PB;      // free: PV(j-2) is complete
+  // P^T[p] (this warpgroup's buffer) is free once the PV of its previous tile is complete; on the
+  // growth path that PV is also the one O^T / L^T must have absorbed before they are rescaled.
+  uint8_t* pbuf = smem + L::OFF_P + pslot * L::PB;
   const bool grow = wg_any(exceed, 2 + p);
   if (grow) {
+    if (need_pv) {
+      mbar_wait(pv_prev, pv_prev_par);
+      tc_fence_after();
+    }
     // column max of d over the 128 tokens: warp redux, then across the 4 warps via smem (the
     // P^T buffer is scratch until P^T is written below)
     float* red = reinterpret_cast<float*>(pbuf);
@@ -251,8 +295,7 @@ __device__ __forceinline__ void softmax_tile(uint8_t* smem, uint32_t tmem, uint3
       if (gc) mrow[t] = mb + cm;
     }
     wg_sync(2 + p, 128);
-    if (had) {   // O^T and L^T columns of this warpgroup follow the new reference: * 2^-shift
-      tc_fence_after();
+    if (had) {   // O^T and L^T of this item follow the new reference: * 2^-shift
 #pragma unroll
       for (int cb = 0; cb < N; cb += 16) {
         uint32_t o[16], l16[16];
@@ -271,29 +314,20 @@ __device__ __forceinline__ void softmax_tile(uint8_t* smem, uint32_t tmem, uint3
       tc_wait_st();
     }
   }
-  // P^T row t (MN-major, 128B swizzle): p = 2^(d - shift), rounded to bf16
+  // P^T row t (MN-major, 128B swizzle): p = 2^(d - shift), rounded to bf16.  The exponentials are
+  // formed in registers before the wait for the previous PV, so that wait overlaps the MUFU work.
+  uint32_t pk[N / 2];
 #pragma unroll
-  for (int cc = 0; cc < N / 8; ++cc) {
-    float sh[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) sh[e] = grow ? shs[cc * 8 + e] : 0.f;
-    uint4 v;
-    v.x = pack_bf16(ex2(__uint_as_float(s[cc * 8 + 0]) - sh[0]), ex2(__uint_as_float(s[cc * 8 + 1]) - sh[1]));
-    v.y = pack_bf16(ex2(__uint_as_float(s[cc * 8 + 2]) - sh[2]), ex2(__uint_as_float(s[cc * 8 + 3]) - sh[3]));
-    v.z = pack_bf16(ex2(__uint_as_float(s[cc * 8 + 4]) - sh[4]), ex2(__uint_as_float(s[cc * 8 + 5]) - sh[5]));
-    v.w = pack_bf16(ex2(__uint_as_float(s[cc * 8 + 6]) - sh[6]), ex2(__uint_as_float(s[cc * 8 + 7]) - sh[7]));
-    if (cc == 0 && grow) wg_sync(2 + p, 128);       // all red reads done before P^T overwrites them
-    *reinterpret_cast<uint4*>(pbuf + t * 128 + ((cc ^ (t & 7)) << 4)) = v;
+  for (int c = 0; c < N; c += 2) {
+    const float s0 = grow ? shs[c] : 0.f, s1 = grow ? shs[c + 1] : 0.f;
+    pk[c / 2] = pack_bf16(ex2(__uint_as_float(s[c]) - s0), ex2(__uint_as_float(s[c + 1]) - s1));
   }
-  if (!valid) {                                      // V rows outside [t0, end): exact zeros
-    uint8_t* vrow = smem + L::OFF_V + vstage * L::KVB + t * 128;
+  if (grow) wg_sync(2 + p, 128);                     // all red reads done before P^T overwrites them
+  else if (need_pv) mbar_wait(pv_prev, pv_prev_par);
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      uint4* p4 = reinterpret_cast<uint4*>(vrow + h * L::HALF_KV);
-#pragma unroll
-      for (int c = 0; c < 8; ++c) p4[c] = make_uint4(0, 0, 0, 0);
-    }
-  }
+  for (int cc = 0; cc < N / 8; ++cc)
+    *reinterpret_cast<uint4*>(pbuf + t * 128 + ((cc ^ (t & 7)) << 4)) =
+        make_uint4(pk[cc * 4 + 0], pk[cc * 4 + 1], pk[cc * 4 + 2], pk[cc * 4 + 3]);
 }
 
 // Per-CTA item schedule entry, produced by the scheduler warp (warp 1) and consumed in order by
@@ -303,7 +337,7 @@ struct Sched {
   int32_t valid, it, pt_off, t0, end, base, ntiles, npad, kv_head, n_rows, slot0, pad[5];
 };
 constexpr int kSched = 8;
-constexpr uint32_t kSchedConsumers = 1 + 1 + 128 + 128;   // TMA lane, MMA lane, WG0, WG1 threads
+constexpr uint32_t kSchedConsumers = 1 + 1 + 1 + 128 + 128;   // K-TMA, V-TMA, MMA lanes, WG0, WG1
 
 __device__ __forceinline__ Sched read_sched(const Sched* ring, uint64_t* full, uint64_t* empty, uint32_t k,
                                             bool arrive) {
@@ -324,14 +358,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* k_empty = k_full + kSK;
   uint64_t* v_full = k_empty + kSK;
   uint64_t* v_empty = v_full + kSV;
-  uint64_t* s_full = v_empty + kSV;
-  uint64_t* s_free = s_full + 2;
-  uint64_t* p_full = s_free + 2;
-  uint64_t* pv_done = p_full + 2;
+  // Barriers a warpgroup waits on are private to it ([2] = per warpgroup): a warpgroup skips the
+  // other's items, and a phase-parity wait on a barrier shared with the other warpgroup could then
+  // run two phases ahead of it and alias.
+  uint64_t* s_full = v_empty + kSV;                 // [2][3]: S^T of warpgroup p's tile in buffer b
+  uint64_t* s_free = s_full + 2 * kSB;              // [3]: S^T buffer read (MMA is the only waiter)
+  uint64_t* p_full = s_free + kSB;                  // [2]: P^T[p] written
+  uint64_t* pv_done = p_full + 2;                   // [2]: PV of warpgroup p's tile complete
   uint64_t* q_full = pv_done + 2;
   uint64_t* q_empty = q_full + 2;
-  uint64_t* o_free = q_empty + 2;
-  uint64_t* sch_full = o_free + 1;
+  uint64_t* o_free = q_empty + 2;                   // [2]: warpgroup p's item epilogue done
+  uint64_t* acc_full = o_free + 2;                  // [2]: last PV of warpgroup p's item complete
+  uint64_t* sch_full = acc_full + 2;
   uint64_t* sch_empty = sch_full + kSched;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sch_empty + kSched);
   float* mall = reinterpret_cast<float*>(smem + L::OFF_M);
@@ -341,11 +379,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (tid == 0) {
     for (int s = 0; s < kSK; ++s) { mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1); }
     for (int s = 0; s < kSV; ++s) { mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1); }
+    for (int b = 0; b < kSB; ++b) { mbar_init(s_full + b, 1); mbar_init(s_full + kSB + b, 1); mbar_init(s_free + b, 128); }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(s_full + b, 1); mbar_init(s_free + b, 128); mbar_init(p_full + b, 128);
-      mbar_init(pv_done + b, 1); mbar_init(q_full + b, 1); mbar_init(q_empty + b, 1);
+      mbar_init(p_full + b, 128); mbar_init(pv_done + b, 1); mbar_init(q_full + b, 1);
+      mbar_init(q_empty + b, 1); mbar_init(o_free + b, 128); mbar_init(acc_full + b, 1);
     }
-    mbar_init(o_free, 256);
     for (int b = 0; b < kSched; ++b) { mbar_init(sch_full + b, 1); mbar_init(sch_empty + b, kSchedConsumers); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmK)) : "memory");
@@ -353,6 +391,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmK16)) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmV16)) : "memory");
   }
+  // V ring starts zeroed: rows a partial tile's boxes never cover must be finite (their P is 0)
+  for (int i = tid; i < kSV * L::KVB / 16; i += kThreads)
+    reinterpret_cast<uint4*>(smem + L::OFF_V)[i] = make_uint4(0, 0, 0, 0);
+  fence_proxy_async();
   if (warp == kWarpAlloc) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
@@ -427,8 +469,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       ring[k % kSched].valid = 0;
       mbar_arrive(sch_full + (k % kSched));
     }
-  } else if (warp == kWarpTMA) {
-    // ------------------------------------------------------------------ TMA producer
+  } else if (warp == kWarpTMA || warp == kWarpTMAV) {
+    // ------------------------------------------------------------------ TMA producers
+    // warp 2 streams K tiles (released at QK completion), warp 0 streams V tiles (released at PV
+    // completion): the two rings never block each other.
+    const bool isk = warp == kWarpTMA;
+    const int nst = isk ? kSK : kSV;
+    uint64_t* full = isk ? k_full : v_full;
+    uint64_t* empty = isk ? k_empty : v_empty;
+    const CUtensorMap* mbig = isk ? &tmK : &tmV;
+    const CUtensorMap* msml = isk ? &tmK16 : &tmV16;
+    const uint32_t base_off = isk ? L::OFF_K : L::OFF_V;
     uint32_t j = 0;
     const int pmask = (1 << a.page_shift) - 1;
     const int big = min(64, 1 << a.page_shift);     // rows of a full-tile box (<= one page)
@@ -437,15 +488,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!e.valid) break;
       for (int tb0 = 0; tb0 < e.ntiles; tb0 += 32) {
         int brow[8];
-        int nbox = 0, first_off = 0, full = 0;
+        int nbox = 0, first_off = 0, full_t = 0;
 #pragma unroll
         for (int b = 0; b < 8; ++b) brow[b] = 0;
         if (tb0 + lane < e.ntiles) {
           const int a0 = e.base + (tb0 + lane) * kTok;
           const int lo = max(a0, e.t0), hi = min(a0 + kTok, e.end);
-          full = (lo == a0 && hi == a0 + kTok);
+          full_t = (lo == a0 && hi == a0 + kTok);
           int pos0, step;
-          if (full) { nbox = kTok / big; pos0 = a0; step = big; }
+          if (full_t) { nbox = kTok / big; pos0 = a0; step = big; }
           else { pos0 = lo & ~(kBox - 1); nbox = (hi - pos0 + kBox - 1) / kBox; step = kBox; first_off = pos0 - a0; }
 #pragma unroll
           for (int b = 0; b < 8; ++b)
@@ -456,42 +507,29 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         const int tend = min(e.ntiles, tb0 + 32);
-        for (int t = tb0; t < tend; ++t, ++j) {
-          const int src = t - tb0;
+        for (int tt = tb0; tt < tend; ++tt, ++j) {
+          const int src = tt - tb0;
           const int tn = __shfl_sync(0xffffffffu, nbox, src);
-          const int tf = __shfl_sync(0xffffffffu, full, src);
+          const int tf = __shfl_sync(0xffffffffu, full_t, src);
           const int to = __shfl_sync(0xffffffffu, first_off, src);
           int rr[8];
 #pragma unroll
           for (int b = 0; b < 8; ++b) rr[b] = __shfl_sync(0xffffffffu, brow[b], src);
-          const int sk = j % kSK, sv = j % kSV;
+          const int st = j % nst;
+          if (lane == 0) DBG_STATE(warp, 0, j);
           const int rpb = tf ? big : kBox;
           const uint32_t bytes = static_cast<uint32_t>(tn * rpb * 128 * 2);
-          const CUtensorMap* mk = tf ? &tmK : &tmK16;
-          const CUtensorMap* mv = tf ? &tmV : &tmV16;
-          TW(0, mbar_wait(k_empty + sk, ((j / kSK) & 1) ^ 1));
+          const CUtensorMap* m = tf ? mbig : msml;
+          TW(0, mbar_wait(empty + st, ((j / nst) & 1) ^ 1));
           if (elect_one()) {
-            mbar_expect_tx(k_full + sk, bytes);
-            const uint32_t dk = smem_u32(smem + L::OFF_K + sk * L::KVB);
+            mbar_expect_tx(full + st, bytes);
+            const uint32_t dst = smem_u32(smem + base_off + st * L::KVB);
 #pragma unroll
             for (int b = 0; b < 8; ++b)
               if (b < tn) {
                 const uint32_t roff = static_cast<uint32_t>(to + b * rpb) * 128;
-                tma_load_2d(dk + roff, mk, 0, rr[b], k_full + sk);
-                tma_load_2d(dk + L::HALF_KV + roff, mk, 64, rr[b], k_full + sk);
-              }
-          }
-          __syncwarp();
-          TW(1, mbar_wait(v_empty + sv, ((j / kSV) & 1) ^ 1));
-          if (elect_one()) {
-            mbar_expect_tx(v_full + sv, bytes);
-            const uint32_t dv = smem_u32(smem + L::OFF_V + sv * L::KVB);
-#pragma unroll
-            for (int b = 0; b < 8; ++b)
-              if (b < tn) {
-                const uint32_t roff = static_cast<uint32_t>(to + b * rpb) * 128;
-                tma_load_2d(dv + roff, mv, 0, rr[b], v_full + sv);
-                tma_load_2d(dv + L::HALF_KV + roff, mv, 64, rr[b], v_full + sv);
+                tma_load_2d(dst + roff, m, 0, rr[b], full + st);
+                tma_load_2d(dst + L::HALF_KV + roff, m, 64, rr[b], full + st);
               }
           }
           __syncwarp();
@@ -501,180 +539,197 @@ __global__ void __launch_bounds__(kThreads, 1)
     TRACE_DUMP("producer");
   } else if (warp == kWarpMMA) {
     // ------------------------------------------------------------------ MMA issuer
-    // Two cursors over the flattened (item, tile) sequence: QK two tiles ahead of PV, never into
-    // item k+2 before every PV of item k is issued (item k+2's Q reuses item k's buffer).
+    // Item k is owned by softmax warpgroup k & 1 (accumulators O^T/L^T[k & 1]).  QK runs up to
+    // three tiles ahead of PV (three S^T buffers) and never into item k+2 before every PV of item
+    // k is issued (item k+2 reuses item k's Q buffer).  A polling loop issues a PV as soon as its
+    // P is published, otherwise a QK whose operands are resident, otherwise sleeps on the oldest
+    // dependency.
     const uint64_t dq0 = sw128_desc(smem_u32(smem + L::OFF_Q), 16, 1024);
     const uint64_t dk0 = sw128_desc(smem_u32(smem + L::OFF_K), 16, 1024);
     const uint64_t dv0 = sw128_desc(smem_u32(smem + L::OFF_V), L::HALF_KV, 1024);   // MN-major A
     const uint64_t dp0 = sw128_desc(smem_u32(smem + L::OFF_P), L::HALF_KV, 1024);   // MN-major B
-    // (ntiles, npad) of items k % 3: the QK cursor may have read item kv + 2's entry while the PV
-    // cursor is still on item kv.
-    int nt0 = 0, nt1 = 0, nt2 = 0, np0 = 16, np1 = 16, np2 = 16;
-    auto nt_of = [&](uint32_t k) { const uint32_t m = k % 3; return m == 0 ? nt0 : (m == 1 ? nt1 : nt2); };
-    auto np_of = [&](uint32_t k) { const uint32_t m = k % 3; return m == 0 ? np0 : (m == 1 ? np1 : np2); };
-    auto set_of = [&](uint32_t k, int nt, int np) {
-      const uint32_t m = k % 3;
-      if (m == 0) { nt0 = nt; np0 = np; } else if (m == 1) { nt1 = nt; np1 = np; } else { nt2 = nt; np2 = np; }
+    // geometry of items k % 4 (QK may have read item kv + 1 while PV is on item kv)
+    int32_t* mi = reinterpret_cast<int32_t*>(smem + L::OFF_MI);   // [4][8]: t0 end base ntiles npad
+    auto set_of = [&](uint32_t k, const Sched& e) {
+      if (lane == 0) {
+        int32_t* r = mi + (k & 3) * 8;
+        r[0] = e.t0; r[1] = e.end; r[2] = e.base; r[3] = e.ntiles; r[4] = e.npad;
+      }
+      __syncwarp();
     };
-    uint32_t kq = 0, tq = 0, jq = 0;                // QK cursor
+    auto nt_of = [&](uint32_t k) { return mi[(k & 3) * 8 + 3]; };
+    auto np_of = [&](uint32_t k) { return mi[(k & 3) * 8 + 4]; };
+    uint32_t kq = 0, tq = 0, jq = 0;                // QK cursor (item, tile in item, global tile)
+    uint32_t kv = 0, tv = 0, jv = 0;                // PV cursor
+    uint32_t ppar = 0;                              // phase parity of p_full[p] (bit p)
     bool q_live;
     {
       const Sched e = read_sched(ring, sch_full, sch_empty, 0, lane == 0);
       q_live = e.valid;
-      set_of(0, e.ntiles, e.npad);
+      set_of(0, e);
     }
-    uint32_t kv = 0, tv = 0, jv = 0;                // PV cursor
-    while (true) {
-      const bool v_live = kv < kq || (kv == kq && q_live);
-      if (!v_live) break;
-      while (q_live && jq <= jv + 2 && kq <= kv + 1) {
-        // ---- S^T(jq) = K(jq) Q^T
-        const uint32_t j = jq;
-        if (tq == 0) TW(1, mbar_wait(q_full + (kq & 1), (kq >> 1) & 1));
-        const int s = j % kSK;
-        TW(2, mbar_wait(k_full + s, (j / kSK) & 1));
-        if (j >= 2) TW(3, mbar_wait(s_free + (j & 1), ((j - 2) >> 1) & 1));
-        tc_fence_after();
-        const int ntq = nt_of(kq);
-        const int npq = np_of(kq);
-        const uint64_t dq = dq0 + static_cast<uint64_t>(((kq & 1) * L::QB) >> 4);
-        const uint64_t dk = dk0 + static_cast<uint64_t>((s * L::KVB) >> 4);
-        const uint32_t id = idesc(npq, false, false);
-        if (elect_one()) {
+    auto issue_qk = [&]() {
+      const uint32_t j = jq;
+      if (lane == 0) { DBG_STATE(warp, 0, jq); DBG_STATE(warp, 1, kq); }
+      if (tq == 0) TW(1, mbar_wait(q_full + (kq & 1), (kq >> 1) & 1));
+      const int s = j % kSK;
+      TW(2, mbar_wait(k_full + s, (j / kSK) & 1));
+      if (j >= static_cast<uint32_t>(kSB)) TW(3, mbar_wait(s_free + (j % kSB), ((j - kSB) / kSB) & 1));
+      tc_fence_after();
+      const int ntq = nt_of(kq);
+      const uint64_t dq = dq0 + static_cast<uint64_t>(((kq & 1) * L::QB) >> 4);
+      const uint64_t dk = dk0 + static_cast<uint64_t>((s * L::KVB) >> 4);
+      const uint32_t id = idesc(np_of(kq), false, false);
+      if (elect_one()) {
 #pragma unroll
-          for (int ks = 0; ks < D / 16; ++ks) {
-            const uint64_t ok = static_cast<uint64_t>(((ks >> 2) * L::HALF_KV + (ks & 3) * 32) >> 4);
-            const uint64_t oq = static_cast<uint64_t>(((ks >> 2) * L::HALF_Q + (ks & 3) * 32) >> 4);
-            mma_ss(tmem + colS(j & 1), dk + ok, dq + oq, id, ks > 0);
-          }
-          tc_commit(s_full + (j & 1));
-          tc_commit(k_empty + s);
-          if (static_cast<int>(tq) + 1 == ntq) tc_commit(q_empty + (kq & 1));   // item's last QK
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint64_t ok = static_cast<uint64_t>(((ks >> 2) * L::HALF_KV + (ks & 3) * 32) >> 4);
+          const uint64_t oq = static_cast<uint64_t>(((ks >> 2) * L::HALF_Q + (ks & 3) * 32) >> 4);
+          mma_ss(tmem + colS(j % kSB), dk + ok, dq + oq, id, ks > 0);
         }
-        __syncwarp();
-        ++jq;
-        if (static_cast<int>(++tq) == ntq) {
-          tq = 0;
-          ++kq;
-          const Sched e = read_sched(ring, sch_full, sch_empty, kq, lane == 0);
-          q_live = e.valid;
-          set_of(kq, e.ntiles, e.npad);
+        tc_commit(s_full + (kq & 1) * kSB + (j % kSB));
+        tc_commit(k_empty + s);
+        if (static_cast<int>(tq) + 1 == ntq) tc_commit(q_empty + (kq & 1));   // item's last QK
+      }
+      __syncwarp();
+      ++jq;
+      if (static_cast<int>(++tq) == ntq) {
+        tq = 0;
+        ++kq;
+        const Sched e = read_sched(ring, sch_full, sch_empty, kq, lane == 0);
+        q_live = e.valid;
+        set_of(kq, e);
+      }
+    };
+    auto issue_pv = [&]() {
+      const uint32_t j = jv;
+      if (lane == 0) { DBG_STATE(warp, 2, jv); DBG_STATE(warp, 3, kv); }
+      const int s = j % kSV;
+      const uint32_t wg = kv & 1;
+      TW(6, mbar_wait(v_full + s, (j / kSV) & 1));
+      {
+        // A partial tile's TMA boxes (16-row granular) may carry rows outside [t0, end) -- e.g.
+        // never-written slots past own_len.  Their P is exactly 0, but 0 x NaN is NaN: zero them.
+        const int32_t* r = mi + (kv & 3) * 8;
+        const int a0 = r[2] + static_cast<int>(tv) * kTok;
+        const int lo = max(a0, r[0]) - a0, hi = min(a0 + kTok, r[1]) - a0;
+        if (lo > 0 || hi < kTok) {
+          const int z0 = lo & ~(kBox - 1), z1 = min(kTok, (hi + kBox - 1) & ~(kBox - 1));
+          uint8_t* vs = smem + L::OFF_V + s * L::KVB;
+          const int nz = (lo - z0) + (z1 - hi);
+          for (int i = lane; i < nz * 16; i += 32) {
+            const int zr = i >> 4, c = i & 15;
+            const int row = zr < lo - z0 ? z0 + zr : hi + (zr - (lo - z0));
+            *reinterpret_cast<uint4*>(vs + (c >> 3) * L::HALF_KV + row * 128 + (c & 7) * 16) = make_uint4(0, 0, 0, 0);
+          }
+          fence_proxy_async();
+          __syncwarp();
         }
       }
-      // ---- O^T += V(jv)^T P^T(jv);  L^T += 1 P^T(jv)
-      const uint32_t j = jv;
-      const int s = j % kSV;
-      const int ntv = nt_of(kv);
-      const int npv = np_of(kv);
-      TW(6, mbar_wait(v_full + s, (j / kSV) & 1));
-      TW(4, mbar_wait(p_full + (j & 1), (j >> 1) & 1));
-      if (tv == 0 && kv > 0) TW(5, mbar_wait(o_free, (kv - 1) & 1));
+      TW(4, mbar_wait(p_full + wg, (ppar >> wg) & 1));
+      ppar ^= 1u << wg;
+      if (tv == 0 && kv >= 2) TW(5, mbar_wait(o_free + wg, ((kv >> 1) - 1) & 1));   // item kv-2 read out
       tc_fence_after();
       const uint64_t dv = dv0 + static_cast<uint64_t>((s * L::KVB) >> 4);
-      const uint64_t dp = dp0 + static_cast<uint64_t>(((j & 1) * L::PB) >> 4);
+      const uint64_t dp = dp0 + static_cast<uint64_t>((wg * L::PB) >> 4);
+      const int npv = np_of(kv);
       const uint32_t id_pv = idesc(npv, true, true);
       const uint32_t id_l = idesc(npv, false, true);
-      const bool first = tv < 2;
+      const bool first = tv == 0;
       if (elect_one()) {
 #pragma unroll
         for (int kt = 0; kt < kTok / 16; ++kt) {
           const uint64_t o = static_cast<uint64_t>((kt * 16 * 128) >> 4);
           const uint32_t acc = (!first || kt > 0) ? 1u : 0u;
-          mma_ss(tmem + colO(j & 1), dv + o, dp + o, id_pv, acc);
-          mma_ts(tmem + colL(j & 1), tmem + kColOnes + kt * 8, dp + o, id_l, acc);
+          mma_ss(tmem + colO(wg), dv + o, dp + o, id_pv, acc);
+          mma_ts(tmem + colL(wg), tmem + kColOnes + kt * 8, dp + o, id_l, acc);
         }
-        tc_commit(pv_done + (j & 1));
+        tc_commit(pv_done + wg);
         tc_commit(v_empty + s);
+        if (static_cast<int>(tv) + 1 == nt_of(kv)) tc_commit(acc_full + wg);   // item complete
       }
       __syncwarp();
       ++jv;
-      if (static_cast<int>(++tv) == ntv) { tv = 0; ++kv; }
+      if (static_cast<int>(++tv) == nt_of(kv)) { tv = 0; ++kv; }
+    };
+    // in-order: keep QK up to 3 tiles ahead (never into item kv+2), then one PV
+    while (true) {
+      while (q_live && jq <= jv + 3 && kq <= kv + 1) issue_qk();
+      const bool v_live = kv < kq || (kv == kq && q_live);
+      if (!v_live) break;
+      issue_pv();
     }
     TRACE_DUMP("mma");
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ softmax / epilogue
-    const int p = (warp - 4) >> 2;                  // warpgroup: tiles with j & 1 == p
+    // Warpgroup p owns the items k with k & 1 == p: every tile of the item, one accumulator
+    // (O^T/L^T[p]), its epilogue overlapping the other warpgroup's next item.
+    const int p = (warp - 4) >> 2;
     const int t = tid - 128 - p * 128;              // token row of S^T / d lane of O^T
     const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    uint32_t j = 0;
+    float* mrow = mall + p * 64;
+    float* shs = reinterpret_cast<float*>(smem + L::OFF_SH) + p * 64;
+    uint32_t j = 0;                                 // global tile index (selects the S^T buffer)
+    uint32_t mj = 0;                                // tiles this warpgroup has processed
+    uint32_t spar = 0;                              // phase parity of s_full[p][b] (bit b)
     for (uint32_t k = 0;; ++k) {
       const Sched e = read_sched(ring, sch_full, sch_empty, k, true);
       if (!e.valid) break;
-      WorkItem w;
-      w.t0 = e.t0;
-      Geom g;
-      g.base = e.base; g.end = e.end; g.ntiles = e.ntiles; g.npad = e.npad;
-      float* mrow = mall + (p * 2 + (k & 1)) * 64;
+      if ((k & 1) != static_cast<uint32_t>(p)) { j += e.ntiles; continue; }
       if (t < 64) mrow[t] = -INFINITY;
       wg_sync(2 + p, 128);
-      bool had = false;
-      uint32_t jl = 0;
-      const uint32_t j0 = j;
-      for (int tt = 0; tt < g.ntiles; ++tt, ++j) {
-        if ((j & 1) != static_cast<uint32_t>(p)) continue;
-        const int tb = g.base + tt * kTok;
-        TW(6, mbar_wait(s_full + p, (j >> 1) & 1));
+      for (int tt = 0; tt < e.ntiles; ++tt, ++j) {
+        const int tb = e.base + tt * kTok;
+        const int lo = max(tb, e.t0), hi = min(tb + kTok, e.end);
+        if ((t & 31) == 0) { DBG_STATE(warp, 0, j); DBG_STATE(warp, 1, k); DBG_STATE(warp, 2, tt); }
+        const uint32_t b = j % kSB;
+        TW(6, mbar_wait(s_full + p * kSB + b, (spar >> b) & 1));
+        spar ^= 1u << b;
         tc_fence_after();
-        if (j >= 2) TW(7, mbar_wait(pv_done + p, ((j - 2) >> 1) & 1));   // P^T[p] free, O^T[p] current
 #ifdef ORION_TC_TRACE
         const unsigned long long tsm = clock64();
 #endif
-        float* shs = reinterpret_cast<float*>(smem + L::OFF_SH) + p * 64;
-        if (g.npad == 16) softmax_tile<16>(smem, tmem, lane_base, p, t, tb, w, g, mrow, shs, had, a.scale_log2, j % kSV, s_free);
-        else if (g.npad == 32) softmax_tile<32>(smem, tmem, lane_base, p, t, tb, w, g, mrow, shs, had, a.scale_log2, j % kSV, s_free);
-        else softmax_tile<64>(smem, tmem, lane_base, p, t, tb, w, g, mrow, shs, had, a.scale_log2, j % kSV, s_free);
+        const bool need_pv = mj > 0;                // P^T[p] still feeds the PV of tile mj-1
+        const uint32_t pvpar = (mj - 1) & 1;
+        if (e.npad == 16) softmax_tile<16>(smem, tmem, lane_base, p, t, colS(b), p, tb, lo, hi, mrow, shs, tt > 0, a.scale_log2, s_free + b, need_pv, pv_done + p, pvpar);
+        else if (e.npad == 32) softmax_tile<32>(smem, tmem, lane_base, p, t, colS(b), p, tb, lo, hi, mrow, shs, tt > 0, a.scale_log2, s_free + b, need_pv, pv_done + p, pvpar);
+        else softmax_tile<64>(smem, tmem, lane_base, p, t, colS(b), p, tb, lo, hi, mrow, shs, tt > 0, a.scale_log2, s_free + b, need_pv, pv_done + p, pvpar);
         fence_proxy_async();
         tc_fence_before();
         mbar_arrive(p_full + p);
+        ++mj;
+        if ((t & 31) == 0) DBG_STATE(warp, 3, 2);
 #ifdef ORION_TC_TRACE
         tr_[1] += clock64() - tsm;
 #endif
-        had = true;
-        jl = j;
       }
+      // ---- epilogue: this item's partial (m, l, acc) per query row
 #ifdef ORION_TC_TRACE
       const unsigned long long tep = clock64();
 #endif
-      if (had) {
-        TW(8, mbar_wait(pv_done + p, (jl >> 1) & 1));
-        tc_fence_after();
-      }
-      TW(9, wg_sync(1, 256));                        // both warpgroups' accumulators final
-      // ---- merge O^T_0 / O^T_1 into one partial per query row; warpgroup p takes the 8-column
-      // chunks cb with (cb / 8) % 2 == p
-      {
-        const float* mA = mall + (0 * 2 + (k & 1)) * 64;
-        const float* mB = mall + (1 * 2 + (k & 1)) * 64;
-        const bool hadA = g.ntiles > 1 || (j0 & 1) == 0;
-        const bool hadB = g.ntiles > 1 || (j0 & 1) == 1;
-        const int n = e.n_rows;
-        float* dst = a.part_acc + static_cast<size_t>(e.slot0) * D + t;
+      // last PV of the item: a dedicated per-warpgroup barrier (pv_done[] could already have moved
+      // on by two phases, driven by the other warpgroup's next item)
+      TW(8, mbar_wait(acc_full + p, (k >> 1) & 1));
+      tc_fence_after();
+      const int n = e.n_rows;
+      float* dst = a.part_acc + static_cast<size_t>(e.slot0) * D + t;
 #pragma unroll 1
-        for (int cb = p * 8; cb < g.npad; cb += 16) {
-          uint32_t oa[8], ob[8], la[8], lb[8];
-          if (hadA) { tmem_ld32x8(tmem + lane_base + colO(0) + cb, oa); tmem_ld32x8(tmem + lane_base + colL(0) + cb, la); }
-          if (hadB) { tmem_ld32x8(tmem + lane_base + colO(1) + cb, ob); tmem_ld32x8(tmem + lane_base + colL(1) + cb, lb); }
-          tc_wait_ld();
+      for (int cb = 0; cb < e.npad; cb += 8) {
+        uint32_t o[8], l8[8];
+        tmem_ld32x8(tmem + lane_base + colO(p) + cb, o);
+        tmem_ld32x8(tmem + lane_base + colL(p) + cb, l8);
+        tc_wait_ld();
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const int col = cb + c;
-            if (col < n) {
-              const float ma = hadA ? mA[col] : -INFINITY, mb = hadB ? mB[col] : -INFINITY;
-              const float M = fmaxf(ma, mb);
-              const float Mb = M == -INFINITY ? 0.f : M;
-              const float fa = hadA ? ex2(ma - Mb) : 0.f, fb = hadB ? ex2(mb - Mb) : 0.f;
-              const float ov = (hadA ? fa * __uint_as_float(oa[c]) : 0.f) + (hadB ? fb * __uint_as_float(ob[c]) : 0.f);
-              dst[static_cast<size_t>(col) * D] = ov;
-              if (t == col) {
-                const float lv = (hadA ? fa * __uint_as_float(la[c]) : 0.f) + (hadB ? fb * __uint_as_float(lb[c]) : 0.f);
-                a.part_ml[e.slot0 + col] = make_float2(M, lv);
-              }
-            }
+        for (int c = 0; c < 8; ++c) {
+          const int col = cb + c;
+          if (col < n) {
+            dst[static_cast<size_t>(col) * D] = __uint_as_float(o[c]);
+            if (t == col) a.part_ml[e.slot0 + col] = make_float2(mrow[col], __uint_as_float(l8[c]));
           }
         }
       }
       tc_fence_before();
-      mbar_arrive(o_free);
+      mbar_arrive(o_free + p);
 #ifdef ORION_TC_TRACE
       tr_[2] += clock64() - tep;
 #endif
@@ -721,8 +776,28 @@ bool make_map_t(CUtensorMap* m, const void* base, int64_t rows, int box_rows) {
 }
 }  // namespace
 
+int* g_dbg_host = nullptr;
+}  // namespace orion
+// Debugging only (ORION_DEBUG_HOST): copy the host-mapped progress counters (16 x 12 x 4 ints).
+extern "C" int orion_debug_state(int* out) {
+  if (!orion::g_dbg_host) return 0;
+  memcpy(out, orion::g_dbg_host, 16 * 12 * 4 * sizeof(int));
+  return 1;
+}
+namespace orion {
+
 orion_status launch_split_tct(const PlanHeader* h, const TcArgs& a, const void* k, const void* v,
                               int32_t num_pages, cudaStream_t st) {
+  if (!g_dbg_host && getenv("ORION_DEBUG_HOST")) {   // debugging only: progress counters survive a fault
+    void* hp = nullptr;
+    if (cudaHostAlloc(&hp, 16 * 12 * 4 * sizeof(int), cudaHostAllocMapped) == cudaSuccess) {
+      memset(hp, 0xff, 16 * 12 * 4 * sizeof(int));
+      void* dp = nullptr;
+      cudaHostGetDevicePointer(&dp, hp, 0);
+      cudaMemcpyToSymbol(tct::g_orion_hstate, &dp, sizeof(dp));
+      g_dbg_host = static_cast<int*>(hp);
+    }
+  }
   static int num_sms = 0;
   static cudaError_t attr_err = cudaSuccess;
   static bool init = false;
@@ -741,7 +816,8 @@ orion_status launch_split_tct(const PlanHeader* h, const TcArgs& a, const void* 
   if (!make_map_t(&mk, k, rows, big) || !make_map_t(&mv, v, rows, big) || !make_map_t(&mk16, k, rows, tct::kBox) ||
       !make_map_t(&mv16, v, rows, tct::kBox))
     return fail(ORION_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-  const int grid = std::min<int>(h->n_items, num_sms > 0 ? num_sms : 148);
+  int grid = std::min<int>(h->n_items, num_sms > 0 ? num_sms : 148);
+  if (const char* g = getenv("ORION_DEBUG_GRID")) grid = std::max(1, std::min(grid, atoi(g)));   // debugging only
   tct::split_tct_kernel<<<grid, tct::kThreads, tct::L::BYTES, st>>>(mk, mv, mk16, mv16, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ORION_ERR_CUDA, "split_tct_kernel: %s", cudaGetErrorString(e));
