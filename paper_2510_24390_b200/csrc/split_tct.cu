@@ -61,12 +61,15 @@ struct L {
   static constexpr int OFF_K = 2 * QB;
   static constexpr int OFF_V = OFF_K + kSK * KVB;
   static constexpr int OFF_P = OFF_V + kSV * KVB;
-  static constexpr int OFF_M = OFF_P + 2 * PB;   // running max m per column: [wg 2][item parity 2][64]
-  static constexpr int OFF_SH = OFF_M + 2 * 2 * 64 * 4;   // growth-path shifts: [wg 2][64]
-  static constexpr int OFF_SCHED = OFF_SH + 2 * 64 * 4;   // item schedule ring: 8 x 64 B
+  // per-warpgroup column state, indexed by the warpgroup's local column (< 32): the column split
+  // moves with npad from item to item while the two warpgroups may be on different tiles
+  static constexpr int OFF_M = OFF_P + 2 * PB;      // running max m: [wg 2][32]
+  static constexpr int OFF_SH = OFF_M + 2 * 32 * 4; // growth-path shifts: [wg 2][32]
+  static constexpr int OFF_RED = OFF_SH + 2 * 32 * 4;  // growth-path column max scratch: [wg 2][4 warps][32]
+  static constexpr int OFF_SCHED = OFF_RED + 2 * 4 * 32 * 4;  // item schedule ring: 8 x 64 B
   static constexpr int OFF_MI = OFF_SCHED + 8 * 64;        // MMA warp's item geometry: 4 x 32 B
   static constexpr int OFF_BAR = OFF_MI + 4 * 32;
-  static constexpr int N_BAR = 2 * kSK + 2 * kSV + 2 * 3 + 3 + 2 + 2 + 2 + 2 + 2 + 2 + 2 * 8;
+  static constexpr int N_BAR = 2 * kSK + 2 * kSV + 3 + 3 + 2 + 2 + 2 + 2 + 2 + 2 + 2 * 8;
   static constexpr int BYTES = OFF_BAR + N_BAR * 8 + 16;
 };
 static_assert(L::BYTES <= 232448, "shared memory budget");
@@ -235,19 +238,21 @@ __device__ __forceinline__ int next_nonempty(const TcArgs& a, int it) {
   return it;
 }
 
-// One softmax tile for a warpgroup: thread t owns token row t of S^T (N = padded query rows).
-// Writes P^T row t; on the rare growth path (first tile of an item, or a running max grown by more
-// than 2^8) it moves the per-column reference m (smem) and rescales O^T / L^T of this warpgroup.
-template <int N>
-__device__ __forceinline__ void softmax_tile(uint8_t* smem, uint32_t tmem, uint32_t lane_base, int p, int t,
-                                             uint32_t scol, uint32_t pslot, int tb, int lo, int hi,
-                                             float* mrow, float* shs, bool had, float scale_log2,
-                                             uint64_t* sfree, bool need_pv, uint64_t* pv_prev,
-                                             uint32_t pv_prev_par) {
-  uint32_t s[N];
-  if constexpr (N == 16) tmem_ld32x16(tmem + lane_base + scol, s);
-  if constexpr (N == 32) tmem_ld32x32(tmem + lane_base + scol, s);
-  if constexpr (N == 64) tmem_ld32x64(tmem + lane_base + scol, s);
+// One softmax tile for one warpgroup's half of the query columns: thread t owns token row t of S^T
+// and columns [c0, c0 + NH) (NH = padded query rows / 2); mrow / shs / red are this warpgroup's
+// arrays indexed by local column.  Writes its columns of P^T row t; on the
+// rare growth path (first tile of an item, or a running max grown by more than 2^8) it moves the
+// per-column reference m and rescales its columns of O^T / L^T.
+template <int NH>
+__device__ __forceinline__ void softmax_tile(uint32_t tmem, uint32_t lane_base, int p, int t, uint32_t scol,
+                                             uint8_t* pbuf, int c0, int tb, int lo, int hi, float* mrow,
+                                             float* shs, float* red, bool had, uint32_t ocol, uint32_t lcol,
+                                             float scale_log2, uint64_t* sfree, bool need_pv, uint64_t* pv_free,
+                                             uint32_t pv_free_par, uint64_t* pv_prev, uint32_t pv_prev_par) {
+  uint32_t s[NH];
+  if constexpr (NH == 8) tmem_ld32x8(tmem + lane_base + scol, s);
+  if constexpr (NH == 16) tmem_ld32x16(tmem + lane_base + scol, s);
+  if constexpr (NH == 32) tmem_ld32x32(tmem + lane_base + scol, s);
   tc_wait_ld();
   tc_fence_before();
   mbar_arrive(sfree);                                // QK(j+3) may overwrite this S^T buffer
@@ -256,7 +261,7 @@ __device__ __forceinline__ void softmax_tile(uint8_t* smem, uint32_t tmem, uint3
   // d = s * scale - mb (log2 domain, relative to the running reference; mb = 0 while unset)
   bool exceed = false;
 #pragma unroll
-  for (int c4 = 0; c4 < N; c4 += 4) {
+  for (int c4 = 0; c4 < NH; c4 += 4) {
     const float4 m4 = *reinterpret_cast<const float4*>(mrow + c4);
     const float mm[4] = {m4.x, m4.y, m4.z, m4.w};
 #pragma unroll
@@ -267,67 +272,62 @@ __device__ __forceinline__ void softmax_tile(uint8_t* smem, uint32_t tmem, uint3
       exceed |= valid && (mm[e] == -INFINITY || d > 8.f);
     }
   }
-  // P^T[p] (this warpgroup's buffer) is free once the PV of its previous tile is complete; on the
-  // growth path that PV is also the one O^T / L^T must have absorbed before they are rescaled.
-  uint8_t* pbuf = smem + L::OFF_P + pslot * L::PB;
   const bool grow = wg_any(exceed, 2 + p);
   if (grow) {
-    if (need_pv) {
-      mbar_wait(pv_prev, pv_prev_par);
-      tc_fence_after();
-    }
-    // column max of d over the 128 tokens: warp redux, then across the 4 warps via smem (the
-    // P^T buffer is scratch until P^T is written below)
-    float* red = reinterpret_cast<float*>(pbuf);
+    // column max of d over the 128 tokens: warp redux, then across the 4 warps via smem
     const int wq = t >> 5, ln = t & 31;
 #pragma unroll
-    for (int c = 0; c < N; ++c) {
+    for (int c = 0; c < NH; ++c) {
       const float wm = warp_max(__uint_as_float(s[c]));
-      if (ln == (c & 31)) red[wq * 64 + c] = wm;
+      if (ln == (c & 31)) red[wq * 32 + c] = wm;
     }
     wg_sync(2 + p, 128);
-    if (t < N) {                                     // column owner: new reference and shift
-      const float cm = fmaxf(fmaxf(red[t], red[64 + t]), fmaxf(red[128 + t], red[192 + t]));
-      const float mo = mrow[t];
+    if (t < NH) {                                    // column owner: new reference and shift
+      const int col = t;
+      const float cm = fmaxf(fmaxf(red[col], red[32 + col]), fmaxf(red[64 + col], red[96 + col]));
+      const float mo = mrow[col];
       const bool gc = cm > -INFINITY && (mo == -INFINITY || cm > 8.f);
       const float mb = mo == -INFINITY ? 0.f : mo;
-      shs[t] = gc ? cm : 0.f;
-      if (gc) mrow[t] = mb + cm;
+      shs[col] = gc ? cm : 0.f;
+      if (gc) mrow[col] = mb + cm;
     }
     wg_sync(2 + p, 128);
-    if (had) {   // O^T and L^T of this item follow the new reference: * 2^-shift
+    if (had) {   // this item's O^T / L^T columns follow the new reference: * 2^-shift, after PV(j-1)
+      mbar_wait(pv_prev, pv_prev_par);
+      tc_fence_after();
 #pragma unroll
-      for (int cb = 0; cb < N; cb += 16) {
-        uint32_t o[16], l16[16];
-        tmem_ld32x16(tmem + lane_base + colO(p) + cb, o);
-        tmem_ld32x16(tmem + lane_base + colL(p) + cb, l16);
+      for (int cb = 0; cb < NH; cb += 8) {
+        uint32_t o[8], l8[8];
+        tmem_ld32x8(tmem + lane_base + ocol + cb, o);
+        tmem_ld32x8(tmem + lane_base + lcol + cb, l8);
         tc_wait_ld();
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
+        for (int c = 0; c < 8; ++c) {
           const float al = ex2(-shs[cb + c]);
           o[c] = __float_as_uint(__uint_as_float(o[c]) * al);
-          l16[c] = __float_as_uint(__uint_as_float(l16[c]) * al);
+          l8[c] = __float_as_uint(__uint_as_float(l8[c]) * al);
         }
-        tmem_st32x16(tmem + lane_base + colO(p) + cb, o);
-        tmem_st32x16(tmem + lane_base + colL(p) + cb, l16);
+        tmem_st32x8(tmem + lane_base + ocol + cb, o);
+        tmem_st32x8(tmem + lane_base + lcol + cb, l8);
       }
       tc_wait_st();
     }
   }
-  // P^T row t (MN-major, 128B swizzle): p = 2^(d - shift), rounded to bf16.  The exponentials are
-  // formed in registers before the wait for the previous PV, so that wait overlaps the MUFU work.
-  uint32_t pk[N / 2];
+  // P^T row t, columns [c0, c0 + NH) (MN-major, 128B swizzle): p = 2^(d - shift) rounded to bf16.
+  // The exponentials are formed before the wait for PV(j-2), which frees this P^T buffer.
+  uint32_t pk[NH / 2];
 #pragma unroll
-  for (int c = 0; c < N; c += 2) {
+  for (int c = 0; c < NH; c += 2) {
     const float s0 = grow ? shs[c] : 0.f, s1 = grow ? shs[c + 1] : 0.f;
     pk[c / 2] = pack_bf16(ex2(__uint_as_float(s[c]) - s0), ex2(__uint_as_float(s[c + 1]) - s1));
   }
-  if (grow) wg_sync(2 + p, 128);                     // all red reads done before P^T overwrites them
-  else if (need_pv) mbar_wait(pv_prev, pv_prev_par);
+  if (need_pv) mbar_wait(pv_free, pv_free_par);
 #pragma unroll
-  for (int cc = 0; cc < N / 8; ++cc)
-    *reinterpret_cast<uint4*>(pbuf + t * 128 + ((cc ^ (t & 7)) << 4)) =
+  for (int cc = 0; cc < NH / 8; ++cc) {
+    const int chunk = (c0 >> 3) + cc;
+    *reinterpret_cast<uint4*>(pbuf + t * 128 + ((chunk ^ (t & 7)) << 4)) =
         make_uint4(pk[cc * 4 + 0], pk[cc * 4 + 1], pk[cc * 4 + 2], pk[cc * 4 + 3]);
+  }
 }
 
 // Per-CTA item schedule entry, produced by the scheduler warp (warp 1) and consumed in order by
@@ -358,31 +358,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* k_empty = k_full + kSK;
   uint64_t* v_full = k_empty + kSK;
   uint64_t* v_empty = v_full + kSV;
-  // Barriers a warpgroup waits on are private to it ([2] = per warpgroup): a warpgroup skips the
-  // other's items, and a phase-parity wait on a barrier shared with the other warpgroup could then
-  // run two phases ahead of it and alias.
-  uint64_t* s_full = v_empty + kSV;                 // [2][3]: S^T of warpgroup p's tile in buffer b
-  uint64_t* s_free = s_full + 2 * kSB;              // [3]: S^T buffer read (MMA is the only waiter)
-  uint64_t* p_full = s_free + kSB;                  // [2]: P^T[p] written
-  uint64_t* pv_done = p_full + 2;                   // [2]: PV of warpgroup p's tile complete
+  // Every waiter consumes the phases of each barrier in order (both softmax warpgroups take part
+  // in every tile), so no phase-parity wait can run two phases ahead and alias.
+  uint64_t* s_full = v_empty + kSV;                 // [3]: S^T of tile j in buffer j % 3
+  uint64_t* s_free = s_full + kSB;                  // [3]: S^T buffer read by both warpgroups
+  uint64_t* p_full = s_free + kSB;                  // [2]: P^T[j & 1] written by both warpgroups
+  uint64_t* pv_done = p_full + 2;                   // [2]: PV(j) complete
   uint64_t* q_full = pv_done + 2;
   uint64_t* q_empty = q_full + 2;
-  uint64_t* o_free = q_empty + 2;                   // [2]: warpgroup p's item epilogue done
-  uint64_t* acc_full = o_free + 2;                  // [2]: last PV of warpgroup p's item complete
+  uint64_t* o_free = q_empty + 2;                   // [2]: epilogue of the item using O^T/L^T[i] done
+  uint64_t* acc_full = o_free + 2;                  // [2]: last PV into O^T/L^T[i] complete
   uint64_t* sch_full = acc_full + 2;
   uint64_t* sch_empty = sch_full + kSched;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sch_empty + kSched);
-  float* mall = reinterpret_cast<float*>(smem + L::OFF_M);
   Sched* ring = reinterpret_cast<Sched*>(smem + L::OFF_SCHED);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < kSK; ++s) { mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1); }
     for (int s = 0; s < kSV; ++s) { mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1); }
-    for (int b = 0; b < kSB; ++b) { mbar_init(s_full + b, 1); mbar_init(s_full + kSB + b, 1); mbar_init(s_free + b, 128); }
+    for (int b = 0; b < kSB; ++b) { mbar_init(s_full + b, 1); mbar_init(s_free + b, 256); }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(p_full + b, 128); mbar_init(pv_done + b, 1); mbar_init(q_full + b, 1);
-      mbar_init(q_empty + b, 1); mbar_init(o_free + b, 128); mbar_init(acc_full + b, 1);
+      mbar_init(p_full + b, 256); mbar_init(pv_done + b, 1); mbar_init(q_full + b, 1);
+      mbar_init(q_empty + b, 1); mbar_init(o_free + b, 256); mbar_init(acc_full + b, 1);
     }
     for (int b = 0; b < kSched; ++b) { mbar_init(sch_full + b, 1); mbar_init(sch_empty + b, kSchedConsumers); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -561,7 +559,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto np_of = [&](uint32_t k) { return mi[(k & 3) * 8 + 4]; };
     uint32_t kq = 0, tq = 0, jq = 0;                // QK cursor (item, tile in item, global tile)
     uint32_t kv = 0, tv = 0, jv = 0;                // PV cursor
-    uint32_t ppar = 0;                              // phase parity of p_full[p] (bit p)
     bool q_live;
     {
       const Sched e = read_sched(ring, sch_full, sch_empty, 0, lane == 0);
@@ -587,7 +584,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t oq = static_cast<uint64_t>(((ks >> 2) * L::HALF_Q + (ks & 3) * 32) >> 4);
           mma_ss(tmem + colS(j % kSB), dk + ok, dq + oq, id, ks > 0);
         }
-        tc_commit(s_full + (kq & 1) * kSB + (j % kSB));
+        tc_commit(s_full + (j % kSB));
         tc_commit(k_empty + s);
         if (static_cast<int>(tq) + 1 == ntq) tc_commit(q_empty + (kq & 1));   // item's last QK
       }
@@ -605,7 +602,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t j = jv;
       if (lane == 0) { DBG_STATE(warp, 2, jv); DBG_STATE(warp, 3, kv); }
       const int s = j % kSV;
-      const uint32_t wg = kv & 1;
+      const uint32_t wg = kv & 1;                   // accumulator pair of item kv
       TW(6, mbar_wait(v_full + s, (j / kSV) & 1));
       {
         // A partial tile's TMA boxes (16-row granular) may carry rows outside [t0, end) -- e.g.
@@ -626,12 +623,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
         }
       }
-      TW(4, mbar_wait(p_full + wg, (ppar >> wg) & 1));
-      ppar ^= 1u << wg;
+      TW(4, mbar_wait(p_full + (j & 1), (j >> 1) & 1));
       if (tv == 0 && kv >= 2) TW(5, mbar_wait(o_free + wg, ((kv >> 1) - 1) & 1));   // item kv-2 read out
       tc_fence_after();
       const uint64_t dv = dv0 + static_cast<uint64_t>((s * L::KVB) >> 4);
-      const uint64_t dp = dp0 + static_cast<uint64_t>((wg * L::PB) >> 4);
+      const uint64_t dp = dp0 + static_cast<uint64_t>(((j & 1) * L::PB) >> 4);
       const int npv = np_of(kv);
       const uint32_t id_pv = idesc(npv, true, true);
       const uint32_t id_l = idesc(npv, false, true);
@@ -644,7 +640,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_ss(tmem + colO(wg), dv + o, dp + o, id_pv, acc);
           mma_ts(tmem + colL(wg), tmem + kColOnes + kt * 8, dp + o, id_l, acc);
         }
-        tc_commit(pv_done + wg);
+        tc_commit(pv_done + (j & 1));
         tc_commit(v_empty + s);
         if (static_cast<int>(tv) + 1 == nt_of(kv)) tc_commit(acc_full + wg);   // item complete
       }
@@ -662,74 +658,73 @@ __global__ void __launch_bounds__(kThreads, 1)
     TRACE_DUMP("mma");
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ softmax / epilogue
-    // Warpgroup p owns the items k with k & 1 == p: every tile of the item, one accumulator
-    // (O^T/L^T[p]), its epilogue overlapping the other warpgroup's next item.
+    // Both warpgroups take part in every tile: warpgroup p owns query columns [p*NH, (p+1)*NH) of
+    // S^T / P^T / O^T / L^T (NH = npad / 2), so the two halves never need merging.  Item k
+    // accumulates into O^T/L^T[k & 1]: its epilogue overlaps the next item's first PVs.
     const int p = (warp - 4) >> 2;
     const int t = tid - 128 - p * 128;              // token row of S^T / d lane of O^T
     const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    float* mrow = mall + p * 64;
-    float* shs = reinterpret_cast<float*>(smem + L::OFF_SH) + p * 64;
-    uint32_t j = 0;                                 // global tile index (selects the S^T buffer)
-    uint32_t mj = 0;                                // tiles this warpgroup has processed
-    uint32_t spar = 0;                              // phase parity of s_full[p][b] (bit b)
+    float* mrow = reinterpret_cast<float*>(smem + L::OFF_M) + p * 32;
+    float* shs = reinterpret_cast<float*>(smem + L::OFF_SH) + p * 32;
+    float* red = reinterpret_cast<float*>(smem + L::OFF_RED) + p * 128;
+    uint32_t j = 0;                                 // global tile index
     for (uint32_t k = 0;; ++k) {
       const Sched e = read_sched(ring, sch_full, sch_empty, k, true);
       if (!e.valid) break;
-      if ((k & 1) != static_cast<uint32_t>(p)) { j += e.ntiles; continue; }
-      if (t < 64) mrow[t] = -INFINITY;
+      const int nh = e.npad >> 1, c0 = p * nh;
+      const uint32_t kp = k & 1;
+      if (t < nh) mrow[t] = -INFINITY;
       wg_sync(2 + p, 128);
       for (int tt = 0; tt < e.ntiles; ++tt, ++j) {
         const int tb = e.base + tt * kTok;
         const int lo = max(tb, e.t0), hi = min(tb + kTok, e.end);
-        if ((t & 31) == 0) { DBG_STATE(warp, 0, j); DBG_STATE(warp, 1, k); DBG_STATE(warp, 2, tt); }
         const uint32_t b = j % kSB;
-        TW(6, mbar_wait(s_full + p * kSB + b, (spar >> b) & 1));
-        spar ^= 1u << b;
+        TW(6, mbar_wait(s_full + b, (j / kSB) & 1));
         tc_fence_after();
 #ifdef ORION_TC_TRACE
         const unsigned long long tsm = clock64();
 #endif
-        const bool need_pv = mj > 0;                // P^T[p] still feeds the PV of tile mj-1
-        const uint32_t pvpar = (mj - 1) & 1;
-        if (e.npad == 16) softmax_tile<16>(smem, tmem, lane_base, p, t, colS(b), p, tb, lo, hi, mrow, shs, tt > 0, a.scale_log2, s_free + b, need_pv, pv_done + p, pvpar);
-        else if (e.npad == 32) softmax_tile<32>(smem, tmem, lane_base, p, t, colS(b), p, tb, lo, hi, mrow, shs, tt > 0, a.scale_log2, s_free + b, need_pv, pv_done + p, pvpar);
-        else softmax_tile<64>(smem, tmem, lane_base, p, t, colS(b), p, tb, lo, hi, mrow, shs, tt > 0, a.scale_log2, s_free + b, need_pv, pv_done + p, pvpar);
+        uint8_t* pbuf = smem + L::OFF_P + (j & 1) * L::PB;
+        const bool need_pv = j >= 2;                // P^T[j & 1] still feeds PV(j-2)
+        const uint32_t pfp = ((j - 2) >> 1) & 1, ppp = ((j - 1) >> 1) & 1;
+        uint64_t* pvf = pv_done + (j & 1);
+        uint64_t* pvp = pv_done + ((j - 1) & 1);
+        const uint32_t oc = colO(kp) + c0, lc = colL(kp) + c0, sc = colS(b) + c0;
+        if (nh == 8) softmax_tile<8>(tmem, lane_base, p, t, sc, pbuf, c0, tb, lo, hi, mrow, shs, red, tt > 0, oc, lc, a.scale_log2, s_free + b, need_pv, pvf, pfp, pvp, ppp);
+        else if (nh == 16) softmax_tile<16>(tmem, lane_base, p, t, sc, pbuf, c0, tb, lo, hi, mrow, shs, red, tt > 0, oc, lc, a.scale_log2, s_free + b, need_pv, pvf, pfp, pvp, ppp);
+        else softmax_tile<32>(tmem, lane_base, p, t, sc, pbuf, c0, tb, lo, hi, mrow, shs, red, tt > 0, oc, lc, a.scale_log2, s_free + b, need_pv, pvf, pfp, pvp, ppp);
         fence_proxy_async();
         tc_fence_before();
-        mbar_arrive(p_full + p);
-        ++mj;
-        if ((t & 31) == 0) DBG_STATE(warp, 3, 2);
+        mbar_arrive(p_full + (j & 1));
 #ifdef ORION_TC_TRACE
         tr_[1] += clock64() - tsm;
 #endif
       }
-      // ---- epilogue: this item's partial (m, l, acc) per query row
+      // ---- epilogue: this warpgroup's columns of the item's partial (m, l, acc)
 #ifdef ORION_TC_TRACE
       const unsigned long long tep = clock64();
 #endif
-      // last PV of the item: a dedicated per-warpgroup barrier (pv_done[] could already have moved
-      // on by two phases, driven by the other warpgroup's next item)
-      TW(8, mbar_wait(acc_full + p, (k >> 1) & 1));
+      TW(8, mbar_wait(acc_full + kp, (k >> 1) & 1));
       tc_fence_after();
       const int n = e.n_rows;
       float* dst = a.part_acc + static_cast<size_t>(e.slot0) * D + t;
 #pragma unroll 1
-      for (int cb = 0; cb < e.npad; cb += 8) {
+      for (int cb = 0; cb < nh; cb += 8) {
         uint32_t o[8], l8[8];
-        tmem_ld32x8(tmem + lane_base + colO(p) + cb, o);
-        tmem_ld32x8(tmem + lane_base + colL(p) + cb, l8);
+        tmem_ld32x8(tmem + lane_base + colO(kp) + c0 + cb, o);
+        tmem_ld32x8(tmem + lane_base + colL(kp) + c0 + cb, l8);
         tc_wait_ld();
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const int col = cb + c;
+          const int col = c0 + cb + c;
           if (col < n) {
             dst[static_cast<size_t>(col) * D] = __uint_as_float(o[c]);
-            if (t == col) a.part_ml[e.slot0 + col] = make_float2(mrow[col], __uint_as_float(l8[c]));
+            if (t == cb + c) a.part_ml[e.slot0 + col] = make_float2(mrow[cb + c], __uint_as_float(l8[c]));
           }
         }
       }
       tc_fence_before();
-      mbar_arrive(o_free + p);
+      mbar_arrive(o_free + kp);
 #ifdef ORION_TC_TRACE
       tr_[2] += clock64() - tep;
 #endif
