@@ -47,9 +47,7 @@ constexpr int kWarpTMAV = 0;              // the TMEM-alloc warp streams V once 
 // TMEM columns
 constexpr int kSB = 3;                    // S^T buffers: tile j uses j % 3
 __device__ __forceinline__ uint32_t colS(uint32_t b) { return b * 64; }
-__device__ __forceinline__ uint32_t colO(uint32_t p) { return 192 + p * 64; }   // per warpgroup
-__device__ __forceinline__ uint32_t colL(uint32_t p) { return 320 + p * 64; }
-constexpr uint32_t kColOnes = 448;        // 64 columns: 128 x 128 bf16 ones (A operand of L)
+__device__ __forceinline__ uint32_t colO(uint32_t i) { return 192 + i * 64; }   // O^T of item parity i
 
 struct L {
   static constexpr int QB = 64 * D * 2;          // 16 KB: [2 halves][64 rows][128 B]
@@ -90,9 +88,6 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
                : "memory");
 }
 __device__ int g_orion_dump[1024];   // debugging: a timed-out wait asks every role of the CTA to report
-__device__ int* g_orion_hstate;   // debugging (ORION_DEBUG_HOST): host-mapped [16][12][4] progress counters
-#define DBG_STATE(w, i, v) do { if (g_orion_hstate && blockIdx.x < 16) \
-    reinterpret_cast<volatile int*>(g_orion_hstate)[(blockIdx.x * 12 + (w)) * 4 + (i)] = (v); } while (0)
 
 // Blocking wait.  try_wait carries a suspend-time hint so a waiting warp sleeps instead of
 // spinning (it resumes as soon as the phase completes); a protocol bug traps after ~2 s instead of
@@ -246,7 +241,7 @@ __device__ __forceinline__ int next_nonempty(const TcArgs& a, int it) {
 template <int NH>
 __device__ __forceinline__ void softmax_tile(uint32_t tmem, uint32_t lane_base, int p, int t, uint32_t scol,
                                              uint8_t* pbuf, int c0, int tb, int lo, int hi, float* mrow,
-                                             float* shs, float* red, bool had, uint32_t ocol, uint32_t lcol,
+                                             float* shs, float* red, bool had, uint32_t ocol, float (&ls)[NH],
                                              float scale_log2, uint64_t* sfree, bool need_pv, uint64_t* pv_free,
                                              uint32_t pv_free_par, uint64_t* pv_prev, uint32_t pv_prev_par) {
   uint32_t s[NH];
@@ -292,23 +287,19 @@ __device__ __forceinline__ void softmax_tile(uint32_t tmem, uint32_t lane_base, 
       if (gc) mrow[col] = mb + cm;
     }
     wg_sync(2 + p, 128);
-    if (had) {   // this item's O^T / L^T columns follow the new reference: * 2^-shift, after PV(j-1)
-      mbar_wait(pv_prev, pv_prev_par);
+    if (had) {   // this item's O^T columns and row sums follow the new reference: * 2^-shift
+#pragma unroll
+      for (int c = 0; c < NH; ++c) ls[c] *= ex2(-shs[c]);
+      mbar_wait(pv_prev, pv_prev_par);             // O^T has absorbed PV(j-1)
       tc_fence_after();
 #pragma unroll
       for (int cb = 0; cb < NH; cb += 8) {
-        uint32_t o[8], l8[8];
+        uint32_t o[8];
         tmem_ld32x8(tmem + lane_base + ocol + cb, o);
-        tmem_ld32x8(tmem + lane_base + lcol + cb, l8);
         tc_wait_ld();
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float al = ex2(-shs[cb + c]);
-          o[c] = __float_as_uint(__uint_as_float(o[c]) * al);
-          l8[c] = __float_as_uint(__uint_as_float(l8[c]) * al);
-        }
+        for (int c = 0; c < 8; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * ex2(-shs[cb + c]));
         tmem_st32x8(tmem + lane_base + ocol + cb, o);
-        tmem_st32x8(tmem + lane_base + lcol + cb, l8);
       }
       tc_wait_st();
     }
@@ -320,6 +311,8 @@ __device__ __forceinline__ void softmax_tile(uint32_t tmem, uint32_t lane_base, 
   for (int c = 0; c < NH; c += 2) {
     const float s0 = grow ? shs[c] : 0.f, s1 = grow ? shs[c + 1] : 0.f;
     pk[c / 2] = pack_bf16(ex2(__uint_as_float(s[c]) - s0), ex2(__uint_as_float(s[c + 1]) - s1));
+    ls[c] += __uint_as_float(pk[c / 2] << 16);       // row sums of exactly the bf16 P fed to PV
+    ls[c + 1] += __uint_as_float(pk[c / 2] & 0xFFFF0000u);
   }
   if (need_pv) mbar_wait(pv_free, pv_free_par);
 #pragma unroll
@@ -347,29 +340,107 @@ __device__ __forceinline__ Sched read_sched(const Sched* ring, uint64_t* full, u
   return e;
 }
 
+// Barrier block layout (shared by the kernel and softmax_item).
+struct Bars {
+  uint64_t *k_full, *k_empty, *v_full, *v_empty, *s_full, *s_free, *p_full, *pv_done, *q_full, *q_empty,
+      *o_free, *acc_full, *sch_full, *sch_empty;
+};
+__device__ __forceinline__ Bars carve_bars(uint8_t* smem) {
+  uint64_t* b = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  Bars r;
+  // Every waiter consumes the phases of each barrier in order (both softmax warpgroups take part
+  // in every tile), so no phase-parity wait can run two phases ahead and alias.
+  r.k_full = b; r.k_empty = b + kSK;
+  r.v_full = r.k_empty + kSK; r.v_empty = r.v_full + kSV;
+  r.s_full = r.v_empty + kSV;                       // [3]: S^T of tile j in buffer j % 3
+  r.s_free = r.s_full + kSB;                        // [3]: S^T buffer read by both warpgroups
+  r.p_full = r.s_free + kSB;                        // [2]: P^T[j & 1] written by both warpgroups
+  r.pv_done = r.p_full + 2;                         // [2]: PV(j) complete
+  r.q_full = r.pv_done + 2; r.q_empty = r.q_full + 2;
+  r.o_free = r.q_empty + 2;                         // [2]: epilogue of the item using O^T[i] done
+  r.acc_full = r.o_free + 2;                        // [2]: last PV into O^T[i] complete
+  r.sch_full = r.acc_full + 2; r.sch_empty = r.sch_full + kSched;
+  return r;
+}
+
+// All tiles of one item for one softmax warpgroup (query columns [p*NH, (p+1)*NH)), then its
+// share of the item's partial: acc from O^T, m from mrow, l from the per-thread row sums reduced
+// over the 128 token rows.
+template <int NH>
+__device__ __forceinline__ void softmax_item(uint8_t* smem, uint32_t tmem, uint32_t lane_base, int p, int t,
+                                             const Sched& e, uint32_t k, uint32_t& j, float* mrow, float* shs,
+                                             float* red, const Bars& B, const TcArgs& a) {
+  const int c0 = p * NH;
+  const uint32_t kp = k & 1;
+  float ls[NH];
+#pragma unroll
+  for (int c = 0; c < NH; ++c) ls[c] = 0.f;
+  if (t < NH) mrow[t] = -INFINITY;
+  wg_sync(2 + p, 128);
+  for (int tt = 0; tt < e.ntiles; ++tt, ++j) {
+    const int tb = e.base + tt * kTok;
+    const int lo = max(tb, e.t0), hi = min(tb + kTok, e.end);
+    const uint32_t b = j % kSB;
+    mbar_wait(B.s_full + b, (j / kSB) & 1);
+    tc_fence_after();
+    uint8_t* pbuf = smem + L::OFF_P + (j & 1) * L::PB;
+    const bool need_pv = j >= 2;                    // P^T[j & 1] still feeds PV(j-2)
+    softmax_tile<NH>(tmem, lane_base, p, t, colS(b) + c0, pbuf, c0, tb, lo, hi, mrow, shs, red, tt > 0,
+                     colO(kp) + c0, ls, a.scale_log2, B.s_free + b, need_pv, B.pv_done + (j & 1),
+                     ((j - 2) >> 1) & 1, B.pv_done + ((j - 1) & 1), ((j - 1) >> 1) & 1);
+    fence_proxy_async();
+    tc_fence_before();
+    mbar_arrive(B.p_full + (j & 1));
+  }
+  // ---- epilogue.  l: butterfly over the warp (plain levels while more lanes than columns, then a
+  // reduce-scatter leaving column ln % NH in lane ln), then across the 4 warps via red.
+  const int ln = t & 31, wq = t >> 5;
+#pragma unroll
+  for (int off = 16; off >= NH; off >>= 1)
+#pragma unroll
+    for (int c = 0; c < NH; ++c) ls[c] += __shfl_xor_sync(0xffffffffu, ls[c], off);
+#pragma unroll
+  for (int off = (NH >= 32 ? 16 : NH / 2), n = (NH >= 32 ? 32 : NH); off >= 1; off >>= 1, n >>= 1) {
+    const bool up = (ln & off) != 0;
+#pragma unroll
+    for (int i = 0; i < n / 2; ++i) {
+      const float send = up ? ls[i] : ls[i + n / 2];
+      const float keep = up ? ls[i + n / 2] : ls[i];
+      ls[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  if (ln < NH) red[wq * 32 + ln] = ls[0];
+  mbar_wait(B.acc_full + kp, (k >> 1) & 1);
+  tc_fence_after();
+  wg_sync(2 + p, 128);
+  const int n = e.n_rows;
+  if (t < NH && c0 + t < n)
+    a.part_ml[e.slot0 + c0 + t] = make_float2(mrow[t], red[t] + red[32 + t] + red[64 + t] + red[96 + t]);
+  float* dst = a.part_acc + static_cast<size_t>(e.slot0) * D + t;
+#pragma unroll
+  for (int cb = 0; cb < NH; cb += 8) {
+    uint32_t o[8];
+    tmem_ld32x8(tmem + lane_base + colO(kp) + c0 + cb, o);
+    tc_wait_ld();
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (c0 + cb + c < n) dst[static_cast<size_t>(c0 + cb + c) * D] = __uint_as_float(o[c]);
+  }
+  tc_fence_before();
+  mbar_arrive(B.o_free + kp);
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     split_tct_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                      const __grid_constant__ CUtensorMap tmK16, const __grid_constant__ CUtensorMap tmV16,
                      const TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   if (smem_u32(smem) & 1023) __trap();               // 128B-swizzle atoms need 1 KB alignment
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
-  uint64_t* k_full = bars;
-  uint64_t* k_empty = k_full + kSK;
-  uint64_t* v_full = k_empty + kSK;
-  uint64_t* v_empty = v_full + kSV;
-  // Every waiter consumes the phases of each barrier in order (both softmax warpgroups take part
-  // in every tile), so no phase-parity wait can run two phases ahead and alias.
-  uint64_t* s_full = v_empty + kSV;                 // [3]: S^T of tile j in buffer j % 3
-  uint64_t* s_free = s_full + kSB;                  // [3]: S^T buffer read by both warpgroups
-  uint64_t* p_full = s_free + kSB;                  // [2]: P^T[j & 1] written by both warpgroups
-  uint64_t* pv_done = p_full + 2;                   // [2]: PV(j) complete
-  uint64_t* q_full = pv_done + 2;
-  uint64_t* q_empty = q_full + 2;
-  uint64_t* o_free = q_empty + 2;                   // [2]: epilogue of the item using O^T/L^T[i] done
-  uint64_t* acc_full = o_free + 2;                  // [2]: last PV into O^T/L^T[i] complete
-  uint64_t* sch_full = acc_full + 2;
-  uint64_t* sch_empty = sch_full + kSched;
+  const Bars bars = carve_bars(smem);
+  uint64_t *k_full = bars.k_full, *k_empty = bars.k_empty, *v_full = bars.v_full, *v_empty = bars.v_empty;
+  uint64_t *s_full = bars.s_full, *s_free = bars.s_free, *p_full = bars.p_full, *pv_done = bars.pv_done;
+  uint64_t *q_full = bars.q_full, *q_empty = bars.q_empty, *o_free = bars.o_free, *acc_full = bars.acc_full;
+  uint64_t *sch_full = bars.sch_full, *sch_empty = bars.sch_empty;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sch_empty + kSched);
   Sched* ring = reinterpret_cast<Sched*>(smem + L::OFF_SCHED);
 
@@ -402,18 +473,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int n_items = a.n_items;
-  if (warp >= 4 && warp < 8) {                      // ones (bf16 pairs) for the l MMA: 64 columns
-    uint32_t one[32];
-#pragma unroll
-    for (int c = 0; c < 32; ++c) one[c] = 0x3F803F80u;
-    const uint32_t lb = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    tmem_st32x32(tmem + lb + kColOnes, one);
-    tmem_st32x32(tmem + lb + kColOnes + 32, one);
-    tc_wait_st();
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
 
   TRACE_DECL
   if (warp == kWarpSched) {
@@ -514,7 +573,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int b = 0; b < 8; ++b) rr[b] = __shfl_sync(0xffffffffu, brow[b], src);
           const int st = j % nst;
-          if (lane == 0) DBG_STATE(warp, 0, j);
           const int rpb = tf ? big : kBox;
           const uint32_t bytes = static_cast<uint32_t>(tn * rpb * 128 * 2);
           const CUtensorMap* m = tf ? mbig : msml;
@@ -567,7 +625,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     auto issue_qk = [&]() {
       const uint32_t j = jq;
-      if (lane == 0) { DBG_STATE(warp, 0, jq); DBG_STATE(warp, 1, kq); }
       if (tq == 0) TW(1, mbar_wait(q_full + (kq & 1), (kq >> 1) & 1));
       const int s = j % kSK;
       TW(2, mbar_wait(k_full + s, (j / kSK) & 1));
@@ -577,6 +634,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t dq = dq0 + static_cast<uint64_t>(((kq & 1) * L::QB) >> 4);
       const uint64_t dk = dk0 + static_cast<uint64_t>((s * L::KVB) >> 4);
       const uint32_t id = idesc(np_of(kq), false, false);
+#ifdef ORION_TC_TRACE
+      const unsigned long long tq0 = clock64();
+#endif
       if (elect_one()) {
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
@@ -589,21 +649,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (static_cast<int>(tq) + 1 == ntq) tc_commit(q_empty + (kq & 1));   // item's last QK
       }
       __syncwarp();
+#ifdef ORION_TC_TRACE
+      tr_[8] += clock64() - tq0;
+#endif
       ++jq;
       if (static_cast<int>(++tq) == ntq) {
         tq = 0;
         ++kq;
-        const Sched e = read_sched(ring, sch_full, sch_empty, kq, lane == 0);
+        Sched e;
+        TW(7, e = read_sched(ring, sch_full, sch_empty, kq, lane == 0));
         q_live = e.valid;
         set_of(kq, e);
       }
     };
     auto issue_pv = [&]() {
       const uint32_t j = jv;
-      if (lane == 0) { DBG_STATE(warp, 2, jv); DBG_STATE(warp, 3, kv); }
       const int s = j % kSV;
       const uint32_t wg = kv & 1;                   // accumulator pair of item kv
       TW(6, mbar_wait(v_full + s, (j / kSV) & 1));
+#ifdef ORION_TC_TRACE
+      const unsigned long long tz0 = clock64();
+#endif
       {
         // A partial tile's TMA boxes (16-row granular) may carry rows outside [t0, end) -- e.g.
         // never-written slots past own_len.  Their P is exactly 0, but 0 x NaN is NaN: zero them.
@@ -623,6 +689,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
         }
       }
+#ifdef ORION_TC_TRACE
+      tr_[0] += clock64() - tz0;
+#endif
       TW(4, mbar_wait(p_full + (j & 1), (j >> 1) & 1));
       if (tv == 0 && kv >= 2) TW(5, mbar_wait(o_free + wg, ((kv >> 1) - 1) & 1));   // item kv-2 read out
       tc_fence_after();
@@ -630,21 +699,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t dp = dp0 + static_cast<uint64_t>(((j & 1) * L::PB) >> 4);
       const int npv = np_of(kv);
       const uint32_t id_pv = idesc(npv, true, true);
-      const uint32_t id_l = idesc(npv, false, true);
       const bool first = tv == 0;
+#ifdef ORION_TC_TRACE
+      const unsigned long long tp0 = clock64();
+#endif
       if (elect_one()) {
 #pragma unroll
         for (int kt = 0; kt < kTok / 16; ++kt) {
           const uint64_t o = static_cast<uint64_t>((kt * 16 * 128) >> 4);
           const uint32_t acc = (!first || kt > 0) ? 1u : 0u;
           mma_ss(tmem + colO(wg), dv + o, dp + o, id_pv, acc);
-          mma_ts(tmem + colL(wg), tmem + kColOnes + kt * 8, dp + o, id_l, acc);
         }
         tc_commit(pv_done + (j & 1));
         tc_commit(v_empty + s);
         if (static_cast<int>(tv) + 1 == nt_of(kv)) tc_commit(acc_full + wg);   // item complete
       }
       __syncwarp();
+#ifdef ORION_TC_TRACE
+      tr_[9] += clock64() - tp0;
+#endif
       ++jv;
       if (static_cast<int>(++tv) == nt_of(kv)) { tv = 0; ++kv; }
     };
@@ -659,8 +732,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ softmax / epilogue
     // Both warpgroups take part in every tile: warpgroup p owns query columns [p*NH, (p+1)*NH) of
-    // S^T / P^T / O^T / L^T (NH = npad / 2), so the two halves never need merging.  Item k
-    // accumulates into O^T/L^T[k & 1]: its epilogue overlaps the next item's first PVs.
+    // S^T / P^T / O^T and of the row sums (NH = npad / 2), so the two halves never need merging.
+    // Item k accumulates into O^T[k & 1]: its epilogue overlaps the next item's first PVs.
     const int p = (warp - 4) >> 2;
     const int t = tid - 128 - p * 128;              // token row of S^T / d lane of O^T
     const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
@@ -671,63 +744,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (uint32_t k = 0;; ++k) {
       const Sched e = read_sched(ring, sch_full, sch_empty, k, true);
       if (!e.valid) break;
-      const int nh = e.npad >> 1, c0 = p * nh;
-      const uint32_t kp = k & 1;
-      if (t < nh) mrow[t] = -INFINITY;
-      wg_sync(2 + p, 128);
-      for (int tt = 0; tt < e.ntiles; ++tt, ++j) {
-        const int tb = e.base + tt * kTok;
-        const int lo = max(tb, e.t0), hi = min(tb + kTok, e.end);
-        const uint32_t b = j % kSB;
-        TW(6, mbar_wait(s_full + b, (j / kSB) & 1));
-        tc_fence_after();
-#ifdef ORION_TC_TRACE
-        const unsigned long long tsm = clock64();
-#endif
-        uint8_t* pbuf = smem + L::OFF_P + (j & 1) * L::PB;
-        const bool need_pv = j >= 2;                // P^T[j & 1] still feeds PV(j-2)
-        const uint32_t pfp = ((j - 2) >> 1) & 1, ppp = ((j - 1) >> 1) & 1;
-        uint64_t* pvf = pv_done + (j & 1);
-        uint64_t* pvp = pv_done + ((j - 1) & 1);
-        const uint32_t oc = colO(kp) + c0, lc = colL(kp) + c0, sc = colS(b) + c0;
-        if (nh == 8) softmax_tile<8>(tmem, lane_base, p, t, sc, pbuf, c0, tb, lo, hi, mrow, shs, red, tt > 0, oc, lc, a.scale_log2, s_free + b, need_pv, pvf, pfp, pvp, ppp);
-        else if (nh == 16) softmax_tile<16>(tmem, lane_base, p, t, sc, pbuf, c0, tb, lo, hi, mrow, shs, red, tt > 0, oc, lc, a.scale_log2, s_free + b, need_pv, pvf, pfp, pvp, ppp);
-        else softmax_tile<32>(tmem, lane_base, p, t, sc, pbuf, c0, tb, lo, hi, mrow, shs, red, tt > 0, oc, lc, a.scale_log2, s_free + b, need_pv, pvf, pfp, pvp, ppp);
-        fence_proxy_async();
-        tc_fence_before();
-        mbar_arrive(p_full + (j & 1));
-#ifdef ORION_TC_TRACE
-        tr_[1] += clock64() - tsm;
-#endif
-      }
-      // ---- epilogue: this warpgroup's columns of the item's partial (m, l, acc)
-#ifdef ORION_TC_TRACE
-      const unsigned long long tep = clock64();
-#endif
-      TW(8, mbar_wait(acc_full + kp, (k >> 1) & 1));
-      tc_fence_after();
-      const int n = e.n_rows;
-      float* dst = a.part_acc + static_cast<size_t>(e.slot0) * D + t;
-#pragma unroll 1
-      for (int cb = 0; cb < nh; cb += 8) {
-        uint32_t o[8], l8[8];
-        tmem_ld32x8(tmem + lane_base + colO(kp) + c0 + cb, o);
-        tmem_ld32x8(tmem + lane_base + colL(kp) + c0 + cb, l8);
-        tc_wait_ld();
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const int col = c0 + cb + c;
-          if (col < n) {
-            dst[static_cast<size_t>(col) * D] = __uint_as_float(o[c]);
-            if (t == cb + c) a.part_ml[e.slot0 + col] = make_float2(mrow[cb + c], __uint_as_float(l8[c]));
-          }
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(o_free + kp);
-#ifdef ORION_TC_TRACE
-      tr_[2] += clock64() - tep;
-#endif
+      if (e.npad == 16) softmax_item<8>(smem, tmem, lane_base, p, t, e, k, j, mrow, shs, red, bars, a);
+      else if (e.npad == 32) softmax_item<16>(smem, tmem, lane_base, p, t, e, k, j, mrow, shs, red, bars, a);
+      else softmax_item<32>(smem, tmem, lane_base, p, t, e, k, j, mrow, shs, red, bars, a);
     }
     TRACE_DUMP("softmax");
   }
@@ -771,28 +790,8 @@ bool make_map_t(CUtensorMap* m, const void* base, int64_t rows, int box_rows) {
 }
 }  // namespace
 
-int* g_dbg_host = nullptr;
-}  // namespace orion
-// Debugging only (ORION_DEBUG_HOST): copy the host-mapped progress counters (16 x 12 x 4 ints).
-extern "C" int orion_debug_state(int* out) {
-  if (!orion::g_dbg_host) return 0;
-  memcpy(out, orion::g_dbg_host, 16 * 12 * 4 * sizeof(int));
-  return 1;
-}
-namespace orion {
-
 orion_status launch_split_tct(const PlanHeader* h, const TcArgs& a, const void* k, const void* v,
                               int32_t num_pages, cudaStream_t st) {
-  if (!g_dbg_host && getenv("ORION_DEBUG_HOST")) {   // debugging only: progress counters survive a fault
-    void* hp = nullptr;
-    if (cudaHostAlloc(&hp, 16 * 12 * 4 * sizeof(int), cudaHostAllocMapped) == cudaSuccess) {
-      memset(hp, 0xff, 16 * 12 * 4 * sizeof(int));
-      void* dp = nullptr;
-      cudaHostGetDevicePointer(&dp, hp, 0);
-      cudaMemcpyToSymbol(tct::g_orion_hstate, &dp, sizeof(dp));
-      g_dbg_host = static_cast<int*>(hp);
-    }
-  }
   static int num_sms = 0;
   static cudaError_t attr_err = cudaSuccess;
   static bool init = false;

@@ -15,17 +15,6 @@ def probe(tag, cfg, dagf=None):
     ma, rel, worst = errors(res["out"], ref)
     print(f"{tag}: items={res['batch'].stats['n_items']} max_abs={ma:.2e} rel={rel:.2e}", flush=True)
 
-def dump():
-    import ctypes
-    from paper_2510_24390_b200 import _lib
-    L = _lib.lib()
-    buf = (ctypes.c_int * (16 * 12 * 4))()
-    if L.orion_debug_state(buf):
-        for w in range(12):
-            print("HOST warp", w, list(buf[w * 4:(w + 1) * 4]), flush=True)
-
-import atexit
-atexit.register(dump)
 base = C.CONFIGS["c1"].with_(hq=8, hkv=2, d=128, page=64)
 probe("wide2 lp128 t64", base.with_(lp=128, t=64, lc=8, n_queries=1), lambda: W.wide(2))
 probe("wide2 lp256 t130", base.with_(lp=256, t=130, lc=8, n_queries=1), lambda: W.wide(2))
