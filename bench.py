@@ -86,13 +86,13 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def load_traffic(config_name):
+def load_traffic(config_name, kernel):
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         d = json.load(f)
-    e = d.get(config_name)
+    e = d.get(config_name if kernel == "tc" else f"{config_name}:{kernel}")
     return None if e is None else e.get("split_dram_bytes_per_launch")
 
 
@@ -326,8 +326,8 @@ def run_orion(args, cfg, layers):
                          f"{layers * (kv_b + q_b + o_b) / 1e9:.1f} GB >> 126 MB L2",
                    "parallelism": f"queries partitioned over {world} GPU(s), no collective"},
         "roofline": {"bound": "hbm",
-                     "kernel": "split_tc_kernel (K2, tcgen05)" if args.kernel == "tc" else "split_kernel (K2, mma.sync)", "achieved": achieved, "peak": peak,
-                     "unit": "GB/s", "frac": achieved / peak, "traffic": load_traffic(cfg.name),
+                     "kernel": "split_tct_kernel (K2, tcgen05 swap-AB)" if args.kernel == "tc" else "split_kernel (K2, mma.sync)", "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": load_traffic(cfg.name, args.kernel),
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": split_bytes,
                      "split_ms_per_launch": split_avg_s * 1e3,
