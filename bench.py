@@ -11,9 +11,11 @@ larger than L2 — no flush needed.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl orion|reference]
 
-Multi-GPU: launched by torchrun, one rank per GPU; the config's queries are partitioned across
-ranks (query q -> rank floor(q*N/Q)), no collective on the data path; rank 0 prints one JSON
-line with the whole-job value (branches of all ranks / max-over-ranks step time).
+Multi-GPU: launched by torchrun, one rank per GPU, no collective on the data path (queries are
+independent).  --scaling weak (default): every rank expands its own full batch of
+the config (own seed); --scaling strong: the config's queries are partitioned across ranks
+(paper_2510_24390_b200/shard.py).  Rank 0 prints one JSON line with the whole-job value
+(branches of all ranks / max-over-ranks device-timed step).
 `--impl reference` times the CPU oracle (the tier's reference arm) on a bounded sample.
 """
 import argparse
@@ -49,7 +51,7 @@ def parse():
                     help="split kernel: tcgen05/TMEM/TMA (default) or legacy mma.sync")
     ap.add_argument("--layers", type=int, default=0, help="override layer count (0 = config)")
     ap.add_argument("--queries", type=int, default=0, help="override query count (0 = config)")
-    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+    ap.add_argument("--scaling", default="weak", choices=["strong", "weak"],
                     help="strong: the config's queries are split across ranks; weak: every rank "
                          "runs the full config")
     ap.add_argument("--no-e2e", action="store_true")
@@ -59,12 +61,6 @@ def parse():
 
 
 # ------------------------------------------------------------------------------ helpers
-def rank_queries(cfg, rank, world, scaling):
-    if scaling == "weak" or world == 1:
-        return list(range(cfg.n_queries))
-    return [q for q in range(cfg.n_queries) if (q * world) // cfg.n_queries == rank]
-
-
 def algorithmic_bytes(cfg, lay):
     """Per layer: unique KV (each valid token row once per (query, kv head)),
     q read and out write.  Returns (kv_bytes, q_bytes, out_bytes)."""
@@ -216,6 +212,7 @@ def run_orion(args, cfg, layers):
     import torch
     import torch.distributed as dist
     import paper_2510_24390_b200 as orion
+    from paper_2510_24390_b200 import shard
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -225,8 +222,8 @@ def run_orion(args, cfg, layers):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    qs = rank_queries(cfg, rank, world, args.scaling)
-    lay = WT.make_layout(cfg, queries=qs, seed=cfg.seed * 101 + rank)
+    qs = shard.rank_queries(cfg.n_queries, rank, world, args.scaling)
+    lay = WT.make_layout(cfg, queries=qs, seed=shard.rank_seed(cfg.seed, rank))
     B = lay.n_branches
     P, H, Hq, D = cfg.page, cfg.hkv, cfg.hq, cfg.d
     kc = torch.empty((layers, lay.num_pages, H, P, D), dtype=torch.bfloat16, device=dev)
@@ -284,15 +281,7 @@ def run_orion(args, cfg, layers):
     elapsed_ms = e0.elapsed_time(e1)
     split_ms = [ev[k][l][0].elapsed_time(ev[k][l][1]) for k in range(args.steps) for l in range(layers)]
     # whole-job aggregation: branches of all ranks / max step time over ranks
-    t = torch.tensor([elapsed_ms, float(B)], dtype=torch.float64, device=dev)
-    if world > 1:
-        tmax = t[:1].clone()
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        tot = t[1:].clone()
-        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-        elapsed_ms, total_b = float(tmax.item()), float(tot.item())
-    else:
-        total_b = float(B)
+    elapsed_ms, total_b = shard.reduce_timing(elapsed_ms, float(B), device=dev)
     ms_step = elapsed_ms / args.steps
     value = total_b / (ms_step / 1e3)
 
@@ -314,7 +303,7 @@ def run_orion(args, cfg, layers):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": args.scaling if world > 1 else "strong", "vs_baseline": None, "dtype": "bf16",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded N(0,1) bf16 q/K/V; random page permutation)",
         "config": {"workload": f"{cfg.name}: Hq/Hkv/d={cfg.hq}/{cfg.hkv}/{cfg.d}, "
                                f"{cfg.n_queries} queries x {cfg.dag}, prefix {cfg.lp}, "
@@ -324,7 +313,9 @@ def run_orion(args, cfg, layers):
                    "append_mode": "rewrite (stationary snapshot)",
                    "l2": "no flush: per-layer KV pools, step working set "
                          f"{layers * (kv_b + q_b + o_b) / 1e9:.1f} GB >> 126 MB L2",
-                   "parallelism": f"queries partitioned over {world} GPU(s), no collective"},
+                   "parallelism": (f"{world} GPU(s), each its own {cfg.n_queries}-query batch, no collective"
+                                   if args.scaling == "weak" else
+                                   f"{cfg.n_queries} queries partitioned over {world} GPU(s), no collective")},
         "roofline": {"bound": "hbm",
                      "kernel": "split_tct_kernel (K2, tcgen05 swap-AB)" if args.kernel == "tc" else "split_kernel (K2, mma.sync)", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": load_traffic(cfg.name, args.kernel),
@@ -356,6 +347,7 @@ def run_e2e(args, batch, layers, q, kn, vn, out, kc, vc, dev, world, total_b):
     import torch
     import torch.distributed as dist
     import paper_2510_24390_b200 as orion
+    from paper_2510_24390_b200 import shard
     hq, hkn, hvn = (t.cpu().pin_memory() for t in (q, kn, vn))
     hout = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
     comp = torch.cuda.current_stream(dev)
@@ -400,10 +392,7 @@ def run_e2e(args, batch, layers, q, kn, vn, out, kc, vc, dev, world, total_b):
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms, _ = shard.reduce_timing(ms, 0.0, device=dev)
     ms_step = ms / args.steps
     bi = layers * (q[0].numel() + kn[0].numel() + vn[0].numel()) * 2
     bo = layers * out[0].numel() * 2

@@ -105,6 +105,27 @@ def test_page_permutation_bitwise_and_determinism():
     assert torch.equal(a["out"], c["out"]) and torch.equal(a["lse"], c["lse"])
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_strong_shards_bitwise(world):
+    """SURVEY.md §8(e) bitwise check: each rank's sub-batch (shard.rank_queries, strong mode) gives
+    exactly the single-GPU outputs of its queries -- queries share no work, so nothing can differ."""
+    from paper_2510_24390_b200 import shard
+    cfg = C.CONFIGS["c3"].with_(lp=1024, t=200)
+    lay = T.make_layout(cfg, ragged=True, extra_tokens=cfg.page)
+    ten = T.make_qkv(cfg, lay)
+    full = run_step(cfg, lay, ten)
+    for rank in range(world):
+        qs = shard.rank_queries(cfg.n_queries, rank, world, "strong")
+        sub, br = T.subset_layout(lay, qs)
+        idx = torch.from_numpy(br)
+        ten_r = dict(ten)
+        for key in ("q", "k_new", "v_new"):
+            ten_r[key] = ten[key][:, idx]
+        got = run_step(cfg, sub, ten_r)
+        assert torch.equal(got["out"], full["out"][idx.cuda()])
+        assert torch.equal(got["lse"], full["lse"][idx.cuda()])
+
+
 def test_advance_three_steps_and_rewrite():
     cfg = C.CONFIGS["c1"].with_(lp=200, t=70, lc=8, hq=8, hkv=2, d=128)
     lay = T.make_layout(cfg, ragged=True, extra_tokens=3 * cfg.page)

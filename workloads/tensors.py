@@ -94,6 +94,29 @@ def make_layout(cfg, queries=None, seed=None, contiguous=False, ragged=False,
                   np.array(own, np.int32), np.array(bq, np.int32), table, pool)
 
 
+def subset_layout(lay, queries):
+    """The sub-batch of `lay` holding only `queries` (in that order), with the same page table and
+    pool: what one rank of a strong-scaling run owns.  Returns (layout, branch ids in `lay`)."""
+    n_points, branch0, edges, pre_off, pre_len, branches = [], [], [], [], [], []
+    b = 0
+    for qi in queries:
+        n = int(lay.n_points[qi])
+        n_points.append(n)
+        branch0.append(b)
+        edges.append(list(lay.edges[qi]))
+        pre_off.append(int(lay.prefix_pt_off[qi]))
+        pre_len.append(int(lay.prefix_len[qi]))
+        branches += range(int(lay.branch0[qi]), int(lay.branch0[qi]) + n)
+        b += n
+    br = np.array(branches, np.int64)
+    bq = np.repeat(np.arange(len(queries), dtype=np.int32), n_points) if queries else np.zeros(0, np.int32)
+    sub = Layout(lay.page_size, len(queries), np.array(n_points, np.int32), np.array(branch0, np.int32),
+                 edges, np.array(pre_off, np.int32), np.array(pre_len, np.int32),
+                 lay.point_pt_off[br].copy(), lay.point_cap[br].copy(), lay.content_len[br].copy(),
+                 lay.own_len[br].copy(), bq, lay.page_table, lay.num_pages)
+    return sub, br
+
+
 def make_qkv(cfg, layout, seed=None, device="cpu", q_scale=1.0, sink=False, layers=1):
     """Per-layer caches and per-step inputs.  Returns a dict of torch bf16 tensors:
     k_cache/v_cache [layers, num_pages, Hkv, P, d], q [layers, B, Hq, d], k_new/v_new [layers, B, Hkv, d]."""
