@@ -327,7 +327,7 @@ def run_orion(args, cfg, layers):
         "plan": {"items": st["n_items"], "pieces": st["n_pieces"], "partials": st["n_partials"],
                  "unique_tokens_per_kvhead": st["unique_tokens"],
                  "logical_tokens_per_kvhead": st["logical_tokens"],
-                 "partial_bytes_per_layer": st["n_partials"] * (cfg.d * 4 + 8) * 2,
+                 "partial_bytes_per_layer": st["workspace_bytes"] * 2,   # written by K2 + read by K3
                  "plan_build_s": plan_s},
         "gpu_launches": args.steps * layers * 3,
         "clocks": clocks,

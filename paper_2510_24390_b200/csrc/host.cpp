@@ -442,8 +442,13 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
   h.comb_off_off = align16(h.readers_off + (int64_t)readers.size() * 4);
   h.comb_slot_off = align16(h.comb_off_off + (n_rows + 1) * 4);
   h.plan_bytes = align16(h.comb_slot_off + (int64_t)n_slots * 4);
-  h.acc_bytes = align16((int64_t)n_slots * shape->head_dim * 4);
-  h.workspace_bytes = h.acc_bytes + align16((int64_t)n_slots * 8);
+  if (partials_fp16(variant)) {
+    h.acc_bytes = align16((int64_t)n_slots * shape->head_dim * 2);
+    h.workspace_bytes = h.acc_bytes + align16((int64_t)n_slots * 4);
+  } else {
+    h.acc_bytes = align16((int64_t)n_slots * shape->head_dim * 4);
+    h.workspace_bytes = h.acc_bytes + align16((int64_t)n_slots * 8);
+  }
   h.n_pieces = (int64_t)pieces.size();
   h.unique_tokens = unique_tokens;
   h.logical_tokens = logical_total;

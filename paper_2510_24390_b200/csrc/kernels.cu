@@ -15,6 +15,7 @@
 //
 // Semantics: include/orion.h.  Design and rooflines: DESIGN.md §"Kernels".
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -345,6 +346,58 @@ __global__ void __launch_bounds__(256) combine_kernel(const int32_t* __restrict_
   if (lse && lane == 0) lse[row] = L > 0.f ? (M + log2f(L)) * kLn2 : -INFINITY;
 }
 
+// K3 for the fp16 partial format (plan_format.h): partial i = (o_i = acc_i / l_i, lse2_i), so
+// out = sum_i 2^(lse2_i - M) o_i / sum_i 2^(lse2_i - M) and lse = (M + log2 sum) ln 2.
+template <int D>
+__global__ void __launch_bounds__(256) combine16_kernel(const int32_t* __restrict__ comb_off,
+                                                        const int32_t* __restrict__ comb_slot,
+                                                        const __half* __restrict__ part_o,
+                                                        const float* __restrict__ part_lse,
+                                                        __nv_bfloat16* __restrict__ out,
+                                                        float* __restrict__ lse, int n_rows) {
+  constexpr int V = D / 32;  // elements per lane
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n_rows) return;
+  const int e0 = __ldg(comb_off + row), e1 = __ldg(comb_off + row + 1);
+  float M = -INFINITY;
+  for (int e = e0 + lane; e < e1; e += 32) M = fmaxf(M, __ldg(part_lse + __ldg(comb_slot + e)));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  const float base = M == -INFINITY ? 0.f : M;
+  float acc[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) acc[i] = 0.f;
+  float L = 0.f;
+  for (int e = e0; e < e1; ++e) {  // fixed plan order -> deterministic
+    const int slot = __ldg(comb_slot + e);
+    const float wgt = fast_exp2(__ldg(part_lse + slot) - base);
+    L += wgt;
+    const __half* src = part_o + static_cast<size_t>(slot) * D + lane * V;
+    if constexpr (V == 4) {
+      const uint2 x = __ldg(reinterpret_cast<const uint2*>(src));
+      const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&x.x));
+      const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&x.y));
+      acc[0] += wgt * a.x; acc[1] += wgt * a.y; acc[2] += wgt * b.x; acc[3] += wgt * b.y;
+    } else {
+      const uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(src));
+      const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&x));
+      acc[0] += wgt * a.x; acc[1] += wgt * a.y;
+    }
+  }
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  __nv_bfloat16* o = out + static_cast<size_t>(row) * D + lane * V;
+  if constexpr (V == 4) {
+    uint2 pk;
+    pk.x = pack_bf16(acc[0] * inv, acc[1] * inv);
+    pk.y = pack_bf16(acc[2] * inv, acc[3] * inv);
+    *reinterpret_cast<uint2*>(o) = pk;
+  } else {
+    *reinterpret_cast<uint32_t*>(o) = pack_bf16(acc[0] * inv, acc[1] * inv);
+  }
+  if (lse && lane == 0) lse[row] = L > 0.f ? (M + log2f(L)) * kLn2 : -INFINITY;
+}
+
 // ------------------------------------------------------------------------------ K1 append
 template <int D>
 __global__ void __launch_bounds__(128) kv_append_kernel(
@@ -404,6 +457,8 @@ orion_status launch_split(const PlanHeader* h, const char* dplan, const void* q,
     t.own_len = own_len;
     t.part_acc = static_cast<float*>(ws);
     t.part_ml = reinterpret_cast<float2*>(static_cast<char*>(ws) + h->acc_bytes);
+    t.part_o = static_cast<__half*>(ws);
+    t.part_lse = reinterpret_cast<float*>(static_cast<char*>(ws) + h->acc_bytes);
     t.n_items = h->n_items;
     t.hq = h->num_q_heads;
     t.hkv = h->num_kv_heads;
@@ -449,6 +504,16 @@ template <int D>
 orion_status launch_combine(const PlanHeader* h, const char* dplan, void* out, float* lse,
                             const void* ws, cudaStream_t st) {
   const int nb = (h->n_rows + 7) / 8;
+  if (partials_fp16(h->variant)) {
+    combine16_kernel<D><<<nb, 256, 0, st>>>(
+        reinterpret_cast<const int32_t*>(dplan + h->comb_off_off),
+        reinterpret_cast<const int32_t*>(dplan + h->comb_slot_off), static_cast<const __half*>(ws),
+        reinterpret_cast<const float*>(static_cast<const char*>(ws) + h->acc_bytes),
+        static_cast<__nv_bfloat16*>(out), lse, h->n_rows);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(ORION_ERR_CUDA, "combine16_kernel: %s", cudaGetErrorString(e));
+    return ORION_OK;
+  }
   const float* acc = static_cast<const float*>(ws);
   const float2* ml = reinterpret_cast<const float2*>(static_cast<const char*>(ws) + h->acc_bytes);
   combine_kernel<D><<<nb, 256, 0, st>>>(reinterpret_cast<const int32_t*>(dplan + h->comb_off_off),

@@ -4,8 +4,15 @@
 // A plan is one contiguous byte buffer:
 //   PlanHeader | WorkItem[n_items] | readers[n_reader_entries] (int32 branch ids)
 //              | comb_off[n_rows + 1] (int32) | comb_slot[n_partials] (int32)
-// Workspace (caller-allocated, device):
-//   part_acc fp32 [n_partials][head_dim] | part_ml fp32 [n_partials][2]  (m in log2 units, l)
+// Workspace (caller-allocated, device), one partial (softmax state of one query row over one
+// work item's tokens) per slot, in one of two formats fixed by the plan's variant:
+//   fp32 (kVariantTC, kVariantMmaSync):
+//     part_acc fp32 [n_partials][head_dim] | part_ml fp32 [n_partials][2]  (m in log2 units, l)
+//     the row's partial output is acc / l, its log2-sum-exp m + log2(l)
+//   fp16 (kVariantTCT):
+//     part_o fp16 [n_partials][head_dim] (= acc / l) | part_lse fp32 [n_partials] (m + log2 l)
+//     half the bytes; fp16's 2^-11 relative rounding is 4x below the bf16 rounding of out.
+// acc_bytes = byte offset of the second array.
 #pragma once
 #include <stdint.h>
 
@@ -18,6 +25,7 @@ constexpr int kRowsPerItemMMA = 64;  // query rows per work item, mma.sync kerne
 constexpr int kRowsPerItem = kRowsPerItemMMA;  // smem sizing of the mma.sync kernel
 constexpr int kRowsPerItemTCT = 64;  // query rows per work item, transposed tcgen05 kernel (MMA N)
 enum : int32_t { kVariantTC = 0, kVariantMmaSync = 1, kVariantTCT = 2 };
+inline bool partials_fp16(int32_t variant) { return variant == kVariantTCT; }
 constexpr int kTileTokens = 64;    // tokens per pipeline stage in the split kernel
 
 struct PlanHeader {

@@ -2,6 +2,7 @@
 // kernel (split_tc.cu).  Product-side only.
 #pragma once
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -18,8 +19,10 @@ struct TcArgs {
   const __nv_bfloat16* q;
   const int32_t* page_table;
   const int32_t* own_len;
-  float* part_acc;
+  float* part_acc;        // fp32 partial format (split_tc)
   float2* part_ml;
+  __half* part_o;         // fp16 partial format (split_tct)
+  float* part_lse;
   int32_t n_items, hq, hkv, group, page_shift;
   float scale_log2;
 };

@@ -413,10 +413,16 @@ __device__ __forceinline__ void softmax_item(uint8_t* smem, uint32_t tmem, uint3
   mbar_wait(B.acc_full + kp, (k >> 1) & 1);
   tc_fence_after();
   wg_sync(2 + p, 128);
+  // fp16 partial format (plan_format.h): o = acc / l, lse2 = m + log2 l.  l >= 1: the column max
+  // that set the reference contributes 2^0 (every item has at least one valid token).
   const int n = e.n_rows;
-  if (t < NH && c0 + t < n)
-    a.part_ml[e.slot0 + c0 + t] = make_float2(mrow[t], red[t] + red[32 + t] + red[64 + t] + red[96 + t]);
-  float* dst = a.part_acc + static_cast<size_t>(e.slot0) * D + t;
+  if (t < NH) {
+    const float l = red[t] + red[32 + t] + red[64 + t] + red[96 + t];
+    shs[t] = 1.f / l;                               // shs is free until the next item's first tile
+    if (c0 + t < n) a.part_lse[e.slot0 + c0 + t] = mrow[t] + log2f(l);
+  }
+  wg_sync(2 + p, 128);
+  __half* dst = a.part_o + static_cast<size_t>(e.slot0) * D + t;
 #pragma unroll
   for (int cb = 0; cb < NH; cb += 8) {
     uint32_t o[8];
@@ -424,7 +430,7 @@ __device__ __forceinline__ void softmax_item(uint8_t* smem, uint32_t tmem, uint3
     tc_wait_ld();
 #pragma unroll
     for (int c = 0; c < 8; ++c)
-      if (c0 + cb + c < n) dst[static_cast<size_t>(c0 + cb + c) * D] = __uint_as_float(o[c]);
+      if (c0 + cb + c < n) dst[static_cast<size_t>(c0 + cb + c) * D] = __float2half_rn(__uint_as_float(o[c]) * shs[cb + c]);
   }
   tc_fence_before();
   mbar_arrive(B.o_free + kp);
@@ -482,9 +488,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const WorkItem w = a.items[it];
       const Geom g = geom(w, a.own_len);
       if (g.ntiles == 0) {                           // empty (dyn end <= t0): neutral partial
-        for (int i = lane; i < w.n_rows * D / 4; i += 32)
-          reinterpret_cast<float4*>(a.part_acc + static_cast<size_t>(w.slot0) * D)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int r = lane; r < w.n_rows; r += 32) a.part_ml[w.slot0 + r] = make_float2(-INFINITY, 0.f);
+        for (int i = lane; i < w.n_rows * D / 8; i += 32)
+          reinterpret_cast<uint4*>(a.part_o + static_cast<size_t>(w.slot0) * D)[i] = make_uint4(0, 0, 0, 0);
+        for (int r = lane; r < w.n_rows; r += 32) a.part_lse[w.slot0 + r] = -INFINITY;
         continue;
       }
       TW(0, mbar_wait(sch_empty + (k % kSched), ((k / kSched) & 1) ^ 1));

@@ -150,7 +150,8 @@ def _check_plan_covers(cfg, lay, offs, segs, own_len):
     h, items, readers, coff, cslot = parse_plan(plan)
     G = cfg.hq // cfg.hkv
     assert h["magic"] == 0x314e524f and h["n_rows"] == lay.n_branches * cfg.hq
-    assert ws >= h["n_partials"] * (cfg.d * 4 + 8)
+    variant = int(h["pad"][0])                      # 2 = tcgen05 swap-AB: fp16 partials (plan_format.h)
+    assert ws >= h["n_partials"] * ((cfg.d * 2 + 4) if variant == 2 else (cfg.d * 4 + 8))
     slot_tokens = {}
     slot_row = {}
     for it in items:
