@@ -57,6 +57,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-prefill", action="store_true",
+                    help="skip the co-scheduled prefill measurement (SURVEY.md §8(a) a8)")
+    ap.add_argument("--prefill-caps", default="148,132,116",
+                    help="split-kernel SM caps tried with the prefill co-stream")
     return ap.parse_args()
 
 
@@ -333,11 +337,120 @@ def run_orion(args, cfg, layers):
         "clocks": clocks,
         "e2e": e2e,
     }
+    if world == 1 and not args.no_prefill:
+        line["prefill_costream"] = run_costream(args, cfg, lay, layers, q, kn, vn, out, kc, vc, dev,
+                                                value)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, layers, args.cpu_seconds)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+# Llama-3-8B decoder-layer prefill of 4096 tokens: QKV, O, gate+up, down.
+PREFILL_TOKENS = 4096
+PREFILL_GEMMS = ((4096, 6144), (4096, 4096), (4096, 28672), (14336, 4096))   # (K, N) of x[T,K]·W[K,N]
+
+
+def run_costream(args, cfg, lay, layers, q, kn, vn, out, kc, vc, dev, expansion_alone):
+    """§8(a) a8: KPG prefill of other queries as a compute-bound load on a low-priority stream
+    (plain library GEMMs: torch.matmul -> cuBLAS/cuBLASLt, bf16) while the expansion step runs on
+    a high-priority stream (decode is memory-bound, prefill compute-bound).
+    Three cases: expansion alone (the headline run), prefill alone, both together -- the latter
+    also with the persistent split kernel capped to fewer SMs (plan opts num_sms), leaving the
+    rest to the GEMMs.  Device-timed with events on each stream."""
+    import torch
+    import paper_2510_24390_b200 as orion
+    hi = torch.cuda.Stream(dev, priority=-1)
+    lo = torch.cuda.Stream(dev, priority=0)
+    g = torch.Generator(device=dev)
+    g.manual_seed(77)
+    acts = {k: torch.randn((PREFILL_TOKENS, k), generator=g, device=dev, dtype=torch.bfloat16)
+            for k in {k for k, _ in PREFILL_GEMMS}}
+    ws = [torch.randn((k, n), generator=g, device=dev, dtype=torch.bfloat16) * 0.02
+          for k, n in PREFILL_GEMMS]
+    outs = [torch.empty((PREFILL_TOKENS, n), device=dev, dtype=torch.bfloat16) for _, n in PREFILL_GEMMS]
+    layer_flop = sum(2.0 * PREFILL_TOKENS * k * n for k, n in PREFILL_GEMMS)
+
+    def prefill_layer():
+        for (k, _), w, o in zip(PREFILL_GEMMS, ws, outs):
+            torch.matmul(acts[k], w, out=o)
+
+    # prefill alone
+    with torch.cuda.stream(lo):
+        for _ in range(5):
+            prefill_layer()
+    torch.cuda.synchronize()
+    n_alone = 40
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(lo)
+    with torch.cuda.stream(lo):
+        for _ in range(n_alone):
+            prefill_layer()
+    e1.record(lo)
+    torch.cuda.synchronize()
+    prefill_ms = e0.elapsed_time(e1) / n_alone
+    prefill_alone = layer_flop / (prefill_ms / 1e3) / 1e12
+
+    queries = [dict(n_points=int(lay.n_points[i]), edges=lay.edges[i],
+                    prefix_pt_off=int(lay.prefix_pt_off[i]), prefix_len=int(lay.prefix_len[i]))
+               for i in range(lay.n_queries)]
+    points = np.stack([lay.point_pt_off, lay.content_len, lay.point_cap], 1)
+    steps = max(3, min(args.steps, 10))
+    REW = orion.APPEND_REWRITE
+    together = []
+    for cap in [int(c) for c in args.prefill_caps.split(",") if c]:
+        batch = orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, lay.page_table,
+                                     lay.own_len, policy=args.policy, device=dev,
+                                     chunk_tokens=args.chunk, num_sms=cap)
+
+        def step():
+            for l in range(layers):
+                batch.step(q[l], kn[l], vn[l], kc[l], vc[l], out[l], mode=REW, stream=hi)
+
+        with torch.cuda.stream(hi):
+            step()
+        torch.cuda.synchronize()
+        # expansion alone at this cap
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(hi)
+        for _ in range(steps):
+            step()
+        a1.record(hi)
+        torch.cuda.synchronize()
+        exp_cap_ms = a0.elapsed_time(a1) / steps
+        # together: enough prefill layers queued on `lo` to outlast the expansion window
+        n_pf = int(steps * exp_cap_ms / prefill_ms * 1.5) + 4
+        s_hi = torch.cuda.Event(enable_timing=True)
+        s_lo = torch.cuda.Event(enable_timing=True)
+        t_hi = torch.cuda.Event(enable_timing=True)
+        pf_ev = [torch.cuda.Event(enable_timing=True) for _ in range(n_pf)]
+        torch.cuda.synchronize()
+        s_lo.record(lo)
+        with torch.cuda.stream(lo):
+            for i in range(n_pf):
+                prefill_layer()
+                pf_ev[i].record(lo)
+        s_hi.record(hi)
+        for _ in range(steps):
+            step()
+        t_hi.record(hi)
+        torch.cuda.synchronize()
+        win = s_hi.elapsed_time(t_hi)
+        lag = s_lo.elapsed_time(s_hi)                 # lo started this much earlier
+        done = sum(1 for ev in pf_ev if lag <= s_lo.elapsed_time(ev) <= lag + win)
+        exp_tok_s = lay.n_branches * steps / (win / 1e3)
+        pf_tflops = done * layer_flop / (win / 1e3) / 1e12
+        together.append({"split_sm_cap": cap, "expansion_alone_tok_s": lay.n_branches / (exp_cap_ms / 1e3),
+                         "expansion_tok_s": exp_tok_s, "expansion_retained": exp_tok_s / expansion_alone,
+                         "prefill_tflops": pf_tflops, "prefill_retained": pf_tflops / prefill_alone,
+                         "prefill_layers_in_window": done})
+    return {"prefill": f"Llama-3-8B layer prefill of {PREFILL_TOKENS} tokens per 'layer': "
+                       "[4096x4096]x[4096x{6144,4096,28672}], [4096x14336]x[14336x4096] bf16, "
+                       "torch.matmul (cuBLAS) on a low-priority stream",
+            "expansion": "the headline step on a high-priority stream",
+            "prefill_alone_tflops": prefill_alone, "prefill_ms_per_layer": prefill_ms,
+            "expansion_alone_tok_s": expansion_alone, "steps": steps, "together": together}
 
 
 def run_e2e(args, batch, layers, q, kn, vn, out, kc, vc, dev, world, total_b):

@@ -115,7 +115,8 @@ typedef struct { int32_t pt_off, content_len, capacity; } orion_point_desc;
 enum { ORION_PLAN_MMA_SYNC = 1, ORION_PLAN_ROWS_ON_LANES = 2 };
 
 typedef struct {
-  int32_t num_sms;        /* SMs to balance for; <= 0 selects 148 (B200) */
+  int32_t num_sms;        /* SMs the persistent split kernel may occupy (grid cap, e.g. to leave
+                             SMs to a co-scheduled prefill stream); <= 0 = all SMs */
   int32_t chunk_tokens;   /* max tokens per work item along a piece; <= 0 selects the default */
   int32_t flags;          /* ORION_PLAN_* bits, 0 = defaults */
 } orion_plan_opts;

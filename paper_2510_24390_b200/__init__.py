@@ -186,7 +186,8 @@ class ExpansionBatch:
     """
 
     def __init__(self, hq, hkv, d, page, queries, points, page_table, own_len,
-                 policy=POLICY_ANCESTORS, device="cuda", chunk_tokens=0, sm_scale=0.0, flags=0):
+                 policy=POLICY_ANCESTORS, device="cuda", chunk_tokens=0, sm_scale=0.0, flags=0,
+                 num_sms=0):
         import torch
         self.hq, self.hkv, self.d, self.page = hq, hkv, d, page
         self.sm_scale = sm_scale
@@ -206,7 +207,8 @@ class ExpansionBatch:
         self.segs = bind_segments(qdesc, pts, self.seg_offsets, self.refs)
         own = np.ascontiguousarray(own_len, dtype=np.int32)
         self.h_plan, ws = expand_plan(hq, hkv, d, page, self.seg_offsets, self.segs, own,
-                                      chunk_tokens=chunk_tokens, sm_scale=sm_scale, flags=flags)
+                                      chunk_tokens=chunk_tokens, sm_scale=sm_scale, flags=flags,
+                                      num_sms=num_sms)
         self.stats = plan_stats(self.h_plan)
         dev = torch.device(device)
         self.d_plan = torch.from_numpy(self.h_plan.copy()).to(dev)

@@ -453,6 +453,7 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
   h.unique_tokens = unique_tokens;
   h.logical_tokens = logical_total;
   h.variant = variant;
+  h.max_ctas = (opts && opts->num_sms > 0) ? opts->num_sms : 0;
   h.sm_scale = shape->sm_scale > 0.f ? shape->sm_scale : 1.0f / std::sqrt((float)shape->head_dim);
   *plan_needed = (size_t)h.plan_bytes;
   *workspace_needed = (size_t)h.workspace_bytes;

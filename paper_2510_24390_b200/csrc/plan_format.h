@@ -38,7 +38,8 @@ struct PlanHeader {
   float sm_scale;
   int32_t variant;  // kVariantTCT (default, d = 128), kVariantTC (d = 64 or ORION_PLAN_ROWS_ON_LANES),
                     // kVariantMmaSync (ORION_PLAN_MMA_SYNC)
-  int32_t pad_[2];
+  int32_t max_ctas; // persistent split kernels: grid cap (opts->num_sms; 0 = all SMs)
+  int32_t pad_;
 };
 static_assert(sizeof(PlanHeader) % 16 == 0, "header must keep 16-byte alignment");
 

@@ -707,7 +707,8 @@ orion_status launch_split_tc(const PlanHeader* h, const TcArgs& a, const void* k
   if (!make_map(&mk, k, D, rows, big) || !make_map(&mv, v, D, rows, big) ||
       !make_map(&mk16, k, D, rows, tc::kBox) || !make_map(&mv16, v, D, rows, tc::kBox))
     return fail(ORION_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-  const int grid = std::min<int>(h->n_items, num_sms > 0 ? num_sms : 148);
+  int grid = std::min<int>(h->n_items, num_sms > 0 ? num_sms : 148);
+  if (h->max_ctas > 0) grid = std::min(grid, h->max_ctas);
   tc::split_tc_kernel<D><<<grid, tc::kThreadsTC, tc::Smem<D>::BYTES + 1024, st>>>(mk, mv, mk16, mv16, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ORION_ERR_CUDA, "split_tc_kernel: %s", cudaGetErrorString(e));

@@ -817,6 +817,7 @@ orion_status launch_split_tct(const PlanHeader* h, const TcArgs& a, const void* 
       !make_map_t(&mv16, v, rows, tct::kBox))
     return fail(ORION_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   int grid = std::min<int>(h->n_items, num_sms > 0 ? num_sms : 148);
+  if (h->max_ctas > 0) grid = std::min(grid, h->max_ctas);
   if (const char* g = getenv("ORION_DEBUG_GRID")) grid = std::max(1, std::min(grid, atoi(g)));   // debugging only
   tct::split_tct_kernel<<<grid, tct::kThreads, tct::L::BYTES, st>>>(mk, mv, mk16, mv16, a);
   cudaError_t e = cudaGetLastError();
