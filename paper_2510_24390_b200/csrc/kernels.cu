@@ -358,6 +358,8 @@ __global__ void __launch_bounds__(256) combine16_kernel(const int32_t* __restric
   constexpr int V = D / 32;  // elements per lane
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
+  pdl_trigger();
+  pdl_wait();
   if (row >= n_rows) return;
   const int e0 = __ldg(comb_off + row), e1 = __ldg(comb_off + row + 1);
   float M = -INFINITY;
@@ -409,6 +411,8 @@ __global__ void __launch_bounds__(128) kv_append_kernel(
   constexpr int CH = D / 8;
   __shared__ int s_pos, s_page, s_len;
   const int b = blockIdx.x;
+  pdl_trigger();
+  pdl_wait();
   if (threadIdx.x == 0) {
     const int len = own_len[b];
     const int pos = mode == ORION_APPEND_REWRITE ? len - 1 : len;
@@ -505,12 +509,13 @@ orion_status launch_combine(const PlanHeader* h, const char* dplan, void* out, f
                             const void* ws, cudaStream_t st) {
   const int nb = (h->n_rows + 7) / 8;
   if (partials_fp16(h->variant)) {
-    combine16_kernel<D><<<nb, 256, 0, st>>>(
+    cudaError_t e = launch_pdl(
+        combine16_kernel<D>, dim3(nb), dim3(256), 0, st,
         reinterpret_cast<const int32_t*>(dplan + h->comb_off_off),
         reinterpret_cast<const int32_t*>(dplan + h->comb_slot_off), static_cast<const __half*>(ws),
         reinterpret_cast<const float*>(static_cast<const char*>(ws) + h->acc_bytes),
         static_cast<__nv_bfloat16*>(out), lse, h->n_rows);
-    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return fail(ORION_ERR_CUDA, "combine16_kernel: %s", cudaGetErrorString(e));
     return ORION_OK;
   }
@@ -568,17 +573,12 @@ extern "C" orion_status orion_kv_append(const orion_attn_shape* shape, int32_t n
   if (n_branches == 0) return ORION_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int shift = log2i(shape->page_size);
-  if (shape->head_dim == 128)
-    kv_append_kernel<128><<<n_branches, 128, 0, s>>>(
-        static_cast<const __nv_bfloat16*>(k_new), static_cast<const __nv_bfloat16*>(v_new),
-        static_cast<__nv_bfloat16*>(k_cache), static_cast<__nv_bfloat16*>(v_cache), own_pt_off,
-        own_cap, page_table, own_len, shape->num_kv_heads, shift, mode);
-  else
-    kv_append_kernel<64><<<n_branches, 128, 0, s>>>(
-        static_cast<const __nv_bfloat16*>(k_new), static_cast<const __nv_bfloat16*>(v_new),
-        static_cast<__nv_bfloat16*>(k_cache), static_cast<__nv_bfloat16*>(v_cache), own_pt_off,
-        own_cap, page_table, own_len, shape->num_kv_heads, shift, mode);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(
+      shape->head_dim == 128 ? kv_append_kernel<128> : kv_append_kernel<64>, dim3(n_branches), dim3(128), 0, s,
+      static_cast<const __nv_bfloat16*>(k_new), static_cast<const __nv_bfloat16*>(v_new),
+      static_cast<__nv_bfloat16*>(k_cache), static_cast<__nv_bfloat16*>(v_cache), own_pt_off,
+      own_cap, page_table, own_len, shape->num_kv_heads, shift, mode);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ORION_ERR_CUDA, "kv_append_kernel: %s", cudaGetErrorString(e));
   return ORION_OK;
 }

@@ -13,6 +13,31 @@ namespace orion {
 
 orion_status fail(orion_status code, const char* fmt, ...);
 
+// Programmatic dependent launch (PDL).  Kernels of one expansion step (append -> split ->
+// combine -> next layer's append) are launched with programmatic stream serialization: the next
+// kernel may be scheduled while the previous one drains, runs its data-independent prologue
+// (barrier init, TMEM allocation, smem zeroing), and blocks in pdl_wait() -- which returns only
+// once the previous grid has completed and its memory is visible -- before it touches global
+// memory.  pdl_trigger() lets the next grid be scheduled early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 struct TcArgs {
   const WorkItem* items;
   const int32_t* readers;

@@ -478,6 +478,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();                                        // KV appended / previous step's reads done
   const int n_items = a.n_items;
 
   TRACE_DECL
@@ -819,8 +821,9 @@ orion_status launch_split_tct(const PlanHeader* h, const TcArgs& a, const void* 
   int grid = std::min<int>(h->n_items, num_sms > 0 ? num_sms : 148);
   if (h->max_ctas > 0) grid = std::min(grid, h->max_ctas);
   if (const char* g = getenv("ORION_DEBUG_GRID")) grid = std::max(1, std::min(grid, atoi(g)));   // debugging only
-  tct::split_tct_kernel<<<grid, tct::kThreads, tct::L::BYTES, st>>>(mk, mv, mk16, mv16, a);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(tct::split_tct_kernel, dim3(grid), dim3(tct::kThreads), tct::L::BYTES, st, mk, mv,
+                             mk16, mv16, a);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ORION_ERR_CUDA, "split_tct_kernel: %s", cudaGetErrorString(e));
   return ORION_OK;
 }
