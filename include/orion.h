@@ -119,6 +119,11 @@ typedef struct {
                              SMs to a co-scheduled prefill stream); <= 0 = all SMs */
   int32_t chunk_tokens;   /* max tokens per work item along a piece; <= 0 selects the default */
   int32_t flags;          /* ORION_PLAN_* bits, 0 = defaults */
+  int32_t prefill_rows;   /* 0: decode plan (one query row per branch and q head).  Lc > 0: point-
+                             prefill plan (orion_point_prefill_attn): every branch contributes the
+                             Lc content tokens of its point as query rows; its OWN segment (the one
+                             whose dyn == the branch) is read causally over [start, start + Lc) and
+                             must have len >= Lc; all points must have content length Lc. */
 } orion_plan_opts;
 
 typedef struct {
@@ -247,6 +252,28 @@ orion_status orion_expand_attn(const orion_attn_shape* shape, int32_t n_branches
                                int32_t num_pages, const int32_t* page_table,
                                const int32_t* own_len, const void* h_plan, const void* d_plan,
                                void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * orion_point_prefill_attn — the attention of the Pre stage (Alg. 1 l.12 / l.19, Eq. (2);
+ * SURVEY.md §8(f) rank 1; oracle O5).  Point j's Lc content tokens P_j are the query rows; content
+ * token i attends to j's bound segments except OWN, in list order, followed by P_j[0 .. i] (its own
+ * run's tokens [0, i], causal):
+ *   out[b,i,h] = softmax(sm_scale * q[b,i,h] . K_ctx_i(b)^T) . V_ctx_i(b),  lse likewise.
+ * The K/V of P_j must already be in the cache (written by the model's QKV projection); the
+ * dependency spans use the current own_len of their points, exactly as in decode.
+ * Same arguments as orion_expand_attn, with a plan built with opts->prefill_rows = Lc and
+ *  q, out   bf16 [n_branches][Lc][Hq][d] (device);  lse  fp32 [n_branches][Lc][Hq], nullable.
+ * Runs the rows-on-lanes tcgen05 split kernel (<= 128 query rows per work item: one MMA M tile)
+ * and the combine kernel.
+ * Errors: as orion_expand_attn; INVALID_ARG if the plan is not a prefill plan (and
+ * orion_expand_attn rejects prefill plans).  orion_expand_split / _combine accept both kinds.
+ */
+orion_status orion_point_prefill_attn(const orion_attn_shape* shape, int32_t n_branches,
+                                      const void* q, void* out, float* lse, const void* k_cache,
+                                      const void* v_cache, int32_t num_pages,
+                                      const int32_t* page_table, const int32_t* own_len,
+                                      const void* h_plan, const void* d_plan, void* workspace,
+                                      size_t workspace_bytes, void* stream);
 
 /*
  * orion_expand_split / orion_expand_combine — the two kernels of orion_expand_attn as separate

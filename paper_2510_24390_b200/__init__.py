@@ -89,13 +89,14 @@ PLAN_ROWS_ON_LANES = 2   # ORION_PLAN_ROWS_ON_LANES: rows-on-lanes tcgen05 split
 
 
 def expand_plan(hq, hkv, d, page, seg_offsets, segs, own_len=None, chunk_tokens=0, num_sms=0,
-                sm_scale=0.0, flags=0):
-    """orion_expand_plan -> (plan: np.uint8 16-byte aligned host buffer, workspace_bytes)."""
+                sm_scale=0.0, flags=0, prefill_rows=0):
+    """orion_expand_plan -> (plan: np.uint8 16-byte aligned host buffer, workspace_bytes).
+    prefill_rows = Lc > 0 builds a point-prefill plan (orion_point_prefill_attn)."""
     shape = _shape(hq, hkv, d, page, sm_scale)
     so = np.ascontiguousarray(seg_offsets, dtype=np.int32)
     sg = np.ascontiguousarray(segs).astype(SEG_DTYPE)
     ol = None if own_len is None else np.ascontiguousarray(own_len, dtype=np.int32)
-    opts = _lib.PlanOpts(int(num_sms), int(chunk_tokens), int(flags))
+    opts = _lib.PlanOpts(int(num_sms), int(chunk_tokens), int(flags), int(prefill_rows))
     need = ctypes.c_size_t(0)
     ws = ctypes.c_size_t(0)
     nb = len(so) - 1
@@ -153,6 +154,19 @@ def expand_attn(hq, hkv, d, page, q, out, lse, k_cache, v_cache, page_table, own
         _stream_ptr(stream)))
 
 
+def point_prefill_attn(hq, hkv, d, page, q, out, lse, k_cache, v_cache, page_table, own_len, h_plan,
+                       d_plan, workspace, stream=None, sm_scale=0.0):
+    """orion_point_prefill_attn: q/out bf16 [B, Lc, Hq, d], lse fp32 [B, Lc, Hq] (nullable)."""
+    _require_cuda(q, out, lse, k_cache, v_cache, page_table, own_len, d_plan, workspace)
+    shape = _shape(hq, hkv, d, page, sm_scale)
+    _lib.check(lib().orion_point_prefill_attn(
+        ctypes.byref(shape), int(q.shape[0]), q.data_ptr(), out.data_ptr(),
+        None if lse is None else lse.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(),
+        int(k_cache.shape[0]), page_table.data_ptr(), own_len.data_ptr(), _lib.ptr(h_plan),
+        d_plan.data_ptr(), workspace.data_ptr(), workspace.numel() * workspace.element_size(),
+        _stream_ptr(stream)))
+
+
 def expand_split(hq, hkv, d, page, q, k_cache, v_cache, page_table, own_len, h_plan, d_plan,
                  workspace, stream=None, sm_scale=0.0):
     """orion_expand_split: K2 only (partials into `workspace`)."""
@@ -187,7 +201,7 @@ class ExpansionBatch:
 
     def __init__(self, hq, hkv, d, page, queries, points, page_table, own_len,
                  policy=POLICY_ANCESTORS, device="cuda", chunk_tokens=0, sm_scale=0.0, flags=0,
-                 num_sms=0):
+                 num_sms=0, prefill_rows=0):
         import torch
         self.hq, self.hkv, self.d, self.page = hq, hkv, d, page
         self.sm_scale = sm_scale
@@ -208,7 +222,8 @@ class ExpansionBatch:
         own = np.ascontiguousarray(own_len, dtype=np.int32)
         self.h_plan, ws = expand_plan(hq, hkv, d, page, self.seg_offsets, self.segs, own,
                                       chunk_tokens=chunk_tokens, sm_scale=sm_scale, flags=flags,
-                                      num_sms=num_sms)
+                                      num_sms=num_sms, prefill_rows=prefill_rows)
+        self.prefill_rows = prefill_rows
         self.stats = plan_stats(self.h_plan)
         dev = torch.device(device)
         self.d_plan = torch.from_numpy(self.h_plan.copy()).to(dev)
@@ -223,9 +238,11 @@ class ExpansionBatch:
                   self.own_pt_off, self.own_cap, self.page_table, self.own_len, mode, stream)
 
     def attend(self, q, out, k_cache, v_cache, lse=None, stream=None):
-        expand_attn(self.hq, self.hkv, self.d, self.page, q, out, lse, k_cache, v_cache,
-                    self.page_table, self.own_len, self.h_plan, self.d_plan, self.workspace,
-                    stream, self.sm_scale)
+        """Decode attention (q/out [B, Hq, d]); with a prefill_rows = Lc batch, the point-prefill
+        attention of the Pre stage (q/out [B, Lc, Hq, d], lse [B, Lc, Hq])."""
+        f = point_prefill_attn if self.prefill_rows else expand_attn
+        f(self.hq, self.hkv, self.d, self.page, q, out, lse, k_cache, v_cache, self.page_table,
+          self.own_len, self.h_plan, self.d_plan, self.workspace, stream, self.sm_scale)
 
     def split(self, q, k_cache, v_cache, stream=None):
         expand_split(self.hq, self.hkv, self.d, self.page, q, k_cache, v_cache, self.page_table,

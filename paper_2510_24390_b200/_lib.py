@@ -19,8 +19,8 @@ APPEND_ADVANCE, APPEND_REWRITE = 0, 1
 
 EXPORTED_SYMBOLS = ("orion_dag_waves", "orion_bind_segments", "orion_expand_plan",
                     "orion_plan_get_stats", "orion_kv_append", "orion_expand_attn",
-                    "orion_expand_split", "orion_expand_combine", "orion_last_error",
-                    "orion_version")
+                    "orion_expand_split", "orion_expand_combine", "orion_point_prefill_attn",
+                    "orion_last_error", "orion_version")
 
 
 class Edge(ctypes.Structure):
@@ -54,7 +54,7 @@ class PointDesc(ctypes.Structure):
 
 class PlanOpts(ctypes.Structure):
     _fields_ = [("num_sms", ctypes.c_int32), ("chunk_tokens", ctypes.c_int32),
-                ("flags", ctypes.c_int32)]
+                ("flags", ctypes.c_int32), ("prefill_rows", ctypes.c_int32)]
 
 
 class PlanStats(ctypes.Structure):
@@ -98,8 +98,9 @@ def lib():
         L.orion_expand_split.argtypes = [P(AttnShape), i32, vp, vp, vp, i32, vp, vp, vp, vp, vp,
                                          sz, vp]
         L.orion_expand_combine.argtypes = [P(AttnShape), i32, vp, vp, vp, vp, vp, sz, vp]
+        L.orion_point_prefill_attn.argtypes = L.orion_expand_attn.argtypes
         for f in ("orion_expand_split", "orion_expand_combine", "orion_dag_waves", "orion_bind_segments", "orion_expand_plan",
-                  "orion_plan_get_stats", "orion_kv_append", "orion_expand_attn"):
+                  "orion_plan_get_stats", "orion_kv_append", "orion_expand_attn", "orion_point_prefill_attn"):
             getattr(L, f).restype = ctypes.c_int32
         L.orion_last_error.restype = ctypes.c_char_p
         L.orion_last_error.argtypes = []

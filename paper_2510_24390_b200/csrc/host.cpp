@@ -309,16 +309,23 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
   const int32_t Hq = shape->num_q_heads, Hkv = shape->num_kv_heads, G = Hq / Hkv;
   int32_t chunk = (opts && opts->chunk_tokens > 0) ? opts->chunk_tokens : 512;
   const int32_t flags = opts ? opts->flags : 0;
+  const int32_t Lc = (opts && opts->prefill_rows > 0) ? opts->prefill_rows : 0;   // prefill plan
+  if (Lc > 0 && (flags & ORION_PLAN_MMA_SYNC))
+    return fail(ORION_ERR_UNSUPPORTED, "point-prefill plans run on the tcgen05 rows-on-lanes kernel");
+  // Point prefill has Lc*G query rows per branch and kv head: the rows-on-lanes kernel (M = 128).
   const int32_t variant = (flags & ORION_PLAN_MMA_SYNC) ? kVariantMmaSync
-                          : ((flags & ORION_PLAN_ROWS_ON_LANES) || shape->head_dim != 128) ? kVariantTC
-                                                                                         : kVariantTCT;
+                          : (Lc > 0 || (flags & ORION_PLAN_ROWS_ON_LANES) || shape->head_dim != 128) ? kVariantTC
+                                                                                                    : kVariantTCT;
+  const int32_t R = (Lc > 0 ? Lc : 1) * G;          // query rows per reader branch and kv head
   const int32_t rows_per_item = variant == kVariantTC    ? kRowsPerItemTC
                                 : variant == kVariantTCT ? kRowsPerItemTCT
                                                          : kRowsPerItemMMA;
   chunk = std::max(kTileTokens, (chunk + kTileTokens - 1) / kTileTokens * kTileTokens);
 
-  // 1. Group bound segments by page run.
+  // 1. Group bound segments by page run.  A prefill plan takes each branch's OWN segment (the one
+  //    growing with the branch itself) out: it is read causally by that branch alone.
   std::map<int32_t, std::vector<Interval>> groups;
+  std::vector<orion_seg> own_causal(Lc > 0 ? n_branches : 0, orion_seg{-1, 0, 0, -1});
   std::vector<int64_t> logical(n_branches, 0);
   int64_t logical_total = 0;
   for (int32_t b = 0; b < n_branches; ++b) {
@@ -328,10 +335,21 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
       const orion_seg& s = h_segs[i];
       if (s.pt_off < 0 || s.start < 0 || s.len < 0 || s.dyn < -1 || s.dyn >= n_branches)
         return fail(ORION_ERR_INVALID_ARG, "branch %d segment %d: bad fields", b, i);
+      if (Lc > 0 && s.dyn == b) {
+        if (own_causal[b].pt_off >= 0)
+          return fail(ORION_ERR_INVALID_ARG, "branch %d has two OWN segments", b);
+        if (s.len < Lc)
+          return fail(ORION_ERR_INVALID_ARG, "branch %d: OWN capacity %d < prefill rows %d", b, s.len, Lc);
+        own_causal[b] = s;
+        logical[b] += Lc;
+        continue;
+      }
       if (s.len == 0) continue;  // zero-length segments are skipped (reading S22)
       groups[s.pt_off].push_back({s.start, s.start + s.len, s.dyn, b});
       logical[b] += s.len;
     }
+    if (Lc > 0 && own_causal[b].pt_off < 0)
+      return fail(ORION_ERR_INVALID_ARG, "branch %d: a prefill plan needs its OWN segment", b);
     if (logical[b] == 0) return fail(ORION_ERR_INVALID_ARG, "branch %d has an empty context", b);
     logical_total += logical[b];
   }
@@ -392,36 +410,52 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
   std::vector<int64_t> cost;
   int64_t unique_tokens = 0;
   int32_t n_slots = 0;
-  std::vector<std::vector<int32_t>> row_slots((size_t)n_branches * Hq);
-  for (size_t pi = 0; pi < pieces.size(); ++pi) {
-    const Piece& p = pieces[pi];
-    unique_tokens += p.t1 - p.t0;
+  const int32_t Lrows = Lc > 0 ? Lc : 1;
+  std::vector<std::vector<int32_t>> row_slots((size_t)n_branches * Lrows * Hq);
+  auto add_items = [&](int32_t pt_off, int32_t t0, int32_t t1, int32_t dyn, int32_t iflags,
+                       const std::vector<int32_t>& rd, int32_t piece_id) {
     const int32_t roff = (int32_t)readers.size();
-    readers.insert(readers.end(), p.readers.begin(), p.readers.end());
-    const int32_t rows = (int32_t)p.readers.size() * G;
+    readers.insert(readers.end(), rd.begin(), rd.end());
+    const int32_t rows = (int32_t)rd.size() * R;
     const int32_t rows_blk = std::min(rows, rows_per_item);
     int32_t ch = std::max(chunk, 32 * rows_blk);
     ch = (ch + kTileTokens - 1) / kTileTokens * kTileTokens;
     for (int32_t g = 0; g < Hkv; ++g)
-      for (int32_t t = p.t0; t < p.t1; t += ch)
+      for (int32_t t = t0; t < t1; t += ch)
         for (int32_t r0 = 0; r0 < rows; r0 += rows_per_item) {
           WorkItem w{};
-          w.pt_off = p.pt_off; w.t0 = t; w.t1 = std::min(p.t1, t + ch); w.dyn = p.dyn;
+          w.pt_off = pt_off; w.t0 = t; w.t1 = std::min(t1, t + ch); w.dyn = dyn;
           w.kv_head = g; w.readers_off = roff; w.row_begin = r0;
-          w.n_rows = std::min(rows_per_item, rows - r0); w.slot0 = n_slots; w.piece = (int32_t)pi;
+          w.n_rows = std::min(rows_per_item, rows - r0); w.slot0 = n_slots; w.piece = piece_id;
+          w.flags = iflags;
           for (int32_t r = r0; r < r0 + w.n_rows; ++r) {
-            const int32_t b = p.readers[r / G], h = g * G + r % G;
-            row_slots[(size_t)b * Hq + h].push_back(n_slots + (r - r0));
+            const int32_t b = rd[r / R], i = (r % R) / G, h = g * G + r % G;
+            row_slots[((size_t)b * Lrows + i) * Hq + h].push_back(n_slots + (r - r0));
           }
           n_slots += w.n_rows;
           items.push_back(w);
           // ~ cycles: stream the tokens, plus the row tiles' MMA work, plus a fixed start-up.
           cost.push_back((int64_t)(w.t1 - w.t0) * (2 + (w.n_rows + 15) / 16) + 256);
         }
+  };
+  for (size_t pi = 0; pi < pieces.size(); ++pi) {
+    const Piece& p = pieces[pi];
+    unique_tokens += p.t1 - p.t0;
+    add_items(p.pt_off, p.t0, p.t1, p.dyn, 0, p.readers, (int32_t)pi);
+  }
+  // Prefill: each branch's own content tokens, causal, one reader.  The causal chunk must hold
+  // all Lc tokens in one item (row i's limit is relative to the item's t0).
+  for (int32_t b = 0; b < (Lc > 0 ? n_branches : 0); ++b) {
+    const orion_seg& s = own_causal[b];
+    if (Lc > std::max(chunk, 32 * std::min(R, rows_per_item)))
+      return fail(ORION_ERR_UNSUPPORTED, "prefill rows %d exceed one work item's chunk", Lc);
+    unique_tokens += Lc;
+    add_items(s.pt_off, s.start, s.start + Lc, -1, kItemCausal, std::vector<int32_t>{b},
+              (int32_t)pieces.size() + b);
   }
   for (size_t r = 0; r < row_slots.size(); ++r)
     if (row_slots[r].empty())
-      return fail(ORION_ERR_INVALID_ARG, "row %zu (branch %zu) has no context", r, r / Hq);
+      return fail(ORION_ERR_INVALID_ARG, "row %zu (branch %zu) has no context", r, r / ((size_t)Lrows * Hq));
 
   // Longest first; row blocks of one chunk stay adjacent (same cost, stable sort) so they run
   // together and share the chunk through L2.
@@ -430,7 +464,7 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
   std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) { return cost[a] > cost[b]; });
 
   // 4. Serialise.
-  const int64_t n_rows = (int64_t)n_branches * Hq;
+  const int64_t n_rows = (int64_t)n_branches * Lrows * Hq;
   PlanHeader h{};
   h.magic = kPlanMagic; h.version = kPlanVersion;
   h.n_branches = n_branches; h.num_q_heads = Hq; h.num_kv_heads = Hkv;
@@ -454,6 +488,7 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
   h.logical_tokens = logical_total;
   h.variant = variant;
   h.max_ctas = (opts && opts->num_sms > 0) ? opts->num_sms : 0;
+  h.prefill_rows = Lc;
   h.sm_scale = shape->sm_scale > 0.f ? shape->sm_scale : 1.0f / std::sqrt((float)shape->head_dim);
   *plan_needed = (size_t)h.plan_bytes;
   *workspace_needed = (size_t)h.workspace_bytes;

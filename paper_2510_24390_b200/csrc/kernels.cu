@@ -469,6 +469,7 @@ orion_status launch_split(const PlanHeader* h, const char* dplan, const void* q,
     t.group = h->group;
     t.page_shift = log2i(h->page_size);
     t.scale_log2 = h->sm_scale * kLog2e;
+    t.lc = h->prefill_rows > 0 ? h->prefill_rows : 1;
     if (h->variant == kVariantTCT) {
       if (D != 128) return fail(ORION_ERR_UNSUPPORTED, "transposed split kernel needs head_dim 128");
       return launch_split_tct(h, t, k, v, num_pages, st);
@@ -628,6 +629,28 @@ extern "C" orion_status orion_expand_attn(const orion_attn_shape* shape, int32_t
                                           const void* d_plan, void* workspace,
                                           size_t workspace_bytes, void* stream) {
   if (!out) return fail(ORION_ERR_INVALID_ARG, "null out");
+  if (h_plan && static_cast<const PlanHeader*>(h_plan)->magic == kPlanMagic &&
+      static_cast<const PlanHeader*>(h_plan)->prefill_rows > 0)
+    return fail(ORION_ERR_INVALID_ARG, "a point-prefill plan needs orion_point_prefill_attn");
+  orion_status st = orion_expand_split(shape, n_branches, q, k_cache, v_cache, num_pages,
+                                       page_table, own_len, h_plan, d_plan, workspace,
+                                       workspace_bytes, stream);
+  if (st != ORION_OK) return st;
+  return orion_expand_combine(shape, n_branches, out, lse, h_plan, d_plan, workspace,
+                              workspace_bytes, stream);
+}
+
+extern "C" orion_status orion_point_prefill_attn(const orion_attn_shape* shape, int32_t n_branches,
+                                                 const void* q, void* out, float* lse,
+                                                 const void* k_cache, const void* v_cache,
+                                                 int32_t num_pages, const int32_t* page_table,
+                                                 const int32_t* own_len, const void* h_plan,
+                                                 const void* d_plan, void* workspace,
+                                                 size_t workspace_bytes, void* stream) {
+  if (!out) return fail(ORION_ERR_INVALID_ARG, "null out");
+  if (!h_plan || static_cast<const PlanHeader*>(h_plan)->magic != kPlanMagic ||
+      static_cast<const PlanHeader*>(h_plan)->prefill_rows <= 0)
+    return fail(ORION_ERR_INVALID_ARG, "orion_point_prefill_attn needs a point-prefill plan");
   orion_status st = orion_expand_split(shape, n_branches, q, k_cache, v_cache, num_pages,
                                        page_table, own_len, h_plan, d_plan, workspace,
                                        workspace_bytes, stream);
@@ -637,6 +660,7 @@ extern "C" orion_status orion_expand_attn(const orion_attn_shape* shape, int32_t
 }
 
 extern "C" const char* orion_version(void) {
-  return "orion-b200 0.2 (sm_100a; K1 append; K2 split: tcgen05.mma + TMEM + TMA (default) | "
-         "mma.sync m16n8k16 + cp.async (ORION_PLAN_MMA_SYNC); K3 combine)";
+  return "orion-b200 0.3 (sm_100a; K1 append; K2 split: tcgen05.mma + TMEM + TMA swap-AB (decode, "
+         "default) | rows-on-lanes (d = 64, point prefill) | mma.sync m16n8k16 (ORION_PLAN_MMA_SYNC); "
+         "K3 combine)";
 }

@@ -26,6 +26,7 @@ constexpr int kRowsPerItem = kRowsPerItemMMA;  // smem sizing of the mma.sync ke
 constexpr int kRowsPerItemTCT = 64;  // query rows per work item, transposed tcgen05 kernel (MMA N)
 enum : int32_t { kVariantTC = 0, kVariantMmaSync = 1, kVariantTCT = 2 };
 inline bool partials_fp16(int32_t variant) { return variant == kVariantTCT; }
+constexpr int32_t kItemCausal = 1;
 constexpr int kTileTokens = 64;    // tokens per pipeline stage in the split kernel
 
 struct PlanHeader {
@@ -39,18 +40,20 @@ struct PlanHeader {
   int32_t variant;  // kVariantTCT (default, d = 128), kVariantTC (d = 64 or ORION_PLAN_ROWS_ON_LANES),
                     // kVariantMmaSync (ORION_PLAN_MMA_SYNC)
   int32_t max_ctas; // persistent split kernels: grid cap (opts->num_sms; 0 = all SMs)
-  int32_t pad_;
+  int32_t prefill_rows;  // 0: decode plan; Lc: point-prefill plan (rows = branch x Lc x Hq)
 };
 static_assert(sizeof(PlanHeader) % 16 == 0, "header must keep 16-byte alignment");
 
 // One split-kernel work item: tokens [t0, min(t1, own_len[dyn])) of the page run at pt_off,
-// kv head `kv_head`, query rows [row_begin, row_begin + n_rows) of the piece's row space
-// (row r -> reader branch readers[readers_off + r / group], q head kv_head*group + r % group).
+// kv head `kv_head`, query rows [row_begin, row_begin + n_rows) of the piece's row space.  With
+// R = Lc * group rows per reader (Lc = 1 for decode, prefill_rows for a prefill plan), row r ->
+// reader branch b = readers[readers_off + r / R], content position i = (r % R) / group, q head
+// h = kv_head*group + r % group; its output row is (b * Lc + i) * Hq + h.
 // Row r writes partial slot slot0 + (r - row_begin).
 struct WorkItem {
   int32_t pt_off, t0, t1, dyn;
   int32_t kv_head, readers_off, row_begin, n_rows;
-  int32_t slot0, piece, pad0, pad1;
+  int32_t slot0, piece, flags, pad1;   // flags & kItemCausal: row i sees tokens < t0 + i + 1
 };
 static_assert(sizeof(WorkItem) == 48, "WorkItem is 3 x 16 bytes");
 

@@ -446,11 +446,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         const WorkItem w = a.items[it];
         const bool ok = r < w.n_rows;
         const __nv_bfloat16* src = a.q;
-        if (ok) {
-          const int rr = w.row_begin + r;
-          const int b = __ldg(a.readers + w.readers_off + rr / a.group);
+        if (ok) {   // row -> (reader b, content position i, q head h): plan_format.h
+          const int rr = w.row_begin + r, rpr = a.lc * a.group;
+          const int b = __ldg(a.readers + w.readers_off + rr / rpr);
+          const int i = (rr % rpr) / a.group;
           const int h = w.kv_head * a.group + rr % a.group;
-          src = a.q + (static_cast<size_t>(b) * a.hq + h) * D;
+          src = a.q + ((static_cast<size_t>(b) * a.lc + i) * a.hq + h) * D;
         }
         uint8_t* qb = smem + L::OFF_Q + (k_item & 1) * L::QB;
 #pragma unroll
@@ -484,6 +485,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         continue;
       }
       const bool active = (warp & 3) * 32 < w.n_rows;   // warp-uniform
+      // point prefill, causal own item: row r (content position i) sees tokens [t0, t0 + i]
+      const bool causal = (w.flags & kItemCausal) != 0;
+      const int row_end = causal ? min(g.end, w.t0 + ((w.row_begin + r) % (a.lc * a.group)) / a.group + 1) : g.end;
       float m_used = -INFINITY;
       bool had = false;
       uint32_t jl = 0;                              // last tile of this WG in the item
@@ -505,7 +509,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         mbar_arrive(s_free + p);                  // QK(j+2) may overwrite S[p] now
         // PV(j-2) complete: P[p] is free and O_p is up to date (needed for a rescale).
         if (j >= 2) TW(7, mbar_wait(pv_done + p, ((j - 2) >> 1) & 1));
-        const bool edge = (tb < w.t0) || (tb + kTok > g.end);
+        const bool edge = causal || (tb < w.t0) || (tb + kTok > g.end);
         uint32_t pk[32];
         if (active) {
           float mx = -INFINITY;                     // raw scores; scale > 0 commutes with max
@@ -513,7 +517,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #pragma unroll
             for (int c = 0; c < 64; ++c) mx = fmaxf(mx, __uint_as_float(sr[c]));
           } else {
-            const int lo_c = w.t0 - tb, hi_c = g.end - tb;   // valid columns [lo_c, hi_c)
+            const int lo_c = w.t0 - tb, hi_c = row_end - tb;   // valid columns [lo_c, hi_c)
 #pragma unroll
             for (int c = 0; c < 64; ++c) {
               const float v = (c >= lo_c && c < hi_c) ? __uint_as_float(sr[c]) : -INFINITY;

@@ -49,6 +49,7 @@ struct TcArgs {
   __half* part_o;         // fp16 partial format (split_tct)
   float* part_lse;
   int32_t n_items, hq, hkv, group, page_shift;
+  int32_t lc;             // query rows per reader and q head: 1 (decode) or Lc (point prefill)
   float scale_log2;
 };
 

@@ -1,0 +1,121 @@
+"""GPU parity of the point-prefill attention (orion_point_prefill_attn)
+against the fp64 oracle O5 on the same seeded bytes.  Gates as for decode (north_star):
+out max-abs <= 2e-2 and rel-L2 <= 5e-3; lse abs <= 5e-3."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2510_24390_b200 as orion
+from oracle import prefill as OP
+from workloads import configs as C, tensors as T, dags as W
+from tests.gpu_helpers import MAX_ABS, REL_L2, LSE_ABS, u16
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def run_prefill(cfg, lay, ten, qp, policy=0):
+    dev = torch.device("cuda")
+    queries = [dict(n_points=int(lay.n_points[i]), edges=lay.edges[i],
+                    prefix_pt_off=int(lay.prefix_pt_off[i]), prefix_len=int(lay.prefix_len[i]))
+               for i in range(lay.n_queries)]
+    points = np.stack([lay.point_pt_off, lay.content_len, lay.point_cap], 1)
+    batch = orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, lay.page_table,
+                                 lay.own_len, policy=policy, device=dev, prefill_rows=cfg.lc)
+    kc = ten["k_cache"][0].to(dev).contiguous()
+    vc = ten["v_cache"][0].to(dev).contiguous()
+    q = qp.to(dev).contiguous()
+    out = torch.empty_like(q)
+    lse = torch.empty(q.shape[:3], dtype=torch.float32, device=dev)
+    batch.attend(q, out, kc, vc, lse)
+    torch.cuda.synchronize()
+    return out, lse, batch
+
+
+def check(cfg, lay, ten, qp, policy=0, branches=None):
+    out, lse, batch = run_prefill(cfg, lay, ten, qp, policy)
+    if branches is None:
+        branches = list(range(lay.n_branches))
+    ref, ref_lse = OP.point_prefill(lay, u16(qp), u16(ten["k_cache"][0]), u16(ten["v_cache"][0]),
+                                    policy=policy, branches=branches)
+    o = out[branches].float().cpu().numpy().astype(np.float64)
+    assert np.isfinite(o).all()
+    diff = o - ref
+    max_abs = float(np.abs(diff).max())
+    rel = float(np.linalg.norm(diff) / np.linalg.norm(ref))
+    lse_err = float(np.abs(lse[branches].cpu().numpy() - ref_lse).max())
+    assert max_abs <= MAX_ABS, (max_abs, rel, lse_err)
+    assert rel <= REL_L2, (max_abs, rel, lse_err)
+    assert lse_err <= LSE_ABS, (max_abs, rel, lse_err)
+    return batch
+
+
+def q_pre(cfg, lay, seed=5, scale=1.0):
+    return T.bf16_randn_u16((lay.n_branches, cfg.lc, cfg.hq, cfg.d), seed, "cpu", scale=scale)
+
+
+@pytest.mark.parametrize("dagf", [W.diamond, W.fig4, W.mixed8, lambda: W.chain(5, 2)])
+@pytest.mark.parametrize("policy", [0, 1])
+@pytest.mark.parametrize("d", [64, 128])
+def test_small_dags(dagf, policy, d):
+    cfg = C.CONFIGS["c1"].with_(lp=150, t=90, lc=8, page=16, d=d, hq=8, hkv=2)
+    lay = T.make_layout(cfg, ragged=True, dag_override=dagf)
+    ten = T.make_qkv(cfg, lay)
+    check(cfg, lay, ten, q_pre(cfg, lay), policy)
+
+
+@pytest.mark.parametrize("lc,hq,hkv", [(32, 8, 2), (32, 32, 8), (16, 28, 4), (64, 8, 4), (40, 8, 2)])
+def test_row_blocks_and_causal_spans(lc, hq, hkv):
+    # R = Lc*G rows per reader: 64 / 128 / 112 / 128 / 160 (> one 128-row MMA tile: two row blocks
+    # and a causal limit crossing the block boundary); Lc up to a whole 64-token tile
+    cfg = C.CONFIGS["c1"].with_(lp=300, t=200, lc=lc, page=32, d=128, hq=hq, hkv=hkv)
+    lay = T.make_layout(cfg, ragged=True, dag_override=W.mixed8)
+    ten = T.make_qkv(cfg, lay, q_scale=2.0)
+    check(cfg, lay, ten, q_pre(cfg, lay, scale=3.0))
+
+
+def test_sink_and_peaky_queries():
+    cfg = C.CONFIGS["c1"].with_(lp=500, t=120, lc=24, page=64, d=128, hq=8, hkv=2)
+    lay = T.make_layout(cfg, ragged=True, dag_override=W.diamond)
+    ten = T.make_qkv(cfg, lay, sink=True)
+    check(cfg, lay, ten, q_pre(cfg, lay, scale=4.0))
+
+
+def test_c2_full():
+    cfg = C.CONFIGS["c2"]
+    lay = T.make_layout(cfg, ragged=True)
+    ten = T.make_qkv(cfg, lay)
+    check(cfg, lay, ten, q_pre(cfg, lay))
+
+
+def test_c4_sampled():
+    cfg = C.CONFIGS["c4"].with_(n_queries=8)
+    lay = T.make_layout(cfg)
+    ten = T.make_qkv(cfg, lay)
+    check(cfg, lay, ten, q_pre(cfg, lay), branches=[0, 5, 15, 37, lay.n_branches - 1])
+
+
+def test_prefill_last_row_matches_decode_kernel():
+    # The method's identity (pin of O5) through both CUDA paths: with every point at own_len = Lc,
+    # the last content row of the prefill and a decode step of q = that row read the same context.
+    from oracle import step as OS
+    from tests.gpu_helpers import batch_for
+    cfg = C.CONFIGS["c1"].with_(lp=200, t=96, lc=32, page=32, d=128, hq=8, hkv=2)
+    lay = T.make_layout(cfg, dag_override=W.mixed8)
+    lay.own_len[:] = cfg.lc
+    ten = T.make_qkv(cfg, lay)
+    qp = q_pre(cfg, lay)
+    pre, _, _ = run_prefill(cfg, lay, ten, qp)
+    dev = torch.device("cuda")
+    q = qp[:, cfg.lc - 1].contiguous()
+    out = torch.empty(q.shape, dtype=q.dtype, device=dev)
+    batch_for(cfg, lay).attend(q.to(dev), out, ten["k_cache"][0].to(dev), ten["v_cache"][0].to(dev))
+    torch.cuda.synchronize()
+    ref, _ = OS.expand_step(lay, u16(q), u16(ten["k_cache"][0]), u16(ten["v_cache"][0]))
+    assert float(np.abs(out.float().cpu().numpy() - ref).max()) <= MAX_ABS
+    assert float(np.abs(pre[:, cfg.lc - 1].float().cpu().numpy() - ref).max()) <= MAX_ABS

@@ -253,3 +253,81 @@ def test_device_entry_points_validate_without_gpu():
     bad = _lib.AttnShape(4, 2, 80, 16, 0.0)
     assert L.orion_kv_append(ctypes.byref(bad), 1, None, None, None, None, None, None, None,
                              None, 0, None) == _lib.ERR_UNSUPPORTED
+
+
+# ------------------------------------------------------------------ point-prefill plans
+def _check_prefill_plan(cfg, lay, offs, segs, own_len):
+    """Row (b, i, h) of a prefill plan: its partials cover b's context without OWN exactly once,
+    plus one causal item over its own run's [0, Lc) (the kernel limits row i to [0, i])."""
+    lc = cfg.lc
+    plan, ws = orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, own_len,
+                                 prefill_rows=lc)
+    h, items, readers, coff, cslot = parse_plan(plan)
+    G = cfg.hq // cfg.hkv
+    R = lc * G
+    assert h["n_rows"] == lay.n_branches * lc * cfg.hq and int(h["pad"][2]) == lc
+    assert int(h["pad"][0]) == 0                     # rows-on-lanes tcgen05 kernel
+    slot = {}
+    for it in items:
+        end = it["t1"] if it["dyn"] < 0 else min(it["t1"], own_len[it["dyn"]])
+        toks = [(int(it["pt_off"]), t, bool(it["p0"] & 1)) for t in range(it["t0"], max(it["t0"], end))]
+        assert it["n_rows"] <= 128
+        for r in range(it["row_begin"], it["row_begin"] + it["n_rows"]):
+            b = readers[it["readers_off"] + r // R]
+            i, hh = (r % R) // G, it["kv_head"] * G + r % G
+            slot[it["slot0"] + r - it["row_begin"]] = ((b * lc + i) * cfg.hq + hh, toks, b)
+    assert sorted(slot) == list(range(h["n_partials"]))
+    for row in range(h["n_rows"]):
+        b = row // (lc * cfg.hq)
+        got, causal = [], []
+        for s in cslot[coff[row]:coff[row + 1]]:
+            srow, toks, sb = slot[s]
+            assert srow == row and sb == b
+            got += [(p, t) for p, t, c in toks if not c]
+            causal += [(p, t) for p, t, c in toks if c]
+        lst = segs[offs[b]:offs[b + 1]]
+        want = []
+        for sg in lst[:-1]:                          # every segment but OWN, in list order
+            eff = sg["len"] if sg["dyn"] < 0 else min(max(own_len[sg["dyn"]] - sg["start"], 0), sg["len"])
+            want += [(int(sg["pt_off"]), t) for t in range(sg["start"], sg["start"] + eff)]
+        assert sorted(got) == sorted(want) and len(got) == len(set(got))
+        own = lst[-1]
+        assert own["dyn"] == b
+        assert causal == [(int(own["pt_off"]), t) for t in range(lc)]
+
+
+@pytest.mark.parametrize("cfgname,policy,hq", [("c1", 0, 4), ("c1", 1, 4), ("c2", 0, 32), ("c3", 1, 28)])
+def test_prefill_plan_covers_context_and_causal_own(cfgname, policy, hq):
+    cfg = C.CONFIGS[cfgname].with_(n_queries=2, lp=min(C.CONFIGS[cfgname].lp, 256),
+                                   t=min(C.CONFIGS[cfgname].t, 96), hq=hq)
+    lay = T.make_layout(cfg, ragged=True, extra_tokens=cfg.page)
+    offs, segs = _bind_layout(cfg, lay, policy)
+    _check_prefill_plan(cfg, lay, offs, segs, lay.own_len)
+
+
+def test_prefill_plan_errors():
+    import ctypes
+    cfg = C.CONFIGS["c1"]
+    lay = T.make_layout(cfg)
+    offs, segs = _bind_layout(cfg, lay, 0)
+    with pytest.raises(orion.OrionError) as ei:          # the mma.sync kernel has no causal rows
+        orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, lay.own_len,
+                          prefill_rows=cfg.lc, flags=orion.PLAN_MMA_SYNC)
+    assert ei.value.code == _lib.ERR_UNSUPPORTED
+    with pytest.raises(orion.OrionError) as ei:          # OWN shorter than Lc
+        orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, lay.own_len,
+                          prefill_rows=int(segs["len"].max()) + 1)
+    assert ei.value.code == _lib.ERR_INVALID_ARG
+    # the two attention entry points refuse the other kind of plan before touching the device
+    L = _lib.lib()
+    shape = _lib.AttnShape(cfg.hq, cfg.hkv, cfg.d, cfg.page, 0.0)
+    pre, _ = orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, lay.own_len,
+                               prefill_rows=cfg.lc)
+    dec, _ = orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, lay.own_len)
+    fake = ctypes.c_void_p(16)
+    args = (fake, fake, None, fake, fake, 1, fake, fake)
+    assert L.orion_expand_attn(ctypes.byref(shape), lay.n_branches, *args, _lib.ptr(pre), fake, fake,
+                               1 << 30, None) == _lib.ERR_INVALID_ARG
+    assert L.orion_point_prefill_attn(ctypes.byref(shape), lay.n_branches, *args, _lib.ptr(dec), fake,
+                                      fake, 1 << 30, None) == _lib.ERR_INVALID_ARG
+    assert b"prefill" in L.orion_last_error()
