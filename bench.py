@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-point-prefill", action="store_true",
+                    help="skip the point-prefill attention measurement (SURVEY.md §8(f) rank 1)")
     ap.add_argument("--no-prefill", action="store_true",
                     help="skip the co-scheduled prefill measurement (SURVEY.md §8(a) a8)")
     ap.add_argument("--prefill-caps", default="148,132,116",
@@ -337,6 +339,8 @@ def run_orion(args, cfg, layers):
         "clocks": clocks,
         "e2e": e2e,
     }
+    if world == 1 and not args.no_point_prefill:
+        line["point_prefill"] = run_point_prefill(args, cfg, lay, layers, kc, vc, dev)
     if world == 1 and not args.no_prefill:
         line["prefill_costream"] = run_costream(args, cfg, lay, layers, q, kn, vn, out, kc, vc, dev,
                                                 value)
@@ -345,6 +349,60 @@ def run_orion(args, cfg, layers):
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_point_prefill(args, cfg, lay, layers, kc, vc, dev):
+    """§8(f) rank 1: the Pre-stage attention of every point of the batch (Alg. 1 l.12/19):
+    Lc content rows per point attend to the point's dependency context plus their own content,
+    causally (orion_point_prefill_attn; oracle O5).  Dense multi-row attention: tensor-bound.
+    Timed on the device over `steps` launches cycling through the layers' KV pools."""
+    import torch
+    import paper_2510_24390_b200 as orion
+    queries = [dict(n_points=int(lay.n_points[i]), edges=lay.edges[i],
+                    prefix_pt_off=int(lay.prefix_pt_off[i]), prefix_len=int(lay.prefix_len[i]))
+               for i in range(lay.n_queries)]
+    points = np.stack([lay.point_pt_off, lay.content_len, lay.point_cap], 1)
+    lc = cfg.lc
+    batch = orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, lay.page_table,
+                                 lay.own_len, policy=args.policy, device=dev, prefill_rows=lc)
+    g = torch.Generator(device=dev)
+    g.manual_seed(cfg.seed * 13)
+    B = lay.n_branches
+    q = torch.randn((B, lc, cfg.hq, cfg.d), generator=g, device=dev).to(torch.bfloat16)
+    out = torch.empty_like(q)
+    stream = torch.cuda.current_stream(dev)
+    for l in range(min(3, layers)):
+        batch.attend(q, out, kc[l], vc[l])
+    torch.cuda.synchronize()
+    n = max(3, min(args.steps, layers))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(n):
+        batch.attend(q, out, kc[i % layers], vc[i % layers])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / n
+    st = batch.stats
+    # useful FLOPs (causal, no padding): per (branch, content row i, q head): (ctx_b + i + 1)
+    # key rows x d x 4 (QK^T and PV).  logical_tokens = sum_b (ctx_b + Lc) per kv head.
+    ctx_sum = st["logical_tokens"] - B * lc
+    flop = cfg.hq * cfg.d * 4.0 * (lc * ctx_sum + B * lc * (lc + 1) / 2)
+    tflops = flop / (ms / 1e3) / 1e12
+    peaks = {}
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            peaks = json.load(f)
+    peak = peaks.get("bf16_tflops", 2250.0)
+    return {"workload": f"{cfg.name} point prefill: {B} points x Lc {lc} content rows x {cfg.hq} heads, "
+                        f"contexts = dependency lists + causal own ({args.policy and 'parents_eq3' or 'ancestors'})",
+            "kernel": "split_tc_kernel (rows-on-lanes tcgen05, causal own items) + combine",
+            "ms_per_layer": ms, "launches": n, "rows": B * lc * cfg.hq,
+            "roofline": {"bound": "tensor", "achieved": tflops, "peak": peak, "unit": "TFLOP/s",
+                         "frac": tflops / peak, "flop_per_launch": flop,
+                         "peak_source": "measured (MEASURED_PEAKS.json bf16_tflops, burst)"
+                                        if "bf16_tflops" in peaks else "nominal dense bf16"},
+            "plan": {"items": st["n_items"], "partials": st["n_partials"]}}
 
 
 # Llama-3-8B decoder-layer prefill of 4096 tokens (SURVEY.md §8(a) a8): QKV, O, gate+up, down.
