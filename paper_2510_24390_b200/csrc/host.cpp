@@ -322,10 +322,13 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
                                                          : kRowsPerItemMMA;
   chunk = std::max(kTileTokens, (chunk + kTileTokens - 1) / kTileTokens * kTileTokens);
 
-  // 1. Group bound segments by page run.  A prefill plan takes each branch's OWN segment (the one
-  //    growing with the branch itself) out: it is read causally by that branch alone.
+  // 1. Group bound segments by page run.  A prefill plan instead keeps every branch's list as a
+  //    range list (reader-stationary: one work item streams the whole context of one branch's
+  //    Lc*G rows, so Q is loaded once and each row gets one partial); its OWN segment (the one
+  //    growing with the branch itself) becomes the last range, read causally over [start, +Lc).
   std::map<int32_t, std::vector<Interval>> groups;
   std::vector<orion_seg> own_causal(Lc > 0 ? n_branches : 0, orion_seg{-1, 0, 0, -1});
+  std::vector<std::vector<Range>> branch_ranges(Lc > 0 ? n_branches : 0);
   std::vector<int64_t> logical(n_branches, 0);
   int64_t logical_total = 0;
   for (int32_t b = 0; b < n_branches; ++b) {
@@ -345,7 +348,8 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
         continue;
       }
       if (s.len == 0) continue;  // zero-length segments are skipped (reading S22)
-      groups[s.pt_off].push_back({s.start, s.start + s.len, s.dyn, b});
+      if (Lc > 0) branch_ranges[b].push_back(Range{s.pt_off, s.start, s.start + s.len, s.dyn, 0, {0, 0, 0}});
+      else groups[s.pt_off].push_back({s.start, s.start + s.len, s.dyn, b});
       logical[b] += s.len;
     }
     if (Lc > 0 && own_causal[b].pt_off < 0)
@@ -443,15 +447,38 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
     unique_tokens += p.t1 - p.t0;
     add_items(p.pt_off, p.t0, p.t1, p.dyn, 0, p.readers, (int32_t)pi);
   }
-  // Prefill: each branch's own content tokens, causal, one reader.  The causal chunk must hold
-  // all Lc tokens in one item (row i's limit is relative to the item's t0).
-  for (int32_t b = 0; b < (Lc > 0 ? n_branches : 0); ++b) {
-    const orion_seg& s = own_causal[b];
-    if (Lc > std::max(chunk, 32 * std::min(R, rows_per_item)))
-      return fail(ORION_ERR_UNSUPPORTED, "prefill rows %d exceed one work item's chunk", Lc);
-    unique_tokens += Lc;
-    add_items(s.pt_off, s.start, s.start + Lc, -1, kItemCausal, std::vector<int32_t>{b},
-              (int32_t)pieces.size() + b);
+  // Prefill: per kv head and branch, one multi-range item per row block: the branch's ranges in
+  // list order, then its own content tokens (causal).  Items of one query's branches are adjacent
+  // for each kv head, so the shared prefix streams through L2 for all of them at about once.
+  std::vector<Range> ranges;
+  if (Lc > 0) {
+    std::vector<int32_t> range_off(n_branches);
+    for (int32_t b = 0; b < n_branches; ++b) {
+      const orion_seg& s = own_causal[b];
+      branch_ranges[b].push_back(Range{s.pt_off, s.start, s.start + Lc, -1, kItemCausal, {0, 0, 0}});
+      range_off[b] = (int32_t)ranges.size();
+      ranges.insert(ranges.end(), branch_ranges[b].begin(), branch_ranges[b].end());
+      unique_tokens += logical[b];
+    }
+    for (int32_t g = 0; g < Hkv; ++g)
+      for (int32_t b = 0; b < n_branches; ++b) {
+        const int32_t roff = (int32_t)readers.size();
+        readers.push_back(b);
+        for (int32_t r0 = 0; r0 < R; r0 += rows_per_item) {
+          WorkItem w{};
+          w.pt_off = range_off[b]; w.t0 = 0; w.t1 = 0; w.dyn = -1;
+          w.kv_head = g; w.readers_off = roff; w.row_begin = r0;
+          w.n_rows = std::min(rows_per_item, R - r0); w.slot0 = n_slots; w.piece = -1;
+          w.flags = kItemRanges; w.n_ranges = (int32_t)branch_ranges[b].size();
+          for (int32_t r = r0; r < r0 + w.n_rows; ++r) {
+            const int32_t i = r / G, h = g * G + r % G;
+            row_slots[((size_t)b * Lrows + i) * Hq + h].push_back(n_slots + (r - r0));
+          }
+          n_slots += w.n_rows;
+          items.push_back(w);
+          cost.push_back(0);                         // generation order kept (see above)
+        }
+      }
   }
   for (size_t r = 0; r < row_slots.size(); ++r)
     if (row_slots[r].empty())
@@ -461,7 +488,8 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
   // together and share the chunk through L2.
   std::vector<int32_t> perm(items.size());
   for (size_t i = 0; i < perm.size(); ++i) perm[i] = (int32_t)i;
-  std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) { return cost[a] > cost[b]; });
+  if (Lc == 0)
+    std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) { return cost[a] > cost[b]; });
 
   // 4. Serialise.
   const int64_t n_rows = (int64_t)n_branches * Lrows * Hq;
@@ -475,7 +503,9 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
   h.readers_off = align16(h.items_off + (int64_t)items.size() * sizeof(WorkItem));
   h.comb_off_off = align16(h.readers_off + (int64_t)readers.size() * 4);
   h.comb_slot_off = align16(h.comb_off_off + (n_rows + 1) * 4);
-  h.plan_bytes = align16(h.comb_slot_off + (int64_t)n_slots * 4);
+  h.ranges_off = align16(h.comb_slot_off + (int64_t)n_slots * 4);
+  h.n_ranges = (int32_t)ranges.size();
+  h.plan_bytes = align16(h.ranges_off + (int64_t)ranges.size() * sizeof(Range));
   if (partials_fp16(variant)) {
     h.acc_bytes = align16((int64_t)n_slots * shape->head_dim * 2);
     h.workspace_bytes = h.acc_bytes + align16((int64_t)n_slots * 4);
@@ -510,6 +540,7 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
     for (int32_t s : row_slots[r]) cslot[o++] = s;
   }
   coff[n_rows] = o;
+  if (!ranges.empty()) std::memcpy(base + h.ranges_off, ranges.data(), ranges.size() * sizeof(Range));
   return ORION_OK;
 }
 

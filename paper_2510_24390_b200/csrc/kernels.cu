@@ -455,6 +455,7 @@ orion_status launch_split(const PlanHeader* h, const char* dplan, const void* q,
   if (h->variant == kVariantTC || h->variant == kVariantTCT) {
     TcArgs t;
     t.items = reinterpret_cast<const WorkItem*>(dplan + h->items_off);
+    t.ranges = reinterpret_cast<const Range*>(dplan + h->ranges_off);
     t.readers = reinterpret_cast<const int32_t*>(dplan + h->readers_off);
     t.q = static_cast<const __nv_bfloat16*>(q);
     t.page_table = page_table;

@@ -3,7 +3,7 @@
 //
 // A plan is one contiguous byte buffer:
 //   PlanHeader | WorkItem[n_items] | readers[n_reader_entries] (int32 branch ids)
-//              | comb_off[n_rows + 1] (int32) | comb_slot[n_partials] (int32)
+//              | comb_off[n_rows + 1] (int32) | comb_slot[n_partials] (int32) | Range[n_ranges]
 // Workspace (caller-allocated, device), one partial (softmax state of one query row over one
 // work item's tokens) per slot, in one of two formats fixed by the plan's variant:
 //   fp32 (kVariantTC, kVariantMmaSync):
@@ -27,6 +27,7 @@ constexpr int kRowsPerItemTCT = 64;  // query rows per work item, transposed tcg
 enum : int32_t { kVariantTC = 0, kVariantMmaSync = 1, kVariantTCT = 2 };
 inline bool partials_fp16(int32_t variant) { return variant == kVariantTCT; }
 constexpr int32_t kItemCausal = 1;
+constexpr int32_t kItemRanges = 2;
 constexpr int kTileTokens = 64;    // tokens per pipeline stage in the split kernel
 
 struct PlanHeader {
@@ -41,6 +42,8 @@ struct PlanHeader {
                     // kVariantMmaSync (ORION_PLAN_MMA_SYNC)
   int32_t max_ctas; // persistent split kernels: grid cap (opts->num_sms; 0 = all SMs)
   int32_t prefill_rows;  // 0: decode plan; Lc: point-prefill plan (rows = branch x Lc x Hq)
+  int64_t ranges_off;    // byte offset of Range[n_ranges] (multi-range items)
+  int32_t n_ranges, pad2_;
 };
 static_assert(sizeof(PlanHeader) % 16 == 0, "header must keep 16-byte alignment");
 
@@ -53,8 +56,16 @@ static_assert(sizeof(PlanHeader) % 16 == 0, "header must keep 16-byte alignment"
 struct WorkItem {
   int32_t pt_off, t0, t1, dyn;
   int32_t kv_head, readers_off, row_begin, n_rows;
-  int32_t slot0, piece, flags, pad1;   // flags & kItemCausal: row i sees tokens < t0 + i + 1
+  int32_t slot0, piece, flags, n_ranges;   // flags: kItemCausal, kItemRanges
 };
+
+// A token range of a multi-range item (kItemRanges: the item streams ranges[pt_off ..
+// pt_off + n_ranges) of the plan in order, as one accumulation): tokens [t0, min(t1,
+// own_len[dyn])) of the page run at pt_off; flags & kItemCausal: row i sees tokens < t0 + i + 1.
+struct Range {
+  int32_t pt_off, t0, t1, dyn, flags, pad_[3];
+};
+static_assert(sizeof(Range) == 32, "Range is 2 x 16 bytes");
 static_assert(sizeof(WorkItem) == 48, "WorkItem is 3 x 16 bytes");
 
 }  // namespace orion

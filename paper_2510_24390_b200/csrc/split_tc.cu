@@ -167,20 +167,38 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int m, int n, bool b_mn_major)
          (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(m >> 4) << 24);
 }
 
-struct ItemGeom {
-  int32_t base, end, ntiles;
+// Geometry of one token range of an item: the item itself, or range r of a multi-range item
+// (kItemRanges, point-prefill plans).  Tiles sit on the 64-token grid of the range's page run.
+struct RangeG {
+  int32_t pt_off, t0, end, base, ntiles, causal;
 };
-__device__ __forceinline__ ItemGeom geom(const WorkItem& w, const int32_t* own_len) {
-  ItemGeom g;
-  g.end = w.t1;
-  if (w.dyn >= 0) g.end = min(g.end, __ldg(own_len + w.dyn));
-  g.base = w.t0 & ~(kTok - 1);
-  g.ntiles = g.end > w.t0 ? (g.end - g.base + kTok - 1) / kTok : 0;
+__device__ __forceinline__ int item_nranges(const WorkItem& w) {
+  return (w.flags & kItemRanges) ? w.n_ranges : 1;
+}
+__device__ __forceinline__ RangeG range_geom(const TcArgs& a, const WorkItem& w, int r) {
+  int32_t t1, dyn, fl;
+  RangeG g;
+  if (w.flags & kItemRanges) {
+    const Range R = a.ranges[w.pt_off + r];
+    g.pt_off = R.pt_off; g.t0 = R.t0; t1 = R.t1; dyn = R.dyn; fl = R.flags;
+  } else {
+    g.pt_off = w.pt_off; g.t0 = w.t0; t1 = w.t1; dyn = w.dyn; fl = w.flags;
+  }
+  g.end = t1;
+  if (dyn >= 0) g.end = min(g.end, __ldg(a.own_len + dyn));
+  g.base = g.t0 & ~(kTok - 1);
+  g.ntiles = g.end > g.t0 ? (g.end - g.base + kTok - 1) / kTok : 0;
+  g.causal = (fl & kItemCausal) != 0;
   return g;
+}
+__device__ __forceinline__ int item_tiles(const TcArgs& a, const WorkItem& w) {
+  int n = 0;
+  for (int r = 0; r < item_nranges(w); ++r) n += range_geom(a, w, r).ntiles;
+  return n;
 }
 
 __device__ __forceinline__ int next_nonempty(const TcArgs& a, int it) {
-  while (it < a.n_items && geom(a.items[it], a.own_len).ntiles == 0) it += gridDim.x;
+  while (it < a.n_items && item_tiles(a, a.items[it]) == 0) it += gridDim.x;
   return it;
 }
 
@@ -253,6 +271,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmK16)) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmV16)) : "memory");
   }
+  for (int i = tid; i < SV * L::KVB / 16; i += blockDim.x)          // V ring starts finite
+    reinterpret_cast<uint4*>(smem + L::OFF_V)[i] = make_uint4(0, 0, 0, 0);
   for (int i = tid; i < 16 * kTok * 2 / 16; i += blockDim.x)       // bf16 1.0 = 0x3F80
     reinterpret_cast<uint4*>(smem + L::OFF_ONES)[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
   fence_proxy_async();
@@ -278,14 +298,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const int big = min(kTok, 1 << a.page_shift);          // rows of a full-tile box
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const WorkItem w = a.items[it];
-      const ItemGeom g = geom(w, a.own_len);
+      for (int rg_i = 0; rg_i < item_nranges(w); ++rg_i) {
+      const RangeG g = range_geom(a, w, rg_i);
       for (int tb0 = 0; tb0 < g.ntiles; tb0 += 32) {
         // lane l describes tile tb0 + l: up to 4 boxes (row coordinate each), kind, offsets
         int brow[4] = {0, 0, 0, 0};
         int nbox = 0, first_off = 0, full = 0;
         if (tb0 + lane < g.ntiles) {
           const int a0 = g.base + (tb0 + lane) * kTok;
-          const int lo = max(a0, w.t0), hi = min(a0 + kTok, g.end);
+          const int lo = max(a0, g.t0), hi = min(a0 + kTok, g.end);
           full = (lo == a0 && hi == a0 + kTok);
           int pos0, step;
           if (full) { nbox = kTok / big; pos0 = a0; step = big; first_off = 0; }
@@ -294,7 +315,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           for (int b = 0; b < 4; ++b) {
             if (b < nbox) {
               const int pos = pos0 + b * step;
-              const int page = __ldg(a.page_table + w.pt_off + (pos >> a.page_shift));
+              const int page = __ldg(a.page_table + g.pt_off + (pos >> a.page_shift));
               brow[b] = ((page * a.hkv + w.kv_head) << a.page_shift) + (pos & pmask);
             }
           }
@@ -341,6 +362,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           __syncwarp();
         }
       }
+      }
     }
     TRACE_DUMP("producer");
   } else if (warp == kWarpMMA) {
@@ -363,14 +385,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     auto start = [&](Cur& c) {
       c.it = next_nonempty(a, blockIdx.x);
       c.t = 0; c.k = 0; c.j = 0;
-      c.nt = c.it < n_items ? geom(a.items[c.it], a.own_len).ntiles : 0;
+      c.nt = c.it < n_items ? item_tiles(a, a.items[c.it]) : 0;
     };
     auto advance = [&](Cur& c) {
       ++c.j;
       if (++c.t == c.nt) {
         c.it = next_nonempty(a, c.it + gridDim.x);
         c.t = 0; ++c.k;
-        c.nt = c.it < n_items ? geom(a.items[c.it], a.own_len).ntiles : 0;
+        c.nt = c.it < n_items ? item_tiles(a, a.items[c.it]) : 0;
       }
     };
     auto issue_qk = [&](const Cur& c) {
@@ -474,8 +496,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     uint32_t j = 0, k = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const WorkItem w = a.items[it];
-      const ItemGeom g = geom(w, a.own_len);
-      if (g.ntiles == 0) {                         // empty (dyn end <= t0): neutral partial
+      if (item_tiles(a, w) == 0) {                 // empty (dyn end <= t0): neutral partial
         if (p == 0 && r < w.n_rows) {
           float* dst = a.part_acc + static_cast<size_t>(w.slot0 + r) * D;
 #pragma unroll
@@ -485,12 +506,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         continue;
       }
       const bool active = (warp & 3) * 32 < w.n_rows;   // warp-uniform
-      // point prefill, causal own item: row r (content position i) sees tokens [t0, t0 + i]
-      const bool causal = (w.flags & kItemCausal) != 0;
-      const int row_end = causal ? min(g.end, w.t0 + ((w.row_begin + r) % (a.lc * a.group)) / a.group + 1) : g.end;
+      // point prefill: this row's content position i; in the causal own range it sees [t0, t0 + i]
+      const int rpos = ((w.row_begin + r) % (a.lc * a.group)) / a.group;
       float m_used = -INFINITY;
       bool had = false;
       uint32_t jl = 0;                              // last tile of this WG in the item
+      for (int rg_i = 0; rg_i < item_nranges(w); ++rg_i) {
+      const RangeG g = range_geom(a, w, rg_i);
+      const int row_end = g.causal ? min(g.end, g.t0 + rpos + 1) : g.end;
       for (int t = 0; t < g.ntiles; ++t, ++j) {
         if ((j & 1) != static_cast<uint32_t>(p)) continue;
         const int tb = g.base + t * kTok;
@@ -509,7 +532,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         mbar_arrive(s_free + p);                  // QK(j+2) may overwrite S[p] now
         // PV(j-2) complete: P[p] is free and O_p is up to date (needed for a rescale).
         if (j >= 2) TW(7, mbar_wait(pv_done + p, ((j - 2) >> 1) & 1));
-        const bool edge = causal || (tb < w.t0) || (tb + kTok > g.end);
+        const bool edge = g.causal || (tb < g.t0) || (tb + kTok > g.end);
         uint32_t pk[32];
         if (active) {
           float mx = -INFINITY;                     // raw scores; scale > 0 commutes with max
@@ -517,7 +540,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #pragma unroll
             for (int c = 0; c < 64; ++c) mx = fmaxf(mx, __uint_as_float(sr[c]));
           } else {
-            const int lo_c = w.t0 - tb, hi_c = row_end - tb;   // valid columns [lo_c, hi_c)
+            const int lo_c = g.t0 - tb, hi_c = row_end - tb;   // valid columns [lo_c, hi_c)
 #pragma unroll
             for (int c = 0; c < 64; ++c) {
               const float v = (c >= lo_c && c < hi_c) ? __uint_as_float(sr[c]) : -INFINITY;
@@ -566,9 +589,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #ifdef ORION_TC_TRACE
         tr_[2] += clock64() - ts0; ts0 = clock64();
 #endif
-        if (edge && r < kTok) {                  // zero V rows outside [t0, end) of this tile
+        if (edge) {   // zero V rows outside [t0, end) once the tile has landed (0 x NaN = NaN);
+                      // alias-free: PV(j-2) done implies V(j - SV) landed
+          mbar_wait(v_full + (j % SV), (j / SV) & 1);
+        }
+        if (edge && r < kTok) {
           const int pos = tb + r;
-          if (pos < w.t0 || pos >= g.end) {
+          if (pos < g.t0 || pos >= g.end) {
             uint8_t* vrow = smem + L::OFF_V + (j % SV) * L::KVB + r * 128;
 #pragma unroll
             for (int h = 0; h < NH; ++h) {
@@ -586,6 +613,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #endif
         had = true;
         jl = j;
+      }
       }
       if (p == 0) {                  // next item's Q was gathered one item ahead: publish it
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");

@@ -40,6 +40,7 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 
 struct TcArgs {
   const WorkItem* items;
+  const Range* ranges;    // multi-range items (kItemRanges)
   const int32_t* readers;
   const __nv_bfloat16* q;
   const int32_t* page_table;

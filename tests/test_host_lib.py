@@ -131,7 +131,9 @@ HDR = np.dtype([("magic", "<i4"), ("version", "<i4"), ("n_branches", "<i4"), ("h
                 ("items_off", "<i8"), ("readers_off", "<i8"), ("comb_off_off", "<i8"),
                 ("comb_slot_off", "<i8"), ("plan_bytes", "<i8"), ("workspace_bytes", "<i8"),
                 ("acc_bytes", "<i8"), ("n_pieces", "<i8"), ("unique_tokens", "<i8"),
-                ("logical_tokens", "<i8"), ("sm_scale", "<f4"), ("pad", "<i4", 3)])
+                ("logical_tokens", "<i8"), ("sm_scale", "<f4"), ("pad", "<i4", 3),
+                ("ranges_off", "<i8"), ("n_ranges", "<i4"), ("pad2", "<i4")])
+RANGE = np.dtype([(n, "<i4") for n in ("pt_off", "t0", "t1", "dyn", "flags", "r0", "r1", "r2")])
 ITEM = np.dtype([(n, "<i4") for n in ("pt_off", "t0", "t1", "dyn", "kv_head", "readers_off",
                                       "row_begin", "n_rows", "slot0", "piece", "p0", "p1")])
 
@@ -257,43 +259,38 @@ def test_device_entry_points_validate_without_gpu():
 
 # ------------------------------------------------------------------ point-prefill plans
 def _check_prefill_plan(cfg, lay, offs, segs, own_len):
-    """Row (b, i, h) of a prefill plan: its partials cover b's context without OWN exactly once,
-    plus one causal item over its own run's [0, Lc) (the kernel limits row i to [0, i])."""
+    """Row (b, i, h) of a prefill plan has exactly one partial, from one reader-stationary item whose
+    ranges are b's list except OWN (same order and extents) followed by the causal own range
+    [0, Lc) of its run (the kernel limits row i to [0, i])."""
     lc = cfg.lc
     plan, ws = orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, own_len,
                                  prefill_rows=lc)
     h, items, readers, coff, cslot = parse_plan(plan)
+    ranges = np.frombuffer(plan, RANGE, int(h["n_ranges"]), int(h["ranges_off"]))
     G = cfg.hq // cfg.hkv
     R = lc * G
     assert h["n_rows"] == lay.n_branches * lc * cfg.hq and int(h["pad"][2]) == lc
     assert int(h["pad"][0]) == 0                     # rows-on-lanes tcgen05 kernel
     slot = {}
     for it in items:
-        end = it["t1"] if it["dyn"] < 0 else min(it["t1"], own_len[it["dyn"]])
-        toks = [(int(it["pt_off"]), t, bool(it["p0"] & 1)) for t in range(it["t0"], max(it["t0"], end))]
-        assert it["n_rows"] <= 128
-        for r in range(it["row_begin"], it["row_begin"] + it["n_rows"]):
-            b = readers[it["readers_off"] + r // R]
-            i, hh = (r % R) // G, it["kv_head"] * G + r % G
-            slot[it["slot0"] + r - it["row_begin"]] = ((b * lc + i) * cfg.hq + hh, toks, b)
-    assert sorted(slot) == list(range(h["n_partials"]))
-    for row in range(h["n_rows"]):
-        b = row // (lc * cfg.hq)
-        got, causal = [], []
-        for s in cslot[coff[row]:coff[row + 1]]:
-            srow, toks, sb = slot[s]
-            assert srow == row and sb == b
-            got += [(p, t) for p, t, c in toks if not c]
-            causal += [(p, t) for p, t, c in toks if c]
+        assert it["p0"] == 2 and it["n_rows"] <= 128          # kItemRanges
+        rg = ranges[it["pt_off"]:it["pt_off"] + it["p1"]]
+        b = readers[it["readers_off"]]
         lst = segs[offs[b]:offs[b + 1]]
-        want = []
-        for sg in lst[:-1]:                          # every segment but OWN, in list order
-            eff = sg["len"] if sg["dyn"] < 0 else min(max(own_len[sg["dyn"]] - sg["start"], 0), sg["len"])
-            want += [(int(sg["pt_off"]), t) for t in range(sg["start"], sg["start"] + eff)]
-        assert sorted(got) == sorted(want) and len(got) == len(set(got))
+        want = [(int(sg["pt_off"]), int(sg["start"]), int(sg["start"] + sg["len"]), int(sg["dyn"]), 0)
+                for sg in lst[:-1] if sg["len"] > 0]
         own = lst[-1]
         assert own["dyn"] == b
-        assert causal == [(int(own["pt_off"]), t) for t in range(lc)]
+        want.append((int(own["pt_off"]), int(own["start"]), int(own["start"]) + lc, -1, 1))
+        assert [tuple(int(x) for x in r)[:5] for r in rg] == want
+        for r in range(it["row_begin"], it["row_begin"] + it["n_rows"]):
+            assert r < R
+            i, hh = r // G, it["kv_head"] * G + r % G
+            slot[it["slot0"] + r - it["row_begin"]] = (b * lc + i) * cfg.hq + hh
+    assert sorted(slot) == list(range(h["n_partials"]))
+    for row in range(h["n_rows"]):
+        ss = cslot[coff[row]:coff[row + 1]]
+        assert len(ss) == 1 and slot[int(ss[0])] == row
 
 
 @pytest.mark.parametrize("cfgname,policy,hq", [("c1", 0, 4), ("c1", 1, 4), ("c2", 0, 32), ("c3", 1, 28)])
