@@ -530,8 +530,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #endif
         tc_fence_before();
         mbar_arrive(s_free + p);                  // QK(j+2) may overwrite S[p] now
-        // PV(j-2) complete: P[p] is free and O_p is up to date (needed for a rescale).
-        if (j >= 2) TW(7, mbar_wait(pv_done + p, ((j - 2) >> 1) & 1));
+        // PV(j-2) must be complete before O_p is rescaled or P[p] rewritten; the wait is taken as
+        // late as possible so that its latency overlaps this tile's exponentials.
+        bool pv_ok = j < 2;
         const bool edge = g.causal || (tb < g.t0) || (tb + kTok > g.end);
         uint32_t pk[32];
         if (active) {
@@ -555,6 +556,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           if (__any_sync(0xffffffffu, mine)) {
             const float alpha = mine ? ex2(m_used - mx) : 1.f;   // 0 when m_used == -inf
             if (had) {
+              if (!pv_ok) { TW(7, mbar_wait(pv_done + p, ((j - 2) >> 1) & 1)); pv_ok = true; }
               tc_fence_after();
 #pragma unroll 1
               for (int cb = 0; cb < D; cb += 16) {
@@ -584,13 +586,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #ifdef ORION_TC_TRACE
         tr_[1] += clock64() - ts0; ts0 = clock64();
 #endif
+        if (!pv_ok) TW(7, mbar_wait(pv_done + p, ((j - 2) >> 1) & 1));
+        tc_fence_after();
         tmem_st32x32(tmem + lane_base + colP(p), pk);
         tc_wait_st();
 #ifdef ORION_TC_TRACE
         tr_[2] += clock64() - ts0; ts0 = clock64();
 #endif
         if (edge) {   // zero V rows outside [t0, end) once the tile has landed (0 x NaN = NaN);
-                      // alias-free: PV(j-2) done implies V(j - SV) landed
+                      // alias-free: PV(j-2) done (waited above) implies V(j - SV) landed
           mbar_wait(v_full + (j % SV), (j / SV) & 1);
         }
         if (edge && r < kTok) {
