@@ -290,6 +290,51 @@ orion_status orion_expand_combine(const orion_attn_shape* shape, int32_t n_branc
                                   float* lse, const void* h_plan, const void* d_plan,
                                   const void* workspace, size_t workspace_bytes, void* stream);
 
+/*
+ * orion_expansion_round — one round of the expansion schedule: PAPER.md Alg. 1 l.9-22 with the
+ * running set R processed as one batch per round (reading D1; Fig. 4 walkthrough
+ * PAPER.md:387; oracle O6).  Host only, reentrant: the schedule state is in caller arrays.
+ * Round r prefills every point not yet prefilled whose stage predecessors (Contextual k->j:
+ * Pre(k); Dependent k->j: Dec(k)) completed in rounds < r, and decodes one token of
+ * every point whose Pre completed in a round < r and whose Dec has not completed.  Pre completes
+ * in the round it runs; Dec completes with the point's last token (with its Pre if it has none).
+ *  queries[n_queries]          n_points / branch0 used (points of query i are global branches
+ *                              branch0 .. branch0 + n_points - 1).
+ *  edge_offsets[n_queries+1], edges[]  query i's edges are edges[edge_offsets[i] ..
+ *                              edge_offsets[i+1]), query-local point ids 1..n_points.
+ *  tokens[n_branches]          decode tokens each point generates (T - Lc).
+ *  pre_round, dec_round [n_branches]  in/out: round in which Pre / Dec completed, -1 = not yet
+ *                              (initialise to -1).
+ *  left[n_branches]            in/out: decode tokens still to generate.
+ *  round                       this round's index (0, 1, ... consecutively).
+ *  pre_out, dec_out [n_branches], n_pre, n_dec  out: this round's prefill / decode branches,
+ *                              ascending.  Both empty: every point has completed.
+ * Errors: INVALID_ARG, UNKNOWN_POINT (edge outside its query), CYCLE (nothing can run but stages
+ * are pending).
+ */
+orion_status orion_expansion_round(int32_t n_queries, const orion_query_desc* queries,
+                                   const int32_t* edge_offsets, const orion_edge* edges,
+                                   int32_t n_branches, const int32_t* tokens, int32_t* pre_round,
+                                   int32_t* dec_round, int32_t* left, int32_t round,
+                                   int32_t* pre_out, int32_t* n_pre, int32_t* dec_out,
+                                   int32_t* n_dec);
+
+/*
+ * orion_select_branches — the bound segment lists of a subset of branches (the running set of a
+ * round), ready for orion_expand_plan over just that subset.  Host only.  Branch sel[i]'s list
+ * becomes list i; a segment growing with a selected branch (dyn = sel[k]) gets dyn = k; one
+ * growing with an unselected branch (a finished ancestor) is frozen to the static extent
+ * [start, start + clamp(own_len[dyn] - start, 0, len)).
+ *  seg_offsets[n_branches+1], segs[]  lists of all branches (orion_bind_segments).
+ *  own_len[n_branches]   current lengths.   sel[n_sel]  distinct branch ids.
+ *  sel_offsets[n_sel+1], sel_segs[segs_cap]  out; segs_needed out (always written).
+ * Errors: INVALID_ARG (bad / repeated ids), CAPACITY (segs_cap < *segs_needed).
+ */
+orion_status orion_select_branches(int32_t n_branches, const int32_t* seg_offsets,
+                                   const orion_seg* segs, const int32_t* own_len, int32_t n_sel,
+                                   const int32_t* sel, int32_t* sel_offsets, orion_seg* sel_segs,
+                                   int32_t segs_cap, int32_t* segs_needed);
+
 /* Thread-local message describing the last non-OK status returned on this thread. */
 const char* orion_last_error(void);
 

@@ -84,6 +84,50 @@ def bind_segments(queries, points, seg_offsets, refs):
     return out
 
 
+def expansion_round(queries, edge_offsets, edges, tokens, pre_round, dec_round, left, rnd):
+    """orion_expansion_round.  queries: [(n_points, branch0, prefix_pt_off, prefix_len)];
+    edge_offsets [Q+1] / edges [E, 3] int32; tokens, pre_round, dec_round, left: np.int32 [B],
+    the last three updated in place.  Returns (prefill branches, decode branches) of round rnd."""
+    qd = np.ascontiguousarray(np.array(queries, dtype=np.int32).reshape(-1, 4))
+    eo = np.ascontiguousarray(edge_offsets, dtype=np.int32)
+    ed = np.ascontiguousarray(np.array(edges, dtype=np.int32).reshape(-1, 3))
+    tk = np.ascontiguousarray(tokens, dtype=np.int32)
+    for a in (pre_round, dec_round, left):
+        if a.dtype != np.int32 or not a.flags.c_contiguous:
+            raise OrionError(_lib.ERR_INVALID_ARG, "state arrays must be contiguous np.int32")
+    nb = len(tk)
+    po = np.zeros(max(nb, 1), np.int32)
+    do = np.zeros(max(nb, 1), np.int32)
+    npre = np.zeros(1, np.int32)
+    ndec = np.zeros(1, np.int32)
+    _lib.check(lib().orion_expansion_round(len(qd), _lib.ptr(qd), _lib.ptr(eo),
+                                           _lib.ptr(ed) if len(ed) else None, nb, _lib.ptr(tk),
+                                           _lib.ptr(pre_round), _lib.ptr(dec_round), _lib.ptr(left),
+                                           int(rnd), _lib.ptr(po), _lib.ptr(npre), _lib.ptr(do),
+                                           _lib.ptr(ndec)))
+    return po[:int(npre[0])].copy(), do[:int(ndec[0])].copy()
+
+
+def select_branches(seg_offsets, segs, own_len, sel):
+    """orion_select_branches -> (seg_offsets [n_sel+1], segs) of the branches `sel`."""
+    so = np.ascontiguousarray(seg_offsets, dtype=np.int32)
+    sg = np.ascontiguousarray(segs).astype(SEG_DTYPE)
+    ol = np.ascontiguousarray(own_len, dtype=np.int32)
+    sl = np.ascontiguousarray(sel, dtype=np.int32)
+    off = np.zeros(len(sl) + 1, np.int32)
+    need = np.zeros(1, np.int32)
+    code = lib().orion_select_branches(len(so) - 1, _lib.ptr(so), _lib.ptr(sg), _lib.ptr(ol), len(sl),
+                                       _lib.ptr(sl) if len(sl) else None, _lib.ptr(off), None, 0,
+                                       _lib.ptr(need))
+    if code != _lib.ERR_CAPACITY and code != _lib.OK:
+        _lib.check(code)
+    out = np.zeros(max(int(need[0]), 1), SEG_DTYPE)
+    _lib.check(lib().orion_select_branches(len(so) - 1, _lib.ptr(so), _lib.ptr(sg), _lib.ptr(ol), len(sl),
+                                           _lib.ptr(sl) if len(sl) else None, _lib.ptr(off),
+                                           _lib.ptr(out), len(out), _lib.ptr(need)))
+    return off, out[:int(need[0])]
+
+
 PLAN_MMA_SYNC = 1        # ORION_PLAN_MMA_SYNC: legacy mma.sync split kernel
 PLAN_ROWS_ON_LANES = 2   # ORION_PLAN_ROWS_ON_LANES: rows-on-lanes tcgen05 split kernel
 
@@ -219,18 +263,41 @@ class ExpansionBatch:
         self.refs = np.concatenate(refs) if refs else np.zeros(0, SEGREF_DTYPE)
         pts = np.array(points, np.int32).reshape(-1, 3)
         self.segs = bind_segments(qdesc, pts, self.seg_offsets, self.refs)
+        self._setup(self.seg_offsets, self.segs, pts[:, 0], pts[:, 2], page_table, own_len, device,
+                    chunk_tokens, flags, num_sms, prefill_rows)
+
+    @classmethod
+    def from_segments(cls, hq, hkv, d, page, seg_offsets, segs, own_pt_off, own_cap, page_table,
+                      own_len, device="cuda", chunk_tokens=0, sm_scale=0.0, flags=0, num_sms=0,
+                      prefill_rows=0):
+        """A batch over already-bound segment lists (e.g. orion_select_branches' running set):
+        own_pt_off / own_cap / own_len per branch of the lists."""
+        self = cls.__new__(cls)
+        self.hq, self.hkv, self.d, self.page = hq, hkv, d, page
+        self.sm_scale = sm_scale
+        self.n_branches = len(seg_offsets) - 1
+        self.seg_offsets = np.ascontiguousarray(seg_offsets, np.int32)
+        self.segs = segs
+        self._setup(self.seg_offsets, segs, own_pt_off, own_cap, page_table, own_len, device,
+                    chunk_tokens, flags, num_sms, prefill_rows)
+        return self
+
+    def _setup(self, seg_offsets, segs, own_pt_off, own_cap, page_table, own_len, device,
+               chunk_tokens, flags, num_sms, prefill_rows):
+        import torch
         own = np.ascontiguousarray(own_len, dtype=np.int32)
-        self.h_plan, ws = expand_plan(hq, hkv, d, page, self.seg_offsets, self.segs, own,
-                                      chunk_tokens=chunk_tokens, sm_scale=sm_scale, flags=flags,
+        self.h_plan, ws = expand_plan(self.hq, self.hkv, self.d, self.page, seg_offsets, segs, own,
+                                      chunk_tokens=chunk_tokens, sm_scale=self.sm_scale, flags=flags,
                                       num_sms=num_sms, prefill_rows=prefill_rows)
         self.prefill_rows = prefill_rows
         self.stats = plan_stats(self.h_plan)
         dev = torch.device(device)
         self.d_plan = torch.from_numpy(self.h_plan.copy()).to(dev)
         self.workspace = torch.empty((ws + 15) // 16 * 4, dtype=torch.float32, device=dev)
-        self.page_table = torch.from_numpy(np.ascontiguousarray(page_table, np.int32)).to(dev)
-        self.own_pt_off = torch.from_numpy(np.ascontiguousarray(pts[:, 0])).to(dev)
-        self.own_cap = torch.from_numpy(np.ascontiguousarray(pts[:, 2])).to(dev)
+        self.page_table = (page_table if isinstance(page_table, torch.Tensor)
+                           else torch.from_numpy(np.ascontiguousarray(page_table, np.int32)).to(dev))
+        self.own_pt_off = torch.from_numpy(np.ascontiguousarray(own_pt_off, np.int32)).to(dev)
+        self.own_cap = torch.from_numpy(np.ascontiguousarray(own_cap, np.int32)).to(dev)
         self.own_len = torch.from_numpy(own.copy()).to(dev)
 
     def append(self, k_new, v_new, k_cache, v_cache, mode=APPEND_ADVANCE, stream=None):

@@ -20,7 +20,8 @@ APPEND_ADVANCE, APPEND_REWRITE = 0, 1
 EXPORTED_SYMBOLS = ("orion_dag_waves", "orion_bind_segments", "orion_expand_plan",
                     "orion_plan_get_stats", "orion_kv_append", "orion_expand_attn",
                     "orion_expand_split", "orion_expand_combine", "orion_point_prefill_attn",
-                    "orion_last_error", "orion_version")
+                    "orion_expansion_round", "orion_select_branches", "orion_last_error",
+                    "orion_version")
 
 
 class Edge(ctypes.Structure):
@@ -99,8 +100,11 @@ def lib():
                                          sz, vp]
         L.orion_expand_combine.argtypes = [P(AttnShape), i32, vp, vp, vp, vp, vp, sz, vp]
         L.orion_point_prefill_attn.argtypes = L.orion_expand_attn.argtypes
+        L.orion_expansion_round.argtypes = [i32, vp, vp, vp, i32, vp, vp, vp, vp, i32, vp, vp, vp, vp]
+        L.orion_select_branches.argtypes = [i32, vp, vp, vp, i32, vp, vp, vp, i32, vp]
         for f in ("orion_expand_split", "orion_expand_combine", "orion_dag_waves", "orion_bind_segments", "orion_expand_plan",
-                  "orion_plan_get_stats", "orion_kv_append", "orion_expand_attn", "orion_point_prefill_attn"):
+                  "orion_plan_get_stats", "orion_kv_append", "orion_expand_attn", "orion_point_prefill_attn",
+                  "orion_expansion_round", "orion_select_branches"):
             getattr(L, f).restype = ctypes.c_int32
         L.orion_last_error.restype = ctypes.c_char_p
         L.orion_last_error.argtypes = []

@@ -559,3 +559,110 @@ extern "C" orion_status orion_plan_get_stats(const void* h_plan, orion_plan_stat
   out->workspace_bytes = h->workspace_bytes;
   return ORION_OK;
 }
+
+// ------------------------------------------------------------------------------ expansion driver
+extern "C" orion_status orion_expansion_round(int32_t n_queries, const orion_query_desc* queries,
+                                              const int32_t* edge_offsets, const orion_edge* edges,
+                                              int32_t n_branches, const int32_t* tokens,
+                                              int32_t* pre_round, int32_t* dec_round, int32_t* left,
+                                              int32_t round, int32_t* pre_out, int32_t* n_pre,
+                                              int32_t* dec_out, int32_t* n_dec) {
+  if (n_queries < 0 || n_branches < 0 || round < 0 || (n_queries > 0 && (!queries || !edge_offsets)) ||
+      !tokens || !pre_round || !dec_round || !left || !pre_out || !n_pre || !dec_out || !n_dec)
+    return fail(ORION_ERR_INVALID_ARG, "bad expansion_round arguments");
+  std::vector<uint8_t> is_pre(n_branches, 0), is_dec(n_branches, 0);
+  int32_t pending = 0;
+  for (int32_t qi = 0; qi < n_queries; ++qi) {
+    const orion_query_desc& q = queries[qi];
+    if (q.n_points < 1 || q.branch0 < 0 || q.branch0 + q.n_points > n_branches)
+      return fail(ORION_ERR_INVALID_ARG, "query %d: bad point range", qi);
+    // stage predecessors of Pre(j): Contextual k->j needs Pre(k), Dependent needs Dec(k)
+    std::vector<std::vector<int32_t>> need_pre(q.n_points + 1), need_dec(q.n_points + 1);
+    for (int32_t e = edge_offsets[qi]; e < edge_offsets[qi + 1]; ++e) {
+      const orion_edge& x = edges[e];
+      if (x.kind < ORION_EDGE_NULL || x.kind > ORION_EDGE_DEPENDENT)
+        return fail(ORION_ERR_INVALID_ARG, "query %d edge %d: bad kind %d", qi, e, x.kind);
+      if (x.from < 1 || x.from > q.n_points || x.to < 1 || x.to > q.n_points)
+        return fail(ORION_ERR_UNKNOWN_POINT, "query %d edge %d: point out of range", qi, e);
+      if (x.kind == ORION_EDGE_CONTEXTUAL) need_pre[x.to].push_back(x.from);
+      if (x.kind == ORION_EDGE_DEPENDENT) need_dec[x.to].push_back(x.from);
+    }
+    for (int32_t j = 1; j <= q.n_points; ++j) {
+      const int32_t b = q.branch0 + j - 1;
+      if (dec_round[b] >= 0) continue;
+      ++pending;
+      if (pre_round[b] >= 0) {
+        if (pre_round[b] < round) is_dec[b] = 1;
+        continue;
+      }
+      bool ready = true;
+      for (int32_t k : need_pre[j]) {
+        const int32_t kb = q.branch0 + k - 1;
+        ready = ready && pre_round[kb] >= 0 && pre_round[kb] < round;
+      }
+      for (int32_t k : need_dec[j]) {
+        const int32_t kb = q.branch0 + k - 1;
+        ready = ready && dec_round[kb] >= 0 && dec_round[kb] < round;
+      }
+      if (ready) is_pre[b] = 1;
+    }
+  }
+  int32_t np = 0, nd = 0;
+  for (int32_t b = 0; b < n_branches; ++b) {
+    if (is_pre[b]) {
+      pre_out[np++] = b;
+      pre_round[b] = round;
+      left[b] = std::max(0, tokens[b]);
+      if (left[b] == 0) dec_round[b] = round;
+    } else if (is_dec[b]) {
+      dec_out[nd++] = b;
+      if (--left[b] <= 0) dec_round[b] = round;
+    }
+  }
+  *n_pre = np;
+  *n_dec = nd;
+  if (pending > 0 && np == 0 && nd == 0)
+    return fail(ORION_ERR_CYCLE, "expansion stalled with %d stages pending (cyclic DAG?)", pending);
+  return ORION_OK;
+}
+
+extern "C" orion_status orion_select_branches(int32_t n_branches, const int32_t* seg_offsets,
+                                              const orion_seg* segs, const int32_t* own_len,
+                                              int32_t n_sel, const int32_t* sel,
+                                              int32_t* sel_offsets, orion_seg* sel_segs,
+                                              int32_t segs_cap, int32_t* segs_needed) {
+  if (n_branches < 0 || n_sel < 0 || !seg_offsets || !segs || !own_len || (n_sel > 0 && !sel) ||
+      !sel_offsets || !segs_needed)
+    return fail(ORION_ERR_INVALID_ARG, "bad select_branches arguments");
+  std::vector<int32_t> pos(n_branches, -1);
+  for (int32_t i = 0; i < n_sel; ++i) {
+    if (sel[i] < 0 || sel[i] >= n_branches || pos[sel[i]] >= 0)
+      return fail(ORION_ERR_INVALID_ARG, "sel[%d] = %d out of range or repeated", i, sel[i]);
+    pos[sel[i]] = i;
+  }
+  int32_t need = 0;
+  sel_offsets[0] = 0;
+  for (int32_t i = 0; i < n_sel; ++i) {
+    need += seg_offsets[sel[i] + 1] - seg_offsets[sel[i]];
+    sel_offsets[i + 1] = need;
+  }
+  *segs_needed = need;
+  if (!sel_segs || segs_cap < need)
+    return fail(ORION_ERR_CAPACITY, "segs_cap=%d < needed %d", segs_cap, need);
+  int32_t o = 0;
+  for (int32_t i = 0; i < n_sel; ++i)
+    for (int32_t s = seg_offsets[sel[i]]; s < seg_offsets[sel[i] + 1]; ++s) {
+      orion_seg x = segs[s];
+      if (x.dyn >= n_branches) return fail(ORION_ERR_INVALID_ARG, "segment %d: dyn out of range", s);
+      if (x.dyn >= 0) {
+        if (pos[x.dyn] >= 0) {
+          x.dyn = pos[x.dyn];                        // still growing inside the selection
+        } else {                                     // finished (or paused): freeze at own_len
+          x.len = std::min(x.len, std::max(0, own_len[x.dyn] - x.start));
+          x.dyn = -1;
+        }
+      }
+      sel_segs[o++] = x;
+    }
+  return ORION_OK;
+}
