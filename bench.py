@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-expansion", action="store_true",
+                    help="skip the whole-expansion run (Alg. 1 l.9-22 driver, SURVEY.md §8(f) rank 2)")
     ap.add_argument("--no-point-prefill", action="store_true",
                     help="skip the point-prefill attention measurement (SURVEY.md §8(f) rank 1)")
     ap.add_argument("--no-prefill", action="store_true",
@@ -339,6 +341,8 @@ def run_orion(args, cfg, layers):
         "clocks": clocks,
         "e2e": e2e,
     }
+    if world == 1 and not args.no_expansion:
+        line["expansion_run"] = run_expansion(args, cfg, lay, layers, q, kn, vn, kc, vc, dev)
     if world == 1 and not args.no_point_prefill:
         line["point_prefill"] = run_point_prefill(args, cfg, lay, layers, kc, vc, dev)
     if world == 1 and not args.no_prefill:
@@ -349,6 +353,68 @@ def run_orion(args, cfg, layers):
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_expansion(args, cfg, lay, layers, q, kn, vn, kc, vc, dev):
+    """§8(f) rank 2: a whole expansion of the config's queries (Alg. 1 l.9-22 with
+    continuous batching, reading D1): rounds of orion_expansion_round; each round prefills the
+    points that became ready (orion_point_prefill_attn, every layer) and decodes one token of the
+    running set through all layers (append + split + combine); plans are rebuilt only when the
+    running set changes.  Every point generates T - Lc tokens.  Device-timed end to end (host
+    scheduling, plan rebuilds and the per-set input gathers inside the timed region)."""
+    import torch
+    from paper_2510_24390_b200.expansion import Expansion
+    queries = [dict(n_points=int(lay.n_points[i]), edges=lay.edges[i],
+                    prefix_pt_off=int(lay.prefix_pt_off[i]), prefix_len=int(lay.prefix_len[i]))
+               for i in range(lay.n_queries)]
+    points = np.stack([lay.point_pt_off, lay.content_len, lay.point_cap], 1)
+    B, lc = lay.n_branches, cfg.lc
+    tokens = (np.asarray(lay.own_len) - lc).astype(np.int32)          # T - Lc per point
+    ex = Expansion(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, lay.page_table, lc, tokens,
+                   policy=args.policy, device=dev, chunk_tokens=args.chunk)
+    g = torch.Generator(device=dev)
+    g.manual_seed(cfg.seed * 17)
+    q_pre = torch.randn((B, lc, cfg.hq, cfg.d), generator=g, device=dev).to(torch.bfloat16)
+    out_pre = torch.empty_like(q_pre)
+    stream = torch.cuda.current_stream(dev)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record(stream)
+    rounds, dec_sum, pre_rounds, cur, subs = 0, 0, 0, None, None
+    while True:
+        pre, dec = ex.next_round()
+        if len(pre) == 0 and len(dec) == 0:
+            break
+        if len(pre):
+            idx = torch.from_numpy(pre.astype(np.int64)).to(dev)
+            qp = q_pre.index_select(0, idx)
+            op = out_pre[:len(pre)]
+            ex.prefill(pre, [qp] * layers, kc[:layers], vc[:layers], [op] * layers)
+            pre_rounds += 1
+        if len(dec):
+            if cur is None or len(cur) != len(dec) or not np.array_equal(cur, dec):
+                idx = torch.from_numpy(dec.astype(np.int64)).to(dev)
+                subs = [t.index_select(1, idx) for t in (q, kn, vn)]
+                subs.append(torch.empty_like(subs[0]))
+                cur = dec.copy()
+            ex.decode(dec, subs[0], subs[1], subs[2], kc[:layers], vc[:layers], subs[3])
+            dec_sum += len(dec)
+        rounds += 1
+    e1.record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    ms = e0.elapsed_time(e1)
+    gen = int(tokens.sum())
+    return {"workload": f"{cfg.name}: whole expansion of {lay.n_queries} queries x {cfg.dag}, "
+                        f"every point prefills Lc {lc} tokens then decodes T - Lc = {int(tokens.max())} "
+                        f"tokens through {layers} layers",
+            "metric": "expansion tokens/sec (whole expansion)", "value": gen / (ms / 1e3), "unit": "tokens/s",
+            "generated_tokens": gen, "rounds": rounds, "rounds_with_prefill": pre_rounds,
+            "mean_running_set": dec_sum / max(1, rounds), "max_branches": B,
+            "plan_rebuilds": ex.rebuilds, "ms": ms, "wall_ms": wall * 1e3,
+            "note": "device-timed (events) around the whole loop; host scheduling and plan "
+                    "rebuilds inside; compare the snapshot value where every point decodes at once"}
 
 
 def run_point_prefill(args, cfg, lay, layers, kc, vc, dev):
