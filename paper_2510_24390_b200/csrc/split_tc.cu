@@ -213,8 +213,7 @@ struct Smem {
   static constexpr int OFF_K = 2 * QB;
   static constexpr int OFF_V = OFF_K + SK * KVB;
   static constexpr int OFF_XCH = OFF_V + SV * KVB;   // WG1 -> WG0 (m, l) per row, x2
-  static constexpr int OFF_ONES = OFF_XCH + 2 * kRows * 8;  // [16][64] bf16 ones: l = P . 1 on the MMA
-  static constexpr int OFF_BAR = OFF_ONES + 16 * kTok * 2;
+  static constexpr int OFF_BAR = OFF_XCH + 2 * kRows * 8;
   static constexpr int N_BAR = 2 * SK + 2 * SV + 2 + 2 + 2 + 2 + 1 + 2;
   static constexpr int BYTES = OFF_BAR + N_BAR * 8 + 16;
 };
@@ -223,7 +222,6 @@ struct Smem {
 __device__ __forceinline__ uint32_t colS(uint32_t p) { return p * 64; }
 __device__ __forceinline__ uint32_t colP(uint32_t p) { return 128 + p * 32; }
 __device__ __forceinline__ uint32_t colO(uint32_t p) { return 256 + p * 128; }
-__device__ __forceinline__ uint32_t colL(uint32_t p) { return 192 + p * 16; }   // row sums l
 constexpr int kThreadsTC = 384;   // warps 0-3: TMEM alloc / idle / TMA / MMA; 4-7: WG0; 8-11: WG1
 // The TMA and MMA warps sit on SM sub-partitions 2 and 3 so that their barrier polling does not
 // steal issue slots from the softmax warps of items with <= 64 rows (TMEM lanes 0-63 are only
@@ -273,8 +271,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   }
   for (int i = tid; i < SV * L::KVB / 16; i += blockDim.x)          // V ring starts finite
     reinterpret_cast<uint4*>(smem + L::OFF_V)[i] = make_uint4(0, 0, 0, 0);
-  for (int i = tid; i < 16 * kTok * 2 / 16; i += blockDim.x)       // bf16 1.0 = 0x3F80
-    reinterpret_cast<uint4*>(smem + L::OFF_ONES)[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
   fence_proxy_async();
   if (warp == kWarpAlloc) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
@@ -373,11 +369,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     // The whole warp runs the control flow (warp-uniform descriptors); one elected lane issues.
     constexpr uint32_t ID_QK = idesc_bf16(kRows, kTok, false);
     constexpr uint32_t ID_PV = idesc_bf16(kRows, D, true);
-    constexpr uint32_t ID_L = idesc_bf16(kRows, 16, false);
     const uint64_t dq0 = sw128_desc(smem_u32(smem + L::OFF_Q), 16, 1024);
     const uint64_t dk0 = sw128_desc(smem_u32(smem + L::OFF_K), 16, 1024);
     const uint64_t dv0 = sw128_desc(smem_u32(smem + L::OFF_V), L::HALF_KV, 1024);
-    const uint64_t d1 = sw128_desc(smem_u32(smem + L::OFF_ONES), 16, 1024);
     struct Cur {
       int it, t, nt;
       uint32_t k, j;
@@ -435,9 +429,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         for (int kt = 0; kt < kTok / 16; ++kt) {
           mma_ts(dO, aP + kt * 8, dv + static_cast<uint64_t>((kt * 16 * 128) >> 4), ID_PV,
                  (!first || kt > 0) ? 1u : 0u);
-          // l += P . 1: the row sums of exactly the bf16 P that enters P.V (reading S17)
-          mma_ts(tmem + colL(j & 1), aP + kt * 8, d1 + static_cast<uint64_t>((kt * 32) >> 4), ID_L,
-                 (!first || kt > 0) ? 1u : 0u);
+
         }
         tc_commit(pv_done + (j & 1));
         tc_commit(v_empty + s);
@@ -509,6 +501,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       // point prefill: this row's content position i; in the causal own range it sees [t0, t0 + i]
       const int rpos = ((w.row_begin + r) % (a.lc * a.group)) / a.group;
       float m_used = -INFINITY;
+      float l_run = 0.f;                            // this row's sum of the bf16 P it published
       bool had = false;
       uint32_t jl = 0;                              // last tile of this WG in the item
       for (int rg_i = 0; rg_i < item_nranges(w); ++rg_i) {
@@ -567,18 +560,19 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 for (int c = 0; c < 16; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
                 tmem_st32x16(tmem + lane_base + colO(p) + cb, o);
               }
-              const uint32_t lv = tmem_ld32x1(tmem + lane_base + colL(p));
-              tc_wait_ld();
-              tmem_st32x1(tmem + lane_base + colL(p), __float_as_uint(__uint_as_float(lv) * alpha));
               tc_wait_st();
             }
             if (mine) m_used = mx;
+            l_run *= alpha;
           }
           const float mb = m_used == -INFINITY ? 0.f : m_used;
 #pragma unroll
-          for (int c = 0; c < 32; ++c)
+          for (int c = 0; c < 32; ++c) {
             pk[c] = pack_bf16(ex2(fmaf(__uint_as_float(sr[2 * c]), a.scale_log2, -mb)),
                               ex2(fmaf(__uint_as_float(sr[2 * c + 1]), a.scale_log2, -mb)));
+            // l: the row sum of exactly the bf16 P that enters P.V (reading S17)
+            l_run += __uint_as_float(pk[c] << 16) + __uint_as_float(pk[c] & 0xFFFF0000u);
+          }
         } else {
 #pragma unroll
           for (int c = 0; c < 32; ++c) pk[c] = 0u;
@@ -630,7 +624,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         tc_fence_after();
       }
       if (p == 1) {
-        xch[(k & 1) * kRows + r] = make_float2(had ? m_used : -INFINITY, 0.f);
+        xch[(k & 1) * kRows + r] = make_float2(had ? m_used : -INFINITY, l_run);
         TW(9, asm volatile("bar.sync 1, 256;\n" ::: "memory"));
       } else {
         TW(9, asm volatile("bar.sync 1, 256;\n" ::: "memory"));
@@ -640,12 +634,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         const float Mb = M == -INFINITY ? 0.f : M;
         const float a0 = had ? ex2(m_used - Mb) : 0.f;
         const float a1 = had1 ? ex2(o1.x - Mb) : 0.f;
-        float l0 = 0.f, l1 = 0.f;
-        if (active) {
-          if (had) l0 = __uint_as_float(tmem_ld32x1(tmem + lane_base + colL(0)));
-          if (had1) l1 = __uint_as_float(tmem_ld32x1(tmem + lane_base + colL(1)));
-          tc_wait_ld();
-        }
+        const float l0 = had ? l_run : 0.f, l1 = had1 ? o1.y : 0.f;
         float* dst = a.part_acc + static_cast<size_t>(w.slot0 + r) * D;
         if (active) {
 #pragma unroll 1
