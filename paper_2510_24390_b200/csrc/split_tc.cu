@@ -226,7 +226,7 @@ constexpr int kThreadsTC = 384;   // warps 0-3: TMEM alloc / idle / TMA / MMA; 4
 // The TMA and MMA warps sit on SM sub-partitions 2 and 3 so that their barrier polling does not
 // steal issue slots from the softmax warps of items with <= 64 rows (TMEM lanes 0-63 are only
 // reachable from warps 4k and 4k+1, i.e. sub-partitions 0 and 1).
-constexpr int kWarpAlloc = 0, kWarpTMA = 2, kWarpMMA = 3;
+constexpr int kWarpAlloc = 0, kWarpQK = 1, kWarpTMA = 2, kWarpMMA = 3;
 
 template <int D>
 __global__ void __launch_bounds__(kThreadsTC, 1)
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       }
     }
     TRACE_DUMP("producer");
-  } else if (warp == kWarpMMA) {
+  } else if (warp == kWarpMMA || warp == kWarpQK) {
     // ------------------------------------------------------------------ MMA issuer
     // Two cursors walk the flattened (item, tile) sequence: QK runs two tiles ahead of PV, so
     // S(j+2) = Q K(j+2)^T is issued as soon as softmax warpgroup j&1 has read S(j) into registers
@@ -436,15 +436,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       }
       __syncwarp();
     };
-    // QK stays <= 2 tiles ahead of PV and never enters item k+2 before every PV of item k is
-    // issued: item k+2's Q reuses item k's buffer, which is refilled only after item k's epilogue.
-    Cur cq, cv;
-    start(cq);
-    start(cv);
-    while (cv.it < n_items) {
-      while (cq.it < n_items && cq.j <= cv.j + 2 && cq.k <= cv.k + 1) { issue_qk(cq); advance(cq); }
-      issue_pv(cv);
-      advance(cv);
+    // Two issuers (tcgen05.commit tracks the issuing thread's own MMAs): warp 1 issues every
+    // S(j) = Q K(j)^T as soon as K(j) landed and softmax warpgroup j&1 has read S(j-2) out
+    // (s_free), warp 3 every O += P(j) V(j) as soon as P(j) is published.  Neither waits behind
+    // the other's dependencies, so one warpgroup's next S never queues behind the other
+    // warpgroup's P.  Q buffer reuse needs no extra guard: warpgroup 0 publishes item k+2's Q
+    // only after item k's epilogue, i.e. after every MMA of item k.
+    Cur c;
+    start(c);
+    if (warp == kWarpQK) {
+      while (c.it < n_items) { issue_qk(c); advance(c); }
+    } else {
+      while (c.it < n_items) { issue_pv(c); advance(c); }
     }
     TRACE_DUMP("mma");
   } else if (warp >= 4) {
