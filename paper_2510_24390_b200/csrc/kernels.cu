@@ -451,9 +451,12 @@ size_t split_smem_bytes() {
 template <int D>
 orion_status launch_split(const PlanHeader* h, const char* dplan, const void* q, const void* k,
                           const void* v, int32_t num_pages, const int32_t* page_table,
-                          const int32_t* own_len, void* ws, cudaStream_t st) {
+                          const int32_t* own_len, void* ws, cudaStream_t st, void* out = nullptr,
+                          float* lse = nullptr) {
   if (h->variant == kVariantTC || h->variant == kVariantTCT) {
     TcArgs t;
+    t.out = static_cast<__nv_bfloat16*>(out);      // direct output (point-prefill plans only)
+    t.lse = lse;
     t.items = reinterpret_cast<const WorkItem*>(dplan + h->items_off);
     t.ranges = reinterpret_cast<const Range*>(dplan + h->ranges_off);
     t.readers = reinterpret_cast<const int32_t*>(dplan + h->readers_off);
@@ -652,12 +655,22 @@ extern "C" orion_status orion_point_prefill_attn(const orion_attn_shape* shape, 
   if (!h_plan || static_cast<const PlanHeader*>(h_plan)->magic != kPlanMagic ||
       static_cast<const PlanHeader*>(h_plan)->prefill_rows <= 0)
     return fail(ORION_ERR_INVALID_ARG, "orion_point_prefill_attn needs a point-prefill plan");
-  orion_status st = orion_expand_split(shape, n_branches, q, k_cache, v_cache, num_pages,
-                                       page_table, own_len, h_plan, d_plan, workspace,
-                                       workspace_bytes, stream);
+  // A prefill plan's items are reader-stationary (one partial per row): the split kernel writes
+  // out / lse itself and no combine pass runs.
+  const PlanHeader* h = nullptr;
+  orion_status st = check_attn(shape, n_branches, h_plan, d_plan, workspace, workspace_bytes, &h);
   if (st != ORION_OK) return st;
-  return orion_expand_combine(shape, n_branches, out, lse, h_plan, d_plan, workspace,
-                              workspace_bytes, stream);
+  if (!q || !k_cache || !v_cache || !page_table || !own_len)
+    return fail(ORION_ERR_INVALID_ARG, "null pointer");
+  if (!aligned16(q) || !aligned16(k_cache) || !aligned16(v_cache) || !aligned16(out))
+    return fail(ORION_ERR_INVALID_ARG, "device pointers must be 16-byte aligned");
+  if (num_pages < 1) return fail(ORION_ERR_INVALID_ARG, "num_pages < 1");
+  if (h->variant != kVariantTC) return fail(ORION_ERR_INVALID_ARG, "prefill plan with a decode kernel variant");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const char* dp = static_cast<const char*>(d_plan);
+  if (shape->head_dim == 128)
+    return launch_split<128>(h, dp, q, k_cache, v_cache, num_pages, page_table, own_len, workspace, s, out, lse);
+  return launch_split<64>(h, dp, q, k_cache, v_cache, num_pages, page_table, own_len, workspace, s, out, lse);
 }
 
 extern "C" const char* orion_version(void) {

@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const WorkItem w = a.items[it];
       if (item_tiles(a, w) == 0) {                 // empty (dyn end <= t0): neutral partial
-        if (p == 0 && r < w.n_rows) {
+        if (p == 0 && r < w.n_rows && !a.out) {     // (direct output: prefill rows are never empty)
           float* dst = a.part_acc + static_cast<size_t>(w.slot0 + r) * D;
 #pragma unroll
           for (int c = 0; c < D; c += 4) *reinterpret_cast<float4*>(dst + c) = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -638,6 +638,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         const float a0 = had ? ex2(m_used - Mb) : 0.f;
         const float a1 = had1 ? ex2(o1.x - Mb) : 0.f;
         const float l0 = had ? l_run : 0.f, l1 = had1 ? o1.y : 0.f;
+        // Direct output (point-prefill plans: the item holds every token of its rows, so this is
+        // the row's only partial): out = acc / l in bf16 and lse, no combine pass.
+        const float Lr = a0 * l0 + a1 * l1;
+        const float inv = Lr > 0.f ? 1.f / Lr : 0.f;
+        size_t orow = 0;
+        if (a.out && r < w.n_rows) {
+          const int rr = w.row_begin + r, rpr = a.lc * a.group;
+          const int b = __ldg(a.readers + w.readers_off + rr / rpr);
+          orow = (static_cast<size_t>(b) * a.lc + (rr % rpr) / a.group) * a.hq + w.kv_head * a.group + rr % a.group;
+        }
         float* dst = a.part_acc + static_cast<size_t>(w.slot0 + r) * D;
         if (active) {
 #pragma unroll 1
@@ -654,12 +664,22 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 v.y = (had ? a0 * __uint_as_float(o[c + 1]) : 0.f) + (had1 ? a1 * __uint_as_float(q1[c + 1]) : 0.f);
                 v.z = (had ? a0 * __uint_as_float(o[c + 2]) : 0.f) + (had1 ? a1 * __uint_as_float(q1[c + 2]) : 0.f);
                 v.w = (had ? a0 * __uint_as_float(o[c + 3]) : 0.f) + (had1 ? a1 * __uint_as_float(q1[c + 3]) : 0.f);
-                *reinterpret_cast<float4*>(dst + cb + c) = v;
+                if (a.out) {
+                  uint2 pk2;
+                  pk2.x = pack_bf16(v.x * inv, v.y * inv);
+                  pk2.y = pack_bf16(v.z * inv, v.w * inv);
+                  *reinterpret_cast<uint2*>(a.out + orow * D + cb + c) = pk2;
+                } else {
+                  *reinterpret_cast<float4*>(dst + cb + c) = v;
+                }
               }
             }
           }
         }
-        if (r < w.n_rows) a.part_ml[w.slot0 + r] = make_float2(M, a0 * l0 + a1 * l1);
+        if (r < w.n_rows) {
+          if (!a.out) a.part_ml[w.slot0 + r] = make_float2(M, Lr);
+          else if (a.lse) a.lse[orow] = Lr > 0.f ? (M + log2f(Lr)) * 0.69314718055994531f : -INFINITY;
+        }
         tc_fence_before();
         mbar_arrive(o_free);
         if (pf < n_items) pf = next_nonempty(a, pf + gridDim.x);

@@ -51,6 +51,8 @@ struct TcArgs {
   float* part_lse;
   int32_t n_items, hq, hkv, group, page_shift;
   int32_t lc;             // query rows per reader and q head: 1 (decode) or Lc (point prefill)
+  __nv_bfloat16* out;     // non-null: every row has exactly one partial (a point-prefill plan) and
+  float* lse;             // the epilogue writes out = acc / l (bf16) and lse directly: no combine
   float scale_log2;
 };
 

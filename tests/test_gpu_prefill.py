@@ -119,3 +119,22 @@ def test_prefill_last_row_matches_decode_kernel():
     ref, _ = OS.expand_step(lay, u16(q), u16(ten["k_cache"][0]), u16(ten["v_cache"][0]))
     assert float(np.abs(out.float().cpu().numpy() - ref).max()) <= MAX_ABS
     assert float(np.abs(pre[:, cfg.lc - 1].float().cpu().numpy() - ref).max()) <= MAX_ABS
+
+
+def test_split_plus_combine_equals_direct_prefill():
+    # orion_expand_split + orion_expand_combine on a prefill plan (fp32 partials, one per row)
+    # reproduce orion_point_prefill_attn's direct-output epilogue bit for bit.
+    cfg = C.CONFIGS["c1"].with_(lp=300, t=120, lc=32, page=32, d=128, hq=8, hkv=2)
+    lay = T.make_layout(cfg, ragged=True, dag_override=W.mixed8)
+    ten = T.make_qkv(cfg, lay)
+    qp = q_pre(cfg, lay, scale=2.0)
+    out, lse, batch = run_prefill(cfg, lay, ten, qp)
+    dev = torch.device("cuda")
+    kc = ten["k_cache"][0].to(dev).contiguous()
+    vc = ten["v_cache"][0].to(dev).contiguous()
+    out2 = torch.empty_like(out)
+    lse2 = torch.empty_like(lse)
+    batch.split(qp.to(dev).contiguous(), kc, vc)
+    batch.combine(out2, lse2)
+    torch.cuda.synchronize()
+    assert torch.equal(out, out2) and torch.equal(lse, lse2)
