@@ -1,25 +1,30 @@
 // split_tc.cu — K2 split attention on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
 //
-// One persistent CTA per SM walks the plan's work items (item = shared piece x kv head x token
-// chunk x <=128 query rows; rows = reader branches x GQA heads).  Roles:
-//   warp 0 (1 lane)  TMA producer: streams the chunk's K and V tokens page by page with
-//                    cp.async.bulk.tensor (16-token x 64-dim boxes, 128B swizzle) into a 4-stage
-//                    shared-memory ring; tokens of a shared prefix / ancestor piece are read from
-//                    HBM once for all rows of the item.  Runs ahead across item boundaries.
-//   warp 1 (1 lane)  MMA issuer: S = Q.K^T (tcgen05.mma kind::f16, A=Q smem, B=K smem, D in TMEM,
-//                    M=128 rows x N=64 tokens) into a double-buffered S; O += P.V (A=P from TMEM,
-//                    B=V smem MN-major, M=128 x N=d) into the TMEM accumulator; tcgen05.commit
-//                    releases ring stages and signals the softmax warps.
-//   warp 2           TMEM allocator (512 columns).
-//   warps 4-7        softmax + epilogue, one thread per query row (TMEM lane = row): tcgen05.ld
-//                    of the S row, masking, online max in the log2 domain with lazy rescaling
-//                    (O and l are rescaled only when the running max grows by > 2^8), P = exp2
-//                    rounded to bf16 and stored to TMEM (l summed from the same rounded values),
-//                    zeroing of V rows outside the item's token range, and at item end the fp32
-//                    partial (m, l, acc) write.  They also gather the next items' Q rows.
-//
-// Layout and numerics match the mma.sync kernel and the combine kernel (kernels.cu): partial m is
-// in log2 units relative to which acc and l are accumulated.
+// Rows-on-lanes orientation (query rows on the MMA M dimension, one TMEM lane / softmax thread
+// per row): used for head_dim 64 decode, ORION_PLAN_ROWS_ON_LANES, and point prefill, whose Lc*G
+// rows per branch fill the 128-row M tile.  One persistent CTA
+// per SM walks the plan's work items (a shared piece x kv head x chunk x <= 128 rows, or for a
+// prefill plan one branch's whole range list).  Roles:
+//   warp 0           TMEM allocator (512 columns).
+//   warp 1           QK issuer: S(j) = Q.K(j)^T (tcgen05.mma kind::f16, A = Q smem, B = K smem,
+//                    M = 128 rows x N = 64 tokens) into S[j & 1] as soon as K(j) landed and the
+//                    softmax warpgroup has read S(j-2) out.
+//   warp 2 (1 lane)  TMA producer: K and V rings of 64-token stages (one box per page run of a
+//                    full tile, 16-row boxes on a ragged edge, 128B swizzle), page-table lookups
+//                    resolved 32 tiles at a time.
+//   warp 3           PV issuer: O[j & 1] += P(j).V(j) (A = P from TMEM, B = V smem MN-major,
+//                    M = 128 x N = d) as soon as P(j) is published.  Two issuers, so one
+//                    warpgroup's next S never waits behind the other's P (tcgen05.commit tracks
+//                    the issuing thread's own MMAs).
+//   warps 4-7 / 8-11 softmax warpgroups owning the even / odd tiles of an item: tcgen05.ld of the
+//                    S row, masking (ragged edges; per-row causal limits in a prefill's own
+//                    range), lazy-rescaled online max in the log2 domain (O and l rescaled only
+//                    when the running max grows by > 2^8), P = exp2 rounded to bf16 into TMEM,
+//                    l summed per thread from the same rounded P, V rows outside the range
+//                    zeroed once the tile has landed.  At item end warpgroup 1 hands (m, l) to
+//                    warpgroup 0, which merges the two accumulators into the fp32 partial
+//                    (m, l, acc) -- or, for a prefill plan, straight into bf16 out and lse.
+//                    Warpgroup 0 also gathers the next items' Q rows.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>

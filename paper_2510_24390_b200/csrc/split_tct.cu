@@ -7,18 +7,24 @@
 //
 //   S^T[128 tok x N]  = K_tile[128 x d] . Q^T            (A = K smem K-major, B = Q smem K-major)
 //   O^T[d x N]       += V_tile^T[d x 128] . P^T[128 x N] (A = V smem MN-major, B = P^T smem MN-major)
-//   L^T[128 x N]     += 1[128 x 128] . P^T               (A = ones in TMEM): every lane gets the
-//                                                         row sums l of exactly the bf16 P used
-// with N = 16/32/64 (query rows, padded).  One softmax thread per token: its N scores, a
-// block-wide "did any running max grow by > 2^8" vote (bar.red.or), and only on that rare path a
-// column max (redux.sync.max.f32 + smem).  The exponentials of a 128-token tile are spread over
-// all four sub-partitions whatever the row count.
+// with N = 16/32/64 (query rows, padded).  One softmax thread per token row of S^T; the two
+// softmax warpgroups split every tile's columns (query rows) in half, so each thread handles N/2
+// scores: a warpgroup-wide "is any running max unset or grown by > 2^8" vote (bar.red.or), and
+// only on that rare path a column max (redux.sync.max.f32 + smem) that moves the reference and
+// rescales this warpgroup's O^T columns.  Row sums l are accumulated per thread from the bf16 P
+// and reduced over the 128 token rows at item end.  The exponentials of a tile are spread over all
+// four sub-partitions whatever the row count.
 //
-// Roles (384 threads, one persistent CTA per SM): warp 0 TMEM alloc; warp 2 TMA producer (K ring
-// 2 x 32 KB released at QK completion, V ring 3 x 32 KB released at PV completion); warp 3 MMA
-// issuer (QK two tiles ahead of PV); warps 4-7 / 8-11 softmax warpgroups 0/1 owning even / odd
-// tiles with their own O^T / L^T accumulators, merged by warpgroup 0 at item end into one fp32
-// partial (m in log2 units, l, acc) per query row, the format combine_kernel consumes.
+// Roles (384 threads, one persistent CTA per SM, items strided over CTAs):
+//   warp 0  TMEM allocation, then the V TMA producer (ring 3 x 32 KB, released at PV completion)
+//   warp 1  per-CTA scheduler: item geometry into an 8-entry smem ring, Q rows gathered with
+//           cp.async into a double buffer
+//   warp 2  K TMA producer (ring 2 x 32 KB, released at QK completion)
+//   warp 3  MMA issuer (QK up to three tiles ahead of PV; zeroes a partial tile's V edge rows once
+//           the tile has landed, so 0 x NaN from never-written slots cannot reach O)
+//   warps 4-7 / 8-11  softmax warpgroups 0 / 1 (query columns [0, N/2) / [N/2, N)); O^T is
+//           double-buffered by item parity, so an item's epilogue (fp16 o = acc / l and fp32
+//           log2-sum-exp per row, plan_format.h) overlaps the next item's first PVs.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
