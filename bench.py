@@ -279,14 +279,19 @@ def run_orion(args, cfg, layers):
         dist.barrier()
     torch.cuda.synchronize()
     e0.record(stream)
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    step_ev[0].record(stream)
     for k in range(args.steps):
         step(ev, k)
+        step_ev[k + 1].record(stream)
     e1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clocks = sampler.stop() if sampler else None
     elapsed_ms = e0.elapsed_time(e1)
+    step_ms = sorted(step_ev[k].elapsed_time(step_ev[k + 1]) for k in range(args.steps))
+    pct = lambda f: step_ms[min(len(step_ms) - 1, int(round(f * (len(step_ms) - 1))))]
     split_ms = [ev[k][l][0].elapsed_time(ev[k][l][1]) for k in range(args.steps) for l in range(layers)]
     # whole-job aggregation: branches of all ranks / max step time over ranks
     elapsed_ms, total_b = shard.reduce_timing(elapsed_ms, float(B), device=dev)
@@ -337,6 +342,7 @@ def run_orion(args, cfg, layers):
                  "logical_tokens_per_kvhead": st["logical_tokens"],
                  "partial_bytes_per_layer": st["workspace_bytes"] * 2,   # written by K2 + read by K3
                  "plan_build_s": plan_s},
+        "step_ms": {"p10": pct(0.1), "median": pct(0.5), "p90": pct(0.9), "rank0_only": world > 1},
         "gpu_launches": args.steps * layers * 3,
         "clocks": clocks,
         "e2e": e2e,
