@@ -65,6 +65,8 @@ def parse():
                     help="skip the co-scheduled prefill measurement (SURVEY.md §8(a) a8)")
     ap.add_argument("--prefill-caps", default="148,132,116",
                     help="split-kernel SM caps tried with the prefill co-stream")
+    ap.add_argument("--green-splits", default="116,100,84",
+                    help="expansion SM counts of the green-context partitions (prefill gets the rest)")
     return ap.parse_args()
 
 
@@ -575,12 +577,93 @@ def run_costream(args, cfg, lay, layers, q, kn, vn, out, kc, vc, dev, expansion_
                          "expansion_tok_s": exp_tok_s, "expansion_retained": exp_tok_s / expansion_alone,
                          "prefill_tflops": pf_tflops, "prefill_retained": pf_tflops / prefill_alone,
                          "prefill_layers_in_window": done})
+    # §8(f) rank 3: the same two workloads on disjoint SM partitions (green contexts).
+    partitioned = []
+    try:
+        from paper_2510_24390_b200.partition import SmPartition
+        for n_exp in [int(c) for c in args.green_splits.split(",") if c]:
+            part = SmPartition(n_exp)
+            es, ps = part.first, part.second
+            batch = orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points,
+                                         lay.page_table, lay.own_len, policy=args.policy, device=dev,
+                                         chunk_tokens=args.chunk, num_sms=part.sms[0])
+
+            def gstep():
+                for l in range(layers):
+                    batch.step(q[l], kn[l], vn[l], kc[l], vc[l], out[l], mode=REW, stream=es)
+
+            torch.cuda.synchronize()
+            part.sync_before()
+            with torch.cuda.stream(es):
+                gstep()
+            with torch.cuda.stream(ps):
+                prefill_layer()
+            part.synchronize()
+            # each alone, in its own partition
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(es)
+            for _ in range(steps):
+                gstep()
+            a1.record(es)
+            part.synchronize()
+            exp_alone_ms = a0.elapsed_time(a1) / steps
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(ps):
+                b0.record(ps)
+                for _ in range(10):
+                    prefill_layer()
+                b1.record(ps)
+            part.synchronize()
+            pf_alone_ms = b0.elapsed_time(b1) / 10
+            # together: the prefill partition stays busy for the whole expansion window
+            n_pf = int(steps * exp_alone_ms / pf_alone_ms * 1.5) + 4
+            s_lo = torch.cuda.Event(enable_timing=True)
+            s_hi = torch.cuda.Event(enable_timing=True)
+            t_hi = torch.cuda.Event(enable_timing=True)
+            pf_ev = [torch.cuda.Event(enable_timing=True) for _ in range(n_pf)]
+            with torch.cuda.stream(ps):
+                s_lo.record(ps)
+                for i in range(n_pf):
+                    prefill_layer()
+                    pf_ev[i].record(ps)
+            s_hi.record(es)
+            for _ in range(steps):
+                gstep()
+            t_hi.record(es)
+            part.synchronize()
+            win = s_hi.elapsed_time(t_hi)
+            lag = s_lo.elapsed_time(s_hi)
+            done = sum(1 for ev in pf_ev if lag <= s_lo.elapsed_time(ev) <= lag + win)
+            exp_tok_s = lay.n_branches * steps / (win / 1e3)
+            pf_tflops = done * layer_flop / (win / 1e3) / 1e12
+            pf_alone_part = layer_flop / (pf_alone_ms / 1e3) / 1e12
+            if pf_alone_part > 1.05 * prefill_alone or done == 0:
+                partitioned.append({"expansion_sms": part.sms[0], "prefill_sms": part.sms[1],
+                                    "invalid": "prefill GEMMs did not run in this partition "
+                                               f"(alone {pf_alone_part:.0f} TFLOP/s, {done} layers in window)"})
+                part.close()
+                continue
+            partitioned.append({
+                "expansion_sms": part.sms[0], "prefill_sms": part.sms[1],
+                "expansion_alone_in_partition_tok_s": lay.n_branches / (exp_alone_ms / 1e3),
+                "prefill_alone_in_partition_tflops": layer_flop / (pf_alone_ms / 1e3) / 1e12,
+                "expansion_tok_s": exp_tok_s, "expansion_retained": exp_tok_s / expansion_alone,
+                "prefill_tflops": pf_tflops, "prefill_retained": pf_tflops / prefill_alone,
+                "sum_retained": exp_tok_s / expansion_alone + pf_tflops / prefill_alone,
+                "prefill_layers_in_window": done})
+            part.close()
+    except Exception as exc:                            # green contexts unavailable: say so
+        partitioned = [{"unavailable": f"{type(exc).__name__}: {exc}"}]
     return {"prefill": f"Llama-3-8B layer prefill of {PREFILL_TOKENS} tokens per 'layer': "
                        "[4096x4096]x[4096x{6144,4096,28672}], [4096x14336]x[14336x4096] bf16, "
                        "torch.matmul (cuBLAS) on a low-priority stream",
             "expansion": "the headline step on a high-priority stream",
             "prefill_alone_tflops": prefill_alone, "prefill_ms_per_layer": prefill_ms,
-            "expansion_alone_tok_s": expansion_alone, "steps": steps, "together": together}
+            "expansion_alone_tok_s": expansion_alone, "steps": steps, "together": together,
+            "partitioned": partitioned,
+            "partitioned_note": "green contexts (paper_2510_24390_b200/partition.py): expansion and "
+                                "prefill on disjoint SM sets, both launched together; retained = "
+                                "rate together / rate alone on the whole GPU"}
 
 
 def run_e2e(args, batch, layers, q, kn, vn, out, kc, vc, dev, world, total_b):
