@@ -83,6 +83,16 @@ def algorithmic_bytes(cfg, lay):
     return kv, qb, qb
 
 
+def context_tokens(batch):
+    """Σ_b |ctx(b)| per kv head for the batch's current lengths (SURVEY.md §8(d) flops / exps)."""
+    segs, own = batch.segs, batch.own_len.cpu().numpy()
+    ln = segs["len"].astype(np.int64)
+    dyn = segs["dyn"]
+    m = dyn >= 0
+    ln[m] = np.clip(own[dyn[m]] - segs["start"][m], 0, ln[m])
+    return int(ln.sum())
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -306,6 +316,20 @@ def run_orion(args, cfg, layers):
         e2e = run_e2e(args, batch, layers, q, kn, vn, out, kc, vc, dev, world, total_b)
 
     kv_b, q_b, o_b = algorithmic_bytes(cfg, lay)
+    # three bounds per launch -- bytes / HBM, flops / tensor, exps / MUFU
+    ctx_tok = context_tokens(batch)
+    peaks_all = {}
+    if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")):
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks_all = json.load(f)
+    sm_mhz = peaks_all.get("sm_max_mhz", 1965.0)
+    flops = 4.0 * cfg.d * cfg.hq * ctx_tok
+    exps = float(cfg.hq * ctx_tok)
+    bounds = {"hbm": (kv_b + q_b) / (load_peaks()[0] * 1e9) * 1e6,
+              "tensor_bf16": flops / (peaks_all.get("bf16_tflops", 2250.0) * 1e12) * 1e6,
+              "mufu_ex2": exps / (16 * 148 * sm_mhz * 1e6) * 1e6,
+              "flops": flops, "exps": exps,
+              "note": "MUFU: 16 ex2/clk/SM x 148 SMs at the max SM clock"}
     split_bytes = kv_b + q_b                        # K2 reads: unique KV + q
     split_avg_s = statistics.mean(split_ms) / 1e3
     peak, peak_src = load_peaks()
@@ -334,6 +358,8 @@ def run_orion(args, cfg, layers):
         "roofline": {"bound": "hbm",
                      "kernel": "split_tct_kernel (K2, tcgen05 swap-AB)" if args.kernel == "tc" else "split_kernel (K2, mma.sync)", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": load_traffic(cfg.name, args.kernel),
+                     "frac_of_nominal_8tbs": achieved / 8000.0,
+                     "bounds_us_per_launch": bounds,
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": split_bytes,
                      "split_ms_per_launch": split_avg_s * 1e3,
@@ -345,10 +371,13 @@ def run_orion(args, cfg, layers):
                  "partial_bytes_per_layer": st["workspace_bytes"] * 2,   # written by K2 + read by K3
                  "plan_build_s": plan_s},
         "step_ms": {"p10": pct(0.1), "median": pct(0.5), "p90": pct(0.9), "rank0_only": world > 1},
+        "per_layer": {"us": ms_step / layers * 1e3, "tokens_per_s": float(B) / (ms_step / layers / 1e3)},
         "gpu_launches": args.steps * layers * 3,
         "clocks": clocks,
         "e2e": e2e,
     }
+    if world == 1:
+        line["contiguous_pages"] = run_contiguous(args, cfg, lay, layers, q, kc, vc, out, dev)
     if world == 1 and not args.no_expansion:
         line["expansion_run"] = run_expansion(args, cfg, lay, layers, q, kn, vn, kc, vc, dev)
     if world == 1 and not args.no_point_prefill:
@@ -361,6 +390,42 @@ def run_orion(args, cfg, layers):
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_contiguous(args, cfg, lay, layers, q, kc, vc, out, dev):
+    """SURVEY.md §8(d) variant: the same step with every page run physically contiguous (page
+    table = identity over the same pools) instead of a random page permutation."""
+    import torch
+    import paper_2510_24390_b200 as orion
+    queries = [dict(n_points=int(lay.n_points[i]), edges=lay.edges[i],
+                    prefix_pt_off=int(lay.prefix_pt_off[i]), prefix_len=int(lay.prefix_len[i]))
+               for i in range(lay.n_queries)]
+    points = np.stack([lay.point_pt_off, lay.content_len, lay.point_cap], 1)
+    ident = np.arange(len(lay.page_table), dtype=np.int32)
+    batch = orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, ident,
+                                 lay.own_len, policy=args.policy, device=dev, chunk_tokens=args.chunk)
+    stream = torch.cuda.current_stream(dev)
+    for l in range(min(3, layers)):
+        batch.attend(q[l], out[l], kc[l], vc[l])
+    torch.cuda.synchronize()
+    n = max(3, min(args.steps, 10))
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n * layers)]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(n):
+        for l in range(layers):
+            evs[i * layers + l][0].record(stream)
+            batch.split(q[l], kc[l], vc[l])
+            evs[i * layers + l][1].record(stream)
+            batch.combine(out[l])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    split_ms = statistics.mean(a.elapsed_time(b) for a, b in evs)
+    kv_b, q_b, _ = algorithmic_bytes(cfg, lay)
+    ms = e0.elapsed_time(e1) / n
+    return {"note": "attention only (split + combine per layer, no append), contiguous page runs",
+            "tokens_per_s": lay.n_branches / (ms / 1e3), "ms_per_step": ms,
+            "split_ms_per_launch": split_ms, "split_gbs": (kv_b + q_b) / (split_ms / 1e3) / 1e9}
 
 
 def run_expansion(args, cfg, lay, layers, q, kn, vn, kc, vc, dev):
