@@ -71,8 +71,8 @@ struct L {
   static constexpr int OFF_SH = OFF_M + 2 * 32 * 4; // growth-path shifts: [wg 2][32]
   static constexpr int OFF_RED = OFF_SH + 2 * 32 * 4;  // growth-path column max scratch: [wg 2][4 warps][32]
   static constexpr int OFF_SCHED = OFF_RED + 2 * 4 * 32 * 4;  // item schedule ring: 8 x 64 B
-  static constexpr int OFF_MI = OFF_SCHED + 8 * 64;        // MMA warp's item geometry: 4 x 32 B
-  static constexpr int OFF_BAR = OFF_MI + 4 * 32;
+  static constexpr int OFF_MI = OFF_SCHED + 8 * 64;        // MMA warp's entry geometry: 8 x 32 B
+  static constexpr int OFF_BAR = OFF_MI + 8 * 32;
   static constexpr int N_BAR = 2 * kSK + 2 * kSV + 3 + 3 + 2 + 2 + 2 + 2 + 2 + 2 + 2 * 8;
   static constexpr int BYTES = OFF_BAR + N_BAR * 8 + 16;
 };
@@ -222,22 +222,27 @@ __device__ __forceinline__ uint32_t idesc(int n, bool a_mn, bool b_mn) {   // M 
          (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
 }
 
-struct Geom {
-  int32_t base, end, ntiles, npad;
+// Geometry of range r of an item (the item itself unless kItemRanges).
+struct RangeT {
+  int32_t pt_off, t0, end, base, ntiles;
 };
-__device__ __forceinline__ Geom geom(const WorkItem& w, const int32_t* own_len) {
-  Geom g;
-  g.end = w.t1;
-  if (w.dyn >= 0) g.end = min(g.end, __ldg(own_len + w.dyn));
-  g.base = w.t0 & ~(kTok - 1);
-  g.ntiles = g.end > w.t0 ? (g.end - g.base + kTok - 1) / kTok : 0;
-  g.npad = w.n_rows <= 16 ? 16 : (w.n_rows <= 32 ? 32 : 64);
+__device__ __forceinline__ int item_nranges(const WorkItem& w) { return (w.flags & kItemRanges) ? w.n_ranges : 1; }
+__device__ __forceinline__ RangeT range_of(const TcArgs& a, const WorkItem& w, int r) {
+  RangeT g;
+  int32_t t1, dyn;
+  if (w.flags & kItemRanges) {
+    const Range R = a.ranges[w.pt_off + r];
+    g.pt_off = R.pt_off; g.t0 = R.t0; t1 = R.t1; dyn = R.dyn;
+  } else {
+    g.pt_off = w.pt_off; g.t0 = w.t0; t1 = w.t1; dyn = w.dyn;
+  }
+  g.end = t1;
+  if (dyn >= 0) g.end = min(g.end, __ldg(a.own_len + dyn));
+  g.base = g.t0 & ~(kTok - 1);
+  g.ntiles = g.end > g.t0 ? (g.end - g.base + kTok - 1) / kTok : 0;
   return g;
 }
-__device__ __forceinline__ int next_nonempty(const TcArgs& a, int it) {
-  while (it < a.n_items && geom(a.items[it], a.own_len).ntiles == 0) it += gridDim.x;
-  return it;
-}
+__device__ __forceinline__ int npad_of(int n_rows) { return n_rows <= 16 ? 16 : (n_rows <= 32 ? 32 : 64); }
 
 // One softmax tile for one warpgroup's half of the query columns: thread t owns token row t of S^T
 // and columns [c0, c0 + NH) (NH = padded query rows / 2); mrow / shs / red are this warpgroup's
@@ -332,8 +337,11 @@ __device__ __forceinline__ void softmax_tile(uint32_t tmem, uint32_t lane_base, 
 // Per-CTA item schedule entry, produced by the scheduler warp (warp 1) and consumed in order by
 // the TMA, MMA and both softmax warpgroups (removes the dependent global loads of the item
 // descriptors from every role's critical path).
+// One entry per token range: an item is one range, or (kItemRanges) a list of ranges streamed as
+// one accumulation.  `item` numbers the CTA's non-empty items (Q / O^T double-buffer parity);
+// `first` / `last` mark an item's first and last non-empty range.
 struct Sched {
-  int32_t valid, it, pt_off, t0, end, base, ntiles, npad, kv_head, n_rows, slot0, pad[5];
+  int32_t valid, it, pt_off, t0, end, base, ntiles, npad, kv_head, n_rows, slot0, item, first, last, pad[2];
 };
 constexpr int kSched = 8;
 constexpr uint32_t kSchedConsumers = 1 + 1 + 1 + 128 + 128;   // K-TMA, V-TMA, MMA lanes, WG0, WG1
@@ -374,18 +382,26 @@ __device__ __forceinline__ Bars carve_bars(uint8_t* smem) {
 // over the 128 token rows.
 template <int NH>
 __device__ __forceinline__ void softmax_item(uint8_t* smem, uint32_t tmem, uint32_t lane_base, int p, int t,
-                                             const Sched& e, uint32_t k, uint32_t& j, float* mrow, float* shs,
-                                             float* red, const Bars& B, const TcArgs& a) {
+                                             const Sched& e, uint32_t& k, uint32_t& j, float* mrow, float* shs,
+                                             float* red, const Bars& B, const TcArgs& a, const Sched* ring) {
+  // `e` is the item's first ring entry (k); its further ranges are the next entries, read here.
   const int c0 = p * NH;
-  const uint32_t kp = k & 1;
+  const uint32_t kp = static_cast<uint32_t>(e.item) & 1;
   float ls[NH];
 #pragma unroll
   for (int c = 0; c < NH; ++c) ls[c] = 0.f;
   if (t < NH) mrow[t] = -INFINITY;
   wg_sync(2 + p, 128);
-  for (int tt = 0; tt < e.ntiles; ++tt, ++j) {
-    const int tb = e.base + tt * kTok;
-    const int lo = max(tb, e.t0), hi = min(tb + kTok, e.end);
+  Sched cur = e;
+  for (int tt = 0, t_in = 0;; ++tt, ++t_in, ++j) {
+    if (t_in == cur.ntiles) {                       // next range of the same item
+      if (cur.last) break;
+      ++k;
+      cur = read_sched(ring, B.sch_full, B.sch_empty, k, true);
+      t_in = 0;
+    }
+    const int tb = cur.base + t_in * kTok;
+    const int lo = max(tb, cur.t0), hi = min(tb + kTok, cur.end);
     const uint32_t b = j % kSB;
     mbar_wait(B.s_full + b, (j / kSB) & 1);
     tc_fence_after();
@@ -416,7 +432,7 @@ __device__ __forceinline__ void softmax_item(uint8_t* smem, uint32_t tmem, uint3
     }
   }
   if (ln < NH) red[wq * 32 + ln] = ls[0];
-  mbar_wait(B.acc_full + kp, (k >> 1) & 1);
+  mbar_wait(B.acc_full + kp, (static_cast<uint32_t>(e.item) >> 1) & 1);
   tc_fence_after();
   wg_sync(2 + p, 128);
   // fp16 partial format (plan_format.h): o = acc / l, lse2 = m + log2 l.  l >= 1: the column max
@@ -491,49 +507,60 @@ __global__ void __launch_bounds__(kThreads, 1)
   TRACE_DECL
   if (warp == kWarpSched) {
     // ------------------------------------------------------------------ scheduler + Q gather
-    uint32_t k = 0;
+    uint32_t k = 0;                                 // ring entries published (one per range)
+    uint32_t iq = 0;                                // non-empty items of this CTA
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const WorkItem w = a.items[it];
-      const Geom g = geom(w, a.own_len);
-      if (g.ntiles == 0) {                           // empty (dyn end <= t0): neutral partial
+      const int nr = item_nranges(w);
+      int rfirst = -1, rlast = -1;
+      for (int r = 0; r < nr; ++r)
+        if (range_of(a, w, r).ntiles > 0) { if (rfirst < 0) rfirst = r; rlast = r; }
+      if (rfirst < 0) {                              // every range empty (dyn end <= t0): neutral partial
         for (int i = lane; i < w.n_rows * D / 8; i += 32)
           reinterpret_cast<uint4*>(a.part_o + static_cast<size_t>(w.slot0) * D)[i] = make_uint4(0, 0, 0, 0);
         for (int r = lane; r < w.n_rows; r += 32) a.part_lse[w.slot0 + r] = -INFINITY;
         continue;
       }
-      TW(0, mbar_wait(sch_empty + (k % kSched), ((k / kSched) & 1) ^ 1));
-      if (lane == 0) {
-        Sched e;
-        e.valid = 1; e.it = it; e.pt_off = w.pt_off; e.t0 = w.t0; e.end = g.end; e.base = g.base;
-        e.ntiles = g.ntiles; e.npad = g.npad; e.kv_head = w.kv_head; e.n_rows = w.n_rows; e.slot0 = w.slot0;
-        ring[k % kSched] = e;
-        mbar_arrive(sch_full + (k % kSched));
-      }
-      // Q rows of item k -> Q buffer k & 1, once item k-2's QKs have completed
-      if (k >= 2) TW(1, mbar_wait(q_empty + (k & 1), ((k >> 1) - 1) & 1));
-      uint8_t* qb = smem + L::OFF_Q + (k & 1) * L::QB;
-#pragma unroll
-      for (int rr = 0; rr < 2; ++rr) {
-        const int r = lane + rr * 32;
-        const bool ok = r < w.n_rows;
-        const __nv_bfloat16* src = a.q;
-        if (ok) {
-          const int row = w.row_begin + r;
-          const int b = __ldg(a.readers + w.readers_off + row / a.group);
-          const int hq = w.kv_head * a.group + row % a.group;
-          src = a.q + (static_cast<size_t>(b) * a.hq + hq) * D;
+      for (int r = rfirst; r <= rlast; ++r) {
+        const RangeT g = range_of(a, w, r);
+        if (g.ntiles == 0) continue;
+        TW(0, mbar_wait(sch_empty + (k % kSched), ((k / kSched) & 1) ^ 1));
+        if (lane == 0) {
+          Sched e;
+          e.valid = 1; e.it = it; e.pt_off = g.pt_off; e.t0 = g.t0; e.end = g.end; e.base = g.base;
+          e.ntiles = g.ntiles; e.npad = npad_of(w.n_rows); e.kv_head = w.kv_head; e.n_rows = w.n_rows;
+          e.slot0 = w.slot0; e.item = static_cast<int32_t>(iq); e.first = r == rfirst; e.last = r == rlast;
+          ring[k % kSched] = e;
+          mbar_arrive(sch_full + (k % kSched));
         }
+        ++k;
+        if (r != rfirst) continue;
+        // Q rows of item iq -> Q buffer iq & 1, once item iq-2's QKs have completed
+        if (iq >= 2) TW(1, mbar_wait(q_empty + (iq & 1), ((iq >> 1) - 1) & 1));
+        uint8_t* qb = smem + L::OFF_Q + (iq & 1) * L::QB;
 #pragma unroll
-        for (int c = 0; c < 16; ++c)
-          cp_async16(smem_u32(qb + (c >> 3) * L::HALF_Q + r * 128 + (((c & 7) ^ (r & 7)) << 4)),
-                     ok ? static_cast<const void*>(src + c * 8) : static_cast<const void*>(a.q), ok);
+        for (int rr = 0; rr < 2; ++rr) {
+          const int rw = lane + rr * 32;
+          const bool ok = rw < w.n_rows;
+          const __nv_bfloat16* src = a.q;
+          if (ok) {
+            const int row = w.row_begin + rw;
+            const int b = __ldg(a.readers + w.readers_off + row / a.group);
+            const int hq = w.kv_head * a.group + row % a.group;
+            src = a.q + (static_cast<size_t>(b) * a.hq + hq) * D;
+          }
+#pragma unroll
+          for (int c = 0; c < 16; ++c)
+            cp_async16(smem_u32(qb + (c >> 3) * L::HALF_Q + rw * 128 + (((c & 7) ^ (rw & 7)) << 4)),
+                       ok ? static_cast<const void*>(src + c * 8) : static_cast<const void*>(a.q), ok);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(q_full + (iq & 1));
       }
-      asm volatile("cp.async.commit_group;\n" ::: "memory");
-      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(q_full + (k & 1));
-      ++k;
+      ++iq;
     }
     TW(0, mbar_wait(sch_empty + (k % kSched), ((k / kSched) & 1) ^ 1));
     if (lane == 0) {                                 // terminator
@@ -618,17 +645,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t dk0 = sw128_desc(smem_u32(smem + L::OFF_K), 16, 1024);
     const uint64_t dv0 = sw128_desc(smem_u32(smem + L::OFF_V), L::HALF_KV, 1024);   // MN-major A
     const uint64_t dp0 = sw128_desc(smem_u32(smem + L::OFF_P), L::HALF_KV, 1024);   // MN-major B
-    // geometry of items k % 4 (QK may have read item kv + 1 while PV is on item kv)
-    int32_t* mi = reinterpret_cast<int32_t*>(smem + L::OFF_MI);   // [4][8]: t0 end base ntiles npad
+    // geometry of ring entries k % 8: QK is at most four tiles (so four entries) past PV, plus
+    // the entry it has read ahead
+    int32_t* mi = reinterpret_cast<int32_t*>(smem + L::OFF_MI);   // [8][8]: t0 end base ntiles npad item first last
     auto set_of = [&](uint32_t k, const Sched& e) {
       if (lane == 0) {
-        int32_t* r = mi + (k & 3) * 8;
+        int32_t* r = mi + (k & 7) * 8;
         r[0] = e.t0; r[1] = e.end; r[2] = e.base; r[3] = e.ntiles; r[4] = e.npad;
+        r[5] = e.item; r[6] = e.first; r[7] = e.last;
       }
       __syncwarp();
     };
-    auto nt_of = [&](uint32_t k) { return mi[(k & 3) * 8 + 3]; };
-    auto np_of = [&](uint32_t k) { return mi[(k & 3) * 8 + 4]; };
+    auto nt_of = [&](uint32_t k) { return mi[(k & 7) * 8 + 3]; };
+    auto np_of = [&](uint32_t k) { return mi[(k & 7) * 8 + 4]; };
+    auto item_of = [&](uint32_t k) { return static_cast<uint32_t>(mi[(k & 7) * 8 + 5]); };
+    auto first_of = [&](uint32_t k) { return mi[(k & 7) * 8 + 6] != 0; };
+    auto last_of = [&](uint32_t k) { return mi[(k & 7) * 8 + 7] != 0; };
     uint32_t kq = 0, tq = 0, jq = 0;                // QK cursor (item, tile in item, global tile)
     uint32_t kv = 0, tv = 0, jv = 0;                // PV cursor
     bool q_live;
@@ -639,13 +671,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     auto issue_qk = [&]() {
       const uint32_t j = jq;
-      if (tq == 0) TW(1, mbar_wait(q_full + (kq & 1), (kq >> 1) & 1));
+      const uint32_t iqq = item_of(kq);
+      if (tq == 0 && first_of(kq)) TW(1, mbar_wait(q_full + (iqq & 1), (iqq >> 1) & 1));
       const int s = j % kSK;
       TW(2, mbar_wait(k_full + s, (j / kSK) & 1));
       if (j >= static_cast<uint32_t>(kSB)) TW(3, mbar_wait(s_free + (j % kSB), ((j - kSB) / kSB) & 1));
       tc_fence_after();
       const int ntq = nt_of(kq);
-      const uint64_t dq = dq0 + static_cast<uint64_t>(((kq & 1) * L::QB) >> 4);
+      const uint64_t dq = dq0 + static_cast<uint64_t>(((iqq & 1) * L::QB) >> 4);
       const uint64_t dk = dk0 + static_cast<uint64_t>((s * L::KVB) >> 4);
       const uint32_t id = idesc(np_of(kq), false, false);
 #ifdef ORION_TC_TRACE
@@ -660,7 +693,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_commit(s_full + (j % kSB));
         tc_commit(k_empty + s);
-        if (static_cast<int>(tq) + 1 == ntq) tc_commit(q_empty + (kq & 1));   // item's last QK
+        if (static_cast<int>(tq) + 1 == ntq && last_of(kq)) tc_commit(q_empty + (iqq & 1));   // item's last QK
       }
       __syncwarp();
 #ifdef ORION_TC_TRACE
@@ -679,7 +712,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto issue_pv = [&]() {
       const uint32_t j = jv;
       const int s = j % kSV;
-      const uint32_t wg = kv & 1;                   // accumulator pair of item kv
+      const uint32_t ivv = item_of(kv);
+      const uint32_t wg = ivv & 1;                  // accumulator of item ivv
       TW(6, mbar_wait(v_full + s, (j / kSV) & 1));
 #ifdef ORION_TC_TRACE
       const unsigned long long tz0 = clock64();
@@ -687,7 +721,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       {
         // A partial tile's TMA boxes (16-row granular) may carry rows outside [t0, end) -- e.g.
         // never-written slots past own_len.  Their P is exactly 0, but 0 x NaN is NaN: zero them.
-        const int32_t* r = mi + (kv & 3) * 8;
+        const int32_t* r = mi + (kv & 7) * 8;
         const int a0 = r[2] + static_cast<int>(tv) * kTok;
         const int lo = max(a0, r[0]) - a0, hi = min(a0 + kTok, r[1]) - a0;
         if (lo > 0 || hi < kTok) {
@@ -707,13 +741,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       tr_[0] += clock64() - tz0;
 #endif
       TW(4, mbar_wait(p_full + (j & 1), (j >> 1) & 1));
-      if (tv == 0 && kv >= 2) TW(5, mbar_wait(o_free + wg, ((kv >> 1) - 1) & 1));   // item kv-2 read out
+      if (tv == 0 && first_of(kv) && ivv >= 2) TW(5, mbar_wait(o_free + wg, ((ivv >> 1) - 1) & 1));   // item ivv-2 read out
       tc_fence_after();
       const uint64_t dv = dv0 + static_cast<uint64_t>((s * L::KVB) >> 4);
       const uint64_t dp = dp0 + static_cast<uint64_t>(((j & 1) * L::PB) >> 4);
       const int npv = np_of(kv);
       const uint32_t id_pv = idesc(npv, true, true);
-      const bool first = tv == 0;
+      const bool first = tv == 0 && first_of(kv);   // the item's first tile: O^T = P V (no accumulate)
 #ifdef ORION_TC_TRACE
       const unsigned long long tp0 = clock64();
 #endif
@@ -726,7 +760,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_commit(pv_done + (j & 1));
         tc_commit(v_empty + s);
-        if (static_cast<int>(tv) + 1 == nt_of(kv)) tc_commit(acc_full + wg);   // item complete
+        if (static_cast<int>(tv) + 1 == nt_of(kv) && last_of(kv)) tc_commit(acc_full + wg);   // item complete
       }
       __syncwarp();
 #ifdef ORION_TC_TRACE
@@ -737,7 +771,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     // in-order: keep QK up to 3 tiles ahead (never into item kv+2), then one PV
     while (true) {
-      while (q_live && jq <= jv + 3 && kq <= kv + 1) issue_qk();
+      while (q_live && jq <= jv + 3 && item_of(kq) <= item_of(kv) + 1) issue_qk();
       const bool v_live = kv < kq || (kv == kq && q_live);
       if (!v_live) break;
       issue_pv();
@@ -758,9 +792,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (uint32_t k = 0;; ++k) {
       const Sched e = read_sched(ring, sch_full, sch_empty, k, true);
       if (!e.valid) break;
-      if (e.npad == 16) softmax_item<8>(smem, tmem, lane_base, p, t, e, k, j, mrow, shs, red, bars, a);
-      else if (e.npad == 32) softmax_item<16>(smem, tmem, lane_base, p, t, e, k, j, mrow, shs, red, bars, a);
-      else softmax_item<32>(smem, tmem, lane_base, p, t, e, k, j, mrow, shs, red, bars, a);
+      if (e.npad == 16) softmax_item<8>(smem, tmem, lane_base, p, t, e, k, j, mrow, shs, red, bars, a, ring);
+      else if (e.npad == 32) softmax_item<16>(smem, tmem, lane_base, p, t, e, k, j, mrow, shs, red, bars, a, ring);
+      else softmax_item<32>(smem, tmem, lane_base, p, t, e, k, j, mrow, shs, red, bars, a, ring);
     }
     TRACE_DUMP("softmax");
   }
