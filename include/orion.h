@@ -112,7 +112,10 @@ typedef struct { int32_t pt_off, content_len, capacity; } orion_point_desc;
  * rows-on-lanes tcgen05 kernel.  ORION_PLAN_ROWS_ON_LANES forces the rows-on-lanes tcgen05 kernel
  * (<= 128 rows per item); ORION_PLAN_MMA_SYNC the legacy mma.sync m16n8k16 + cp.async kernel
  * (<= 64 rows per item).  All variants compute the same result (same plan semantics). */
-enum { ORION_PLAN_MMA_SYNC = 1, ORION_PLAN_ROWS_ON_LANES = 2 };
+enum { ORION_PLAN_MMA_SYNC = 1, ORION_PLAN_ROWS_ON_LANES = 2, ORION_PLAN_NO_MERGE = 4 };
+/* ORION_PLAN_NO_MERGE: one work item per (piece, kv head, chunk, row block) -- without it, the
+ * tcgen05 decode plans group rows into fixed reader blocks and merge every chunk one block reads
+ * with the same reader subset into a multi-range item (one partial per row for the lot). */
 
 typedef struct {
   int32_t num_sms;        /* SMs the persistent split kernel may occupy (grid cap, e.g. to leave

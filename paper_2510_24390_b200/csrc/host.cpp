@@ -442,15 +442,100 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
           cost.push_back((int64_t)(w.t1 - w.t0) * (2 + (w.n_rows + 15) / 16) + 256);
         }
   };
-  for (size_t pi = 0; pi < pieces.size(); ++pi) {
-    const Piece& p = pieces[pi];
-    unique_tokens += p.t1 - p.t0;
-    add_items(p.pt_off, p.t0, p.t1, p.dyn, 0, p.readers, (int32_t)pi);
+  std::vector<Range> ranges;                         // multi-range items' ranges (plan Range[])
+  // Decode plans on the tcgen05 kernels: rows are grouped into fixed reader blocks (R readers =
+  // one <= rows_per_item row block; a block never straddles queries, whose branches are
+  // consecutive), and every chunk a block's rows read in full with the same reader subset joins
+  // one multi-range item.  A Dependent chain's shared history then streams once per block as one
+  // accumulation (one partial per row) instead of one short item and one partial per ancestor.
+  const bool merge = Lc == 0 && variant != kVariantMmaSync && !(flags & ORION_PLAN_NO_MERGE);
+  if (!merge) {
+    for (size_t pi = 0; pi < pieces.size(); ++pi) {
+      const Piece& p = pieces[pi];
+      unique_tokens += p.t1 - p.t0;
+      add_items(p.pt_off, p.t0, p.t1, p.dyn, 0, p.readers, (int32_t)pi);
+    }
+  } else {
+    const int32_t RB = std::max(1, rows_per_item / G);
+    // Blocks are counted from each query's first branch, so a query's plan does not depend on
+    // what else is in the batch (a strong-scaling shard reproduces the single-GPU plan and its
+    // results bitwise).  The planner has no query ids: every list starts with its query's PREFIX
+    // segment, whose page run identifies the query.
+    std::map<int32_t, int32_t> first_branch;
+    std::vector<int32_t> qkey(n_branches);
+    for (int32_t b = 0; b < n_branches; ++b) {
+      qkey[b] = h_seg_offsets[b] < h_seg_offsets[b + 1] ? h_segs[h_seg_offsets[b]].pt_off : -1 - b;
+      auto f = first_branch.find(qkey[b]);
+      if (f == first_branch.end()) first_branch.emplace(qkey[b], b);
+      else f->second = std::min(f->second, b);
+    }
+    auto block_of = [&](int32_t b) { return (int64_t)qkey[b] * 1000003 + (b - first_branch[qkey[b]]) / RB; };
+    std::map<std::pair<int32_t, std::vector<int32_t>>, int32_t> key_index;
+    std::vector<std::pair<int32_t, std::vector<int32_t>>> gkeys;
+    std::vector<std::vector<Range>> gchunks;
+    std::vector<int32_t> gpiece;
+    for (size_t pi = 0; pi < pieces.size(); ++pi) {
+      const Piece& p = pieces[pi];
+      unique_tokens += p.t1 - p.t0;
+      for (size_t i = 0; i < p.readers.size();) {
+        const int64_t blk = block_of(p.readers[i]);
+        std::vector<int32_t> S;
+        while (i < p.readers.size() && block_of(p.readers[i]) == blk) S.push_back(p.readers[i++]);
+        const int32_t rows = (int32_t)S.size() * G;
+        int32_t ch = std::max(chunk, 32 * rows);
+        ch = (ch + kTileTokens - 1) / kTileTokens * kTileTokens;
+        for (int32_t g = 0; g < Hkv; ++g) {
+          auto key = std::make_pair(g, S);
+          auto f = key_index.find(key);
+          int32_t idx;
+          if (f == key_index.end()) {
+            idx = (int32_t)gkeys.size();
+            key_index.emplace(key, idx);
+            gkeys.push_back(key);
+            gchunks.emplace_back();
+            gpiece.push_back((int32_t)pi);
+          } else {
+            idx = f->second;
+          }
+          for (int32_t t = p.t0; t < p.t1; t += ch)
+            gchunks[idx].push_back(Range{p.pt_off, t, std::min(p.t1, t + ch), p.dyn, 0, {0, 0, 0}});
+        }
+      }
+    }
+    for (size_t gi = 0; gi < gkeys.size(); ++gi) {
+      const int32_t g = gkeys[gi].first;
+      const std::vector<int32_t>& S = gkeys[gi].second;
+      const int32_t rows = (int32_t)S.size() * G;
+      const int32_t roff = (int32_t)readers.size();
+      readers.insert(readers.end(), S.begin(), S.end());
+      const std::vector<Range>& cs = gchunks[gi];
+      for (size_t c0 = 0; c0 < cs.size();) {
+        size_t c1 = c0;
+        int64_t tok = 0;
+        while (c1 < cs.size() && (c1 == c0 || tok + (cs[c1].t1 - cs[c1].t0) <= kMergeTokens))
+          tok += cs[c1].t1 - cs[c1].t0, ++c1;
+        WorkItem w{};
+        if (c1 - c0 == 1) {
+          w.pt_off = cs[c0].pt_off; w.t0 = cs[c0].t0; w.t1 = cs[c0].t1; w.dyn = cs[c0].dyn;
+        } else {
+          w.pt_off = (int32_t)ranges.size(); w.dyn = -1;
+          w.flags = kItemRanges; w.n_ranges = (int32_t)(c1 - c0);
+          ranges.insert(ranges.end(), cs.begin() + c0, cs.begin() + c1);
+        }
+        w.kv_head = g; w.readers_off = roff; w.row_begin = 0; w.n_rows = rows;
+        w.slot0 = n_slots; w.piece = gpiece[gi];
+        for (int32_t r = 0; r < rows; ++r)
+          row_slots[(size_t)S[r / G] * Hq + g * G + r % G].push_back(n_slots + r);
+        n_slots += rows;
+        items.push_back(w);
+        cost.push_back(tok * (2 + (rows + 15) / 16) + 256 * (int64_t)(c1 - c0));
+        c0 = c1;
+      }
+    }
   }
   // Prefill: per kv head and branch, one multi-range item per row block: the branch's ranges in
   // list order, then its own content tokens (causal).  Items of one query's branches are adjacent
   // for each kv head, so the shared prefix streams through L2 for all of them at about once.
-  std::vector<Range> ranges;
   if (Lc > 0) {
     std::vector<int32_t> range_off(n_branches);
     for (int32_t b = 0; b < n_branches; ++b) {

@@ -28,6 +28,7 @@ enum : int32_t { kVariantTC = 0, kVariantMmaSync = 1, kVariantTCT = 2 };
 inline bool partials_fp16(int32_t variant) { return variant == kVariantTCT; }
 constexpr int32_t kItemCausal = 1;
 constexpr int32_t kItemRanges = 2;
+constexpr int64_t kMergeTokens = 8192;   // token cap of a merged multi-range decode item
 constexpr int kTileTokens = 64;    // tokens per pipeline stage in the split kernel
 
 struct PlanHeader {

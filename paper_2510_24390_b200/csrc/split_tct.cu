@@ -513,8 +513,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const WorkItem w = a.items[it];
       const int nr = item_nranges(w);
       int rfirst = -1, rlast = -1;
-      for (int r = 0; r < nr; ++r)
-        if (range_of(a, w, r).ntiles > 0) { if (rfirst < 0) rfirst = r; rlast = r; }
+      RangeT g0 = range_of(a, w, 0);
+      if (nr == 1) {                                 // the common single-range item: one lookup
+        if (g0.ntiles > 0) rfirst = rlast = 0;
+      } else {
+        for (int r = 0; r < nr; ++r)
+          if (range_of(a, w, r).ntiles > 0) { if (rfirst < 0) rfirst = r; rlast = r; }
+      }
       if (rfirst < 0) {                              // every range empty (dyn end <= t0): neutral partial
         for (int i = lane; i < w.n_rows * D / 8; i += 32)
           reinterpret_cast<uint4*>(a.part_o + static_cast<size_t>(w.slot0) * D)[i] = make_uint4(0, 0, 0, 0);
@@ -522,7 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         continue;
       }
       for (int r = rfirst; r <= rlast; ++r) {
-        const RangeT g = range_of(a, w, r);
+        const RangeT g = nr == 1 ? g0 : range_of(a, w, r);
         if (g.ntiles == 0) continue;
         TW(0, mbar_wait(sch_empty + (k % kSched), ((k / kSched) & 1) ^ 1));
         if (lane == 0) {
@@ -659,6 +664,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto nt_of = [&](uint32_t k) { return mi[(k & 7) * 8 + 3]; };
     auto np_of = [&](uint32_t k) { return mi[(k & 7) * 8 + 4]; };
     auto item_of = [&](uint32_t k) { return static_cast<uint32_t>(mi[(k & 7) * 8 + 5]); };
+    uint32_t q_item = 0, v_item = 0;                // item numbers of the QK / PV cursors' entries
     auto first_of = [&](uint32_t k) { return mi[(k & 7) * 8 + 6] != 0; };
     auto last_of = [&](uint32_t k) { return mi[(k & 7) * 8 + 7] != 0; };
     uint32_t kq = 0, tq = 0, jq = 0;                // QK cursor (item, tile in item, global tile)
@@ -668,6 +674,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Sched e = read_sched(ring, sch_full, sch_empty, 0, lane == 0);
       q_live = e.valid;
       set_of(0, e);
+      q_item = v_item = static_cast<uint32_t>(e.item);
     }
     auto issue_qk = [&]() {
       const uint32_t j = jq;
@@ -707,6 +714,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         TW(7, e = read_sched(ring, sch_full, sch_empty, kq, lane == 0));
         q_live = e.valid;
         set_of(kq, e);
+        if (e.valid) q_item = static_cast<uint32_t>(e.item);
       }
     };
     auto issue_pv = [&]() {
@@ -767,11 +775,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       tr_[9] += clock64() - tp0;
 #endif
       ++jv;
-      if (static_cast<int>(++tv) == nt_of(kv)) { tv = 0; ++kv; }
+      if (static_cast<int>(++tv) == nt_of(kv)) {
+        tv = 0;
+        ++kv;
+        if (kv < kq || (kv == kq && q_live)) v_item = item_of(kv);
+      }
     };
     // in-order: keep QK up to 3 tiles ahead (never into item kv+2), then one PV
     while (true) {
-      while (q_live && jq <= jv + 3 && item_of(kq) <= item_of(kv) + 1) issue_qk();
+      while (q_live && jq <= jv + 3 && q_item <= v_item + 1) issue_qk();
       const bool v_live = kv < kq || (kv == kq && q_live);
       if (!v_live) break;
       issue_pv();

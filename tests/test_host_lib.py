@@ -156,9 +156,18 @@ def _check_plan_covers(cfg, lay, offs, segs, own_len):
     assert ws >= h["n_partials"] * ((cfg.d * 2 + 4) if variant == 2 else (cfg.d * 4 + 8))
     slot_tokens = {}
     slot_row = {}
+    ranges = np.frombuffer(plan, RANGE, int(h["n_ranges"]), int(h["ranges_off"]))
     for it in items:
-        end = it["t1"] if it["dyn"] < 0 else min(it["t1"], own_len[it["dyn"]])
-        toks = [(int(it["pt_off"]), t) for t in range(it["t0"], max(it["t0"], end))]
+        if it["p0"] & 2:                             # multi-range item: its ranges' tokens
+            rl = [(int(r["pt_off"]), int(r["t0"]), int(r["t1"]), int(r["dyn"]))
+                  for r in ranges[it["pt_off"]:it["pt_off"] + it["p1"]]]
+            assert len(rl) >= 2
+        else:
+            rl = [(int(it["pt_off"]), int(it["t0"]), int(it["t1"]), int(it["dyn"]))]
+        toks = []
+        for pt, t0, t1, dyn in rl:
+            end = t1 if dyn < 0 else min(t1, own_len[dyn])
+            toks += [(pt, t) for t in range(t0, max(t0, end))]
         for r in range(it["row_begin"], it["row_begin"] + it["n_rows"]):
             b = readers[it["readers_off"] + r // G]
             hh = it["kv_head"] * G + r % G
@@ -328,3 +337,21 @@ def test_prefill_plan_errors():
     assert L.orion_point_prefill_attn(ctypes.byref(shape), lay.n_branches, *args, _lib.ptr(dec), fake,
                                       fake, 1 << 30, None) == _lib.ERR_INVALID_ARG
     assert b"prefill" in L.orion_last_error()
+
+
+def test_chain_plan_merges_history_per_reader_block():
+    # Dependent chain under ANCESTORS: point j reads the full runs of points 1..j-1.  With fixed
+    # reader blocks, a block's shared history becomes multi-range items (kItemRanges) -- far fewer
+    # partials than one per (ancestor, reader) -- and every context is still covered exactly once.
+    cfg = C.CONFIGS["c5c"].with_(n_queries=1, lp=512, t=96, lc=16, dag="chain64")
+    lay = T.make_layout(cfg, dag_override=lambda: W.chain(48, 2))
+    offs, segs = _bind_layout(cfg, lay, 0)
+    merged, _ = orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, lay.own_len)
+    plain, _ = orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, lay.own_len,
+                                 flags=orion.PLAN_NO_MERGE)
+    hm, im, *_ = parse_plan(merged)
+    hp, ip, *_ = parse_plan(plain)
+    assert (im["p0"] & 2).any() and not (ip["p0"] & 2).any()
+    assert hm["n_partials"] * 2 < hp["n_partials"]            # 3x fewer at this size
+    assert hm["unique_tokens"] == hp["unique_tokens"] and hm["logical_tokens"] == hp["logical_tokens"]
+    _check_plan_covers(cfg, lay, offs, segs, lay.own_len)
