@@ -47,8 +47,10 @@ def parse():
     ap.add_argument("--impl", default="orion", choices=["orion", "reference"])
     ap.add_argument("--policy", type=int, default=0, help="0 ANCESTORS, 1 PARENTS_EQ3")
     ap.add_argument("--chunk", type=int, default=0, help="plan chunk_tokens (0 = default)")
-    ap.add_argument("--kernel", default="tc", choices=["tc", "mma"],
-                    help="split kernel: tcgen05/TMEM/TMA (default) or legacy mma.sync")
+    ap.add_argument("--no-merge", action="store_true",
+                    help="plan without multi-range item merging (ORION_PLAN_NO_MERGE), for comparison")
+    ap.add_argument("--kernel", default="tc", choices=["tc", "rol", "mma"],
+                    help="split kernel: tcgen05 swap-AB (default), tcgen05 rows-on-lanes (rol) or legacy mma.sync")
     ap.add_argument("--layers", type=int, default=0, help="override layer count (0 = config)")
     ap.add_argument("--queries", type=int, default=0, help="override query count (0 = config)")
     ap.add_argument("--scaling", default="weak", choices=["strong", "weak"],
@@ -265,7 +267,9 @@ def run_orion(args, cfg, layers):
     batch = orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, lay.page_table,
                                  lay.own_len, policy=args.policy, device=dev,
                                  chunk_tokens=args.chunk,
-                                 flags=orion.PLAN_MMA_SYNC if args.kernel == "mma" else 0)
+                                 flags={"tc": 0, "rol": orion.PLAN_ROWS_ON_LANES,
+                                        "mma": orion.PLAN_MMA_SYNC}[args.kernel]
+                                       | (orion.PLAN_NO_MERGE if args.no_merge else 0))
     plan_s = time.perf_counter() - t0
     stream = torch.cuda.current_stream(dev)
     REW = orion.APPEND_REWRITE
@@ -356,7 +360,8 @@ def run_orion(args, cfg, layers):
                                    if args.scaling == "weak" else
                                    f"{cfg.n_queries} queries partitioned over {world} GPU(s), no collective")},
         "roofline": {"bound": "hbm",
-                     "kernel": "split_tct_kernel (K2, tcgen05 swap-AB)" if args.kernel == "tc" else "split_kernel (K2, mma.sync)", "achieved": achieved, "peak": peak,
+                     "kernel": {"tc": "split_tct_kernel (K2, tcgen05 swap-AB)", "rol": "split_tc_kernel (K2, tcgen05 rows-on-lanes)",
+                                "mma": "split_kernel (K2, mma.sync)"}[args.kernel], "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": load_traffic(cfg.name, args.kernel),
                      "frac_of_nominal_8tbs": achieved / 8000.0,
                      "bounds_us_per_launch": bounds,
