@@ -20,6 +20,7 @@
 #include <stdint.h>
 
 #include <cmath>
+#include <map>
 #include <mutex>
 
 #include "../../include/orion.h"
@@ -437,6 +438,40 @@ __global__ void __launch_bounds__(128) kv_append_kernel(
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+std::mutex g_setup_mu;
+std::map<int, int> g_sms;                                   // device -> SM count
+std::map<std::pair<int, const void*>, cudaError_t> g_smem;  // (device, kernel) -> attribute status
+}  // namespace
+
+namespace orion {
+int current_device_sms() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  std::lock_guard<std::mutex> lk(g_setup_mu);
+  auto f = g_sms.find(dev);
+  if (f != g_sms.end()) return f->second;
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  g_sms[dev] = n;
+  return n;
+}
+
+cudaError_t ensure_dynamic_smem(const void* func, int bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_setup_mu);
+  auto key = std::make_pair(dev, func);
+  auto f = g_smem.find(key);
+  if (f != g_smem.end()) return f->second;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  g_smem[key] = e;
+  return e;
+}
+}  // namespace orion
+
+namespace {
+
 int log2i(int x) {
   int s = 0;
   while ((1 << s) < x) ++s;
@@ -480,12 +515,8 @@ orion_status launch_split(const PlanHeader* h, const char* dplan, const void* q,
     }
     return launch_split_tc<D>(h, t, k, v, num_pages, st);
   }
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(split_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)split_smem_bytes<D>());
-  });
+  const cudaError_t attr_err =
+      ensure_dynamic_smem(reinterpret_cast<const void*>(split_kernel<D>), (int)split_smem_bytes<D>());
   if (attr_err != cudaSuccess)
     return fail(ORION_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
   SplitArgs a;

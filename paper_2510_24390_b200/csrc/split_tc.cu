@@ -741,17 +741,9 @@ bool make_map(CUtensorMap* m, const void* base, int d, int64_t rows, int box_row
 template <int D>
 orion_status launch_split_tc(const PlanHeader* h, const TcArgs& a, const void* k, const void* v,
                              int32_t num_pages, cudaStream_t st) {
-  static int num_sms = 0;
-  static cudaError_t attr_err = cudaSuccess;
-  static bool init = false;
-  if (!init) {
-    init = true;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    attr_err = cudaFuncSetAttribute(tc::split_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    tc::Smem<D>::BYTES + 1024);
-  }
+  const int num_sms = current_device_sms();
+  const cudaError_t attr_err = ensure_dynamic_smem(reinterpret_cast<const void*>(tc::split_tc_kernel<D>),
+                                                   tc::Smem<D>::BYTES + 1024);
   if (attr_err != cudaSuccess)
     return fail(ORION_ERR_CUDA, "cudaFuncSetAttribute(split_tc): %s", cudaGetErrorString(attr_err));
   CUtensorMap mk, mv, mk16, mv16;

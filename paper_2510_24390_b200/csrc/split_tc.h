@@ -13,6 +13,12 @@ namespace orion {
 
 orion_status fail(orion_status code, const char* fmt, ...);
 
+// Per-device launch setup, thread-safe: the SM count of the current device, and the opt-in
+// dynamic shared-memory size of `func` on it (set once per (device, function); the attribute is
+// per device, so a process driving several GPUs needs it on each).
+int current_device_sms();
+cudaError_t ensure_dynamic_smem(const void* func, int bytes);
+
 // Programmatic dependent launch (PDL).  Kernels of one expansion step (append -> split ->
 // combine -> next layer's append) are launched with programmatic stream serialization: the next
 // kernel may be scheduled while the previous one drains, runs its data-independent prologue

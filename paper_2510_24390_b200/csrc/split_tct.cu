@@ -852,16 +852,9 @@ bool make_map_t(CUtensorMap* m, const void* base, int64_t rows, int box_rows) {
 
 orion_status launch_split_tct(const PlanHeader* h, const TcArgs& a, const void* k, const void* v,
                               int32_t num_pages, cudaStream_t st) {
-  static int num_sms = 0;
-  static cudaError_t attr_err = cudaSuccess;
-  static bool init = false;
-  if (!init) {
-    init = true;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    attr_err = cudaFuncSetAttribute(tct::split_tct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tct::L::BYTES);
-  }
+  const int num_sms = current_device_sms();
+  const cudaError_t attr_err =
+      ensure_dynamic_smem(reinterpret_cast<const void*>(tct::split_tct_kernel), tct::L::BYTES);
   if (attr_err != cudaSuccess)
     return fail(ORION_ERR_CUDA, "cudaFuncSetAttribute(split_tct): %s", cudaGetErrorString(attr_err));
   CUtensorMap mk, mv, mk16, mv16;
