@@ -240,8 +240,11 @@ orion_status orion_kv_append(const orion_attn_shape* shape, int32_t n_branches,
  * q head h:  out[b,h] = softmax(sm_scale * q[b,h] . K_ctx(b)^T) . V_ctx(b), where ctx(b) is the
  * concatenation of b's bound segments with their current (dyn) lengths; lse[b,h] = natural-log
  * sum-exp of the scaled scores.  The current token's K/V must already be appended.
- * Device; enqueues the split kernel (fp32 partials (m, l, acc) per piece chunk) and the combine
- * kernel (LSE merge in plan order, RNE to bf16) on `stream`.
+ * Device; enqueues the split kernel (partials per work item) and the combine kernel (LSE merge in
+ * plan order, RNE to bf16) on `stream`.  The default (swap-AB, head_dim 128) kernel keeps each
+ * partial as fp16 o = acc / l, a convex combination of V rows: V entries must lie within fp16
+ * range (|v| <= 65504) -- far above LLM value activations; ORION_PLAN_ROWS_ON_LANES keeps fp32
+ * partials for inputs that do not.
  *  q, out        bf16 [n_branches][Hq][d] (device).   lse  fp32 [n_branches][Hq], nullable.
  *  k_cache, v_cache, num_pages, page_table  as for orion_kv_append.
  *  own_len       device int32 [n_branches] (dyn segment lengths).

@@ -11,7 +11,9 @@
 //     the row's partial output is acc / l, its log2-sum-exp m + log2(l)
 //   fp16 (kVariantTCT):
 //     part_o fp16 [n_partials][head_dim] (= acc / l) | part_lse fp32 [n_partials] (m + log2 l)
-//     half the bytes; fp16's 2^-11 relative rounding is 4x below the bf16 rounding of out.
+//     half the bytes; fp16's 2^-11 relative rounding is 4x below the bf16 rounding of out.  o is
+//     a convex combination of V rows, so |o| <= max |V|: V entries must stay within fp16 range
+//     (|v| <= 65504; include/orion.h).
 // acc_bytes = byte offset of the second array.
 #pragma once
 #include <stdint.h>
