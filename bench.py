@@ -314,6 +314,35 @@ def run_orion(args, cfg, layers):
     ms_step = elapsed_ms / args.steps
     value = total_b / (ms_step / 1e3)
 
+    # ---- the same step captured once as a CUDA graph and replayed (SURVEY.md §8(d) protocol)
+    graph = None
+    try:
+        gs = torch.cuda.Stream(dev)
+        gs.wait_stream(stream)
+        with torch.cuda.stream(gs):
+            step()                                     # warm the capture stream
+        torch.cuda.synchronize()
+        cg = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(cg, stream=gs):
+            step()
+        for _ in range(max(3, args.warmup)):
+            cg.replay()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            cg.replay()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gms, _ = shard.reduce_timing(g0.elapsed_time(g1), 0.0, device=dev)
+        graph = {"ms_per_step": gms / args.steps, "tokens_per_s": total_b / (gms / args.steps / 1e3),
+                 "note": f"one step ({layers} layers x append/split/combine) captured once, replayed {args.steps}x"}
+        del cg
+    except Exception as exc:                             # capture unsupported here: say so
+        graph = {"unavailable": f"{type(exc).__name__}: {exc}"}
+
     # ---- end to end through the public API with host buffers (pinned), copies inside timing
     e2e = None
     if not args.no_e2e:
@@ -376,6 +405,7 @@ def run_orion(args, cfg, layers):
                  "partial_bytes_per_layer": st["workspace_bytes"] * 2,   # written by K2 + read by K3
                  "plan_build_s": plan_s},
         "step_ms": {"p10": pct(0.1), "median": pct(0.5), "p90": pct(0.9), "rank0_only": world > 1},
+        "cuda_graph": graph,
         "per_layer": {"us": ms_step / layers * 1e3, "tokens_per_s": float(B) / (ms_step / layers / 1e3)},
         "gpu_launches": args.steps * layers * 3,
         "clocks": clocks,
