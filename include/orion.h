@@ -99,6 +99,10 @@ typedef struct {
   int32_t head_dim;      /* 64 or 128 */
   int32_t page_size;     /* power of two in [16, 256] */
   float sm_scale;        /* softmax scale; <= 0 selects 1/sqrt(head_dim) (reading S16) */
+  int32_t kv_interleaved; /* 0: K and V caches are separate [num_pages][Hkv][P][d] arrays.
+                             1: one [num_pages][Hkv][2][P][d] array (K and V of a (page, kv head)
+                             adjacent: a decode tile's K and V are one 32 KB run); pass
+                             k_cache = base and v_cache = base + P*d elements */
 } orion_attn_shape;
 
 /* Per query: its points are global branches [branch0, branch0 + n_points). */

@@ -31,8 +31,8 @@ def version():
     return lib().orion_version().decode()
 
 
-def _shape(hq, hkv, d, page, sm_scale=0.0):
-    return _lib.AttnShape(hq, hkv, d, page, float(sm_scale))
+def _shape(hq, hkv, d, page, sm_scale=0.0, kv_interleaved=False):
+    return _lib.AttnShape(hq, hkv, d, page, float(sm_scale), int(bool(kv_interleaved)))
 
 
 def dag_waves(n_points, edges, policy=POLICY_ANCESTORS):
@@ -175,10 +175,10 @@ def _require_cuda(*ts):
 
 
 def kv_append(hq, hkv, d, page, k_new, v_new, k_cache, v_cache, own_pt_off, own_cap, page_table,
-              own_len, mode=APPEND_ADVANCE, stream=None):
+              own_len, mode=APPEND_ADVANCE, stream=None, kv_interleaved=False):
     """orion_kv_append on `stream` (default: torch's current stream).  All tensors on the GPU."""
     _require_cuda(k_new, v_new, k_cache, v_cache, own_pt_off, own_cap, page_table, own_len)
-    shape = _shape(hq, hkv, d, page)
+    shape = _shape(hq, hkv, d, page, 0.0, kv_interleaved)
     _lib.check(lib().orion_kv_append(ctypes.byref(shape), int(own_len.shape[0]), k_new.data_ptr(),
                                      v_new.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(),
                                      own_pt_off.data_ptr(), own_cap.data_ptr(),
@@ -187,10 +187,10 @@ def kv_append(hq, hkv, d, page, k_new, v_new, k_cache, v_cache, own_pt_off, own_
 
 
 def expand_attn(hq, hkv, d, page, q, out, lse, k_cache, v_cache, page_table, own_len, h_plan,
-                d_plan, workspace, stream=None, sm_scale=0.0):
+                d_plan, workspace, stream=None, sm_scale=0.0, kv_interleaved=False):
     """orion_expand_attn on `stream` (default: torch's current stream)."""
     _require_cuda(q, out, lse, k_cache, v_cache, page_table, own_len, d_plan, workspace)
-    shape = _shape(hq, hkv, d, page, sm_scale)
+    shape = _shape(hq, hkv, d, page, sm_scale, kv_interleaved)
     _lib.check(lib().orion_expand_attn(
         ctypes.byref(shape), int(q.shape[0]), q.data_ptr(), out.data_ptr(),
         None if lse is None else lse.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(),
@@ -200,10 +200,10 @@ def expand_attn(hq, hkv, d, page, q, out, lse, k_cache, v_cache, page_table, own
 
 
 def point_prefill_attn(hq, hkv, d, page, q, out, lse, k_cache, v_cache, page_table, own_len, h_plan,
-                       d_plan, workspace, stream=None, sm_scale=0.0):
+                       d_plan, workspace, stream=None, sm_scale=0.0, kv_interleaved=False):
     """orion_point_prefill_attn: q/out bf16 [B, Lc, Hq, d], lse fp32 [B, Lc, Hq] (nullable)."""
     _require_cuda(q, out, lse, k_cache, v_cache, page_table, own_len, d_plan, workspace)
-    shape = _shape(hq, hkv, d, page, sm_scale)
+    shape = _shape(hq, hkv, d, page, sm_scale, kv_interleaved)
     _lib.check(lib().orion_point_prefill_attn(
         ctypes.byref(shape), int(q.shape[0]), q.data_ptr(), out.data_ptr(),
         None if lse is None else lse.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(),
@@ -213,10 +213,10 @@ def point_prefill_attn(hq, hkv, d, page, q, out, lse, k_cache, v_cache, page_tab
 
 
 def expand_split(hq, hkv, d, page, q, k_cache, v_cache, page_table, own_len, h_plan, d_plan,
-                 workspace, stream=None, sm_scale=0.0):
+                 workspace, stream=None, sm_scale=0.0, kv_interleaved=False):
     """orion_expand_split: K2 only (partials into `workspace`)."""
     _require_cuda(q, k_cache, v_cache, page_table, own_len, d_plan, workspace)
-    shape = _shape(hq, hkv, d, page, sm_scale)
+    shape = _shape(hq, hkv, d, page, sm_scale, kv_interleaved)
     _lib.check(lib().orion_expand_split(
         ctypes.byref(shape), int(q.shape[0]), q.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(),
         int(k_cache.shape[0]), page_table.data_ptr(), own_len.data_ptr(), _lib.ptr(h_plan),
@@ -225,10 +225,10 @@ def expand_split(hq, hkv, d, page, q, k_cache, v_cache, page_table, own_len, h_p
 
 
 def expand_combine(hq, hkv, d, page, n_branches, out, lse, h_plan, d_plan, workspace, stream=None,
-                   sm_scale=0.0):
+                   sm_scale=0.0, kv_interleaved=False):
     """orion_expand_combine: K3 only (partials in `workspace` -> out / lse)."""
     _require_cuda(out, lse, d_plan, workspace)
-    shape = _shape(hq, hkv, d, page, sm_scale)
+    shape = _shape(hq, hkv, d, page, sm_scale, kv_interleaved)
     _lib.check(lib().orion_expand_combine(
         ctypes.byref(shape), int(n_branches), out.data_ptr(), None if lse is None else lse.data_ptr(),
         _lib.ptr(h_plan), d_plan.data_ptr(), workspace.data_ptr(),
@@ -246,10 +246,11 @@ class ExpansionBatch:
 
     def __init__(self, hq, hkv, d, page, queries, points, page_table, own_len,
                  policy=POLICY_ANCESTORS, device="cuda", chunk_tokens=0, sm_scale=0.0, flags=0,
-                 num_sms=0, prefill_rows=0):
+                 num_sms=0, prefill_rows=0, kv_interleaved=False):
         import torch
         self.hq, self.hkv, self.d, self.page = hq, hkv, d, page
         self.sm_scale = sm_scale
+        self.kv_interleaved = bool(kv_interleaved)
         qdesc, offs, refs, b0 = [], [0], [], 0
         for q in queries:
             w = dag_waves(q["n_points"], q["edges"], policy)
@@ -270,12 +271,13 @@ class ExpansionBatch:
     @classmethod
     def from_segments(cls, hq, hkv, d, page, seg_offsets, segs, own_pt_off, own_cap, page_table,
                       own_len, device="cuda", chunk_tokens=0, sm_scale=0.0, flags=0, num_sms=0,
-                      prefill_rows=0):
+                      prefill_rows=0, kv_interleaved=False):
         """A batch over already-bound segment lists (e.g. orion_select_branches' running set):
         own_pt_off / own_cap / own_len per branch of the lists."""
         self = cls.__new__(cls)
         self.hq, self.hkv, self.d, self.page = hq, hkv, d, page
         self.sm_scale = sm_scale
+        self.kv_interleaved = bool(kv_interleaved)
         self.n_branches = len(seg_offsets) - 1
         self.seg_offsets = np.ascontiguousarray(seg_offsets, np.int32)
         self.segs = segs
@@ -303,22 +305,26 @@ class ExpansionBatch:
 
     def append(self, k_new, v_new, k_cache, v_cache, mode=APPEND_ADVANCE, stream=None):
         kv_append(self.hq, self.hkv, self.d, self.page, k_new, v_new, k_cache, v_cache,
-                  self.own_pt_off, self.own_cap, self.page_table, self.own_len, mode, stream)
+                  self.own_pt_off, self.own_cap, self.page_table, self.own_len, mode, stream,
+                  self.kv_interleaved)
 
     def attend(self, q, out, k_cache, v_cache, lse=None, stream=None):
         """Decode attention (q/out [B, Hq, d]); with a prefill_rows = Lc batch, the point-prefill
         attention of the Pre stage (q/out [B, Lc, Hq, d], lse [B, Lc, Hq])."""
         f = point_prefill_attn if self.prefill_rows else expand_attn
         f(self.hq, self.hkv, self.d, self.page, q, out, lse, k_cache, v_cache, self.page_table,
-          self.own_len, self.h_plan, self.d_plan, self.workspace, stream, self.sm_scale)
+          self.own_len, self.h_plan, self.d_plan, self.workspace, stream, self.sm_scale,
+          self.kv_interleaved)
 
     def split(self, q, k_cache, v_cache, stream=None):
         expand_split(self.hq, self.hkv, self.d, self.page, q, k_cache, v_cache, self.page_table,
-                     self.own_len, self.h_plan, self.d_plan, self.workspace, stream, self.sm_scale)
+                     self.own_len, self.h_plan, self.d_plan, self.workspace, stream, self.sm_scale,
+                     self.kv_interleaved)
 
     def combine(self, out, lse=None, stream=None):
         expand_combine(self.hq, self.hkv, self.d, self.page, self.n_branches, out, lse,
-                       self.h_plan, self.d_plan, self.workspace, stream, self.sm_scale)
+                       self.h_plan, self.d_plan, self.workspace, stream, self.sm_scale,
+                       self.kv_interleaved)
 
     def step(self, q, k_new, v_new, k_cache, v_cache, out, lse=None, mode=APPEND_ADVANCE,
              stream=None):

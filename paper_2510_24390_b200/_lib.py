@@ -40,7 +40,7 @@ class Seg(ctypes.Structure):
 class AttnShape(ctypes.Structure):
     _fields_ = [("num_q_heads", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32),
                 ("head_dim", ctypes.c_int32), ("page_size", ctypes.c_int32),
-                ("sm_scale", ctypes.c_float)]
+                ("sm_scale", ctypes.c_float), ("kv_interleaved", ctypes.c_int32)]
 
 
 class QueryDesc(ctypes.Structure):

@@ -286,6 +286,8 @@ orion_status check_shape(const orion_attn_shape* s) {
     return fail(ORION_ERR_UNSUPPORTED, "head_dim %d not in {64,128}", s->head_dim);
   if (s->page_size < 16 || s->page_size > 256 || (s->page_size & (s->page_size - 1)))
     return fail(ORION_ERR_UNSUPPORTED, "page_size %d not a power of two in [16,256]", s->page_size);
+  if (s->kv_interleaved != 0 && s->kv_interleaved != 1)
+    return fail(ORION_ERR_INVALID_ARG, "kv_interleaved must be 0 or 1");
   return ORION_OK;
 }
 

@@ -104,6 +104,7 @@ struct SplitArgs {
   float* part_acc;
   float2* part_ml;
   int32_t hq, hkv, group, page_shift;
+  int32_t kvs;  // (page, kv head) block stride: 1 separate K/V caches, 2 interleaved
   float scale_log2;
 };
 
@@ -126,7 +127,7 @@ __global__ void __launch_bounds__(kThreads, 2) split_kernel(const SplitArgs a) {
   const int ntok = max(0, end - w.t0);
   const int ntiles = (ntok + kTileTokens - 1) / kTileTokens;
   const int pmask = (1 << a.page_shift) - 1;
-  const size_t head_stride = static_cast<size_t>(D) << a.page_shift;  // one (page, kv head) block
+  const size_t head_stride = (static_cast<size_t>(D) << a.page_shift) * a.kvs;  // (page, kv head) block stride
 
   // Q rows of this item -> sQ (zero rows past n_rows).
   for (int i = tid; i < kRowsPerItem * CH; i += kThreads) {
@@ -408,7 +409,7 @@ __global__ void __launch_bounds__(128) kv_append_kernel(
     __nv_bfloat16* __restrict__ k_cache, __nv_bfloat16* __restrict__ v_cache,
     const int32_t* __restrict__ own_pt_off, const int32_t* __restrict__ own_cap,
     const int32_t* __restrict__ page_table, int32_t* __restrict__ own_len, int hkv,
-    int page_shift, int mode) {
+    int page_shift, int mode, int kvs) {
   constexpr int CH = D / 8;
   __shared__ int s_pos, s_page, s_len;
   const int b = blockIdx.x;
@@ -428,7 +429,7 @@ __global__ void __launch_bounds__(128) kv_append_kernel(
   const size_t row = static_cast<size_t>(pos & ((1 << page_shift) - 1)) * D;
   for (int i = threadIdx.x; i < hkv * CH; i += blockDim.x) {
     const int g = i / CH, c = i % CH;
-    const size_t dst = ((static_cast<size_t>(page) * hkv + g) << page_shift) * D + row + c * 8;
+    const size_t dst = (((static_cast<size_t>(page) * hkv + g) * kvs) << page_shift) * D + row + c * 8;
     const size_t src = (static_cast<size_t>(b) * hkv + g) * D + c * 8;
     *reinterpret_cast<uint4*>(k_cache + dst) = *reinterpret_cast<const uint4*>(k_new + src);
     *reinterpret_cast<uint4*>(v_cache + dst) = *reinterpret_cast<const uint4*>(v_new + src);
@@ -486,7 +487,7 @@ size_t split_smem_bytes() {
 template <int D>
 orion_status launch_split(const PlanHeader* h, const char* dplan, const void* q, const void* k,
                           const void* v, int32_t num_pages, const int32_t* page_table,
-                          const int32_t* own_len, void* ws, cudaStream_t st, void* out = nullptr,
+                          const int32_t* own_len, void* ws, cudaStream_t st, int kvs, void* out = nullptr,
                           float* lse = nullptr) {
   if (h->variant == kVariantTC || h->variant == kVariantTCT) {
     TcArgs t;
@@ -507,6 +508,7 @@ orion_status launch_split(const PlanHeader* h, const char* dplan, const void* q,
     t.hkv = h->num_kv_heads;
     t.group = h->group;
     t.page_shift = log2i(h->page_size);
+    t.kvs = kvs;
     t.scale_log2 = h->sm_scale * kLog2e;
     t.lc = h->prefill_rows > 0 ? h->prefill_rows : 1;
     if (h->variant == kVariantTCT) {
@@ -533,6 +535,7 @@ orion_status launch_split(const PlanHeader* h, const char* dplan, const void* q,
   a.hkv = h->num_kv_heads;
   a.group = h->group;
   a.page_shift = log2i(h->page_size);
+  a.kvs = kvs;
   a.scale_log2 = h->sm_scale * kLog2e;
   split_kernel<D><<<h->n_items, kThreads, split_smem_bytes<D>(), st>>>(a);
   cudaError_t e = cudaGetLastError();
@@ -613,7 +616,7 @@ extern "C" orion_status orion_kv_append(const orion_attn_shape* shape, int32_t n
       shape->head_dim == 128 ? kv_append_kernel<128> : kv_append_kernel<64>, dim3(n_branches), dim3(128), 0, s,
       static_cast<const __nv_bfloat16*>(k_new), static_cast<const __nv_bfloat16*>(v_new),
       static_cast<__nv_bfloat16*>(k_cache), static_cast<__nv_bfloat16*>(v_cache), own_pt_off,
-      own_cap, page_table, own_len, shape->num_kv_heads, shift, mode);
+      own_cap, page_table, own_len, shape->num_kv_heads, shift, mode, 1 + shape->kv_interleaved);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ORION_ERR_CUDA, "kv_append_kernel: %s", cudaGetErrorString(e));
   return ORION_OK;
@@ -637,8 +640,10 @@ extern "C" orion_status orion_expand_split(const orion_attn_shape* shape, int32_
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const char* dp = static_cast<const char*>(d_plan);
   if (shape->head_dim == 128)
-    return launch_split<128>(h, dp, q, k_cache, v_cache, num_pages, page_table, own_len, workspace, s);
-  return launch_split<64>(h, dp, q, k_cache, v_cache, num_pages, page_table, own_len, workspace, s);
+    return launch_split<128>(h, dp, q, k_cache, v_cache, num_pages, page_table, own_len, workspace, s,
+                             1 + shape->kv_interleaved);
+  return launch_split<64>(h, dp, q, k_cache, v_cache, num_pages, page_table, own_len, workspace, s,
+                          1 + shape->kv_interleaved);
 }
 
 extern "C" orion_status orion_expand_combine(const orion_attn_shape* shape, int32_t n_branches,
@@ -700,8 +705,10 @@ extern "C" orion_status orion_point_prefill_attn(const orion_attn_shape* shape, 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const char* dp = static_cast<const char*>(d_plan);
   if (shape->head_dim == 128)
-    return launch_split<128>(h, dp, q, k_cache, v_cache, num_pages, page_table, own_len, workspace, s, out, lse);
-  return launch_split<64>(h, dp, q, k_cache, v_cache, num_pages, page_table, own_len, workspace, s, out, lse);
+    return launch_split<128>(h, dp, q, k_cache, v_cache, num_pages, page_table, own_len, workspace, s,
+                             1 + shape->kv_interleaved, out, lse);
+  return launch_split<64>(h, dp, q, k_cache, v_cache, num_pages, page_table, own_len, workspace, s,
+                          1 + shape->kv_interleaved, out, lse);
 }
 
 extern "C" const char* orion_version(void) {

@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             if (b < nbox) {
               const int pos = pos0 + b * step;
               const int page = __ldg(a.page_table + g.pt_off + (pos >> a.page_shift));
-              brow[b] = ((page * a.hkv + w.kv_head) << a.page_shift) + (pos & pmask);
+              brow[b] = (((page * a.hkv + w.kv_head) * a.kvs) << a.page_shift) + (pos & pmask);
             }
           }
         }
@@ -747,7 +747,7 @@ orion_status launch_split_tc(const PlanHeader* h, const TcArgs& a, const void* k
   if (attr_err != cudaSuccess)
     return fail(ORION_ERR_CUDA, "cudaFuncSetAttribute(split_tc): %s", cudaGetErrorString(attr_err));
   CUtensorMap mk, mv, mk16, mv16;
-  const int64_t rows = static_cast<int64_t>(num_pages) * h->num_kv_heads * h->page_size;
+  const int64_t rows = static_cast<int64_t>(num_pages) * h->num_kv_heads * a.kvs * h->page_size;
   const int big = std::min(tc::kTok, h->page_size);
   if (!make_map(&mk, k, D, rows, big) || !make_map(&mv, v, D, rows, big) ||
       !make_map(&mk16, k, D, rows, tc::kBox) || !make_map(&mv16, v, D, rows, tc::kBox))

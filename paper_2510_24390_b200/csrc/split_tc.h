@@ -56,6 +56,7 @@ struct TcArgs {
   __half* part_o;         // fp16 partial format (split_tct)
   float* part_lse;
   int32_t n_items, hq, hkv, group, page_shift;
+  int32_t kvs;            // (page, kv head) block stride in blocks: 1 separate K/V, 2 interleaved
   int32_t lc;             // query rows per reader and q head: 1 (decode) or Lc (point prefill)
   __nv_bfloat16* out;     // non-null: every row has exactly one partial (a point-prefill plan) and
   float* lse;             // the epilogue writes out = acc / l (bf16) and lse directly: no combine

@@ -606,7 +606,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (b < nbox) {
               const int pos = pos0 + b * step;
               const int page = __ldg(a.page_table + e.pt_off + (pos >> a.page_shift));
-              brow[b] = ((page * a.hkv + e.kv_head) << a.page_shift) + (pos & pmask);
+              brow[b] = (((page * a.hkv + e.kv_head) * a.kvs) << a.page_shift) + (pos & pmask);
             }
         }
         const int tend = min(e.ntiles, tb0 + 32);
@@ -858,7 +858,7 @@ orion_status launch_split_tct(const PlanHeader* h, const TcArgs& a, const void* 
   if (attr_err != cudaSuccess)
     return fail(ORION_ERR_CUDA, "cudaFuncSetAttribute(split_tct): %s", cudaGetErrorString(attr_err));
   CUtensorMap mk, mv, mk16, mv16;
-  const int64_t rows = static_cast<int64_t>(num_pages) * h->num_kv_heads * h->page_size;
+  const int64_t rows = static_cast<int64_t>(num_pages) * h->num_kv_heads * a.kvs * h->page_size;
   const int big = std::min(64, h->page_size);
   if (!make_map_t(&mk, k, rows, big) || !make_map_t(&mv, v, rows, big) || !make_map_t(&mk16, k, rows, tct::kBox) ||
       !make_map_t(&mv16, v, rows, tct::kBox))

@@ -16,22 +16,28 @@ def u16(t):
     return t.detach().cpu().contiguous().view(torch.int16).numpy().view(np.uint16)
 
 
-def batch_for(cfg, lay, policy=0, chunk_tokens=0, device="cuda", flags=0):
+def batch_for(cfg, lay, policy=0, chunk_tokens=0, device="cuda", flags=0, interleaved=False):
     queries = [dict(n_points=int(lay.n_points[i]), edges=lay.edges[i],
                     prefix_pt_off=int(lay.prefix_pt_off[i]), prefix_len=int(lay.prefix_len[i]))
                for i in range(lay.n_queries)]
     points = np.stack([lay.point_pt_off, lay.content_len, lay.point_cap], 1)
     return orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, lay.page_table,
                                 lay.own_len, policy=policy, device=device, chunk_tokens=chunk_tokens,
-                                flags=flags)
+                                flags=flags, kv_interleaved=interleaved)
 
 
-def run_step(cfg, lay, ten, policy=0, mode=orion.APPEND_ADVANCE, chunk_tokens=0, layer=0, flags=0):
-    """Returns dict(out, lse, k_cache, v_cache, own_len) from the GPU after one step."""
+def run_step(cfg, lay, ten, policy=0, mode=orion.APPEND_ADVANCE, chunk_tokens=0, layer=0, flags=0,
+             interleaved=False):
+    """Returns dict(out, lse, k_cache, v_cache, own_len) from the GPU after one step.  interleaved:
+    the caches live in one [pages][Hkv][2][P][d] array (K/V views of it are passed)."""
     dev = torch.device("cuda")
-    batch = batch_for(cfg, lay, policy, chunk_tokens, flags=flags)
-    kc = ten["k_cache"][layer].to(dev).contiguous()
-    vc = ten["v_cache"][layer].to(dev).contiguous()
+    batch = batch_for(cfg, lay, policy, chunk_tokens, flags=flags, interleaved=interleaved)
+    if interleaved:
+        kv = torch.stack([ten["k_cache"][layer], ten["v_cache"][layer]], dim=2).to(dev).contiguous()
+        kc, vc = kv[:, :, 0], kv[:, :, 1]
+    else:
+        kc = ten["k_cache"][layer].to(dev).contiguous()
+        vc = ten["v_cache"][layer].to(dev).contiguous()
     q = ten["q"][layer].to(dev).contiguous()
     kn = ten["k_new"][layer].to(dev).contiguous()
     vn = ten["v_new"][layer].to(dev).contiguous()
@@ -62,9 +68,9 @@ def errors(out_gpu, ref):
 
 
 def check_parity(cfg, lay, ten, policy=0, branches=None, mode=orion.APPEND_ADVANCE, chunk_tokens=0,
-                 flags=0):
+                 flags=0, interleaved=False):
     """Full GPU step vs oracle on `branches` (default all).  Asserts the gates; returns errors."""
-    res = run_step(cfg, lay, ten, policy, mode, chunk_tokens, flags=flags)
+    res = run_step(cfg, lay, ten, policy, mode, chunk_tokens, flags=flags, interleaved=interleaved)
     rewrite = mode == orion.APPEND_REWRITE
     k2, v2, own = oracle_after_append(cfg, lay, ten, rewrite=rewrite)
     assert np.array_equal(res["own_len"], own)

@@ -179,3 +179,16 @@ def test_single_token_contexts_bitwise_v():
         page = lay.page_table[lay.point_pt_off[b]]
         for h in range(cfg.hq):
             assert torch.equal(res["out"][b, h].cpu(), kc[page, h // cfg.g, 0])
+
+
+@pytest.mark.parametrize("cfgname,flags", [("c2", 0), ("c3", 0), ("c1", 0), ("c2", orion.PLAN_MMA_SYNC),
+                                           ("c2", orion.PLAN_ROWS_ON_LANES)])
+def test_interleaved_kv_layout(cfgname, flags):
+    # K and V of a (page, kv head) adjacent in one [pages][Hkv][2][P][d] array (kv_interleaved):
+    # append bit-exact into the interleaved blocks, attention within the gates, every kernel.
+    cfg = C.CONFIGS[cfgname]
+    if cfgname == "c3":
+        cfg = cfg.with_(n_queries=4)
+    lay = T.make_layout(cfg, ragged=True, extra_tokens=cfg.page)
+    ten = T.make_qkv(cfg, lay, q_scale=2.0)
+    check_parity(cfg, lay, ten, flags=flags, interleaved=True)

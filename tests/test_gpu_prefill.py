@@ -19,16 +19,21 @@ def _cuda():
         pytest.skip("no CUDA device")
 
 
-def run_prefill(cfg, lay, ten, qp, policy=0):
+def run_prefill(cfg, lay, ten, qp, policy=0, interleaved=False):
     dev = torch.device("cuda")
     queries = [dict(n_points=int(lay.n_points[i]), edges=lay.edges[i],
                     prefix_pt_off=int(lay.prefix_pt_off[i]), prefix_len=int(lay.prefix_len[i]))
                for i in range(lay.n_queries)]
     points = np.stack([lay.point_pt_off, lay.content_len, lay.point_cap], 1)
     batch = orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, lay.page_table,
-                                 lay.own_len, policy=policy, device=dev, prefill_rows=cfg.lc)
-    kc = ten["k_cache"][0].to(dev).contiguous()
-    vc = ten["v_cache"][0].to(dev).contiguous()
+                                 lay.own_len, policy=policy, device=dev, prefill_rows=cfg.lc,
+                                 kv_interleaved=interleaved)
+    if interleaved:
+        kv = torch.stack([ten["k_cache"][0], ten["v_cache"][0]], dim=2).to(dev).contiguous()
+        kc, vc = kv[:, :, 0], kv[:, :, 1]
+    else:
+        kc = ten["k_cache"][0].to(dev).contiguous()
+        vc = ten["v_cache"][0].to(dev).contiguous()
     q = qp.to(dev).contiguous()
     out = torch.empty_like(q)
     lse = torch.empty(q.shape[:3], dtype=torch.float32, device=dev)
@@ -37,8 +42,8 @@ def run_prefill(cfg, lay, ten, qp, policy=0):
     return out, lse, batch
 
 
-def check(cfg, lay, ten, qp, policy=0, branches=None):
-    out, lse, batch = run_prefill(cfg, lay, ten, qp, policy)
+def check(cfg, lay, ten, qp, policy=0, branches=None, interleaved=False):
+    out, lse, batch = run_prefill(cfg, lay, ten, qp, policy, interleaved)
     if branches is None:
         branches = list(range(lay.n_branches))
     ref, ref_lse = OP.point_prefill(lay, u16(qp), u16(ten["k_cache"][0]), u16(ten["v_cache"][0]),
@@ -138,3 +143,10 @@ def test_split_plus_combine_equals_direct_prefill():
     batch.combine(out2, lse2)
     torch.cuda.synchronize()
     assert torch.equal(out, out2) and torch.equal(lse, lse2)
+
+
+def test_prefill_interleaved_kv_layout():
+    cfg = C.CONFIGS["c1"].with_(lp=300, t=120, lc=32, page=32, d=128, hq=8, hkv=2)
+    lay = T.make_layout(cfg, ragged=True, dag_override=W.mixed8)
+    ten = T.make_qkv(cfg, lay)
+    check(cfg, lay, ten, q_pre(cfg, lay, scale=2.0), interleaved=True)
