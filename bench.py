@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--impl", default="orion", choices=["orion", "reference"])
     ap.add_argument("--policy", type=int, default=0, help="0 ANCESTORS, 1 PARENTS_EQ3")
     ap.add_argument("--chunk", type=int, default=0, help="plan chunk_tokens (0 = default)")
+    ap.add_argument("--kv-layout", default="separate", choices=["separate", "interleaved"],
+                    help="KV cache layout: separate K / V pools, or K and V of a (page, kv head) adjacent")
     ap.add_argument("--no-merge", action="store_true",
                     help="plan without multi-range item merging (ORION_PLAN_NO_MERGE), for comparison")
     ap.add_argument("--kernel", default="tc", choices=["tc", "rol", "mma"],
@@ -248,8 +250,12 @@ def run_orion(args, cfg, layers):
     lay = WT.make_layout(cfg, queries=qs, seed=shard.rank_seed(cfg.seed, rank))
     B = lay.n_branches
     P, H, Hq, D = cfg.page, cfg.hkv, cfg.hq, cfg.d
-    kc = torch.empty((layers, lay.num_pages, H, P, D), dtype=torch.bfloat16, device=dev)
-    vc = torch.empty_like(kc)
+    if args.kv_layout == "interleaved":          # one [pages][Hkv][2][P][d] pool per layer
+        kv = torch.empty((layers, lay.num_pages, H, 2, P, D), dtype=torch.bfloat16, device=dev)
+        kc, vc = kv[:, :, :, 0], kv[:, :, :, 1]
+    else:
+        kc = torch.empty((layers, lay.num_pages, H, P, D), dtype=torch.bfloat16, device=dev)
+        vc = torch.empty_like(kc)
     q = torch.empty((layers, B, Hq, D), dtype=torch.bfloat16, device=dev)
     kn = torch.empty((layers, B, H, D), dtype=torch.bfloat16, device=dev)
     vn = torch.empty_like(kn)
@@ -266,7 +272,7 @@ def run_orion(args, cfg, layers):
     t0 = time.perf_counter()
     batch = orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, lay.page_table,
                                  lay.own_len, policy=args.policy, device=dev,
-                                 chunk_tokens=args.chunk,
+                                 chunk_tokens=args.chunk, kv_interleaved=args.kv_layout == "interleaved",
                                  flags={"tc": 0, "rol": orion.PLAN_ROWS_ON_LANES,
                                         "mma": orion.PLAN_MMA_SYNC}[args.kernel]
                                        | (orion.PLAN_NO_MERGE if args.no_merge else 0))
@@ -383,6 +389,7 @@ def run_orion(args, cfg, layers):
                    "branches_per_step": int(total_b), "layers": layers,
                    "policy": "parents_eq3" if args.policy else "ancestors",
                    "append_mode": "rewrite (stationary snapshot)",
+                   "kv_layout": args.kv_layout,
                    "l2": "no flush: per-layer KV pools, step working set "
                          f"{layers * (kv_b + q_b + o_b) / 1e9:.1f} GB >> 126 MB L2",
                    "parallelism": (f"{world} GPU(s), each its own {cfg.n_queries}-query batch, no collective"
@@ -438,7 +445,7 @@ def run_contiguous(args, cfg, lay, layers, q, kc, vc, out, dev):
     points = np.stack([lay.point_pt_off, lay.content_len, lay.point_cap], 1)
     ident = np.arange(len(lay.page_table), dtype=np.int32)
     batch = orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, ident,
-                                 lay.own_len, policy=args.policy, device=dev, chunk_tokens=args.chunk)
+                                 lay.own_len, policy=args.policy, device=dev, chunk_tokens=args.chunk, kv_interleaved=args.kv_layout == "interleaved")
     stream = torch.cuda.current_stream(dev)
     for l in range(min(3, layers)):
         batch.attend(q[l], out[l], kc[l], vc[l])
@@ -479,7 +486,8 @@ def run_expansion(args, cfg, lay, layers, q, kn, vn, kc, vc, dev):
     B, lc = lay.n_branches, cfg.lc
     tokens = (np.asarray(lay.own_len) - lc).astype(np.int32)          # T - Lc per point
     ex = Expansion(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, lay.page_table, lc, tokens,
-                   policy=args.policy, device=dev, chunk_tokens=args.chunk)
+                   policy=args.policy, device=dev, chunk_tokens=args.chunk,
+                   kv_interleaved=args.kv_layout == "interleaved")
     g = torch.Generator(device=dev)
     g.manual_seed(cfg.seed * 17)
     q_pre = torch.randn((B, lc, cfg.hq, cfg.d), generator=g, device=dev).to(torch.bfloat16)
@@ -538,7 +546,7 @@ def run_point_prefill(args, cfg, lay, layers, kc, vc, dev):
     points = np.stack([lay.point_pt_off, lay.content_len, lay.point_cap], 1)
     lc = cfg.lc
     batch = orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, lay.page_table,
-                                 lay.own_len, policy=args.policy, device=dev, prefill_rows=lc)
+                                 lay.own_len, policy=args.policy, device=dev, prefill_rows=lc, kv_interleaved=args.kv_layout == "interleaved")
     g = torch.Generator(device=dev)
     g.manual_seed(cfg.seed * 13)
     B = lay.n_branches
@@ -634,7 +642,7 @@ def run_costream(args, cfg, lay, layers, q, kn, vn, out, kc, vc, dev, expansion_
     for cap in [int(c) for c in args.prefill_caps.split(",") if c]:
         batch = orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, lay.page_table,
                                      lay.own_len, policy=args.policy, device=dev,
-                                     chunk_tokens=args.chunk, num_sms=cap)
+                                     chunk_tokens=args.chunk, num_sms=cap, kv_interleaved=args.kv_layout == "interleaved")
 
         def step():
             for l in range(layers):
@@ -686,7 +694,7 @@ def run_costream(args, cfg, lay, layers, q, kn, vn, out, kc, vc, dev, expansion_
             es, ps = part.first, part.second
             batch = orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points,
                                          lay.page_table, lay.own_len, policy=args.policy, device=dev,
-                                         chunk_tokens=args.chunk, num_sms=part.sms[0])
+                                         chunk_tokens=args.chunk, num_sms=part.sms[0], kv_interleaved=args.kv_layout == "interleaved")
 
             def gstep():
                 for l in range(layers):

@@ -24,11 +24,12 @@ class Expansion:
     content length lc and generates tokens[b] decode tokens (T_b - lc)."""
 
     def __init__(self, hq, hkv, d, page, queries, points, page_table, lc, tokens,
-                 policy=POLICY_ANCESTORS, device="cuda", chunk_tokens=0):
+                 policy=POLICY_ANCESTORS, device="cuda", chunk_tokens=0, kv_interleaved=False):
         import torch
         self.hq, self.hkv, self.d, self.page, self.lc = hq, hkv, d, page, lc
         self.device = torch.device(device)
         self.chunk_tokens = chunk_tokens
+        self.kv_interleaved = kv_interleaved
         qdesc, offs, refs, eoffs, edges, b0 = [], [0], [], [0], [], 0
         for q in queries:
             w = dag_waves(q["n_points"], q["edges"], policy)
@@ -72,7 +73,7 @@ class Expansion:
         return ExpansionBatch.from_segments(self.hq, self.hkv, self.d, self.page, so, sg, pts[:, 0],
                                             pts[:, 2], self.page_table, self.own_len[sel],
                                             device=self.device, chunk_tokens=self.chunk_tokens,
-                                            prefill_rows=prefill_rows)
+                                            prefill_rows=prefill_rows, kv_interleaved=self.kv_interleaved)
 
     # -- the two kinds of work of a round ------------------------------------------------------
     def prefill(self, pre, q_pre, k_caches, v_caches, out, stream=None):

@@ -37,9 +37,11 @@ __global__ void __launch_bounds__(64, 1) stream(const __grid_constant__ CUtensor
       const int s = i % stages;
       wait(empty + s, ((i / stages) & 1) ^ 1);
       asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(smem_u32(full + s)), "r"(32768));
-      const CUtensorMap* m = (two && (i & 1)) ? &tb : &ta;
+      const CUtensorMap* m = (two == 1 && (i & 1)) ? &tb : &ta;
       for (int b = 0; b < 4; ++b) {
-        const int blk = ord[2 * i + (b >> 1)];
+        // two == 2: one 32 KB run (two consecutive 64-row blocks) per stage, e.g. K and V of one
+        // (page, kv head) interleaved; otherwise two independent 16 KB blocks
+        const int blk = two == 2 ? (ord[2 * i] & ~1) + (b >> 1) : ord[2 * i + (b >> 1)];
         asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
                      ::"r"(smem_u32(sm + s * 32768 + b * 8192)), "l"((uint64_t)m), "r"((b & 1) * 64), "r"(blk * 64), "r"(smem_u32(full + s)) : "memory");
       }
@@ -87,7 +89,7 @@ int main() {
   for (int stages : {2, 3, 4, 5, 6}) {
     const int smem = stages * 32768 + 1024;
     cudaFuncSetAttribute(stream, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    for (int two = 0; two < 2; ++two)
+    for (int two = 0; two < 3; ++two)
       for (int r = 0; r < 2; ++r) {
         const int* o = r ? drnd : dseq;
         stream<<<148, 64, smem>>>(ta, tb, o, 64, stages, two);
@@ -98,7 +100,7 @@ int main() {
         float ms; cudaEventElapsedTime(&ms, e0, e1);
         const double bytes = 148.0 * per_cta * 16384;
         printf("stages=%d (%3d KB in flight) %s %s: %.0f GB/s (%s)\n", stages, stages * 32, r ? "random" : "seq   ",
-               two ? "K/V alternating" : "one tensor     ", bytes / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
+               two == 2 ? "32 KB runs      " : two ? "K/V alternating" : "one tensor     ", bytes / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
       }
   }
   return 0;
