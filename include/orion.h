@@ -346,6 +346,42 @@ orion_status orion_select_branches(int32_t n_branches, const int32_t* seg_offset
                                    const int32_t* sel, int32_t* sel_offsets, orion_seg* sel_segs,
                                    int32_t segs_cap, int32_t* segs_needed);
 
+/*
+ * Decoder-layer steps around the attention (oracle O7; reading M1: bf16
+ * storage, fp32 arithmetic).  Device; enqueued on `stream`.  The GEMMs between them are plain
+ * library calls by the caller.
+ *
+ * orion_rmsnorm — per row: r = bf16(a + b) (b nullable: r = a); residual_out = r (nullable);
+ *   out = bf16(r * rsqrt(mean(r^2) + eps) * weight) (nullable; needs weight).
+ *   a, b, out, residual_out  bf16 [n_rows][hidden];  weight bf16 [hidden]; hidden a multiple of 8,
+ *   <= 8192; all 16-byte aligned.  Errors: INVALID_ARG, UNSUPPORTED, CUDA.
+ */
+orion_status orion_rmsnorm(int32_t n_rows, int32_t hidden, const void* a, const void* b,
+                           const void* weight, float eps, void* out, void* residual_out, void* stream);
+
+/*
+ * orion_rope_append — RoPE fused into the KV append of the decode step.  Per branch b the qkv row
+ * [q (Hq*d) | k (Hkv*d) | v (Hkv*d)] (bf16, the QKV GEMM output) is split; q and k are rotated
+ * at position pos = pos_base[b] + slot (rotate_half pairs (i, i + d/2), inv_freq_i =
+ * rope_theta^(-2i/d); slot = own_len[b] for ADVANCE, own_len[b] - 1 for REWRITE, as in
+ * orion_kv_append); q goes to q_out bf16 [n_branches][Hq][d], k and v to the slot of b's own run
+ * in the paged caches (skipped when the slot is outside [0, own_cap)); ADVANCE then increments
+ * own_len.  pos_base[b] = the number of context tokens before b's own run (reading M2: a token's
+ * position is its index in its branch's concatenated context).  shape->kv_interleaved as for the
+ * attention calls.  Errors: INVALID_ARG, UNSUPPORTED, CUDA.
+ */
+orion_status orion_rope_append(const orion_attn_shape* shape, int32_t n_branches, const void* qkv,
+                               void* q_out, void* k_cache, void* v_cache, const int32_t* own_pt_off,
+                               const int32_t* own_cap, const int32_t* page_table, int32_t* own_len,
+                               const int32_t* pos_base, float rope_theta, int32_t mode, void* stream);
+
+/*
+ * orion_silu_mul — out = bf16(SiLU(g) * u) per row of gate_up = [g (inter) | u (inter)] (the fused
+ * gate/up GEMM output), SiLU(g) = g / (1 + e^-g).  bf16, inter a multiple of 8, 16-byte aligned.
+ */
+orion_status orion_silu_mul(int32_t n_rows, int32_t inter, const void* gate_up, void* out,
+                            void* stream);
+
 /* Thread-local message describing the last non-OK status returned on this thread. */
 const char* orion_last_error(void);
 

@@ -235,6 +235,21 @@ def expand_combine(hq, hkv, d, page, n_branches, out, lse, h_plan, d_plan, works
         workspace.numel() * workspace.element_size(), _stream_ptr(stream)))
 
 
+def rmsnorm(a, weight, out=None, b=None, residual_out=None, eps=1e-5, stream=None):
+    """orion_rmsnorm: r = a (+ b), residual_out = r, out = r * rsqrt(mean(r^2) + eps) * weight."""
+    _require_cuda(a, b, weight, out, residual_out)
+    p = lambda t: None if t is None else t.data_ptr()
+    _lib.check(lib().orion_rmsnorm(int(a.shape[0]), int(a.shape[-1]), a.data_ptr(), p(b), p(weight),
+                                   float(eps), p(out), p(residual_out), _stream_ptr(stream)))
+
+
+def silu_mul(gate_up, out, stream=None):
+    """orion_silu_mul: out = SiLU(gate) * up for gate_up = [gate | up] per row."""
+    _require_cuda(gate_up, out)
+    _lib.check(lib().orion_silu_mul(int(gate_up.shape[0]), int(out.shape[-1]), gate_up.data_ptr(),
+                                    out.data_ptr(), _stream_ptr(stream)))
+
+
 class ExpansionBatch:
     """The in-flight set of one GPU: several queries, each a point DAG whose points all decode.
 
@@ -302,6 +317,30 @@ class ExpansionBatch:
         self.own_pt_off = torch.from_numpy(np.ascontiguousarray(own_pt_off, np.int32)).to(dev)
         self.own_cap = torch.from_numpy(np.ascontiguousarray(own_cap, np.int32)).to(dev)
         self.own_len = torch.from_numpy(own.copy()).to(dev)
+
+    def pos_base(self):
+        """Per branch, the number of context tokens before its own run (its lists' segments other
+        than the last, OWN, at the current lengths): the RoPE position of its token at own slot s
+        is pos_base + s (reading M2)."""
+        own = self.own_len.cpu().numpy()
+        ln = self.segs["len"].astype(np.int64)
+        dyn = self.segs["dyn"]
+        m = dyn >= 0
+        ln[m] = np.clip(own[dyn[m]] - self.segs["start"][m], 0, ln[m])
+        so = self.seg_offsets
+        return np.array([int(ln[so[b]:so[b + 1] - 1].sum()) for b in range(self.n_branches)], np.int32)
+
+    def rope_append(self, qkv, q_out, k_cache, v_cache, pos_base, rope_theta=500000.0,
+                    mode=APPEND_ADVANCE, stream=None):
+        """orion_rope_append: rotate q / k of the QKV GEMM output at pos_base + slot, write q,
+        append k / v to the branches' own runs.  pos_base: device int32 [n_branches]."""
+        _require_cuda(qkv, q_out, k_cache, v_cache, pos_base)
+        shape = _shape(self.hq, self.hkv, self.d, self.page, self.sm_scale, self.kv_interleaved)
+        _lib.check(lib().orion_rope_append(
+            ctypes.byref(shape), self.n_branches, qkv.data_ptr(), q_out.data_ptr(), k_cache.data_ptr(),
+            v_cache.data_ptr(), self.own_pt_off.data_ptr(), self.own_cap.data_ptr(),
+            self.page_table.data_ptr(), self.own_len.data_ptr(), pos_base.data_ptr(),
+            float(rope_theta), int(mode), _stream_ptr(stream)))
 
     def append(self, k_new, v_new, k_cache, v_cache, mode=APPEND_ADVANCE, stream=None):
         kv_append(self.hq, self.hkv, self.d, self.page, k_new, v_new, k_cache, v_cache,

@@ -12,6 +12,7 @@
 namespace orion {
 
 orion_status fail(orion_status code, const char* fmt, ...);
+orion_status check_shape_public(const orion_attn_shape* s);
 
 // Per-device launch setup, thread-safe: the SM count of the current device, and the opt-in
 // dynamic shared-memory size of `func` on it (set once per (device, function); the attribute is

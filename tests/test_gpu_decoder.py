@@ -1,0 +1,154 @@
+"""GPU parity of the decoder-layer path against oracle O7: each orion
+kernel at its bf16 interface (RMSNorm with the fused residual add, RoPE fused into the append,
+SiLU * up), then whole multi-layer steps of the model over a DAG batch, caches included.
+
+Tolerance (reading M1): the GPU accumulates in fp32 where O7 uses fp64 and both round to bf16 at
+the same interfaces, so a single op's output differs by at most a few bf16 ulps (2^-8 relative).
+Through a layer those flips feed later ops; over two layers of this small model we gate the
+residual stream at max-abs 5e-2 and rel-L2 1e-2, and the appended K / V at 2 ulps."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2510_24390_b200 as orion
+from paper_2510_24390_b200.model import DecoderModel
+from oracle import decoder as DE, step as OS
+from workloads import configs as C, tensors as T, dags as W
+from tests.gpu_helpers import u16, batch_for
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def f64(t):
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+def ulps(a, b):
+    """Max distance in bf16 ulps of the larger magnitude."""
+    scale = np.maximum(np.abs(a), np.abs(b))
+    ulp = np.where(scale > 0, 2.0 ** (np.floor(np.log2(np.maximum(scale, 1e-30))) - 7), 2.0 ** -133)
+    return float(np.max(np.abs(a - b) / ulp))
+
+
+@pytest.mark.parametrize("hidden,fused", [(256, False), (4096, True), (1000, True)])
+def test_rmsnorm_kernel(hidden, fused):
+    rng = np.random.default_rng(hidden)
+    n = 37
+    a = DE.bf16(rng.standard_normal((n, hidden)) * 3)
+    b = DE.bf16(rng.standard_normal((n, hidden)))
+    w = DE.bf16(1 + 0.1 * rng.standard_normal(hidden))
+    dev = torch.device("cuda")
+    ta, tb, tw = (torch.from_numpy(x).to(torch.bfloat16).to(dev) for x in (a, b, w))
+    out = torch.empty_like(ta)
+    res = torch.empty_like(ta)
+    orion.rmsnorm(ta, tw, out=out, b=tb if fused else None, residual_out=res)
+    torch.cuda.synchronize()
+    r = DE.bf16(a + b) if fused else a
+    assert np.array_equal(f64(res), r)
+    assert ulps(f64(out), DE.bf16(DE.rmsnorm(r, w))) <= 1.0
+
+
+def test_silu_mul_kernel():
+    rng = np.random.default_rng(5)
+    n, inter = 19, 1792
+    gu = DE.bf16(rng.standard_normal((n, 2 * inter)) * 2)
+    dev = torch.device("cuda")
+    t = torch.from_numpy(gu).to(torch.bfloat16).to(dev)
+    out = torch.empty((n, inter), dtype=torch.bfloat16, device=dev)
+    orion.silu_mul(t, out)
+    torch.cuda.synchronize()
+    ref = DE.bf16(DE.silu(gu[:, :inter]) * gu[:, inter:])
+    assert ulps(f64(out), ref) <= 1.0
+
+
+def rope_close(got, ref, x_mag, pos_max):
+    """Small positions: within 2 bf16 ulps.  Large ones: the angle pos * inv_freq is formed in fp32
+    (as in the HF reference), |d angle| <= (pos + 1) * 2^-22, so |d out| <= that * |x| + 2 ulps."""
+    if pos_max < 64:
+        return ulps(got, ref) <= 2.0
+    bound = 2 * 2.0 ** (np.floor(np.log2(np.maximum(np.abs(ref), 1e-30))) - 7) + (pos_max + 1) * 2.0 ** -22 * 2 * x_mag
+    return bool(np.all(np.abs(got - ref) <= bound))
+
+
+@pytest.mark.parametrize("mode", [orion.APPEND_ADVANCE, orion.APPEND_REWRITE])
+@pytest.mark.parametrize("d,pos_hi", [(64, 5000), (128, 5000), (128, 8)])
+def test_rope_append_kernel(mode, d, pos_hi):
+    cfg = C.CONFIGS["c1"].with_(hq=8, hkv=2, d=d, page=16, lp=50, t=40, lc=8)
+    lay = T.make_layout(cfg, ragged=True, extra_tokens=16, dag_override=W.mixed8)
+    ten = T.make_qkv(cfg, lay)
+    dev = torch.device("cuda")
+    batch = batch_for(cfg, lay)
+    rng = np.random.default_rng(d)
+    B = lay.n_branches
+    qkv = DE.bf16(rng.standard_normal((B, (cfg.hq + 2 * cfg.hkv) * d)))
+    pos_base = rng.integers(0, pos_hi, B).astype(np.int32)
+    kc = ten["k_cache"][0].to(dev).contiguous()
+    vc = ten["v_cache"][0].to(dev).contiguous()
+    q = torch.empty((B, cfg.hq, d), dtype=torch.bfloat16, device=dev)
+    batch.rope_append(torch.from_numpy(qkv).to(torch.bfloat16).to(dev), q, kc, vc,
+                      torch.from_numpy(pos_base).to(dev), 500000.0, mode)
+    torch.cuda.synchronize()
+    slot = lay.own_len - (1 if mode == orion.APPEND_REWRITE else 0)
+    pos = pos_base + slot
+    qr = DE.bf16(DE.rope(qkv[:, :cfg.hq * d].reshape(B, cfg.hq, d), pos))
+    kr = DE.bf16(DE.rope(qkv[:, cfg.hq * d:(cfg.hq + cfg.hkv) * d].reshape(B, cfg.hkv, d), pos))
+    vr = qkv[:, (cfg.hq + cfg.hkv) * d:].reshape(B, cfg.hkv, d)
+    xm = float(np.abs(qkv).max())
+    pmax = int(pos.max()) if pos_hi > 8 else 0
+    assert rope_close(f64(q), qr, xm, pmax)
+    kcn, vcn = f64(kc), f64(vc)
+    for b in range(B):
+        pg = lay.page_table[lay.point_pt_off[b] + slot[b] // cfg.page]
+        assert rope_close(kcn[pg, :, slot[b] % cfg.page], kr[b], xm, pmax)
+        assert np.array_equal(vcn[pg, :, slot[b] % cfg.page], vr[b])
+    want_len = lay.own_len + (1 if mode == orion.APPEND_ADVANCE else 0)
+    assert np.array_equal(batch.own_len.cpu().numpy(), want_len)
+
+
+@pytest.mark.parametrize("d,dagf", [(128, W.mixed8), (64, W.diamond)])
+def test_model_steps_match_oracle(d, dagf):
+    hidden, hq, hkv, inter, L = 256, 8, 2, 384, 2
+    cfg = C.CONFIGS["c1"].with_(hq=hq, hkv=hkv, d=d, page=16, lp=60, t=30, lc=8)
+    lay = T.make_layout(cfg, ragged=True, extra_tokens=32, dag_override=dagf)
+    ten = T.make_qkv(cfg, lay, layers=L)
+    dev = torch.device("cuda")
+    model = DecoderModel(L, hidden, hq, hkv, d, inter, device=dev, seed=3)
+    batch = batch_for(cfg, lay)
+    pos_base = batch.pos_base()
+    kcs = [ten["k_cache"][l].to(dev).contiguous() for l in range(L)]
+    vcs = [ten["v_cache"][l].to(dev).contiguous() for l in range(L)]
+    B = lay.n_branches
+    rng = np.random.default_rng(7)
+    x0 = DE.bf16(rng.standard_normal((B, hidden)))
+    buf = model.buffers(B, dev)
+    y = model.step(torch.from_numpy(x0).to(torch.bfloat16).to(dev), batch, kcs, vcs,
+                   torch.from_numpy(pos_base).to(dev), buf)
+    torch.cuda.synchronize()
+    # oracle: O7 layer by layer on its own cache copies, every layer appending at the same slot
+    own = lay.own_len.copy()
+    bound = OS.bound_segments(lay, own_len=own + 1)
+    x = x0
+    kref = [u16(ten["k_cache"][l]) for l in range(L)]
+    vref = [u16(ten["v_cache"][l]) for l in range(L)]
+    for l, lw in enumerate(model.layers):
+        w = {k: f64(v) for k, v in lw.items()}
+        w = dict(w_in=w["w_in"], w_qkv=w["w_qkv"], w_o=w["w_o"], w_post=w["w_post"],
+                 w_gate=w["w_gu"][:, :inter], w_up=w["w_gu"][:, inter:], w_down=w["w_down"])
+        x, kref[l], vref[l] = DE.decoder_layer(x, w, kref[l], vref[l], lay, bound, own, pos_base + own, hq, hkv)
+    got = f64(y)
+    err = np.abs(got - x)
+    assert np.isfinite(got).all()
+    assert err.max() <= 5e-2 and np.linalg.norm(got - x) / np.linalg.norm(x) <= 1e-2, (err.max(),)
+    for l in range(L):
+        for b in range(B):
+            pg = lay.page_table[lay.point_pt_off[b] + own[b] // cfg.page]
+            k_gpu = f64(kcs[l][pg, :, own[b] % cfg.page])
+            k_or = DE.bf16_to_f64(kref[l][pg, :, own[b] % cfg.page])
+            assert np.abs(k_gpu - k_or).max() <= 4 * 2.0 ** -8 * max(1.0, np.abs(k_or).max())
+    assert np.array_equal(batch.own_len.cpu().numpy(), own + 1)
