@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-model", action="store_true",
+                    help="skip the whole-model step (random Llama-3-8B-shaped layers, SURVEY.md §8(f) rank 4)")
     ap.add_argument("--no-expansion", action="store_true",
                     help="skip the whole-expansion run (Alg. 1 l.9-22 driver, SURVEY.md §8(f) rank 2)")
     ap.add_argument("--no-point-prefill", action="store_true",
@@ -420,6 +422,8 @@ def run_orion(args, cfg, layers):
     }
     if world == 1:
         line["contiguous_pages"] = run_contiguous(args, cfg, lay, layers, q, kc, vc, out, dev)
+    if world == 1 and not args.no_model:
+        line["model_step"] = run_model_step(args, cfg, lay, layers, kc, vc, dev, value)
     if world == 1 and not args.no_expansion:
         line["expansion_run"] = run_expansion(args, cfg, lay, layers, q, kn, vn, kc, vc, dev)
     if world == 1 and not args.no_point_prefill:
@@ -468,6 +472,55 @@ def run_contiguous(args, cfg, lay, layers, q, kc, vc, out, dev):
     return {"note": "attention only (split + combine per layer, no append), contiguous page runs",
             "tokens_per_s": lay.n_branches / (ms / 1e3), "ms_per_step": ms,
             "split_ms_per_launch": split_ms, "split_gbs": (kv_b + q_b) / (split_ms / 1e3) / 1e9}
+
+
+def run_model_step(args, cfg, lay, layers, kc, vc, dev, attention_only):
+    """§8(f) rank 4: the whole-model expansion step -- every branch generates one token through
+    `layers` Llama-3-8B-shaped decoder layers with random weights (hidden 4096, 32 / 8 heads of 128,
+    SwiGLU 14336): per layer RMSNorm, QKV GEMM, RoPE fused into the KV append, the expansion
+    attention, O GEMM, RMSNorm, gate|up GEMM, SiLU*up, down GEMM (GEMMs: cuBLAS; the rest: orion
+    kernels).  The paper's metric is exactly this: generated tokens / s.  The KV
+    slot is rewritten (REWRITE) so the snapshot stays stationary across steps."""
+    import torch
+    import paper_2510_24390_b200 as orion
+    from paper_2510_24390_b200.model import DecoderModel
+    hidden, inter = 4096, 14336
+    model = DecoderModel(layers, hidden, cfg.hq, cfg.hkv, cfg.d, inter, device=dev, seed=11, init_scale=0.5)
+    queries = [dict(n_points=int(lay.n_points[i]), edges=lay.edges[i],
+                    prefix_pt_off=int(lay.prefix_pt_off[i]), prefix_len=int(lay.prefix_len[i]))
+               for i in range(lay.n_queries)]
+    points = np.stack([lay.point_pt_off, lay.content_len, lay.point_cap], 1)
+    batch = orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, lay.page_table,
+                                 lay.own_len, policy=args.policy, device=dev, chunk_tokens=args.chunk,
+                                 kv_interleaved=args.kv_layout == "interleaved")
+    B = lay.n_branches
+    pos_base = torch.from_numpy(batch.pos_base()).to(dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(cfg.seed * 19)
+    x = torch.randn((B, hidden), generator=g, device=dev).to(torch.bfloat16)
+    buf = model.buffers(B, dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(2):
+        y = model.step(x, batch, kc[:layers], vc[:layers], pos_base, buf, first_mode=orion.APPEND_REWRITE)
+    torch.cuda.synchronize()
+    n = max(3, min(args.steps, 10))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(n):
+        y = model.step(x, batch, kc[:layers], vc[:layers], pos_base, buf, first_mode=orion.APPEND_REWRITE)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / n
+    finite = bool(torch.isfinite(y.float()).all().item())
+    gemm_flop = model.flops_per_token() * B
+    return {"workload": f"{cfg.name}: {B} branches x {layers} decoder layers (hidden {hidden}, "
+                        f"{cfg.hq}/{cfg.hkv} heads of {cfg.d}, SwiGLU {inter}), random weights",
+            "metric": "generated tokens/sec (whole model)", "value": B / (ms / 1e3), "unit": "tokens/s",
+            "ms_per_step": ms, "steps": n, "weights_gb": model.weight_bytes() / 1e9,
+            "gemm_tflop_per_step": gemm_flop / 1e12,
+            "attention_only_tok_s": attention_only,
+            "attention_share_est": (B / attention_only) / (ms / 1e3) if attention_only else None,
+            "output_finite": finite}
 
 
 def run_expansion(args, cfg, lay, layers, q, kn, vn, kc, vc, dev):
