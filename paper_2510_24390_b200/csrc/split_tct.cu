@@ -70,7 +70,8 @@ struct L {
   static constexpr int OFF_M = OFF_P + 2 * PB;      // running max m: [wg 2][32]
   static constexpr int OFF_SH = OFF_M + 2 * 32 * 4; // growth-path shifts: [wg 2][32]
   static constexpr int OFF_RED = OFF_SH + 2 * 32 * 4;  // growth-path column max scratch: [wg 2][4 warps][32]
-  static constexpr int OFF_SCHED = OFF_RED + 2 * 4 * 32 * 4;  // item schedule ring: 8 x 64 B
+  static constexpr int OFF_LI = OFF_RED + 2 * 4 * 32 * 4;  // 1 / l of the pending item: [wg 2][32]
+  static constexpr int OFF_SCHED = OFF_LI + 2 * 32 * 4;    // item schedule ring: 8 x 64 B
   static constexpr int OFF_MI = OFF_SCHED + 8 * 64;        // MMA warp's entry geometry: 8 x 32 B
   static constexpr int OFF_BAR = OFF_MI + 8 * 32;
   static constexpr int N_BAR = 2 * kSK + 2 * kSV + 3 + 3 + 2 + 2 + 2 + 2 + 2 + 2 + 2 * 8;
@@ -137,6 +138,7 @@ __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
 }
 #ifdef ORION_TC_TRACE
 #define TRACE_DECL unsigned long long tr_[12] = {0}; const unsigned long long tr_t0 = clock64();
+#define TRP tr_
 #define TW(slot, stmt) do { const unsigned long long t_ = clock64(); stmt; tr_[slot] += clock64() - t_; } while (0)
 #define TRACE_DUMP(role) do { if (blockIdx.x < 2 && (threadIdx.x & 31) == 0) printf( \
     "TRACE blk %d warp %2d %-8s tot %llu | %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu\n", blockIdx.x, \
@@ -144,8 +146,14 @@ __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
     tr_[8], tr_[9]); } while (0)
 #else
 #define TRACE_DECL
+#define TRP nullptr
 #define TW(slot, stmt) stmt
 #define TRACE_DUMP(role) do {} while (0)
+#endif
+#ifdef ORION_TC_TRACE
+#define STW(slot, stmt) do { const unsigned long long t_ = clock64(); stmt; trp[slot] += clock64() - t_; } while (0)
+#else
+#define STW(slot, stmt) stmt
 #endif
 
 __device__ __forceinline__ bool elect_one() {
@@ -254,7 +262,8 @@ __device__ __forceinline__ void softmax_tile(uint32_t tmem, uint32_t lane_base, 
                                              uint8_t* pbuf, int c0, int tb, int lo, int hi, float* mrow,
                                              float* shs, float* red, bool had, uint32_t ocol, float (&ls)[NH],
                                              float scale_log2, uint64_t* sfree, bool need_pv, uint64_t* pv_free,
-                                             uint32_t pv_free_par, uint64_t* pv_prev, uint32_t pv_prev_par) {
+                                             uint32_t pv_free_par, uint64_t* pv_prev, uint32_t pv_prev_par,
+                                             unsigned long long* trp) {
   uint32_t s[NH];
   if constexpr (NH == 8) tmem_ld32x8(tmem + lane_base + scol, s);
   if constexpr (NH == 16) tmem_ld32x16(tmem + lane_base + scol, s);
@@ -325,7 +334,7 @@ __device__ __forceinline__ void softmax_tile(uint32_t tmem, uint32_t lane_base, 
     ls[c] += __uint_as_float(pk[c / 2] << 16);       // row sums of exactly the bf16 P fed to PV
     ls[c + 1] += __uint_as_float(pk[c / 2] & 0xFFFF0000u);
   }
-  if (need_pv) mbar_wait(pv_free, pv_free_par);
+  if (need_pv) STW(6, mbar_wait(pv_free, pv_free_par));
 #pragma unroll
   for (int cc = 0; cc < NH / 8; ++cc) {
     const int chunk = (c0 >> 3) + cc;
@@ -377,13 +386,45 @@ __device__ __forceinline__ Bars carve_bars(uint8_t* smem) {
   return r;
 }
 
+// A finished item whose O^T readout is deferred: its last PV completes while the next item's first
+// tile is processed (O^T is double-buffered by item parity; the MMA reuses this buffer only after
+// o_free).  Its lse is already written and its 1 / l per column sits in the warpgroup's `linv`.
+struct Pend {
+  int32_t valid, slot0, n_rows, nh, kp, item;
+};
+
+// The deferred part of an item's epilogue: fp16 o = acc / l from O^T (plan_format.h), then
+// o_free.  Runs after the next item's first tile (or at the very end).  linv was written before a
+// warpgroup barrier (the next item's start) and is rewritten only after the next item's
+// end-of-item barrier, which every thread reaches after this readout: no barrier needed here.
+__device__ __forceinline__ void finish_item(const Pend& pd, uint32_t tmem, uint32_t lane_base, int p, int t,
+                                            const float* linv, const Bars& B, const TcArgs& a,
+                                            unsigned long long* trp) {
+  const int c0 = p * pd.nh;
+  STW(5, mbar_wait(B.acc_full + pd.kp, (static_cast<uint32_t>(pd.item) >> 1) & 1));
+  tc_fence_after();
+  __half* dst = a.part_o + static_cast<size_t>(pd.slot0) * D + t;
+  for (int cb = 0; cb < pd.nh; cb += 8) {
+    uint32_t o[8];
+    tmem_ld32x8(tmem + lane_base + colO(pd.kp) + c0 + cb, o);
+    tc_wait_ld();
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (c0 + cb + c < pd.n_rows)
+        dst[static_cast<size_t>(c0 + cb + c) * D] = __float2half_rn(__uint_as_float(o[c]) * linv[cb + c]);
+  }
+  tc_fence_before();
+  mbar_arrive(B.o_free + pd.kp);
+}
+
 // All tiles of one item for one softmax warpgroup (query columns [p*NH, (p+1)*NH)), then its
 // share of the item's partial: acc from O^T, m from mrow, l from the per-thread row sums reduced
 // over the 128 token rows.
 template <int NH>
 __device__ __forceinline__ void softmax_item(uint8_t* smem, uint32_t tmem, uint32_t lane_base, int p, int t,
                                              const Sched& e, uint32_t& k, uint32_t& j, float* mrow, float* shs,
-                                             float* red, const Bars& B, const TcArgs& a, const Sched* ring) {
+                                             float* red, float* linv, const Bars& B, const TcArgs& a,
+                                             const Sched* ring, Pend& pend, unsigned long long* trp) {
   // `e` is the item's first ring entry (k); its further ranges are the next entries, read here.
   const int c0 = p * NH;
   const uint32_t kp = static_cast<uint32_t>(e.item) & 1;
@@ -403,17 +444,31 @@ __device__ __forceinline__ void softmax_item(uint8_t* smem, uint32_t tmem, uint3
     const int tb = cur.base + t_in * kTok;
     const int lo = max(tb, cur.t0), hi = min(tb + kTok, cur.end);
     const uint32_t b = j % kSB;
-    mbar_wait(B.s_full + b, (j / kSB) & 1);
+    STW(1, mbar_wait(B.s_full + b, (j / kSB) & 1));
     tc_fence_after();
+#ifdef ORION_TC_TRACE
+    const unsigned long long ts_ = clock64();
+#endif
     uint8_t* pbuf = smem + L::OFF_P + (j & 1) * L::PB;
     const bool need_pv = j >= 2;                    // P^T[j & 1] still feeds PV(j-2)
     softmax_tile<NH>(tmem, lane_base, p, t, colS(b) + c0, pbuf, c0, tb, lo, hi, mrow, shs, red, tt > 0,
                      colO(kp) + c0, ls, a.scale_log2, B.s_free + b, need_pv, B.pv_done + (j & 1),
-                     ((j - 2) >> 1) & 1, B.pv_done + ((j - 1) & 1), ((j - 1) >> 1) & 1);
+                     ((j - 2) >> 1) & 1, B.pv_done + ((j - 1) & 1), ((j - 1) >> 1) & 1, trp);
     fence_proxy_async();
     tc_fence_before();
     mbar_arrive(B.p_full + (j & 1));
+#ifdef ORION_TC_TRACE
+    trp[2] += clock64() - ts_;
+    trp[0] += 1;
+#endif
+    if (tt == 0 && pend.valid) {                    // the previous item's deferred readout
+      finish_item(pend, tmem, lane_base, p, t, linv, B, a, trp);
+      pend.valid = 0;
+    }
   }
+#ifdef ORION_TC_TRACE
+  const unsigned long long te_ = clock64();
+#endif
   // ---- epilogue.  l: butterfly over the warp (plain levels while more lanes than columns, then a
   // reduce-scatter leaving column ln % NH in lane ln), then across the 4 warps via red.
   const int ln = t & 31, wq = t >> 5;
@@ -432,30 +487,22 @@ __device__ __forceinline__ void softmax_item(uint8_t* smem, uint32_t tmem, uint3
     }
   }
   if (ln < NH) red[wq * 32 + ln] = ls[0];
-  mbar_wait(B.acc_full + kp, (static_cast<uint32_t>(e.item) >> 1) & 1);
-  tc_fence_after();
   wg_sync(2 + p, 128);
   // fp16 partial format (plan_format.h): o = acc / l, lse2 = m + log2 l.  l >= 1: the column max
-  // that set the reference contributes 2^0 (every item has at least one valid token).
-  const int n = e.n_rows;
+  // that set the reference contributes 2^0 (every item has at least one valid token).  The O^T
+  // readout waits for the item's last PV: deferred to the next item's first tile (Pend).
   if (t < NH) {
     const float l = red[t] + red[32 + t] + red[64 + t] + red[96 + t];
-    shs[t] = 1.f / l;                               // shs is free until the next item's first tile
-    if (c0 + t < n) a.part_lse[e.slot0 + c0 + t] = mrow[t] + log2f(l);
+    linv[t] = 1.f / l;
+    if (c0 + t < e.n_rows) a.part_lse[e.slot0 + c0 + t] = mrow[t] + log2f(l);
   }
-  wg_sync(2 + p, 128);
-  __half* dst = a.part_o + static_cast<size_t>(e.slot0) * D + t;
-#pragma unroll
-  for (int cb = 0; cb < NH; cb += 8) {
-    uint32_t o[8];
-    tmem_ld32x8(tmem + lane_base + colO(kp) + c0 + cb, o);
-    tc_wait_ld();
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-      if (c0 + cb + c < n) dst[static_cast<size_t>(c0 + cb + c) * D] = __float2half_rn(__uint_as_float(o[c]) * shs[cb + c]);
-  }
-  tc_fence_before();
-  mbar_arrive(B.o_free + kp);
+  pend.valid = 1;
+  pend.slot0 = e.slot0; pend.n_rows = e.n_rows; pend.nh = NH; pend.kp = static_cast<int32_t>(kp);
+  pend.item = e.item;
+#ifdef ORION_TC_TRACE
+  trp[4] += clock64() - te_;
+  trp[3] += 1;
+#endif
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -800,13 +847,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* mrow = reinterpret_cast<float*>(smem + L::OFF_M) + p * 32;
     float* shs = reinterpret_cast<float*>(smem + L::OFF_SH) + p * 32;
     float* red = reinterpret_cast<float*>(smem + L::OFF_RED) + p * 128;
+    float* linv = reinterpret_cast<float*>(smem + L::OFF_LI) + p * 32;
     uint32_t j = 0;                                 // global tile index
+    Pend pend;
+    pend.valid = 0;
     for (uint32_t k = 0;; ++k) {
       const Sched e = read_sched(ring, sch_full, sch_empty, k, true);
       if (!e.valid) break;
-      if (e.npad == 16) softmax_item<8>(smem, tmem, lane_base, p, t, e, k, j, mrow, shs, red, bars, a, ring);
-      else if (e.npad == 32) softmax_item<16>(smem, tmem, lane_base, p, t, e, k, j, mrow, shs, red, bars, a, ring);
-      else softmax_item<32>(smem, tmem, lane_base, p, t, e, k, j, mrow, shs, red, bars, a, ring);
+      if (e.npad == 16) softmax_item<8>(smem, tmem, lane_base, p, t, e, k, j, mrow, shs, red, linv, bars, a, ring, pend, TRP);
+      else if (e.npad == 32) softmax_item<16>(smem, tmem, lane_base, p, t, e, k, j, mrow, shs, red, linv, bars, a, ring, pend, TRP);
+      else softmax_item<32>(smem, tmem, lane_base, p, t, e, k, j, mrow, shs, red, linv, bars, a, ring, pend, TRP);
+    }
+    if (pend.valid) {
+      wg_sync(2 + p, 128);                          // the last item's linv
+      finish_item(pend, tmem, lane_base, p, t, linv, bars, a, TRP);
     }
     TRACE_DUMP("softmax");
   }
