@@ -663,11 +663,40 @@ def run_costream(args, cfg, lay, layers, q, kn, vn, out, kc, vc, dev, expansion_
     ws = [torch.randn((k, n), generator=g, device=dev, dtype=torch.bfloat16) * 0.02
           for k, n in PREFILL_GEMMS]
     outs = [torch.empty((PREFILL_TOKENS, n), device=dev, dtype=torch.bfloat16) for _, n in PREFILL_GEMMS]
-    layer_flop = sum(2.0 * PREFILL_TOKENS * k * n for k, n in PREFILL_GEMMS)
+    gemm_flop = sum(2.0 * PREFILL_TOKENS * k * n for k, n in PREFILL_GEMMS)
+    # ... plus the Pre-stage attention (§8(f) rank 1, orion_point_prefill_attn) of enough points
+    # that their content rows match the GEMMs' token count: the first queries' points, each Lc
+    # rows attending to its dependency context plus its own content (reads this layer pool)
+    lc = cfg.lc
+    n_pq = 0
+    rows = 0
+    while n_pq < lay.n_queries and rows < PREFILL_TOKENS:
+        rows += int(lay.n_points[n_pq]) * lc
+        n_pq += 1
+    psub, _ = WT.subset_layout(lay, list(range(n_pq)))
+    pqueries = [dict(n_points=int(psub.n_points[i]), edges=psub.edges[i],
+                     prefix_pt_off=int(psub.prefix_pt_off[i]), prefix_len=int(psub.prefix_len[i]))
+                for i in range(psub.n_queries)]
+    ppoints = np.stack([psub.point_pt_off, psub.content_len, psub.point_cap], 1)
 
-    def prefill_layer():
+    def prefill_batch(cap):
+        return orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, pqueries, ppoints, psub.page_table,
+                                    psub.own_len, policy=args.policy, device=dev, num_sms=cap,
+                                    prefill_rows=lc, kv_interleaved=args.kv_layout == "interleaved")
+
+    pbatch = prefill_batch(0)
+    qpf = torch.randn((psub.n_branches, lc, cfg.hq, cfg.d), generator=g, device=dev).to(torch.bfloat16)
+    opf = torch.empty_like(qpf)
+    pst = pbatch.stats
+    ctx_sum = pst["logical_tokens"] - psub.n_branches * lc
+    attn_flop = cfg.hq * cfg.d * 4.0 * (lc * ctx_sum + psub.n_branches * lc * (lc + 1) / 2)
+    layer_flop = gemm_flop + attn_flop
+    pf_pool = layers - 1                               # decode rewrites own slots only: benign reads
+
+    def prefill_layer(pb=None):
         for (k, _), w, o in zip(PREFILL_GEMMS, ws, outs):
             torch.matmul(acts[k], w, out=o)
+        (pb or pbatch).attend(qpf, opf, kc[pf_pool], vc[pf_pool])
 
     # prefill alone
     with torch.cuda.stream(lo):
@@ -745,6 +774,7 @@ def run_costream(args, cfg, lay, layers, q, kn, vn, out, kc, vc, dev, expansion_
         for n_exp in [int(c) for c in args.green_splits.split(",") if c]:
             part = SmPartition(n_exp)
             es, ps = part.first, part.second
+            pb_part = prefill_batch(part.sms[1])
             batch = orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points,
                                          lay.page_table, lay.own_len, policy=args.policy, device=dev,
                                          chunk_tokens=args.chunk, num_sms=part.sms[0], kv_interleaved=args.kv_layout == "interleaved")
@@ -758,7 +788,7 @@ def run_costream(args, cfg, lay, layers, q, kn, vn, out, kc, vc, dev, expansion_
             with torch.cuda.stream(es):
                 gstep()
             with torch.cuda.stream(ps):
-                prefill_layer()
+                prefill_layer(pb_part)
             part.synchronize()
             # each alone, in its own partition
             a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -772,7 +802,7 @@ def run_costream(args, cfg, lay, layers, q, kn, vn, out, kc, vc, dev, expansion_
             with torch.cuda.stream(ps):
                 b0.record(ps)
                 for _ in range(10):
-                    prefill_layer()
+                    prefill_layer(pb_part)
                 b1.record(ps)
             part.synchronize()
             pf_alone_ms = b0.elapsed_time(b1) / 10
@@ -785,7 +815,7 @@ def run_costream(args, cfg, lay, layers, q, kn, vn, out, kc, vc, dev, expansion_
             with torch.cuda.stream(ps):
                 s_lo.record(ps)
                 for i in range(n_pf):
-                    prefill_layer()
+                    prefill_layer(pb_part)
                     pf_ev[i].record(ps)
             s_hi.record(es)
             for _ in range(steps):
@@ -817,7 +847,9 @@ def run_costream(args, cfg, lay, layers, q, kn, vn, out, kc, vc, dev, expansion_
         partitioned = [{"unavailable": f"{type(exc).__name__}: {exc}"}]
     return {"prefill": f"Llama-3-8B layer prefill of {PREFILL_TOKENS} tokens per 'layer': "
                        "[4096x4096]x[4096x{6144,4096,28672}], [4096x14336]x[14336x4096] bf16, "
-                       "torch.matmul (cuBLAS) on a low-priority stream",
+                       "torch.matmul (cuBLAS), plus the point-prefill attention (orion_point_prefill_attn) "
+                       f"of {psub.n_branches} points x Lc {lc} rows ({n_pq} queries), on a low-priority stream",
+            "prefill_flop_per_layer": {"gemm": gemm_flop, "point_prefill_attn": attn_flop},
             "expansion": "the headline step on a high-priority stream",
             "prefill_alone_tflops": prefill_alone, "prefill_ms_per_layer": prefill_ms,
             "expansion_alone_tok_s": expansion_alone, "steps": steps, "together": together,
