@@ -116,10 +116,14 @@ typedef struct { int32_t pt_off, content_len, capacity; } orion_point_desc;
  * rows-on-lanes tcgen05 kernel.  ORION_PLAN_ROWS_ON_LANES forces the rows-on-lanes tcgen05 kernel
  * (<= 128 rows per item); ORION_PLAN_MMA_SYNC the legacy mma.sync m16n8k16 + cp.async kernel
  * (<= 64 rows per item).  All variants compute the same result (same plan semantics). */
-enum { ORION_PLAN_MMA_SYNC = 1, ORION_PLAN_ROWS_ON_LANES = 2, ORION_PLAN_NO_MERGE = 4 };
+enum { ORION_PLAN_MMA_SYNC = 1, ORION_PLAN_ROWS_ON_LANES = 2, ORION_PLAN_NO_MERGE = 4, ORION_PLAN_PAIR = 8 };
 /* ORION_PLAN_NO_MERGE: one work item per (piece, kv head, chunk, row block) -- without it, the
  * tcgen05 decode plans group rows into fixed reader blocks and merge every chunk one block reads
- * with the same reader subset into a multi-range item (one partial per row for the lot). */
+ * with the same reader subset into a multi-range item (one partial per row for the lot).
+ * ORION_PLAN_PAIR (point-prefill plans, opt-in): consecutive items (two readers of one kv head)
+ * run as a pair on one CTA, and every K/V tile of the ranges their lists share (the query's
+ * prefix, common dependencies) is streamed once for both -- 38 % fewer K/V bytes through L2 on
+ * c4, but measured slower than one item per pass, so not the default. */
 
 typedef struct {
   int32_t num_sms;        /* SMs the persistent split kernel may occupy (grid cap, e.g. to leave
@@ -142,6 +146,9 @@ typedef struct {
   int64_t logical_tokens;   /* sum over branches of their context capacity (per kv head) */
   int64_t plan_bytes;
   int64_t workspace_bytes;
+  int64_t streamed_tokens;  /* K/V token rows the split kernel streams, all kv heads (capacity
+                               bound): a paired prefill plan streams its pairs' shared ranges once */
+  int64_t paired;           /* 1: point-prefill plan run as item pairs (ORION_PLAN_PAIR) */
 } orion_plan_stats;
 
 /*

@@ -131,6 +131,7 @@ def select_branches(seg_offsets, segs, own_len, sel):
 PLAN_MMA_SYNC = 1        # ORION_PLAN_MMA_SYNC: legacy mma.sync split kernel
 PLAN_ROWS_ON_LANES = 2   # ORION_PLAN_ROWS_ON_LANES: rows-on-lanes tcgen05 split kernel
 PLAN_NO_MERGE = 4        # ORION_PLAN_NO_MERGE: one item per piece chunk (no multi-range merging)
+PLAN_PAIR = 8            # ORION_PLAN_PAIR: point-prefill items run in pairs sharing K/V tiles (opt-in)
 
 
 def expand_plan(hq, hkv, d, page, seg_offsets, segs, own_len=None, chunk_tokens=0, num_sms=0,

@@ -567,6 +567,36 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
         }
       }
   }
+  // Prefill pairs: items 2u and 2u+1 (adjacent readers of one kv head, or two row blocks of one
+  // reader) run on one CTA; the leading ranges their lists share -- the query's prefix, common
+  // dependencies, or everything for two row blocks of a branch -- stream one K/V tile for both.
+  const bool paired = Lc > 0 && (flags & ORION_PLAN_PAIR);
+  if (paired)
+    for (size_t u = 0; u + 1 < items.size(); u += 2) {
+      WorkItem& A = items[u];
+      const WorkItem& B = items[u + 1];
+      int32_t n_sh = 0;
+      if (A.kv_head == B.kv_head)
+        while (n_sh < A.n_ranges && n_sh < B.n_ranges) {
+          const Range& x = ranges[A.pt_off + n_sh];
+          const Range& y = ranges[B.pt_off + n_sh];
+          if (x.pt_off != y.pt_off || x.t0 != y.t0 || x.t1 != y.t1 || x.dyn != y.dyn || x.flags != y.flags) break;
+          ++n_sh;
+        }
+      A.t1 = n_sh;
+    }
+  int64_t streamed = 0;
+  for (size_t i = 0; i < items.size(); ++i) {
+    const WorkItem& w = items[i];
+    if (w.flags & kItemRanges) {
+      for (int32_t r = 0; r < w.n_ranges; ++r) {
+        const Range& x = ranges[w.pt_off + r];
+        if (!(paired && (i & 1) && r < items[i - 1].t1)) streamed += x.t1 - x.t0;   // pair: once
+      }
+    } else {
+      streamed += w.t1 - w.t0;
+    }
+  }
   for (size_t r = 0; r < row_slots.size(); ++r)
     if (row_slots[r].empty())
       return fail(ORION_ERR_INVALID_ARG, "row %zu (branch %zu) has no context", r, r / ((size_t)Lrows * Hq));
@@ -600,12 +630,18 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
     h.acc_bytes = align16((int64_t)n_slots * shape->head_dim * 4);
     h.workspace_bytes = h.acc_bytes + align16((int64_t)n_slots * 8);
   }
+  if (paired) {   // the pair kernel's dynamic work counter (zeroed by the launcher)
+    h.counter_off = h.workspace_bytes;
+    h.workspace_bytes += 16;
+  }
   h.n_pieces = (int64_t)pieces.size();
   h.unique_tokens = unique_tokens;
   h.logical_tokens = logical_total;
   h.variant = variant;
   h.max_ctas = (opts && opts->num_sms > 0) ? opts->num_sms : 0;
   h.prefill_rows = Lc;
+  h.paired = paired ? 1 : 0;
+  h.streamed_tokens = streamed;
   h.sm_scale = shape->sm_scale > 0.f ? shape->sm_scale : 1.0f / std::sqrt((float)shape->head_dim);
   *plan_needed = (size_t)h.plan_bytes;
   *workspace_needed = (size_t)h.workspace_bytes;
@@ -644,6 +680,8 @@ extern "C" orion_status orion_plan_get_stats(const void* h_plan, orion_plan_stat
   out->logical_tokens = h->logical_tokens;
   out->plan_bytes = h->plan_bytes;
   out->workspace_bytes = h->workspace_bytes;
+  out->streamed_tokens = h->streamed_tokens;
+  out->paired = h->paired;
   return ORION_OK;
 }
 

@@ -46,8 +46,12 @@ struct PlanHeader {
   int32_t max_ctas; // persistent split kernels: grid cap (opts->num_sms; 0 = all SMs)
   int32_t prefill_rows;  // 0: decode plan; Lc: point-prefill plan (rows = branch x Lc x Hq)
   int64_t ranges_off;    // byte offset of Range[n_ranges] (multi-range items)
-  int32_t n_ranges, pad2_;
-};
+  int32_t n_ranges;
+  int32_t paired;
+  int64_t streamed_tokens;  // orion_plan_stats::streamed_tokens
+  int64_t counter_off;      // paired plans: workspace byte offset of the pair-unit work counter (int32)
+};        // prefill plans: items 2u, 2u+1 run as one pair unit (split_pair.cu);
+                         // items[2u].t1 = number of leading ranges the two lists share
 static_assert(sizeof(PlanHeader) % 16 == 0, "header must keep 16-byte alignment");
 
 // One split-kernel work item: tokens [t0, min(t1, own_len[dyn])) of the page run at pt_off,

@@ -1,6 +1,7 @@
 // split_tc.h — internal interface between the launchers (kernels.cu) and the tcgen05 split
 // kernel (split_tc.cu).  Product-side only.
 #pragma once
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -62,11 +63,17 @@ struct TcArgs {
   __nv_bfloat16* out;     // non-null: every row has exactly one partial (a point-prefill plan) and
   float* lse;             // the epilogue writes out = acc / l (bf16) and lse directly: no combine
   float scale_log2;
+  int32_t* work_counter;  // paired prefill plans: pair units handed out by atomicAdd (split_pair.cu)
 };
 
 template <int D>
 orion_status launch_split_tc(const PlanHeader* h, const TcArgs& a, const void* k, const void* v,
                              int32_t num_pages, cudaStream_t st);
+
+// Point-prefill plans with paired items (PlanHeader::paired): split_pair.cu.  maps = K, V tensor
+// maps with full-tile boxes, then K, V with 16-row boxes.
+template <int D>
+orion_status launch_split_pair(const PlanHeader* h, const TcArgs& a, const CUtensorMap maps[4], cudaStream_t st);
 
 orion_status launch_split_tct(const PlanHeader* h, const TcArgs& a, const void* k, const void* v,
                               int32_t num_pages, cudaStream_t st);

@@ -19,7 +19,7 @@ def _cuda():
         pytest.skip("no CUDA device")
 
 
-def run_prefill(cfg, lay, ten, qp, policy=0, interleaved=False):
+def run_prefill(cfg, lay, ten, qp, policy=0, interleaved=False, flags=0):
     dev = torch.device("cuda")
     queries = [dict(n_points=int(lay.n_points[i]), edges=lay.edges[i],
                     prefix_pt_off=int(lay.prefix_pt_off[i]), prefix_len=int(lay.prefix_len[i]))
@@ -27,7 +27,7 @@ def run_prefill(cfg, lay, ten, qp, policy=0, interleaved=False):
     points = np.stack([lay.point_pt_off, lay.content_len, lay.point_cap], 1)
     batch = orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, lay.page_table,
                                  lay.own_len, policy=policy, device=dev, prefill_rows=cfg.lc,
-                                 kv_interleaved=interleaved)
+                                 kv_interleaved=interleaved, flags=flags)
     if interleaved:
         kv = torch.stack([ten["k_cache"][0], ten["v_cache"][0]], dim=2).to(dev).contiguous()
         kc, vc = kv[:, :, 0], kv[:, :, 1]
@@ -42,8 +42,8 @@ def run_prefill(cfg, lay, ten, qp, policy=0, interleaved=False):
     return out, lse, batch
 
 
-def check(cfg, lay, ten, qp, policy=0, branches=None, interleaved=False):
-    out, lse, batch = run_prefill(cfg, lay, ten, qp, policy, interleaved)
+def check(cfg, lay, ten, qp, policy=0, branches=None, interleaved=False, flags=0):
+    out, lse, batch = run_prefill(cfg, lay, ten, qp, policy, interleaved, flags)
     if branches is None:
         branches = list(range(lay.n_branches))
     ref, ref_lse = OP.point_prefill(lay, u16(qp), u16(ten["k_cache"][0]), u16(ten["v_cache"][0]),
@@ -64,24 +64,56 @@ def q_pre(cfg, lay, seed=5, scale=1.0):
     return T.bf16_randn_u16((lay.n_branches, cfg.lc, cfg.hq, cfg.d), seed, "cpu", scale=scale)
 
 
+PAIRING = [0, orion.PLAN_PAIR]   # one item per pass (default) / paired items sharing K/V tiles (split_pair.cu)
+
+
+@pytest.mark.parametrize("flags", PAIRING)
 @pytest.mark.parametrize("dagf", [W.diamond, W.fig4, W.mixed8, lambda: W.chain(5, 2)])
 @pytest.mark.parametrize("policy", [0, 1])
 @pytest.mark.parametrize("d", [64, 128])
-def test_small_dags(dagf, policy, d):
+def test_small_dags(dagf, policy, d, flags):
     cfg = C.CONFIGS["c1"].with_(lp=150, t=90, lc=8, page=16, d=d, hq=8, hkv=2)
     lay = T.make_layout(cfg, ragged=True, dag_override=dagf)
     ten = T.make_qkv(cfg, lay)
-    check(cfg, lay, ten, q_pre(cfg, lay), policy)
+    check(cfg, lay, ten, q_pre(cfg, lay), policy, flags=flags)
 
 
+@pytest.mark.parametrize("flags", PAIRING)
 @pytest.mark.parametrize("lc,hq,hkv", [(32, 8, 2), (32, 32, 8), (16, 28, 4), (64, 8, 4), (40, 8, 2)])
-def test_row_blocks_and_causal_spans(lc, hq, hkv):
+def test_row_blocks_and_causal_spans(lc, hq, hkv, flags):
     # R = Lc*G rows per reader: 64 / 128 / 112 / 128 / 160 (> one 128-row MMA tile: two row blocks
-    # and a causal limit crossing the block boundary); Lc up to a whole 64-token tile
+    # and a causal limit crossing the block boundary -- paired, the two blocks of one reader share
+    # every range, the causal own range included); Lc up to a whole 64-token tile
     cfg = C.CONFIGS["c1"].with_(lp=300, t=200, lc=lc, page=32, d=128, hq=hq, hkv=hkv)
     lay = T.make_layout(cfg, ragged=True, dag_override=W.mixed8)
     ten = T.make_qkv(cfg, lay, q_scale=2.0)
-    check(cfg, lay, ten, q_pre(cfg, lay, scale=3.0))
+    check(cfg, lay, ten, q_pre(cfg, lay, scale=3.0), flags=flags)
+
+
+@pytest.mark.parametrize("dagf,hq,hkv", [(lambda: W.chain(5, 2), 4, 1), (W.fig4, 8, 2), (lambda: W.wide(7), 8, 4)])
+def test_pairs_odd_and_across_kv_heads(dagf, hq, hkv):
+    # An odd item count (the last pair unit has no second item), pairs straddling two kv heads (no
+    # shared range: every tile unique, alternating), pairs of different queries' readers.
+    cfg = C.CONFIGS["c1"].with_(n_queries=3, lp=130, t=100, lc=16, page=16, d=128, hq=hq, hkv=hkv)
+    lay = T.make_layout(cfg, ragged=True, dag_override=dagf)
+    ten = T.make_qkv(cfg, lay, q_scale=2.0)
+    batch = check(cfg, lay, ten, q_pre(cfg, lay, scale=2.0), flags=orion.PLAN_PAIR)
+    assert batch.stats["paired"] == 1
+
+
+def test_paired_equals_unpaired_within_rounding():
+    # Both kernels compute the same rows from the same plan geometry; they differ only in the
+    # order of fp32 accumulation (one O per row vs two alternating-tile accumulators merged).
+    cfg = C.CONFIGS["c1"].with_(lp=400, t=160, lc=32, page=64, d=128, hq=8, hkv=2)
+    lay = T.make_layout(cfg, ragged=True, dag_override=W.mixed8)
+    ten = T.make_qkv(cfg, lay)
+    qp = q_pre(cfg, lay, scale=2.0)
+    o1, l1, b1 = run_prefill(cfg, lay, ten, qp, flags=orion.PLAN_PAIR)
+    o2, l2, b2 = run_prefill(cfg, lay, ten, qp)
+    assert b1.stats["paired"] == 1 and b2.stats["paired"] == 0
+    assert b1.stats["streamed_tokens"] < b2.stats["streamed_tokens"]
+    assert float((o1.float() - o2.float()).abs().max()) <= 1e-2
+    assert float((l1 - l2).abs().max()) <= LSE_ABS   # P rounded to bf16 against different running maxima
 
 
 def test_sink_and_peaky_queries():
@@ -126,14 +158,15 @@ def test_prefill_last_row_matches_decode_kernel():
     assert float(np.abs(pre[:, cfg.lc - 1].float().cpu().numpy() - ref).max()) <= MAX_ABS
 
 
-def test_split_plus_combine_equals_direct_prefill():
+@pytest.mark.parametrize("flags", PAIRING)
+def test_split_plus_combine_equals_direct_prefill(flags):
     # orion_expand_split + orion_expand_combine on a prefill plan (fp32 partials, one per row)
     # reproduce orion_point_prefill_attn's direct-output epilogue bit for bit.
     cfg = C.CONFIGS["c1"].with_(lp=300, t=120, lc=32, page=32, d=128, hq=8, hkv=2)
     lay = T.make_layout(cfg, ragged=True, dag_override=W.mixed8)
     ten = T.make_qkv(cfg, lay)
     qp = q_pre(cfg, lay, scale=2.0)
-    out, lse, batch = run_prefill(cfg, lay, ten, qp)
+    out, lse, batch = run_prefill(cfg, lay, ten, qp, flags=flags)
     dev = torch.device("cuda")
     kc = ten["k_cache"][0].to(dev).contiguous()
     vc = ten["v_cache"][0].to(dev).contiguous()

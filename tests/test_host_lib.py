@@ -132,7 +132,8 @@ HDR = np.dtype([("magic", "<i4"), ("version", "<i4"), ("n_branches", "<i4"), ("h
                 ("comb_slot_off", "<i8"), ("plan_bytes", "<i8"), ("workspace_bytes", "<i8"),
                 ("acc_bytes", "<i8"), ("n_pieces", "<i8"), ("unique_tokens", "<i8"),
                 ("logical_tokens", "<i8"), ("sm_scale", "<f4"), ("pad", "<i4", 3),
-                ("ranges_off", "<i8"), ("n_ranges", "<i4"), ("pad2", "<i4")])
+                ("ranges_off", "<i8"), ("n_ranges", "<i4"), ("paired", "<i4"),
+                ("streamed_tokens", "<i8"), ("counter_off", "<i8")])
 RANGE = np.dtype([(n, "<i4") for n in ("pt_off", "t0", "t1", "dyn", "flags", "r0", "r1", "r2")])
 ITEM = np.dtype([(n, "<i4") for n in ("pt_off", "t0", "t1", "dyn", "kv_head", "readers_off",
                                       "row_begin", "n_rows", "slot0", "piece", "p0", "p1")])
@@ -267,13 +268,15 @@ def test_device_entry_points_validate_without_gpu():
 
 
 # ------------------------------------------------------------------ point-prefill plans
-def _check_prefill_plan(cfg, lay, offs, segs, own_len):
+def _check_prefill_plan(cfg, lay, offs, segs, own_len, flags=0):
     """Row (b, i, h) of a prefill plan has exactly one partial, from one reader-stationary item whose
     ranges are b's list except OWN (same order and extents) followed by the causal own range
-    [0, Lc) of its run (the kernel limits row i to [0, i])."""
+    [0, Lc) of its run (the kernel limits row i to [0, i]).  Paired (default): item 2u records in
+    t1 how many leading ranges it shares with item 2u+1 (same kv head, equal spans), and the plan
+    streams those once per pair (ORION_PLAN_PAIR)."""
     lc = cfg.lc
     plan, ws = orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, own_len,
-                                 prefill_rows=lc)
+                                 prefill_rows=lc, flags=flags)
     h, items, readers, coff, cslot = parse_plan(plan)
     ranges = np.frombuffer(plan, RANGE, int(h["n_ranges"]), int(h["ranges_off"]))
     G = cfg.hq // cfg.hkv
@@ -300,6 +303,22 @@ def _check_prefill_plan(cfg, lay, offs, segs, own_len):
     for row in range(h["n_rows"]):
         ss = cslot[coff[row]:coff[row + 1]]
         assert len(ss) == 1 and slot[int(ss[0])] == row
+    paired = bool(flags & orion.PLAN_PAIR)
+    assert int(h["paired"]) == int(paired)
+    lists = [[tuple(int(x) for x in r)[:5] for r in ranges[it["pt_off"]:it["pt_off"] + it["p1"]]]
+             for it in items]
+    streamed = sum(r[2] - r[1] for lst in lists for r in lst)
+    if paired:
+        for u in range(0, len(items) - 1, 2):
+            a, b = lists[u], lists[u + 1]
+            n_sh = 0
+            if items[u]["kv_head"] == items[u + 1]["kv_head"]:
+                while n_sh < min(len(a), len(b)) and a[n_sh] == b[n_sh]:
+                    n_sh += 1
+            assert int(items[u]["t1"]) == n_sh
+            streamed -= sum(r[2] - r[1] for r in a[:n_sh])
+    assert int(h["streamed_tokens"]) == streamed
+    return h
 
 
 @pytest.mark.parametrize("cfgname,policy,hq", [("c1", 0, 4), ("c1", 1, 4), ("c2", 0, 32), ("c3", 1, 28)])
@@ -309,6 +328,21 @@ def test_prefill_plan_covers_context_and_causal_own(cfgname, policy, hq):
     lay = T.make_layout(cfg, ragged=True, extra_tokens=cfg.page)
     offs, segs = _bind_layout(cfg, lay, policy)
     _check_prefill_plan(cfg, lay, offs, segs, lay.own_len)
+    _check_prefill_plan(cfg, lay, offs, segs, lay.own_len, flags=orion.PLAN_PAIR)
+
+
+def test_prefill_pairs_share_the_prefix_closed_form():
+    # Edgeless DAG (every list = [PREFIX, OWN]), even point count: every pair is two readers of
+    # one query and kv head sharing exactly the prefix, so the paired plan streams
+    # Hkv * (sum_b (Lp + Lc) - (n_branches / 2) * Lp) token rows, the unpaired one Hkv * sum_b (Lp + Lc).
+    cfg = C.CONFIGS["c1"].with_(n_queries=3, lp=200, t=64, lc=16, page=16, hq=8, hkv=2)
+    lay = T.make_layout(cfg, dag_override=lambda: W.wide(6))
+    offs, segs = _bind_layout(cfg, lay, 0)
+    B = lay.n_branches
+    h = _check_prefill_plan(cfg, lay, offs, segs, lay.own_len, flags=orion.PLAN_PAIR)
+    assert int(h["streamed_tokens"]) == cfg.hkv * (B * (cfg.lp + cfg.lc) - (B // 2) * cfg.lp)
+    h = _check_prefill_plan(cfg, lay, offs, segs, lay.own_len)
+    assert int(h["streamed_tokens"]) == cfg.hkv * B * (cfg.lp + cfg.lc)
 
 
 def test_prefill_plan_errors():
