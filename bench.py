@@ -523,6 +523,34 @@ def run_model_step(args, cfg, lay, layers, kc, vc, dev, attention_only):
             "output_finite": finite}
 
 
+def expansion_decode_bytes(cfg, lay, ex, schedule, layers):
+    """Algorithmic HBM bytes of the decode rounds of a whole expansion (SURVEY.md 8(d)'s formula per
+    round).  Replays the lengths: a round's attention sees each running branch's own segment with
+    the token just appended.  A point's spans (CONTENT [0, Lc), FULL [0, T), OUTPUT [Lc, T), OWN
+    [0, own)) and the prefix [0, Lp) overlap or touch, so a page run's union is max end - min start."""
+    so, sg = ex.seg_offsets, ex.segs
+    own = np.full(ex.n_branches, cfg.lc, np.int64)
+    per_tok = cfg.hkv * cfg.d * 2 * 2
+    total = 0
+    for dec in schedule:
+        cur = own.copy()
+        cur[dec] += 1
+        idx = np.concatenate([np.arange(so[b], so[b + 1]) for b in dec])
+        seg = sg[idx]
+        dyn = seg["dyn"].astype(np.int64)
+        ln = seg["len"].astype(np.int64)
+        eff = np.where(dyn >= 0, np.clip(cur[np.maximum(dyn, 0)] - seg["start"], 0, ln), ln)
+        keep = eff > 0
+        pt, st, en = seg["pt_off"][keep], seg["start"][keep].astype(np.int64), (seg["start"][keep] + eff[keep])
+        order = np.argsort(pt, kind="stable")
+        pt, st, en = pt[order], st[order], en[order]
+        starts = np.flatnonzero(np.r_[True, pt[1:] != pt[:-1]])
+        uniq = int((np.maximum.reduceat(en, starts) - np.minimum.reduceat(st, starts)).sum())
+        total += layers * (uniq * per_tok + len(dec) * cfg.hq * cfg.d * 2 * 2)
+        own[dec] += 1
+    return total
+
+
 def run_expansion(args, cfg, lay, layers, q, kn, vn, kc, vc, dev):
     """§8(f) rank 2: a whole expansion of the config's queries (Alg. 1 l.9-22 with
     continuous batching, reading D1): rounds of orion_expansion_round; each round prefills the
@@ -551,6 +579,7 @@ def run_expansion(args, cfg, lay, layers, q, kn, vn, kc, vc, dev):
     t0 = time.perf_counter()
     e0.record(stream)
     rounds, dec_sum, pre_rounds, cur, subs = 0, 0, 0, None, None
+    schedule = []                                  # running set of every decode round
     while True:
         pre, dec = ex.next_round()
         if len(pre) == 0 and len(dec) == 0:
@@ -569,12 +598,15 @@ def run_expansion(args, cfg, lay, layers, q, kn, vn, kc, vc, dev):
                 cur = dec.copy()
             ex.decode(dec, subs[0], subs[1], subs[2], kc[:layers], vc[:layers], subs[3])
             dec_sum += len(dec)
+            schedule.append(dec)
         rounds += 1
     e1.record(stream)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     ms = e0.elapsed_time(e1)
     gen = int(tokens.sum())
+    kv_bytes = expansion_decode_bytes(cfg, lay, ex, schedule, layers)
+    peak, peak_src = load_peaks()
     return {"workload": f"{cfg.name}: whole expansion of {lay.n_queries} queries x {cfg.dag}, "
                         f"every point prefills Lc {lc} tokens then decodes T - Lc = {int(tokens.max())} "
                         f"tokens through {layers} layers",
@@ -582,6 +614,13 @@ def run_expansion(args, cfg, lay, layers, q, kn, vn, kc, vc, dev):
             "generated_tokens": gen, "rounds": rounds, "rounds_with_prefill": pre_rounds,
             "mean_running_set": dec_sum / max(1, rounds), "max_branches": B,
             "plan_rebuilds": ex.rebuilds, "ms": ms, "wall_ms": wall * 1e3,
+            "roofline": {"bound": "hbm", "algorithmic_bytes": kv_bytes, "achieved": kv_bytes / (ms / 1e3) / 1e9,
+                         "peak": peak, "unit": "GB/s", "frac": kv_bytes / (ms / 1e3) / 1e9 / peak,
+                         "peak_source": peak_src,
+                         "note": "all decode rounds: per round and layer, every (query, kv head)'s unique "
+                                 "context tokens (union of its running branches' spans at their current "
+                                 "lengths) x d x 2 (K, V) x 2 B, plus q read and out write (SURVEY.md "
+                                 "8(d)); prefill rounds, appends and plan rebuilds count as time only"},
             "note": "device-timed (events) around the whole loop; host scheduling and plan "
                     "rebuilds inside; compare the snapshot value where every point decodes at once"}
 
