@@ -89,3 +89,49 @@ def test_select_branches_matches_oracle_binding(policy):
                 assert (int(s["start"]), int(eff)) == (start, length)
     with pytest.raises(orion.OrionError):
         orion.select_branches(offs, segs, lay.own_len, [0, 0])
+
+
+def _expansion(cfg, lay, policy=0):
+    from paper_2510_24390_b200.expansion import Expansion
+    queries = [dict(n_points=int(lay.n_points[i]), edges=lay.edges[i],
+                    prefix_pt_off=int(lay.prefix_pt_off[i]), prefix_len=int(lay.prefix_len[i]))
+               for i in range(lay.n_queries)]
+    points = np.stack([lay.point_pt_off, lay.content_len, lay.point_cap], 1)
+    tokens = (np.asarray(lay.own_len) - cfg.lc).astype(np.int32)
+    return Expansion(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, lay.page_table, cfg.lc,
+                     tokens, policy=policy, device="cpu")
+
+
+@pytest.mark.parametrize("policy", [0, 1])
+def test_expansion_roofline_bytes_brute_force(policy):
+    # bench.expansion_decode_bytes (the whole-expansion roofline numerator) against a brute-force
+    # count: per decode round, the set of distinct (page run, token) pairs the running branches'
+    # oracle-bound contexts (O2, lengths at attention time) touch, x Hkv x d x 2 x 2 B, plus q/out.
+    import bench
+    cfg = C.CONFIGS["c1"].with_(n_queries=2, lp=40, t=24, lc=8, page=16)
+    lay = T.make_layout(cfg, dag_override=W.mixed8)
+    ex = _expansion(cfg, lay, policy)
+    schedule = []
+    while True:
+        pre, dec = ex.next_round()
+        if len(pre) == 0 and len(dec) == 0:
+            break
+        if len(pre):
+            ex.own_len[pre] = cfg.lc
+        if len(dec):
+            schedule.append(np.array(dec))
+            ex.own_len[dec] += 1
+    got = bench.expansion_decode_bytes(cfg, lay, ex, schedule, layers=1)
+    own = np.full(lay.n_branches, cfg.lc)
+    want = 0
+    for dec in schedule:
+        cur = own.copy()
+        cur[dec] += 1
+        bound = OS.bound_segments(lay, policy, own_len=cur)
+        toks = set()
+        for b in dec:
+            for pages, start, ln in bound[b]:
+                toks.update((int(pages[(start + t) // cfg.page]), (start + t) % cfg.page) for t in range(ln))
+        want += len(toks) * cfg.hkv * cfg.d * 4 + len(dec) * cfg.hq * cfg.d * 4
+        own[dec] += 1
+    assert got == want
