@@ -273,21 +273,34 @@ __device__ __forceinline__ void softmax_tile(uint32_t tmem, uint32_t lane_base, 
   mbar_arrive(sfree);                                // QK(j+3) may overwrite this S^T buffer
   const int pos = tb + t;
   const bool valid = pos >= lo && pos < hi;
-  // d = s * scale - mb (log2 domain, relative to the running reference; mb = 0 while unset)
-  bool exceed = false;
+  // d = s * scale - mb (log2 domain, relative to the per-column running reference mb).  On an
+  // item's first tile (had == false) no column has a reference yet: d = s * scale, and the growth
+  // path below always runs (every tile has a valid token), so no vote is needed.  Afterwards every
+  // column has one, and the vote is "does any valid d exceed 2^8" -- a max, not per-element tests.
+  bool grow = true;
+  if (!had) {
 #pragma unroll
-  for (int c4 = 0; c4 < NH; c4 += 4) {
-    const float4 m4 = *reinterpret_cast<const float4*>(mrow + c4);
-    const float mm[4] = {m4.x, m4.y, m4.z, m4.w};
+    for (int c = 0; c < NH; ++c) s[c] = __float_as_uint(valid ? __uint_as_float(s[c]) * scale_log2 : -INFINITY);
+  } else {
+    float dmax = -INFINITY;
+    if (valid) {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float mb = mm[e] == -INFINITY ? 0.f : mm[e];
-      const float d = valid ? fmaf(__uint_as_float(s[c4 + e]), scale_log2, -mb) : -INFINITY;
-      s[c4 + e] = __float_as_uint(d);
-      exceed |= valid && (mm[e] == -INFINITY || d > 8.f);
+      for (int c4 = 0; c4 < NH; c4 += 4) {
+        const float4 m4 = *reinterpret_cast<const float4*>(mrow + c4);
+        const float mm[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float d = fmaf(__uint_as_float(s[c4 + e]), scale_log2, -mm[e]);
+          s[c4 + e] = __float_as_uint(d);
+          dmax = fmaxf(dmax, d);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < NH; ++c) s[c] = __float_as_uint(-INFINITY);
     }
+    grow = wg_any(dmax > 8.f, 2 + p);
   }
-  const bool grow = wg_any(exceed, 2 + p);
   if (grow) {
     // column max of d over the 128 tokens: warp redux, then across the 4 warps via smem
     const int wq = t >> 5, ln = t & 31;
@@ -307,6 +320,8 @@ __device__ __forceinline__ void softmax_tile(uint32_t tmem, uint32_t lane_base, 
       if (gc) mrow[col] = mb + cm;
     }
     wg_sync(2 + p, 128);
+#pragma unroll
+    for (int c = 0; c < NH; ++c) s[c] = __float_as_uint(__uint_as_float(s[c]) - shs[c]);   // d relative to the new reference
     if (had) {   // this item's O^T columns and row sums follow the new reference: * 2^-shift
 #pragma unroll
       for (int c = 0; c < NH; ++c) ls[c] *= ex2(-shs[c]);
@@ -328,11 +343,13 @@ __device__ __forceinline__ void softmax_tile(uint32_t tmem, uint32_t lane_base, 
   // The exponentials are formed before the wait for PV(j-2), which frees this P^T buffer.
   uint32_t pk[NH / 2];
 #pragma unroll
-  for (int c = 0; c < NH; c += 2) {
-    const float s0 = grow ? shs[c] : 0.f, s1 = grow ? shs[c + 1] : 0.f;
-    pk[c / 2] = pack_bf16(ex2(__uint_as_float(s[c]) - s0), ex2(__uint_as_float(s[c + 1]) - s1));
-    ls[c] += __uint_as_float(pk[c / 2] << 16);       // row sums of exactly the bf16 P fed to PV
-    ls[c + 1] += __uint_as_float(pk[c / 2] & 0xFFFF0000u);
+  for (int c = 0; c < NH; c += 2) pk[c / 2] = pack_bf16(ex2(__uint_as_float(s[c])), ex2(__uint_as_float(s[c + 1])));
+#pragma unroll
+  for (int c = 0; c < NH; c += 2) {                  // row sums of exactly the bf16 P fed to PV
+    const float2 v = __fadd2_rn(make_float2(ls[c], ls[c + 1]),
+                                make_float2(__uint_as_float(pk[c / 2] << 16), __uint_as_float(pk[c / 2] & 0xFFFF0000u)));
+    ls[c] = v.x;
+    ls[c + 1] = v.y;
   }
   if (need_pv) STW(6, mbar_wait(pv_free, pv_free_par));
 #pragma unroll
