@@ -141,9 +141,9 @@ __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
 #define TRP tr_
 #define TW(slot, stmt) do { const unsigned long long t_ = clock64(); stmt; tr_[slot] += clock64() - t_; } while (0)
 #define TRACE_DUMP(role) do { if (blockIdx.x < 2 && (threadIdx.x & 31) == 0) printf( \
-    "TRACE blk %d warp %2d %-8s tot %llu | %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu\n", blockIdx.x, \
+    "TRACE blk %d warp %2d %-8s tot %llu | %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu\n", blockIdx.x, \
     threadIdx.x >> 5, role, clock64() - tr_t0, tr_[0], tr_[1], tr_[2], tr_[3], tr_[4], tr_[5], tr_[6], tr_[7], \
-    tr_[8], tr_[9]); } while (0)
+    tr_[8], tr_[9], tr_[10], tr_[11]); } while (0)
 #else
 #define TRACE_DECL
 #define TRP nullptr
@@ -265,10 +265,17 @@ __device__ __forceinline__ void softmax_tile(uint32_t tmem, uint32_t lane_base, 
                                              uint32_t pv_free_par, uint64_t* pv_prev, uint32_t pv_prev_par,
                                              unsigned long long* trp) {
   uint32_t s[NH];
+#ifdef ORION_TC_TRACE
+  unsigned long long tq_ = clock64();
+#define SLOT_END(i) do { trp[i] += clock64() - tq_; tq_ = clock64(); } while (0)
+#else
+#define SLOT_END(i) do {} while (0)
+#endif
   if constexpr (NH == 8) tmem_ld32x8(tmem + lane_base + scol, s);
   if constexpr (NH == 16) tmem_ld32x16(tmem + lane_base + scol, s);
   if constexpr (NH == 32) tmem_ld32x32(tmem + lane_base + scol, s);
   tc_wait_ld();
+  SLOT_END(7);
   tc_fence_before();
   mbar_arrive(sfree);                                // QK(j+3) may overwrite this S^T buffer
   const int pos = tb + t;
@@ -299,7 +306,9 @@ __device__ __forceinline__ void softmax_tile(uint32_t tmem, uint32_t lane_base, 
 #pragma unroll
       for (int c = 0; c < NH; ++c) s[c] = __float_as_uint(-INFINITY);
     }
+    SLOT_END(3);
     grow = wg_any(dmax > 8.f, 2 + p);
+    SLOT_END(8);
   }
   if (grow) {
     // column max of d over the 128 tokens: warp redux, then across the 4 warps via smem
@@ -341,6 +350,7 @@ __device__ __forceinline__ void softmax_tile(uint32_t tmem, uint32_t lane_base, 
   }
   // P^T row t, columns [c0, c0 + NH) (MN-major, 128B swizzle): p = 2^(d - shift) rounded to bf16.
   // The exponentials are formed before the wait for PV(j-2), which frees this P^T buffer.
+  SLOT_END(10);
   uint32_t pk[NH / 2];
 #pragma unroll
   for (int c = 0; c < NH; c += 2) pk[c / 2] = pack_bf16(ex2(__uint_as_float(s[c])), ex2(__uint_as_float(s[c + 1])));
@@ -351,6 +361,7 @@ __device__ __forceinline__ void softmax_tile(uint32_t tmem, uint32_t lane_base, 
     ls[c] = v.x;
     ls[c + 1] = v.y;
   }
+  SLOT_END(9);
   if (need_pv) STW(6, mbar_wait(pv_free, pv_free_par));
 #pragma unroll
   for (int cc = 0; cc < NH / 8; ++cc) {
@@ -471,10 +482,14 @@ __device__ __forceinline__ void softmax_item(uint8_t* smem, uint32_t tmem, uint3
     softmax_tile<NH>(tmem, lane_base, p, t, colS(b) + c0, pbuf, c0, tb, lo, hi, mrow, shs, red, tt > 0,
                      colO(kp) + c0, ls, a.scale_log2, B.s_free + b, need_pv, B.pv_done + (j & 1),
                      ((j - 2) >> 1) & 1, B.pv_done + ((j - 1) & 1), ((j - 1) >> 1) & 1, trp);
+#ifdef ORION_TC_TRACE
+    const unsigned long long tf_ = clock64();
+#endif
     fence_proxy_async();
     tc_fence_before();
     mbar_arrive(B.p_full + (j & 1));
 #ifdef ORION_TC_TRACE
+    trp[11] += clock64() - tf_;
     trp[2] += clock64() - ts_;
     trp[0] += 1;
 #endif
@@ -518,7 +533,6 @@ __device__ __forceinline__ void softmax_item(uint8_t* smem, uint32_t tmem, uint3
   pend.item = e.item;
 #ifdef ORION_TC_TRACE
   trp[4] += clock64() - te_;
-  trp[3] += 1;
 #endif
 }
 
