@@ -207,6 +207,12 @@ def cpu_baseline(cfg, layers, seconds):
                       f"1 layer), {spent:.1f} s CPU; scaled by {layers} layers"}
 
 
+def workload_str(cfg, layers):
+    """config.workload of both arms (the same workload; the reference arm times a sample of it)."""
+    return (f"{cfg.name}: Hq/Hkv/d={cfg.hq}/{cfg.hkv}/{cfg.d}, {cfg.n_queries} queries x {cfg.dag}, "
+            f"prefix {cfg.lp}, {cfg.t} tok/point (Lc {cfg.lc}), page {cfg.page}, {layers} layers")
+
+
 def run_reference(args, cfg, layers):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -224,11 +230,12 @@ def run_reference(args, cfg, layers):
             "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": f"{cfg.name} (oracle sample: 1 query x 1 layer per step, "
-                                   f"scaled by {layers} layers)", "policy": "ancestors"},
+            "config": {"workload": workload_str(cfg, layers), "policy": "ancestors"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"per step 1 query of {cfg.name} (all {n_br} branches), "
-                                       f"1 layer, append + attention"},
+                                       f"1 layer, append + attention; the rate scaled by {layers} "
+                                       f"layers (queries are independent: the config's value is "
+                                       f"branches / (per-query time x layers))"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -385,9 +392,7 @@ def run_orion(args, cfg, layers):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded N(0,1) bf16 q/K/V; random page permutation)",
-        "config": {"workload": f"{cfg.name}: Hq/Hkv/d={cfg.hq}/{cfg.hkv}/{cfg.d}, "
-                               f"{cfg.n_queries} queries x {cfg.dag}, prefix {cfg.lp}, "
-                               f"{cfg.t} tok/point (Lc {cfg.lc}), page {cfg.page}, {layers} layers",
+        "config": {"workload": workload_str(cfg, layers),
                    "branches_per_step": int(total_b), "layers": layers,
                    "policy": "parents_eq3" if args.policy else "ancestors",
                    "append_mode": "rewrite (stationary snapshot)",

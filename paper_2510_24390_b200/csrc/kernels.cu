@@ -714,6 +714,7 @@ extern "C" orion_status orion_point_prefill_attn(const orion_attn_shape* shape, 
 
 extern "C" const char* orion_version(void) {
   return "orion-b200 0.3 (sm_100a; K1 append; K2 split: tcgen05.mma + TMEM + TMA swap-AB (decode, "
-         "default) | rows-on-lanes (d = 64, point prefill) | mma.sync m16n8k16 (ORION_PLAN_MMA_SYNC); "
+         "default) | rows-on-lanes (d = 64, point prefill; K/V-sharing item pairs with ORION_PLAN_PAIR) | "
+         "mma.sync m16n8k16 (ORION_PLAN_MMA_SYNC); "
          "K3 combine)";
 }
