@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 import torch
 
+import paper_2510_24390_b200 as orion
 from oracle import prefill as OP, step as OS
 from workloads import configs as C, tensors as T, dags as W
 from tests.gpu_helpers import MAX_ABS, REL_L2, check_parity, u16
@@ -50,7 +51,8 @@ def test_fuzz_prefill(seed):
     ten = T.make_qkv(cfg, lay)
     policy = rng.choice([0, 1])
     qp = T.bf16_randn_u16((lay.n_branches, cfg.lc, cfg.hq, cfg.d), seed, "cpu", scale=2.0)
-    out, lse, _ = run_prefill(cfg, lay, ten, qp, policy)
+    # odd seeds run the paired kernel (ORION_PLAN_PAIR: shared K/V tiles, alternating tails)
+    out, lse, _ = run_prefill(cfg, lay, ten, qp, policy, flags=orion.PLAN_PAIR if seed % 2 else 0)
     ref, _ = OP.point_prefill(lay, u16(qp), u16(ten["k_cache"][0]), u16(ten["v_cache"][0]), policy=policy)
     o = out.float().cpu().numpy().astype(np.float64)
     assert np.isfinite(o).all()
