@@ -4,6 +4,7 @@
 // blocks of a [rows, 128] bf16 tensor; blocks visited sequentially or in a random permutation,
 // from one tensor or alternating between two (K and V).
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <vector>
 #include <algorithm>
@@ -59,7 +60,9 @@ typedef CUresult (*EncFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, 
                           const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                           CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-int main() {
+int main(int argc, char** argv) {
+  // argv[1] = working set in 16 KB blocks (0: the whole 2 GiB per tensor; e.g. 2048 = 32 MB, L2-resident)
+  const int ws = argc > 1 ? atoi(argv[1]) : 0;
   const int rows = 8 * 1024 * 1024;   // 2 GiB per tensor of [rows, 128] bf16
   const int blocks = rows / 64;       // 16 KB blocks
   void *pa, *pb;
@@ -77,11 +80,11 @@ int main() {
       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   const int per_cta = (blocks / 148) & ~1;
   std::vector<int> seq(148 * per_cta), rnd(148 * per_cta);
-  for (int i = 0; i < 148 * per_cta; ++i) seq[i] = i;
+  for (int i = 0; i < 148 * per_cta; ++i) seq[i] = ws ? i % ws : i;
   std::vector<int> perm(blocks);
   for (int i = 0; i < blocks; ++i) perm[i] = i;
   std::shuffle(perm.begin(), perm.end(), std::mt19937(7));
-  for (int i = 0; i < 148 * per_cta; ++i) rnd[i] = perm[i];
+  for (int i = 0; i < 148 * per_cta; ++i) rnd[i] = ws ? perm[i] % ws : perm[i];
   int *dseq, *drnd;
   cudaMalloc(&dseq, seq.size() * 4); cudaMalloc(&drnd, rnd.size() * 4);
   cudaMemcpy(dseq, seq.data(), seq.size() * 4, cudaMemcpyHostToDevice);
