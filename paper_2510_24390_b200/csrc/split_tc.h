@@ -63,7 +63,7 @@ struct TcArgs {
   __nv_bfloat16* out;     // non-null: every row has exactly one partial (a point-prefill plan) and
   float* lse;             // the epilogue writes out = acc / l (bf16) and lse directly: no combine
   float scale_log2;
-  int32_t* work_counter;  // paired prefill plans: pair units handed out by atomicAdd (split_pair.cu)
+  int32_t* work_counter;  // items (split_tct) / pair units (split_pair) handed out by atomicAdd
 };
 
 template <int D>

@@ -587,7 +587,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------------ scheduler + Q gather
     uint32_t k = 0;                                 // ring entries published (one per range)
     uint32_t iq = 0;                                // non-empty items of this CTA
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    // Items are handed out by an atomic counter (zeroed by the launcher) in the planner's
+    // longest-first order: greedy LPT over the SMs.  A static stride left the busiest SM ~5 %
+    // above the mean (ncu sm__cycles_active max / avg on c4).
+    for (;;) {
+      int it = 0;
+      if (lane == 0) it = atomicAdd(a.work_counter, 1);
+      it = __shfl_sync(0xffffffffu, it, 0);
+      if (it >= n_items) break;
       const WorkItem w = a.items[it];
       const int nr = item_nranges(w);
       int rfirst = -1, rlast = -1;
@@ -951,6 +958,9 @@ orion_status launch_split_tct(const PlanHeader* h, const TcArgs& a, const void* 
   int grid = std::min<int>(h->n_items, num_sms > 0 ? num_sms : 148);
   if (h->max_ctas > 0) grid = std::min(grid, h->max_ctas);
   if (const char* g = getenv("ORION_DEBUG_GRID")) grid = std::max(1, std::min(grid, atoi(g)));   // debugging only
+  if (!a.work_counter) return fail(ORION_ERR_INVALID_ARG, "split_tct without a work counter");
+  const cudaError_t me = cudaMemsetAsync(a.work_counter, 0, sizeof(int32_t), st);
+  if (me != cudaSuccess) return fail(ORION_ERR_CUDA, "split_tct counter reset: %s", cudaGetErrorString(me));
   cudaError_t e = launch_pdl(tct::split_tct_kernel, dim3(grid), dim3(tct::kThreads), tct::L::BYTES, st, mk, mv,
                              mk16, mv16, a);
   if (e == cudaSuccess) e = cudaGetLastError();
