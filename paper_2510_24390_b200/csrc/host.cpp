@@ -630,7 +630,7 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
     h.acc_bytes = align16((int64_t)n_slots * shape->head_dim * 4);
     h.workspace_bytes = h.acc_bytes + align16((int64_t)n_slots * 8);
   }
-  if (paired || variant == kVariantTCT) {   // dynamic work counter (zeroed by the launcher)
+  if (variant != kVariantMmaSync) {   // the tcgen05 kernels' dynamic work counter (zeroed by the launcher)
     h.counter_off = h.workspace_bytes;
     h.workspace_bytes += 16;
   }

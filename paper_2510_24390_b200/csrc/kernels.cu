@@ -511,8 +511,7 @@ orion_status launch_split(const PlanHeader* h, const char* dplan, const void* q,
     t.kvs = kvs;
     t.scale_log2 = h->sm_scale * kLog2e;
     t.lc = h->prefill_rows > 0 ? h->prefill_rows : 1;
-    t.work_counter = (h->paired || h->variant == kVariantTCT)
-                         ? reinterpret_cast<int32_t*>(static_cast<char*>(ws) + h->counter_off) : nullptr;
+    t.work_counter = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + h->counter_off);
     if (h->variant == kVariantTCT) {
       if (D != 128) return fail(ORION_ERR_UNSUPPORTED, "transposed split kernel needs head_dim 128");
       return launch_split_tct(h, t, k, v, num_pages, st);

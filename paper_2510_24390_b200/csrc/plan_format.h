@@ -49,7 +49,7 @@ struct PlanHeader {
   int32_t n_ranges;
   int32_t paired;
   int64_t streamed_tokens;  // orion_plan_stats::streamed_tokens
-  int64_t counter_off;      // paired and kVariantTCT plans: workspace byte offset of the work counter (int32)
+  int64_t counter_off;      // tcgen05 plans: workspace byte offset of the split kernel's work counter (int32)
 };        // prefill plans: items 2u, 2u+1 run as one pair unit (split_pair.cu);
                          // items[2u].t1 = number of leading ranges the two lists share
 static_assert(sizeof(PlanHeader) % 16 == 0, "header must keep 16-byte alignment");

@@ -61,8 +61,9 @@ struct Smem {
   static constexpr int OFF_K = 2 * QB;
   static constexpr int OFF_V = OFF_K + SK * KVB;
   static constexpr int OFF_XCH = OFF_V + SV * KVB;   // WG1 -> WG0 (m, l) per row, x2
-  static constexpr int OFF_BAR = OFF_XCH + 2 * kRows * 8;
-  static constexpr int N_BAR = 2 * SK + 2 * SV + 2 + 2 + 2 + 2 + 1 + 2;
+  static constexpr int OFF_RING = OFF_XCH + 2 * kRows * 8;   // scheduled item indices
+  static constexpr int OFF_BAR = OFF_RING + 64;
+  static constexpr int N_BAR = 2 * SK + 2 * SV + 2 + 2 + 2 + 2 + 1 + 2 + 2 * 8;
   static constexpr int BYTES = OFF_BAR + N_BAR * 8 + 16;
 };
 
@@ -75,6 +76,8 @@ constexpr int kThreadsTC = 384;   // warps 0-3: TMEM alloc / idle / TMA / MMA; 4
 // steal issue slots from the softmax warps of items with <= 64 rows (TMEM lanes 0-63 are only
 // reachable from warps 4k and 4k+1, i.e. sub-partitions 0 and 1).
 constexpr int kWarpAlloc = 0, kWarpQK = 1, kWarpTMA = 2, kWarpMMA = 3;
+constexpr int kRing = 8;          // item ring entries (warp 0 schedules after TMEM allocation)
+constexpr int kRingReaders = 11;  // producer, QK and PV warps + the 8 softmax warps
 
 template <int D>
 __global__ void __launch_bounds__(kThreadsTC, 1)
@@ -97,7 +100,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   uint64_t* q_full = pv_done + 2;
   uint64_t* o_free = q_full + 2;
   uint64_t* s_free = o_free + 1;                  // softmax WG has read S[b] into registers
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_free + 2);
+  uint64_t* u_full = s_free + 2;                  // [kRing] scheduler published an item index
+  uint64_t* u_empty = u_full + kRing;             // [kRing] every reader warp took it
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(u_empty + kRing);
+  volatile int32_t* ring = reinterpret_cast<volatile int32_t*>(smem + L::OFF_RING);
   float2* xch = reinterpret_cast<float2*>(smem + L::OFF_XCH);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -111,6 +117,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     mbar_init(o_free, 128);
     mbar_init(s_free + 0, 128);
     mbar_init(s_free + 1, 128);
+    for (int s = 0; s < kRing; ++s) { mbar_init(u_full + s, 1); mbar_init(u_empty + s, kRingReaders); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmK)) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmV)) : "memory");
@@ -131,7 +138,34 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   const int n_items = a.n_items;
 
   TRACE_DECL
-  if (warp == kWarpTMA) {
+  // Items are handed out by an atomic counter (zeroed by the launcher) in plan order: greedy list
+  // scheduling over the SMs (a static grid stride left the busiest SM 19 % above the mean on the
+  // c4 point prefill).  Warp 0 publishes the k-th item this CTA runs in ring entry k (-1: done);
+  // every other role takes every entry in order.
+  auto take = [&](uint32_t k) -> int {
+    const int s = k % kRing;
+    mbar_wait(u_full + s, (k / kRing) & 1);
+    const int it = ring[s];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(u_empty + s);
+    return it;
+  };
+  if (warp == kWarpAlloc) {
+    // ------------------------------------------------------------------ scheduler
+    for (uint32_t k = 0;; ++k) {
+      const int s = k % kRing;
+      mbar_wait(u_empty + s, ((k / kRing) & 1) ^ 1);
+      int it = 0;
+      if (lane == 0) {
+        it = atomicAdd(a.work_counter, 1);
+        if (it >= n_items) it = -1;
+        ring[s] = it;
+        mbar_arrive(u_full + s);
+      }
+      it = __shfl_sync(0xffffffffu, it, 0);
+      if (it < 0) break;
+    }
+  } else if (warp == kWarpTMA) {
     // ------------------------------------------------------------------ TMA producer
     // Tiles sit on the 64-token grid.  A tile fully inside [t0, end) is fetched with one box of
     // min(64, P) token rows per page (map *_big); an item's first/last partial tile with 16-row
@@ -140,7 +174,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     uint32_t j = 0;
     const int pmask = (1 << a.page_shift) - 1;
     const int big = min(kTok, 1 << a.page_shift);          // rows of a full-tile box
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    for (uint32_t ke = 0;; ++ke) {
+      const int it = take(ke);
+      if (it < 0) break;
       const WorkItem w = a.items[it];
       for (int rg_i = 0; rg_i < item_nranges(w); ++rg_i) {
       const RangeG g = range_geom(a, w, rg_i);
@@ -222,19 +258,25 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const uint64_t dv0 = sw128_desc(smem_u32(smem + L::OFF_V), L::HALF_KV, 1024);
     struct Cur {
       int it, t, nt;
-      uint32_t k, j;
+      uint32_t k, j, e;                             // e: ring entries taken
+    };
+    auto next_ne = [&](Cur& c) {                    // next non-empty item of the ring, or the end
+      for (;;) {
+        const int it = take(c.e++);
+        if (it < 0) { c.it = n_items; c.nt = 0; return; }
+        const int nt = item_tiles(a, a.items[it]);
+        if (nt > 0) { c.it = it; c.nt = nt; return; }
+      }
     };
     auto start = [&](Cur& c) {
-      c.it = next_nonempty(a, blockIdx.x);
-      c.t = 0; c.k = 0; c.j = 0;
-      c.nt = c.it < n_items ? item_tiles(a, a.items[c.it]) : 0;
+      c.t = 0; c.k = 0; c.j = 0; c.e = 0;
+      next_ne(c);
     };
     auto advance = [&](Cur& c) {
       ++c.j;
       if (++c.t == c.nt) {
-        c.it = next_nonempty(a, c.it + gridDim.x);
+        next_ne(c);
         c.t = 0; ++c.k;
-        c.nt = c.it < n_items ? item_tiles(a, a.items[c.it]) : 0;
       }
     };
     auto issue_qk = [&](const Cur& c) {
@@ -307,7 +349,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const int r = tid - 128 - p * 128;             // query row == TMEM lane
     const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
     auto load_q = [&](int k_item, int it) {        // WG0 only
-      if (it < n_items) {
+      if (it >= 0) {
         const WorkItem w = a.items[it];
         const bool ok = r < w.n_rows;
         const __nv_bfloat16* src = a.q;
@@ -327,27 +369,34 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       }
       asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
-    int pf = next_nonempty(a, blockIdx.x);
-    if (p == 0) {                                   // Q of item 0 now, item 1 ahead
-      load_q(0, pf);
-      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-      fence_proxy_async();
-      mbar_arrive(q_full + 0);
-      if (pf < n_items) pf = next_nonempty(a, pf + gridDim.x);
-      load_q(1, pf);
-    }
-    uint32_t j = 0, k = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-      const WorkItem w = a.items[it];
-      if (item_tiles(a, w) == 0) {                 // empty (dyn end <= t0): neutral partial
-        if (p == 0 && r < w.n_rows && !a.out) {     // (direct output: prefill rows are never empty)
+    uint32_t ke = 0;                                // ring entries taken by this warp
+    auto next_item = [&]() -> int {                 // next non-empty item, or -1
+      for (;;) {
+        const int it = take(ke++);
+        if (it < 0) return -1;
+        const WorkItem w = a.items[it];
+        if (item_tiles(a, w) > 0) return it;
+        // empty (dyn end <= t0): neutral partial (direct output: prefill rows are never empty)
+        if (p == 0 && r < w.n_rows && !a.out) {
           float* dst = a.part_acc + static_cast<size_t>(w.slot0 + r) * D;
 #pragma unroll
           for (int c = 0; c < D; c += 4) *reinterpret_cast<float4*>(dst + c) = make_float4(0.f, 0.f, 0.f, 0.f);
           a.part_ml[w.slot0 + r] = make_float2(-INFINITY, 0.f);
         }
-        continue;
       }
+    };
+    int cur = next_item(), pf = -1;
+    if (p == 0) {                                   // Q of item 0 now, item 1 ahead
+      load_q(0, cur);
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      fence_proxy_async();
+      mbar_arrive(q_full + 0);
+      if (cur >= 0) pf = next_item();
+      load_q(1, pf);
+    }
+    uint32_t j = 0, k = 0;
+    while (cur >= 0) {
+      const WorkItem w = a.items[cur];
       const bool active = (warp & 3) * 32 < w.n_rows;   // warp-uniform
       // point prefill: this row's content position i; in the causal own range it sees [t0, t0 + i]
       const int rpos = ((w.row_begin + r) % (a.lc * a.group)) / a.group;
@@ -477,6 +526,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       if (p == 1) {
         xch[(k & 1) * kRows + r] = make_float2(had ? m_used : -INFINITY, l_run);
         TW(9, asm volatile("bar.sync 1, 256;\n" ::: "memory"));
+        cur = next_item();
       } else {
         TW(9, asm volatile("bar.sync 1, 256;\n" ::: "memory"));
         const float2 o1 = xch[(k & 1) * kRows + r];
@@ -530,8 +580,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
         tc_fence_before();
         mbar_arrive(o_free);
-        if (pf < n_items) pf = next_nonempty(a, pf + gridDim.x);
+        const int nx = pf;
+        pf = pf >= 0 ? next_item() : -1;
         load_q(k, pf);               // Q buffer (k & 1) is free: every QK of item k completed
+        cur = nx;
       }
       ++k;
     }
@@ -601,6 +653,9 @@ orion_status launch_split_tc(const PlanHeader* h, const TcArgs& a, const void* k
   }
   int grid = std::min<int>(h->n_items, num_sms > 0 ? num_sms : 148);
   if (h->max_ctas > 0) grid = std::min(grid, h->max_ctas);
+  if (!a.work_counter) return fail(ORION_ERR_INVALID_ARG, "split_tc without a work counter");
+  const cudaError_t me = cudaMemsetAsync(a.work_counter, 0, sizeof(int32_t), st);
+  if (me != cudaSuccess) return fail(ORION_ERR_CUDA, "split_tc counter reset: %s", cudaGetErrorString(me));
   tc::split_tc_kernel<D><<<grid, tc::kThreadsTC, tc::Smem<D>::BYTES + 1024, st>>>(mk, mv, mk16, mv16, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ORION_ERR_CUDA, "split_tc_kernel: %s", cudaGetErrorString(e));
