@@ -536,8 +536,9 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
     }
   }
   // Prefill: per kv head and branch, one multi-range item per row block: the branch's ranges in
-  // list order, then its own content tokens (causal).  Items of one query's branches are adjacent
-  // for each kv head, so the shared prefix streams through L2 for all of them at about once.
+  // list order, then its own content tokens (causal).  Items are then ordered longest context
+  // first (stable: equal-length items of a query and kv head stay adjacent) for the kernels' atomic
+  // item hand-out; a paired plan keeps generation order (pairs are adjacent items).
   if (Lc > 0) {
     std::vector<int32_t> range_off(n_branches);
     for (int32_t b = 0; b < n_branches; ++b) {
@@ -563,7 +564,7 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
           }
           n_slots += w.n_rows;
           items.push_back(w);
-          cost.push_back(0);                         // generation order kept (see above)
+          cost.push_back(logical[b]);                // context tokens: longest first
         }
       }
   }
@@ -605,7 +606,7 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
   // together and share the chunk through L2.
   std::vector<int32_t> perm(items.size());
   for (size_t i = 0; i < perm.size(); ++i) perm[i] = (int32_t)i;
-  if (Lc == 0)
+  if (Lc == 0 || !paired)
     std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) { return cost[a] > cost[b]; });
 
   // 4. Serialise.
