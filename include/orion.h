@@ -260,7 +260,9 @@ orion_status orion_kv_append(const orion_attn_shape* shape, int32_t n_branches,
  *  k_cache, v_cache, num_pages, page_table  as for orion_kv_append.
  *  own_len       device int32 [n_branches] (dyn segment lengths).
  *  h_plan, d_plan  the host plan and its device copy (same bytes).
- *  workspace     device, >= workspace_needed bytes from orion_expand_plan, 16-byte aligned.
+ *  workspace     device, >= workspace_needed bytes from orion_expand_plan, 16-byte aligned.  The
+ *                split kernels keep their work-distribution counter in it (reset by every launch,
+ *                so a workspace serves one launch at a time, in stream order).
  * Errors: INVALID_ARG (null/unaligned pointers, plan/shape mismatch, workspace too small),
  * UNSUPPORTED (shape), CUDA.
  */

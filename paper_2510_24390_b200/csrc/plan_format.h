@@ -14,7 +14,8 @@
 //     half the bytes; fp16's 2^-11 relative rounding is 4x below the bf16 rounding of out.  o is
 //     a convex combination of V rows, so |o| <= max |V|: V entries must stay within fp16 range
 //     (|v| <= 65504; include/orion.h).
-// acc_bytes = byte offset of the second array.
+// acc_bytes = byte offset of the second array.  tcgen05 plans end the workspace with 16 bytes at
+// counter_off: the split kernel's atomic item counter, zeroed by the launcher before each launch.
 #pragma once
 #include <stdint.h>
 
