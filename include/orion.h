@@ -284,7 +284,7 @@ orion_status orion_expand_attn(const orion_attn_shape* shape, int32_t n_branches
  *  q, out   bf16 [n_branches][Lc][Hq][d] (device);  lse  fp32 [n_branches][Lc][Hq], nullable.
  * Runs the rows-on-lanes tcgen05 split kernel (<= 128 query rows per work item: one MMA M tile)
  * over reader-stationary items (one item streams a branch's whole list for its rows), which
- * writes out / lse itself: no combine pass.  The workspace is unused but still validated.
+ * writes out / lse itself: no combine pass.  The workspace holds only the kernel's work counter.
  * Errors: as orion_expand_attn; INVALID_ARG if the plan is not a prefill plan (and
  * orion_expand_attn rejects prefill plans).  orion_expand_split / _combine accept both kinds.
  */
