@@ -548,8 +548,22 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
       ranges.insert(ranges.end(), branch_ranges[b].begin(), branch_ranges[b].end());
       unique_tokens += logical[b];
     }
+    // Paired plans: a query's branches (same leading range: its prefix) ordered by context length,
+    // so the two items of a pair have similar unique tails (a warpgroup whose item ended idles
+    // while its partner finishes alone).
+    std::vector<int32_t> border(n_branches);
+    for (int32_t b = 0; b < n_branches; ++b) border[b] = b;
+    if (flags & ORION_PLAN_PAIR)
+      std::stable_sort(border.begin(), border.end(), [&](int32_t x, int32_t y) {
+        const Range& rx = branch_ranges[x][0];
+        const Range& ry = branch_ranges[y][0];
+        if (rx.pt_off != ry.pt_off) return rx.pt_off < ry.pt_off;
+        if (rx.t0 != ry.t0) return rx.t0 < ry.t0;
+        return logical[x] < logical[y];
+      });
     for (int32_t g = 0; g < Hkv; ++g)
-      for (int32_t b = 0; b < n_branches; ++b) {
+      for (int32_t bi = 0; bi < n_branches; ++bi) {
+        const int32_t b = border[bi];
         const int32_t roff = (int32_t)readers.size();
         readers.push_back(b);
         for (int32_t r0 = 0; r0 < R; r0 += rows_per_item) {
