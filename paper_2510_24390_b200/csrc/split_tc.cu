@@ -5,14 +5,14 @@
 // rows per branch fill the 128-row M tile.  One persistent CTA
 // per SM walks the plan's work items (a shared piece x kv head x chunk x <= 128 rows, or for a
 // prefill plan one branch's whole range list).  Roles:
-//   warp 0           TMEM allocator (512 columns).
+//   warp 0           TMEM allocator (512 columns), then the item scheduler (atomic counter -> ring).
 //   warp 1           QK issuer: S(j) = Q.K(j)^T (tcgen05.mma kind::f16, A = Q smem, B = K smem,
-//                    M = 128 rows x N = 64 tokens) into S[j & 1] as soon as K(j) landed and the
+//                    M = 128 rows x N = 64 tokens) into S[t & 1] (t: tile index in its item) once K landed and the
 //                    softmax warpgroup has read S(j-2) out.
 //   warp 2 (1 lane)  TMA producer: K and V rings of 64-token stages (one box per page run of a
 //                    full tile, 16-row boxes on a ragged edge, 128B swizzle), page-table lookups
 //                    resolved 32 tiles at a time.
-//   warp 3           PV issuer: O[j & 1] += P(j).V(j) (A = P from TMEM, B = V smem MN-major,
+//   warp 3           PV issuer: O[t & 1] += P.V (A = P from TMEM, B = V smem MN-major,
 //                    M = 128 x N = d) as soon as P(j) is published.  Two issuers, so one
 //                    warpgroup's next S never waits behind the other's P (tcgen05.commit tracks
 //                    the issuing thread's own MMAs).
@@ -279,18 +279,23 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         c.t = 0; ++c.k;
       }
     };
+    // Tile t of an item goes to softmax warpgroup t & 1 (item-relative, so an item's arithmetic does
+    // not depend on which CTA runs it or what ran before: results are deterministic under the
+    // atomic item hand-out); n*[p] count warpgroup p's tiles for its barrier phases.
+    uint32_t nq[2] = {0, 0}, nv[2] = {0, 0};
     auto issue_qk = [&](const Cur& c) {
       const uint32_t j = c.j;
+      const uint32_t p = c.t & 1;
       if (c.t == 0) {
         TW(1, mbar_wait(q_full + (c.k & 1), (c.k >> 1) & 1));
       }
       const int s = j % SK;
       TW(2, mbar_wait(k_full + s, (j / SK) & 1));
-      if (j >= 2) TW(3, mbar_wait(s_free + (j & 1), ((j - 2) >> 1) & 1));   // S[j&1] read out
+      if (nq[p] > 0) TW(3, mbar_wait(s_free + p, (nq[p] - 1) & 1));   // S[p] read out
       tc_fence_after();
       const uint64_t dq = dq0 + static_cast<uint64_t>(((c.k & 1) * L::QB) >> 4);
       const uint64_t dk = dk0 + static_cast<uint64_t>((s * L::KVB) >> 4);
-      const uint32_t dS = tmem + colS(j & 1);
+      const uint32_t dS = tmem + colS(p);
       if (elect_one()) {
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
@@ -298,21 +303,23 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           const uint64_t offq = static_cast<uint64_t>(((ks >> 2) * L::HALF_Q + (ks & 3) * 32) >> 4);
           mma_ss(dS, dq + offq, dk + off, ID_QK, ks > 0);
         }
-        tc_commit(s_full + (j & 1));
+        tc_commit(s_full + p);
         tc_commit(k_empty + s);
       }
       __syncwarp();
+      ++nq[p];
     };
     auto issue_pv = [&](const Cur& c) {
       const uint32_t j = c.j;
+      const uint32_t p = c.t & 1;
       const int s = j % SV;
       TW(6, mbar_wait(v_full + s, (j / SV) & 1));
-      TW(4, mbar_wait(p_full + (j & 1), (j >> 1) & 1));
+      TW(4, mbar_wait(p_full + p, nv[p] & 1));
       if (c.t == 0 && c.k > 0) TW(5, mbar_wait(o_free, (c.k - 1) & 1));   // previous item's O read
       tc_fence_after();
       const uint64_t dv = dv0 + static_cast<uint64_t>((s * L::KVB) >> 4);
-      const uint32_t aP = tmem + colP(j & 1);
-      const uint32_t dO = tmem + colO(j & 1);
+      const uint32_t aP = tmem + colP(p);
+      const uint32_t dO = tmem + colO(p);
       const bool first = c.t < 2;        // first tile of this parity in the item
       if (elect_one()) {
 #pragma unroll
@@ -321,10 +328,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                  (!first || kt > 0) ? 1u : 0u);
 
         }
-        tc_commit(pv_done + (j & 1));
+        tc_commit(pv_done + p);
         tc_commit(v_empty + s);
       }
       __syncwarp();
+      ++nv[p];
     };
     // Two issuers (tcgen05.commit tracks the issuing thread's own MMAs): warp 1 issues every
     // S(j) = Q K(j)^T as soon as K(j) landed and softmax warpgroup j&1 has read S(j-2) out
@@ -394,7 +402,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       if (cur >= 0) pf = next_item();
       load_q(1, pf);
     }
-    uint32_t j = 0, k = 0;
+    uint32_t j = 0, k = 0, np = 0;                  // np: this warpgroup's tiles so far
     while (cur >= 0) {
       const WorkItem w = a.items[cur];
       const bool active = (warp & 3) * 32 < w.n_rows;   // warp-uniform
@@ -403,14 +411,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       float m_used = -INFINITY;
       float l_run = 0.f;                            // this row's sum of the bf16 P it published
       bool had = false;
-      uint32_t jl = 0;                              // last tile of this WG in the item
+      int ti = 0;                                   // tile index within the item (WG ti & 1)
       for (int rg_i = 0; rg_i < item_nranges(w); ++rg_i) {
       const RangeG g = range_geom(a, w, rg_i);
       const int row_end = g.causal ? min(g.end, g.t0 + rpos + 1) : g.end;
-      for (int t = 0; t < g.ntiles; ++t, ++j) {
-        if ((j & 1) != static_cast<uint32_t>(p)) continue;
+      for (int t = 0; t < g.ntiles; ++t, ++j, ++ti) {
+        if ((ti & 1) != p) continue;
         const int tb = g.base + t * kTok;
-        TW(6, mbar_wait(s_full + p, (j >> 1) & 1));
+        TW(6, mbar_wait(s_full + p, np & 1));
         tc_fence_after();
         uint32_t sr[64];
 #ifdef ORION_TC_TRACE
@@ -425,7 +433,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         mbar_arrive(s_free + p);                  // QK(j+2) may overwrite S[p] now
         // PV(j-2) must be complete before O_p is rescaled or P[p] rewritten; the wait is taken as
         // late as possible so that its latency overlaps this tile's exponentials.
-        bool pv_ok = j < 2;
+        bool pv_ok = np == 0;
         const bool edge = g.causal || (tb < g.t0) || (tb + kTok > g.end);
         uint32_t pk[32];
         if (active) {
@@ -449,7 +457,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           if (__any_sync(0xffffffffu, mine)) {
             const float alpha = mine ? ex2(m_used - mx) : 1.f;   // 0 when m_used == -inf
             if (had) {
-              if (!pv_ok) { TW(7, mbar_wait(pv_done + p, ((j - 2) >> 1) & 1)); pv_ok = true; }
+              if (!pv_ok) { TW(7, mbar_wait(pv_done + p, (np - 1) & 1)); pv_ok = true; }
               tc_fence_after();
 #pragma unroll 1
               for (int cb = 0; cb < D; cb += 16) {
@@ -480,7 +488,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #ifdef ORION_TC_TRACE
         tr_[1] += clock64() - ts0; ts0 = clock64();
 #endif
-        if (!pv_ok) TW(7, mbar_wait(pv_done + p, ((j - 2) >> 1) & 1));
+        if (!pv_ok) TW(7, mbar_wait(pv_done + p, (np - 1) & 1));
         tc_fence_after();
         tmem_st32x32(tmem + lane_base + colP(p), pk);
         tc_wait_st();
@@ -488,7 +496,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         tr_[2] += clock64() - ts0; ts0 = clock64();
 #endif
         if (edge) {   // zero V rows outside [t0, end) once the tile has landed (0 x NaN = NaN);
-                      // alias-free: PV(j-2) done (waited above) implies V(j - SV) landed
+                      // alias-free: S(j) landed, so K(j) and every earlier V stage, V(j - SV) included, did
           mbar_wait(v_full + (j % SV), (j / SV) & 1);
         }
         if (edge && r < kTok) {
@@ -510,7 +518,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         tr_[3] += clock64() - ts0;
 #endif
         had = true;
-        jl = j;
+        ++np;
       }
       }
       if (p == 0) {                  // next item's Q was gathered one item ahead: publish it
@@ -520,7 +528,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       }
       // ---- epilogue
       if (had) {
-        TW(8, mbar_wait(pv_done + p, (jl >> 1) & 1));      // last PV of this WG complete
+        TW(8, mbar_wait(pv_done + p, (np - 1) & 1));      // last PV of this WG complete
         tc_fence_after();
       }
       if (p == 1) {

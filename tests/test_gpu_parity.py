@@ -192,3 +192,29 @@ def test_interleaved_kv_layout(cfgname, flags):
     lay = T.make_layout(cfg, ragged=True, extra_tokens=cfg.page)
     ten = T.make_qkv(cfg, lay, q_scale=2.0)
     check_parity(cfg, lay, ten, flags=flags, interleaved=True)
+
+
+@pytest.mark.parametrize("flags", [0, orion.PLAN_ROWS_ON_LANES, orion.PLAN_MMA_SYNC])
+def test_grid_size_does_not_change_results(flags):
+    # Items are handed out by an atomic counter (any CTA may run any item); each item's arithmetic
+    # and its partial slots are fixed by the plan, so a 3-CTA grid (the ring wraps many times) and
+    # the full grid must give the same bytes.
+    cfg = C.CONFIGS["c2"].with_(layers=1)
+    lay = T.make_layout(cfg, ragged=True)
+    ten = T.make_qkv(cfg, lay)
+    dev = torch.device("cuda")
+    outs = []
+    for num_sms in (0, 3):
+        queries = [dict(n_points=int(lay.n_points[i]), edges=lay.edges[i],
+                        prefix_pt_off=int(lay.prefix_pt_off[i]), prefix_len=int(lay.prefix_len[i]))
+                   for i in range(lay.n_queries)]
+        points = np.stack([lay.point_pt_off, lay.content_len, lay.point_cap], 1)
+        batch = orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, lay.page_table,
+                                     lay.own_len, device=dev, flags=flags, num_sms=num_sms)
+        q = ten["q"][0].to(dev).contiguous()
+        out = torch.empty_like(q)
+        lse = torch.empty(q.shape[:2], dtype=torch.float32, device=dev)
+        batch.attend(q, out, ten["k_cache"][0].to(dev).contiguous(), ten["v_cache"][0].to(dev).contiguous(), lse)
+        torch.cuda.synchronize()
+        outs.append((out.cpu(), lse.cpu()))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])

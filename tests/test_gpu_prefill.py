@@ -183,3 +183,29 @@ def test_prefill_interleaved_kv_layout():
     lay = T.make_layout(cfg, ragged=True, dag_override=W.mixed8)
     ten = T.make_qkv(cfg, lay)
     check(cfg, lay, ten, q_pre(cfg, lay, scale=2.0), interleaved=True)
+
+
+@pytest.mark.parametrize("flags", PAIRING)
+def test_prefill_grid_size_does_not_change_results(flags):
+    # Atomic item (or pair-unit) hand-out: a 3-CTA grid and the full grid give the same bytes.
+    cfg = C.CONFIGS["c1"].with_(n_queries=2, lp=300, t=120, lc=32, page=32, d=128, hq=8, hkv=2)
+    lay = T.make_layout(cfg, ragged=True, dag_override=W.mixed8)
+    ten = T.make_qkv(cfg, lay)
+    qp = q_pre(cfg, lay, scale=2.0)
+    dev = torch.device("cuda")
+    res = []
+    for num_sms in (0, 3):
+        queries = [dict(n_points=int(lay.n_points[i]), edges=lay.edges[i],
+                        prefix_pt_off=int(lay.prefix_pt_off[i]), prefix_len=int(lay.prefix_len[i]))
+                   for i in range(lay.n_queries)]
+        points = np.stack([lay.point_pt_off, lay.content_len, lay.point_cap], 1)
+        batch = orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, lay.page_table,
+                                     lay.own_len, device=dev, prefill_rows=cfg.lc, flags=flags,
+                                     num_sms=num_sms)
+        q = qp.to(dev).contiguous()
+        out = torch.empty_like(q)
+        lse = torch.empty(q.shape[:3], dtype=torch.float32, device=dev)
+        batch.attend(q, out, ten["k_cache"][0].to(dev).contiguous(), ten["v_cache"][0].to(dev).contiguous(), lse)
+        torch.cuda.synchronize()
+        res.append((out.cpu(), lse.cpu()))
+    assert torch.equal(res[0][0], res[1][0]) and torch.equal(res[0][1], res[1][1])
