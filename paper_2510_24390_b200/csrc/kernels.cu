@@ -10,7 +10,8 @@
 //                         tensor cores (mma.sync m16n8k16 bf16 -> fp32), with an fp32 online
 //                         softmax in the log2 domain (row max / sum by warp shuffles).  Each
 //                         row's partial (m, l, acc) goes to the fp32 workspace.
-//   K3 combine_kernel     one warp per (branch, q head): LSE-merge of its partials in plan order,
+//   K3 combine_kernel     one warp (fp32 partials) or 8 lanes (fp16 partials) per (branch, q head):
+//                         LSE-merge of its partials in plan order,
 //                         out = acc / l rounded to bf16 (RNE), lse = ln-sum-exp.
 //
 // Semantics: include/orion.h.  Design and rooflines: DESIGN.md §"Kernels".
@@ -350,56 +351,104 @@ __global__ void __launch_bounds__(256) combine_kernel(const int32_t* __restrict_
 
 // K3 for the fp16 partial format (plan_format.h): partial i = (o_i = acc_i / l_i, lse2_i), so
 // out = sum_i 2^(lse2_i - M) o_i / sum_i 2^(lse2_i - M) and lse = (M + log2 sum) ln 2.
+// Eight lanes per row (four rows per warp, kCombRowsPerBlock per block): each lane owns D/8
+// consecutive elements (one or two 16-B loads per partial).  Lane j of a row's group holds the
+// slot and lse of partials j, j+8, ... in turn, so the dependent chain comb_off -> comb_slot ->
+// part_lse -> part_o is walked once per chunk of 8 partials (c4: ~4.4 partials per row, one
+// chunk) and the o loads of 4 partials issue together; with 4 rows per warp the grid is ~1.5
+// waves instead of ~5.5, so the chain is paid ~1.5 times, not ~5.5.  Accumulation is in the
+// fixed plan order (deterministic, and the same expression sequence as a serial loop).
+constexpr int kCombLanes = 8;
+constexpr int kCombThreads = 128;
+constexpr int kCombRowsPerBlock = kCombThreads / kCombLanes;
+
 template <int D>
-__global__ void __launch_bounds__(256) combine16_kernel(const int32_t* __restrict__ comb_off,
-                                                        const int32_t* __restrict__ comb_slot,
-                                                        const __half* __restrict__ part_o,
-                                                        const float* __restrict__ part_lse,
-                                                        __nv_bfloat16* __restrict__ out,
-                                                        float* __restrict__ lse, int n_rows) {
-  constexpr int V = D / 32;  // elements per lane
-  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(kCombThreads) combine16_kernel(const int32_t* __restrict__ comb_off,
+                                                                 const int32_t* __restrict__ comb_slot,
+                                                                 const __half* __restrict__ part_o,
+                                                                 const float* __restrict__ part_lse,
+                                                                 __nv_bfloat16* __restrict__ out,
+                                                                 float* __restrict__ lse, int n_rows) {
+  constexpr int E = D / kCombLanes;  // elements per lane (8 or 16)
+  constexpr int U = E / 8;           // 16-B loads per lane per partial
+  const int row = blockIdx.x * kCombRowsPerBlock + (threadIdx.x / kCombLanes);
+  const int sub = threadIdx.x & (kCombLanes - 1);
+  const unsigned full = 0xffffffffu;
   pdl_trigger();
   pdl_wait();
-  if (row >= n_rows) return;
-  const int e0 = __ldg(comb_off + row), e1 = __ldg(comb_off + row + 1);
-  float M = -INFINITY;
-  for (int e = e0 + lane; e < e1; e += 32) M = fmaxf(M, __ldg(part_lse + __ldg(comb_slot + e)));
+  const bool valid = row < n_rows;
+  const int e0 = valid ? __ldg(comb_off + row) : 0;
+  const int n = valid ? __ldg(comb_off + row + 1) - e0 : 0;
+  int nmax = n;  // the warp walks chunks uniformly (shuffles need every lane)
 #pragma unroll
-  for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  for (int o = 16; o >= kCombLanes; o >>= 1) nmax = max(nmax, __shfl_xor_sync(full, nmax, o));
+  // Pass 1: M = max lse2 of the row; chunk 0's slot / lse stay in registers.
+  const int slot0 = sub < n ? __ldg(comb_slot + e0 + sub) : 0;
+  const float lse0 = sub < n ? __ldg(part_lse + slot0) : -INFINITY;
+  float M = lse0;
+  for (int c = kCombLanes; c < nmax; c += kCombLanes)
+    if (c + sub < n) M = fmaxf(M, __ldg(part_lse + __ldg(comb_slot + e0 + c + sub)));
+#pragma unroll
+  for (int o = kCombLanes / 2; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(full, M, o, kCombLanes));
   const float base = M == -INFINITY ? 0.f : M;
-  float acc[V];
+  float acc[E];
 #pragma unroll
-  for (int i = 0; i < V; ++i) acc[i] = 0.f;
+  for (int i = 0; i < E; ++i) acc[i] = 0.f;
   float L = 0.f;
-  for (int e = e0; e < e1; ++e) {  // fixed plan order -> deterministic
-    const int slot = __ldg(comb_slot + e);
-    const float wgt = fast_exp2(__ldg(part_lse + slot) - base);
-    L += wgt;
-    const __half* src = part_o + static_cast<size_t>(slot) * D + lane * V;
-    if constexpr (V == 4) {
-      const uint2 x = __ldg(reinterpret_cast<const uint2*>(src));
-      const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&x.x));
-      const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&x.y));
-      acc[0] += wgt * a.x; acc[1] += wgt * a.y; acc[2] += wgt * b.x; acc[3] += wgt * b.y;
-    } else {
-      const uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(src));
-      const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&x));
-      acc[0] += wgt * a.x; acc[1] += wgt * a.y;
+  // Pass 2: weights and the weighted sum of o, chunk by chunk, 4 partials per batch.
+  for (int c = 0; c < nmax; c += kCombLanes) {
+    int slot_l = slot0;
+    float lse_l = lse0;
+    if (c > 0) {
+      slot_l = c + sub < n ? __ldg(comb_slot + e0 + c + sub) : 0;
+      lse_l = c + sub < n ? __ldg(part_lse + slot_l) : -INFINITY;
+    }
+    const float w_l = c + sub < n ? fast_exp2(lse_l - base) : 0.f;
+    const int cn = min(nmax - c, kCombLanes);
+    for (int j0 = 0; j0 < cn; j0 += 4) {
+      uint4 x[4][U];
+      float wt[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int s = __shfl_sync(full, slot_l, (j0 + j) & (kCombLanes - 1), kCombLanes);
+        wt[j] = __shfl_sync(full, w_l, (j0 + j) & (kCombLanes - 1), kCombLanes);
+        if (c + j0 + j < n) {
+          const uint4* src = reinterpret_cast<const uint4*>(part_o + static_cast<size_t>(s) * D + sub * E);
+#pragma unroll
+          for (int u = 0; u < U; ++u) x[j][u] = __ldg(src + u);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (c + j0 + j < n) {
+          L += wt[j];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const __half2* h2 = reinterpret_cast<const __half2*>(&x[j][u]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float2 f = __half22float2(h2[i]);
+              acc[u * 8 + 2 * i] += wt[j] * f.x;
+              acc[u * 8 + 2 * i + 1] += wt[j] * f.y;
+            }
+          }
+        }
+      }
     }
   }
+  if (!valid) return;
   const float inv = L > 0.f ? 1.f / L : 0.f;
-  __nv_bfloat16* o = out + static_cast<size_t>(row) * D + lane * V;
-  if constexpr (V == 4) {
-    uint2 pk;
-    pk.x = pack_bf16(acc[0] * inv, acc[1] * inv);
-    pk.y = pack_bf16(acc[2] * inv, acc[3] * inv);
-    *reinterpret_cast<uint2*>(o) = pk;
-  } else {
-    *reinterpret_cast<uint32_t*>(o) = pack_bf16(acc[0] * inv, acc[1] * inv);
+  uint4* o = reinterpret_cast<uint4*>(out + static_cast<size_t>(row) * D + sub * E);
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    uint4 pk;
+    pk.x = pack_bf16(acc[u * 8 + 0] * inv, acc[u * 8 + 1] * inv);
+    pk.y = pack_bf16(acc[u * 8 + 2] * inv, acc[u * 8 + 3] * inv);
+    pk.z = pack_bf16(acc[u * 8 + 4] * inv, acc[u * 8 + 5] * inv);
+    pk.w = pack_bf16(acc[u * 8 + 6] * inv, acc[u * 8 + 7] * inv);
+    o[u] = pk;
   }
-  if (lse && lane == 0) lse[row] = L > 0.f ? (M + log2f(L)) * kLn2 : -INFINITY;
+  if (lse && sub == 0) lse[row] = L > 0.f ? (M + log2f(L)) * kLn2 : -INFINITY;
 }
 
 // ------------------------------------------------------------------------------ K1 append
@@ -550,7 +599,8 @@ orion_status launch_combine(const PlanHeader* h, const char* dplan, void* out, f
   const int nb = (h->n_rows + 7) / 8;
   if (partials_fp16(h->variant)) {
     cudaError_t e = launch_pdl(
-        combine16_kernel<D>, dim3(nb), dim3(256), 0, st,
+        combine16_kernel<D>, dim3((h->n_rows + kCombRowsPerBlock - 1) / kCombRowsPerBlock),
+        dim3(kCombThreads), 0, st,
         reinterpret_cast<const int32_t*>(dplan + h->comb_off_off),
         reinterpret_cast<const int32_t*>(dplan + h->comb_slot_off), static_cast<const __half*>(ws),
         reinterpret_cast<const float*>(static_cast<const char*>(ws) + h->acc_bytes),
