@@ -264,7 +264,12 @@ orion_status orion_kv_append(const orion_attn_shape* shape, int32_t n_branches,
  *                split kernels keep their work-distribution counter in it (reset by every launch,
  *                so a workspace serves one launch at a time, in stream order).
  * Errors: INVALID_ARG (null/unaligned pointers, plan/shape mismatch, workspace too small),
- * UNSUPPORTED (shape), CUDA.
+ * UNSUPPORTED (shape), CUDA.  Page-table contents are not checked by the release library (K/V
+ * tiles are read by TMA, which zero-fills a box outside the cache instead of faulting): the debug
+ * build liborion_check.so (`make check`, select with ORION_LIB) walks every work item's ranges on
+ * the device before each split launch and returns INVALID_ARG naming the item for a page id
+ * outside [0, num_pages), a negative own_len or a dynamic range past n_branches; it synchronises
+ * `stream` (not CUDA-graph capturable).
  */
 orion_status orion_expand_attn(const orion_attn_shape* shape, int32_t n_branches, const void* q,
                                void* out, float* lse, const void* k_cache, const void* v_cache,

@@ -533,11 +533,87 @@ size_t split_smem_bytes() {
   return static_cast<size_t>(kRowsPerItem) * D * 2 + 2ull * kStages * kTileTokens * D * 2;
 }
 
+#ifdef ORION_CHECK
+// Debug build only (`make check` -> liborion_check.so, selected with ORION_LIB): the content
+// checks include/orion.h leaves out of the release library.  Before every split launch, each work
+// item's token ranges are walked as the kernels will walk them (tokens [t0, min(t1, own_len[dyn])),
+// plan_format.h) and every page id they read must lie in [0, num_pages); a dynamic range's branch
+// must exist and its own_len be >= 0.  The release kernels read pages through TMA, which
+// zero-fills out-of-range boxes instead of faulting, so a bad page table would otherwise give
+// silently wrong output.  The check synchronises the stream (not capturable in a CUDA graph).
+__device__ int g_check_err[4];  // first failing item + 1, what, value, index
+
+__device__ void check_report(int item, int what, int value, int index) {
+  if (atomicCAS(&g_check_err[0], 0, item + 1) == 0) {
+    g_check_err[1] = what;
+    g_check_err[2] = value;
+    g_check_err[3] = index;
+  }
+}
+
+__global__ void check_plan_kernel(const WorkItem* __restrict__ items, const Range* __restrict__ ranges,
+                                  int n_items, const int32_t* __restrict__ page_table,
+                                  const int32_t* __restrict__ own_len, int n_branches, int num_pages,
+                                  int page_shift) {
+  const int it = blockIdx.x * blockDim.x + threadIdx.x;
+  if (it >= n_items) return;
+  const WorkItem w = items[it];
+  const int nr = (w.flags & kItemRanges) ? w.n_ranges : 1;
+  for (int r = 0; r < nr; ++r) {
+    int pt_off = w.pt_off, t0 = w.t0, t1 = w.t1, dyn = w.dyn;
+    if (w.flags & kItemRanges) {
+      const Range R = ranges[w.pt_off + r];
+      pt_off = R.pt_off; t0 = R.t0; t1 = R.t1; dyn = R.dyn;
+    }
+    int end = t1;
+    if (dyn >= 0) {
+      if (dyn >= n_branches) return check_report(it, 1, dyn, r);
+      const int ol = own_len[dyn];
+      if (ol < 0) return check_report(it, 2, ol, dyn);
+      end = min(end, ol);
+    }
+    for (int t = t0 & ~((1 << page_shift) - 1); t < end; t += 1 << page_shift) {
+      const int pg = page_table[pt_off + (t >> page_shift)];
+      if (pg < 0 || pg >= num_pages) return check_report(it, 3, pg, pt_off + (t >> page_shift));
+    }
+  }
+}
+
+orion_status check_plan_contents(const PlanHeader* h, const char* dplan, const int32_t* page_table,
+                                 const int32_t* own_len, int num_pages, cudaStream_t st) {
+  static const int zero[4] = {0, 0, 0, 0};
+  int res[4] = {0, 0, 0, 0};
+  cudaError_t e = cudaMemcpyToSymbolAsync(g_check_err, zero, sizeof zero, 0, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) {
+    check_plan_kernel<<<(h->n_items + 127) / 128, 128, 0, st>>>(
+        reinterpret_cast<const WorkItem*>(dplan + h->items_off),
+        reinterpret_cast<const Range*>(dplan + h->ranges_off), h->n_items, page_table, own_len,
+        h->n_branches, num_pages, log2i(h->page_size));
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpyFromSymbolAsync(res, g_check_err, sizeof res, 0, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return fail(ORION_ERR_CUDA, "ORION_CHECK: %s", cudaGetErrorString(e));
+  static const char* what[4] = {"", "dynamic range names a branch >= n_branches", "own_len < 0",
+                                "page id outside [0, num_pages)"};
+  if (res[0])
+    return fail(ORION_ERR_INVALID_ARG, "ORION_CHECK: work item %d: %s (value %d, index %d)", res[0] - 1,
+                what[res[1] & 3], res[2], res[3]);
+  return ORION_OK;
+}
+#endif
+
 template <int D>
 orion_status launch_split(const PlanHeader* h, const char* dplan, const void* q, const void* k,
                           const void* v, int32_t num_pages, const int32_t* page_table,
                           const int32_t* own_len, void* ws, cudaStream_t st, int kvs, void* out = nullptr,
                           float* lse = nullptr) {
+#ifdef ORION_CHECK
+  {
+    const orion_status cs = check_plan_contents(h, dplan, page_table, own_len, num_pages, st);
+    if (cs != ORION_OK) return cs;
+  }
+#endif
   if (h->variant == kVariantTC || h->variant == kVariantTCT) {
     TcArgs t;
     t.out = static_cast<__nv_bfloat16*>(out);      // direct output (point-prefill plans only)
