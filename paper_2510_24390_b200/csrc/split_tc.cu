@@ -474,13 +474,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             l_run *= alpha;
           }
           const float mb = m_used == -INFINITY ? 0.f : m_used;
+          float la[4] = {0.f, 0.f, 0.f, 0.f};   // 4 chains: the mixed adds are dependent
 #pragma unroll
           for (int c = 0; c < 32; ++c) {
             pk[c] = pack_bf16(ex2(fmaf(__uint_as_float(sr[2 * c]), a.scale_log2, -mb)),
                               ex2(fmaf(__uint_as_float(sr[2 * c + 1]), a.scale_log2, -mb)));
             // l: the row sum of exactly the bf16 P that enters P.V (reading S17)
-            l_run += __uint_as_float(pk[c] << 16) + __uint_as_float(pk[c] & 0xFFFF0000u);
+            la[c & 3] = add_bf16x2_f32(pk[c], la[c & 3]);
           }
+          l_run += (la[0] + la[1]) + (la[2] + la[3]);
         } else {
 #pragma unroll
           for (int c = 0; c < 32; ++c) pk[c] = 0u;

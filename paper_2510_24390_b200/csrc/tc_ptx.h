@@ -134,6 +134,15 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
   return y;
 }
+// acc + lo + hi of a packed bf16x2 word in fp32 without unpacking: two mixed-precision adds
+// (add.rn.f32.bf16, sm_100; SASS FHADD.BF16 with a half selector) instead of shift, and, 2 FADD.
+__device__ __forceinline__ float add_bf16x2_f32(uint32_t pk, float acc) {
+  float r;
+  asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %1;\n\tadd.rn.f32.bf16 %0, lo, %2;\n\t"
+      "add.rn.f32.bf16 %0, hi, %0;\n\t}"
+      : "=f"(r) : "r"(pk), "f"(acc));
+  return r;
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
