@@ -234,6 +234,13 @@ __device__ __forceinline__ uint32_t idesc(int n, bool a_mn, bool b_mn) {   // M 
 struct RangeT {
   int32_t pt_off, t0, end, base, ntiles;
 };
+// (a, b) += (lo, hi) of a packed bf16x2 word, each in fp32: bit-identical to unpacking and adding
+// (bf16 -> f32 is exact), in two instructions (add.rn.f32.bf16 -> FHADD.BF16 with a half selector).
+__device__ __forceinline__ void add_bf16x2_f32x2(uint32_t pk, float& a, float& b) {
+  asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\tadd.rn.f32.bf16 %0, lo, %0;\n\t"
+      "add.rn.f32.bf16 %1, hi, %1;\n\t}"
+      : "+f"(a), "+f"(b) : "r"(pk));
+}
 __device__ __forceinline__ int item_nranges(const WorkItem& w) { return (w.flags & kItemRanges) ? w.n_ranges : 1; }
 __device__ __forceinline__ RangeT range_of(const TcArgs& a, const WorkItem& w, int r) {
   RangeT g;
@@ -355,12 +362,8 @@ __device__ __forceinline__ void softmax_tile(uint32_t tmem, uint32_t lane_base, 
 #pragma unroll
   for (int c = 0; c < NH; c += 2) pk[c / 2] = pack_bf16(ex2(__uint_as_float(s[c])), ex2(__uint_as_float(s[c + 1])));
 #pragma unroll
-  for (int c = 0; c < NH; c += 2) {                  // row sums of exactly the bf16 P fed to PV
-    const float2 v = __fadd2_rn(make_float2(ls[c], ls[c + 1]),
-                                make_float2(__uint_as_float(pk[c / 2] << 16), __uint_as_float(pk[c / 2] & 0xFFFF0000u)));
-    ls[c] = v.x;
-    ls[c + 1] = v.y;
-  }
+  for (int c = 0; c < NH; c += 2)                    // row sums of exactly the bf16 P fed to PV
+    add_bf16x2_f32x2(pk[c / 2], ls[c], ls[c + 1]);
   SLOT_END(9);
   if (need_pv) STW(6, mbar_wait(pv_free, pv_free_par));
 #pragma unroll
