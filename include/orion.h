@@ -361,6 +361,23 @@ orion_status orion_select_branches(int32_t n_branches, const int32_t* seg_offset
                                    int32_t segs_cap, int32_t* segs_needed);
 
 /*
+ * orion_context_base — the RoPE position base of every branch's decode token (reading M2,
+ * DESIGN.md §2): a token sits at its index in its branch's concatenated context, Eq. (2)'s
+ * Concat(Prompt_Pre, (+)_k f(k,j), P_j) order, so branch b's token in slot s of
+ * its own run is at position base[b] + s with
+ *   base[b] = sum of the effective lengths of b's bound segments that precede its OWN segment
+ *             (the first segment whose dyn == b; orion_bind_segments puts it last),
+ * effective length = len for a static segment, clamp(own_len[dyn] - start, 0, len) for a growing
+ * one (the lengths at the call, i.e. at plan time in the all-points snapshot).  Host only.
+ *  seg_offsets[n_branches+1], segs[]  bound lists;  own_len[n_branches]  host int32.
+ *  base[n_branches]  out.
+ * Errors: INVALID_ARG (null pointers, non-monotone offsets, dyn out of range, a list without its
+ * OWN segment, a base above INT32_MAX).
+ */
+orion_status orion_context_base(int32_t n_branches, const int32_t* seg_offsets, const orion_seg* segs,
+                                const int32_t* own_len, int32_t* base);
+
+/*
  * Decoder-layer steps around the attention (oracle O7; reading M1: bf16
  * storage, fp32 arithmetic).  Device; enqueued on `stream`.  The GEMMs between them are plain
  * library calls by the caller.

@@ -14,14 +14,19 @@ import numpy as np
 
 def bf16_to_f64(u16):
     """Exact widening of raw bf16 bits (uint16 array) to float64."""
-    u = np.asarray(u16, dtype=np.uint16).astype(np.uint32) << 16
+    u = np.left_shift(np.asarray(u16, dtype=np.uint16), 16, dtype=np.uint32)
     return u.view(np.float32).astype(np.float64)
 
 
 def gather_tokens(cache, pages, start, length, g, page_size):
-    """Rows [start, start+length) of the segment whose t-th token is on page pages[t // P]."""
-    t = np.arange(start, start + length)
-    return cache[np.asarray(pages, dtype=np.int64)[t // page_size], g, t % page_size]
+    """Rows [start, start+length) of the segment whose t-th token is on page pages[t // P], row
+    t % P: the pages covering the range, read whole in order, then the range cut out of them."""
+    if length <= 0:
+        return cache[:0, g, 0]
+    p0, p1 = start // page_size, (start + length - 1) // page_size + 1
+    blk = cache[np.asarray(pages, dtype=np.int64)[p0:p1], g].reshape(-1, cache.shape[-1])
+    off = start - p0 * page_size
+    return blk[off:off + length]
 
 
 def context(cache, segs, g, page_size):
@@ -45,18 +50,18 @@ def expand_attn(q_u16, k_u16, v_u16, bound, page_size, scale=None):
     """q_u16 [B,Hq,d], k/v_u16 [pages,Hkv,P,d] (raw bf16 bits); bound[b] = [(pages,start,len)].
     Returns out [B,Hq,d] float64 and lse [B,Hq] float64."""
     q = bf16_to_f64(q_u16)
-    k = bf16_to_f64(k_u16)
-    v = bf16_to_f64(v_u16)
     B, Hq, d = q.shape
-    Hkv = k.shape[1]
+    Hkv = k_u16.shape[1]
     G = Hq // Hkv
     scale = 1.0 / np.sqrt(d) if scale is None else scale
     out = np.zeros((B, Hq, d))
     lse = np.zeros((B, Hq))
     for b in range(B):
         for g in range(Hkv):
-            kc = context(k, bound[b], g, page_size)
-            vc = context(v, bound[b], g, page_size)
+            # gather the raw bf16 rows, then widen them exactly (the same values as widening the
+            # whole cache first, without materialising an fp64 copy of it)
+            kc = bf16_to_f64(context(k_u16, bound[b], g, page_size))
+            vc = bf16_to_f64(context(v_u16, bound[b], g, page_size))
             o, l = attend(q[b, g * G:(g + 1) * G], kc, vc, scale)
             out[b, g * G:(g + 1) * G] = o
             lse[b, g * G:(g + 1) * G] = l

@@ -21,7 +21,8 @@ arithmetic inside each op.  For branch b with residual x_b:
 RoPE (HF `rotate_half` convention, theta = 500000 for Llama-3): for i < d/2 with
 f_i = theta^(-2i/d) and angle = pos * f_i: out_i = x_i cos - x_{i+d/2} sin,
 out_{i+d/2} = x_{i+d/2} cos + x_i sin.  Reading M2: the position of branch b's new token is its
-index in b's concatenated context (its list order, O1/O2), i.e. |ctx(b)| - 1 after the append.
+index in b's concatenated context (its list order, O1/O2), i.e. |ctx(b)| - 1 after the append --
+`token_positions` below, computed from O2's bound lists (never from the product).
 """
 import numpy as np
 
@@ -57,6 +58,16 @@ def rope(x, pos, theta=500000.0):
     c, s = np.cos(ang), np.sin(ang)
     x1, x2 = x[..., :half], x[..., half:]
     return np.concatenate([x1 * c - x2 * s, x2 * c + x1 * s], axis=-1)
+
+
+def token_positions(bound, slot):
+    """Reading M2 -- the position of a branch's new token is its index in the branch's context
+    Concat(Prompt_Pre, (+)_k f(k,j), P_j) of Eq. (2), concatenated in list order
+    (O1 reading S9): the lengths of its bound segments before OWN (O2 puts OWN last) plus its slot in
+    its own run.  bound[b] = [(pages, start, length)] (O2, at the lengths the step starts from);
+    slot[b] = the own-run slot the token is written to.  Returns int64 [B]."""
+    return np.array([sum(int(n) for (_, _, n) in segs[:-1]) + int(s) for segs, s in zip(bound, slot)],
+                    dtype=np.int64)
 
 
 def silu(x):

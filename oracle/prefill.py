@@ -30,10 +30,8 @@ def point_prefill(layout, q_u16, k_u16, v_u16, policy=dag.ANCESTORS, branches=No
     lse [nb, Lc, Hq] f64) for `branches` (default all), one query row at a time."""
     bound = bound_segments(layout, policy, own_len)
     q = bf16_to_f64(q_u16)
-    k = bf16_to_f64(k_u16)
-    v = bf16_to_f64(v_u16)
     B, Lc, Hq, d = q.shape
-    Hkv = k.shape[1]
+    Hkv = k_u16.shape[1]
     G = Hq // Hkv
     P = layout.page_size
     scale = 1.0 / np.sqrt(d) if scale is None else scale
@@ -48,10 +46,11 @@ def point_prefill(layout, q_u16, k_u16, v_u16, policy=dag.ANCESTORS, branches=No
         own_pages, own_start, _ = segs[-1]          # OWN(j) is the last entry of every list (O1)
         assert own_start == 0
         for g in range(Hkv):
-            kc = context(k, segs[:-1], g, P) if len(segs) > 1 else np.zeros((0, d))
-            vc = context(v, segs[:-1], g, P) if len(segs) > 1 else np.zeros((0, d))
-            ko = gather_tokens(k, own_pages, 0, Lc, g, P)
-            vo = gather_tokens(v, own_pages, 0, Lc, g, P)
+            # raw bf16 rows gathered, then widened exactly (as widening the whole cache first)
+            kc = bf16_to_f64(context(k_u16, segs[:-1], g, P)) if len(segs) > 1 else np.zeros((0, d))
+            vc = bf16_to_f64(context(v_u16, segs[:-1], g, P)) if len(segs) > 1 else np.zeros((0, d))
+            ko = bf16_to_f64(gather_tokens(k_u16, own_pages, 0, Lc, g, P))
+            vo = bf16_to_f64(gather_tokens(v_u16, own_pages, 0, Lc, g, P))
             for i in range(Lc):
                 kk = np.concatenate([kc, ko[:i + 1]], axis=0)
                 vv = np.concatenate([vc, vo[:i + 1]], axis=0)

@@ -21,7 +21,7 @@ from ._lib import (OrionError, POLICY_ANCESTORS, POLICY_PARENTS_EQ3, APPEND_ADVA
                    APPEND_REWRITE, SEG_PREFIX, SEG_CONTENT, SEG_FULL, SEG_OUTPUT, SEG_OWN,
                    EDGE_NULL, EDGE_CONTEXTUAL, EDGE_DEPENDENT, SEG_DTYPE, SEGREF_DTYPE, lib)
 
-__all__ = ["dag_waves", "bind_segments", "expand_plan", "plan_stats", "kv_append", "expand_attn",
+__all__ = ["dag_waves", "bind_segments", "expand_plan", "context_base", "plan_stats", "kv_append", "expand_attn",
            "expand_split", "expand_combine",
            "ExpansionBatch", "OrionError", "version", "POLICY_ANCESTORS", "POLICY_PARENTS_EQ3",
            "APPEND_ADVANCE", "APPEND_REWRITE"]
@@ -126,6 +126,17 @@ def select_branches(seg_offsets, segs, own_len, sel):
                                            _lib.ptr(sl) if len(sl) else None, _lib.ptr(off),
                                            _lib.ptr(out), len(out), _lib.ptr(need)))
     return off, out[:int(need[0])]
+
+
+def context_base(seg_offsets, segs, own_len):
+    """orion_context_base -> np.int32 [n_branches]: per branch, the context tokens before its OWN
+    segment at the lengths own_len (reading M2: its token in own slot s sits at base + s)."""
+    so = np.ascontiguousarray(seg_offsets, dtype=np.int32)
+    sg = np.ascontiguousarray(segs).astype(SEG_DTYPE)
+    ol = np.ascontiguousarray(own_len, dtype=np.int32)
+    out = np.zeros(max(len(so) - 1, 1), np.int32)
+    _lib.check(lib().orion_context_base(len(so) - 1, _lib.ptr(so), _lib.ptr(sg), _lib.ptr(ol), _lib.ptr(out)))
+    return out[:len(so) - 1]
 
 
 PLAN_MMA_SYNC = 1        # ORION_PLAN_MMA_SYNC: legacy mma.sync split kernel
@@ -320,16 +331,9 @@ class ExpansionBatch:
         self.own_len = torch.from_numpy(own.copy()).to(dev)
 
     def pos_base(self):
-        """Per branch, the number of context tokens before its own run (its lists' segments other
-        than the last, OWN, at the current lengths): the RoPE position of its token at own slot s
-        is pos_base + s (reading M2)."""
-        own = self.own_len.cpu().numpy()
-        ln = self.segs["len"].astype(np.int64)
-        dyn = self.segs["dyn"]
-        m = dyn >= 0
-        ln[m] = np.clip(own[dyn[m]] - self.segs["start"][m], 0, ln[m])
-        so = self.seg_offsets
-        return np.array([int(ln[so[b]:so[b + 1] - 1].sum()) for b in range(self.n_branches)], np.int32)
+        """orion_context_base at the current lengths: per branch, the context tokens before its
+        own run; the RoPE position of its token at own slot s is pos_base + s (reading M2)."""
+        return context_base(self.seg_offsets, self.segs, self.own_len.cpu().numpy())
 
     def rope_append(self, qkv, q_out, k_cache, v_cache, pos_base, rope_theta=500000.0,
                     mode=APPEND_ADVANCE, stream=None):

@@ -20,7 +20,7 @@ APPEND_ADVANCE, APPEND_REWRITE = 0, 1
 EXPORTED_SYMBOLS = ("orion_dag_waves", "orion_bind_segments", "orion_expand_plan",
                     "orion_plan_get_stats", "orion_kv_append", "orion_expand_attn",
                     "orion_expand_split", "orion_expand_combine", "orion_point_prefill_attn",
-                    "orion_expansion_round", "orion_select_branches", "orion_rmsnorm",
+                    "orion_expansion_round", "orion_select_branches", "orion_context_base", "orion_rmsnorm",
                     "orion_rope_append", "orion_silu_mul", "orion_last_error", "orion_version")
 
 
@@ -102,13 +102,14 @@ def lib():
         L.orion_point_prefill_attn.argtypes = L.orion_expand_attn.argtypes
         L.orion_expansion_round.argtypes = [i32, vp, vp, vp, i32, vp, vp, vp, vp, i32, vp, vp, vp, vp]
         L.orion_select_branches.argtypes = [i32, vp, vp, vp, i32, vp, vp, vp, i32, vp]
+        L.orion_context_base.argtypes = [i32, vp, vp, vp, vp]
         L.orion_rmsnorm.argtypes = [i32, i32, vp, vp, vp, ctypes.c_float, vp, vp, vp]
         L.orion_rope_append.argtypes = [P(AttnShape), i32, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                         ctypes.c_float, i32, vp]
         L.orion_silu_mul.argtypes = [i32, i32, vp, vp, vp]
         for f in ("orion_expand_split", "orion_expand_combine", "orion_dag_waves", "orion_bind_segments", "orion_expand_plan",
                   "orion_plan_get_stats", "orion_kv_append", "orion_expand_attn", "orion_point_prefill_attn",
-                  "orion_expansion_round", "orion_select_branches", "orion_rmsnorm",
+                  "orion_expansion_round", "orion_select_branches", "orion_context_base", "orion_rmsnorm",
                   "orion_rope_append", "orion_silu_mul"):
             getattr(L, f).restype = ctypes.c_int32
         L.orion_last_error.restype = ctypes.c_char_p

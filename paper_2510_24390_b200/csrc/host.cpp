@@ -766,6 +766,30 @@ extern "C" orion_status orion_expansion_round(int32_t n_queries, const orion_que
   return ORION_OK;
 }
 
+extern "C" orion_status orion_context_base(int32_t n_branches, const int32_t* seg_offsets,
+                                           const orion_seg* segs, const int32_t* own_len,
+                                           int32_t* base) {
+  if (n_branches < 0 || !seg_offsets || (n_branches > 0 && (!segs || !own_len || !base)))
+    return fail(ORION_ERR_INVALID_ARG, "bad context_base arguments");
+  for (int32_t b = 0; b < n_branches; ++b) {
+    if (seg_offsets[b] < 0 || seg_offsets[b] > seg_offsets[b + 1])
+      return fail(ORION_ERR_INVALID_ARG, "seg_offsets not monotone at %d", b);
+    int64_t sum = 0;
+    bool own = false;
+    for (int32_t i = seg_offsets[b]; i < seg_offsets[b + 1] && !own; ++i) {
+      const orion_seg& s = segs[i];
+      if (s.dyn < -1 || s.dyn >= n_branches || s.len < 0 || s.start < 0)
+        return fail(ORION_ERR_INVALID_ARG, "branch %d segment %d: bad fields (dyn %d)", b, i, s.dyn);
+      if (s.dyn == b) { own = true; break; }
+      sum += s.dyn >= 0 ? std::min(s.len, std::max(0, own_len[s.dyn] - s.start)) : s.len;
+    }
+    if (!own) return fail(ORION_ERR_INVALID_ARG, "branch %d: list has no OWN segment (dyn == %d)", b, b);
+    if (sum > INT32_MAX) return fail(ORION_ERR_INVALID_ARG, "branch %d: position base overflows", b);
+    base[b] = (int32_t)sum;
+  }
+  return ORION_OK;
+}
+
 extern "C" orion_status orion_select_branches(int32_t n_branches, const int32_t* seg_offsets,
                                               const orion_seg* segs, const int32_t* own_len,
                                               int32_t n_sel, const int32_t* sel,

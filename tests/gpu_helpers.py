@@ -78,8 +78,13 @@ def check_parity(cfg, lay, ten, policy=0, branches=None, mode=orion.APPEND_ADVAN
     assert np.array_equal(u16(res["v_cache"]), v2), "K1 append not bit-exact (V)"
     if branches is None:
         branches = list(range(lay.n_branches))
-    ref, ref_lse = OS.expand_step(lay, u16(ten["q"][0]), k2, v2, policy=policy, branches=branches,
-                                  own_len=own)
+    if len(branches) > 128:           # full-size configs: the same oracle, in worker processes
+        from tests.oracle_pool import expand_step_parallel
+        ref, ref_lse = expand_step_parallel(lay, u16(ten["q"][0]), k2, v2, policy=policy,
+                                            branches=branches, own_len=own)
+    else:
+        ref, ref_lse = OS.expand_step(lay, u16(ten["q"][0]), k2, v2, policy=policy, branches=branches,
+                                      own_len=own)
     out = res["out"][branches]
     max_abs, rel, worst = errors(out, ref)
     lse_err = float(np.abs(res["lse"][branches].cpu().numpy() - ref_lse).max())

@@ -133,6 +133,8 @@ def test_model_steps_match_oracle(d, dagf):
     # oracle: O7 layer by layer on its own cache copies, every layer appending at the same slot
     own = lay.own_len.copy()
     bound = OS.bound_segments(lay, own_len=own + 1)
+    # positions from the oracle's own binding (reading M2), not from the product's pos_base
+    pos = DE.token_positions(OS.bound_segments(lay, own_len=own), own)
     x = x0
     kref = [u16(ten["k_cache"][l]) for l in range(L)]
     vref = [u16(ten["v_cache"][l]) for l in range(L)]
@@ -140,7 +142,7 @@ def test_model_steps_match_oracle(d, dagf):
         w = {k: f64(v) for k, v in lw.items()}
         w = dict(w_in=w["w_in"], w_qkv=w["w_qkv"], w_o=w["w_o"], w_post=w["w_post"],
                  w_gate=w["w_gu"][:, :inter], w_up=w["w_gu"][:, inter:], w_down=w["w_down"])
-        x, kref[l], vref[l] = DE.decoder_layer(x, w, kref[l], vref[l], lay, bound, own, pos_base + own, hq, hkv)
+        x, kref[l], vref[l] = DE.decoder_layer(x, w, kref[l], vref[l], lay, bound, own, pos, hq, hkv)
     got = f64(y)
     err = np.abs(got - x)
     assert np.isfinite(got).all()

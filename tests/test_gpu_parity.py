@@ -65,25 +65,58 @@ def _sample(lay, k, seed):
     return sorted(rng.sample(range(lay.n_branches), k))
 
 
-@pytest.mark.parametrize("flags", KERNELS)
-def test_c4_full_size_sampled(flags):
-    # The bench workload at full size (64 queries x mixed16, 4K prefix, 512 tok/point); outputs
-    # are checked on a sample of branches the oracle computes one by one.
-    cfg = C.CONFIGS["c4"]
+def _full_size(name, n_queries=None, **kw):
+    cfg = C.CONFIGS[name]
+    if n_queries:
+        cfg = cfg.with_(n_queries=n_queries)
     lay = T.make_layout(cfg, extra_tokens=cfg.page)
-    ten = T.make_qkv(cfg, lay, device="cuda")
-    ten = {k: v.cpu() for k, v in ten.items()}
-    check_parity(cfg, lay, ten, 0, branches=_sample(lay, 24, 4) + [lay.n_branches - 1], flags=flags)
+    ten = T.make_qkv(cfg, lay, device="cuda", **kw)       # generated on the GPU (fast), same bytes
+    return cfg, lay, {k: v.cpu() for k, v in ten.items()}
 
 
-@pytest.mark.parametrize("flags", KERNELS)
+@pytest.mark.parametrize("policy", [0, 1])
+def test_c4_full_size_every_branch(policy):
+    """The bench workload at full size (64 queries x mixed16, 4K prefix, 512 tok/point, 1024
+    branches x 32 heads), in the bench's launch configuration (default kernel and plan): every
+    branch and head element-wise against the oracle (north_star: "matches the CPU oracle on all 5
+    configs")."""
+    cfg, lay, ten = _full_size("c4")
+    r = check_parity(cfg, lay, ten, policy)
+    print(f"c4 policy {policy}: max_abs {r['max_abs']:.2e} rel_l2 {r['rel_l2']:.2e} "
+          f"worst branch {r['worst_branch_rel']:.2e} lse {r['lse_err']:.2e}")
+
+
+@pytest.mark.parametrize("variant", ["peaky", "sink"])
+def test_c4_full_size_peaky_and_sink(variant):
+    """S18: at c4's context lengths N(0,1) data gives outputs of ~1/sqrt(n_eff), so the absolute
+    gate says little; q x 4 (peaky softmax) and an attention sink (prefix token 0's K x 8) make the
+    outputs O(0.1-1) and exercise the running-max rescaling."""
+    cfg, lay, ten = _full_size("c4", q_scale=4.0 if variant == "peaky" else 1.0, sink=variant == "sink")
+    check_parity(cfg, lay, ten, 0)
+
+
+def test_c4_full_size_mma_sync_sampled():
+    cfg, lay, ten = _full_size("c4")
+    check_parity(cfg, lay, ten, 0, branches=_sample(lay, 24, 4) + [lay.n_branches - 1],
+                 flags=orion.PLAN_MMA_SYNC)
+
+
+@pytest.mark.parametrize("policy", [0, 1])
 @pytest.mark.parametrize("name", ["c5w", "c5c"])
-def test_c5_per_gpu_share_sampled(name, flags):
-    cfg = C.CONFIGS[name].with_(n_queries=8)     # one GPU's share at 8 GPUs
-    lay = T.make_layout(cfg, extra_tokens=cfg.page)
-    ten = T.make_qkv(cfg, lay, device="cuda", q_scale=2.0)
-    ten = {k: v.cpu() for k, v in ten.items()}
-    check_parity(cfg, lay, ten, 0, branches=_sample(lay, 12, 5) + [63, lay.n_branches - 1], flags=flags)
+def test_c5_per_gpu_share_every_branch(name, policy):
+    """c5 (BASELINE configs[4]) at one GPU's share of the 8-GPU run (8 queries x wide-64 / chain-64,
+    8K prefix, 512 branches): every branch and head."""
+    cfg, lay, ten = _full_size(name, n_queries=8, q_scale=2.0)
+    r = check_parity(cfg, lay, ten, policy)
+    print(f"{name} policy {policy}: max_abs {r['max_abs']:.2e} rel_l2 {r['rel_l2']:.2e} "
+          f"worst branch {r['worst_branch_rel']:.2e}")
+
+
+@pytest.mark.parametrize("name", ["c5w", "c5c"])
+def test_c5_per_gpu_share_mma_sync_sampled(name):
+    cfg, lay, ten = _full_size(name, n_queries=8, q_scale=2.0)
+    check_parity(cfg, lay, ten, 0, branches=_sample(lay, 12, 5) + [63, lay.n_branches - 1],
+                 flags=orion.PLAN_MMA_SYNC)
 
 
 def test_page_permutation_bitwise_and_determinism():

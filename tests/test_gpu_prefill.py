@@ -46,8 +46,13 @@ def check(cfg, lay, ten, qp, policy=0, branches=None, interleaved=False, flags=0
     out, lse, batch = run_prefill(cfg, lay, ten, qp, policy, interleaved, flags)
     if branches is None:
         branches = list(range(lay.n_branches))
-    ref, ref_lse = OP.point_prefill(lay, u16(qp), u16(ten["k_cache"][0]), u16(ten["v_cache"][0]),
-                                    policy=policy, branches=branches)
+    if len(branches) > 32:            # larger configs: the same oracle, in worker processes
+        from tests.oracle_pool import point_prefill_parallel
+        ref, ref_lse = point_prefill_parallel(lay, u16(qp), u16(ten["k_cache"][0]),
+                                              u16(ten["v_cache"][0]), policy=policy, branches=branches)
+    else:
+        ref, ref_lse = OP.point_prefill(lay, u16(qp), u16(ten["k_cache"][0]), u16(ten["v_cache"][0]),
+                                        policy=policy, branches=branches)
     o = out[branches].float().cpu().numpy().astype(np.float64)
     assert np.isfinite(o).all()
     diff = o - ref
@@ -130,11 +135,13 @@ def test_c2_full():
     check(cfg, lay, ten, q_pre(cfg, lay))
 
 
-def test_c4_sampled():
+def test_c4_eight_queries_every_point():
+    """c4's shapes (mixed16, 4K prefix, 512 tok/point, 32/8 heads) on an 8-query batch: every point,
+    content row and head against O5 (128 points x 32 rows x 32 heads)."""
     cfg = C.CONFIGS["c4"].with_(n_queries=8)
     lay = T.make_layout(cfg)
     ten = T.make_qkv(cfg, lay)
-    check(cfg, lay, ten, q_pre(cfg, lay), branches=[0, 5, 15, 37, lay.n_branches - 1])
+    check(cfg, lay, ten, q_pre(cfg, lay))
 
 
 def test_prefill_last_row_matches_decode_kernel():

@@ -124,6 +124,40 @@ def test_bind_matches_oracle_binding(cfgname, policy):
             assert list(lay.page_table[s["pt_off"]:s["pt_off"] + npg]) == list(pages[:npg])
 
 
+@pytest.mark.parametrize("cfgname", ["c1", "c2", "c3"])
+@pytest.mark.parametrize("policy", [0, 1])
+def test_context_base_matches_oracle_positions(cfgname, policy):
+    """orion_context_base (the product's RoPE position base, reading M2) against the oracle's own
+    derivation from O1/O2 (oracle.decoder.token_positions), at two sets of lengths."""
+    from oracle import decoder as DE
+    cfg = C.CONFIGS[cfgname].with_(n_queries=min(C.CONFIGS[cfgname].n_queries, 3))
+    lay = T.make_layout(cfg, ragged=True, extra_tokens=cfg.page)
+    offs, segs = _bind_layout(cfg, lay, policy)
+    for own in (lay.own_len, np.maximum(lay.own_len - 7, 0)):
+        got = orion.context_base(offs, segs, own)
+        want = DE.token_positions(OS.bound_segments(lay, policy, own_len=own), np.zeros_like(own))
+        assert np.array_equal(got, want)
+
+
+def test_context_base_random_dags_and_errors():
+    from oracle import decoder as DE
+    rng = random.Random(9)
+    for trial in range(60):
+        cfg = C.CONFIGS["c1"].with_(lp=rng.randint(0, 90), t=rng.randint(9, 70), lc=8, page=16)
+        n = rng.randint(1, 9)
+        dag = W.random_dag(rng, n, 0.4)
+        lay = T.make_layout(cfg, ragged=True, extra_tokens=16, dag_override=lambda: dag)
+        policy = trial % 2
+        offs, segs = _bind_layout(cfg, lay, policy)
+        got = orion.context_base(offs, segs, lay.own_len)
+        want = DE.token_positions(OS.bound_segments(lay, policy), np.zeros(lay.n_branches, np.int64))
+        assert np.array_equal(got, want)
+    bad = segs.copy()
+    bad["dyn"][offs[1] - 1] = -1                     # branch 0 loses its OWN segment
+    with pytest.raises(orion.OrionError):
+        orion.context_base(offs, bad, lay.own_len)
+
+
 # ------------------------------------------------------------------ plan parsing (test side)
 HDR = np.dtype([("magic", "<i4"), ("version", "<i4"), ("n_branches", "<i4"), ("hq", "<i4"),
                 ("hkv", "<i4"), ("d", "<i4"), ("page", "<i4"), ("group", "<i4"),

@@ -121,3 +121,104 @@ def test_zero_output_projections_leave_the_residual():
     x = DE.bf16(rng.standard_normal((lay.n_branches, 128)))
     y, _, _ = DE.decoder_layer(x, w, kc, vc, lay, OS.bound_segments(lay), own, own + 20, 4, 2)
     assert np.array_equal(y, x)
+
+
+# ---- reading M2: the RoPE position of a branch's token, derived from O1/O2 (not the product)
+def test_token_positions_closed_forms():
+    """Dependent chain (ANCESTORS: [PREFIX, FULL(1..j-1), OWN(j)]): branch j's token sits where
+    ordinary causal decode of [prefix | S_1 | ... | S_j] puts it, Lp + sum_{k<j} |S_k| + slot.
+    Wide (edgeless): Lp + slot.  Diamond under PARENTS_EQ3: point 4 reads [PREFIX, OUTPUT(2),
+    OUTPUT(3), OWN(4)] (Eq. (3) f = Output_k), so Lp + (|S_2| - Lc) + (|S_3| - Lc) +
+    slot; under ANCESTORS [PREFIX, CONTENT(1), FULL(2), FULL(3), OWN(4)]: Lp + Lc + |S_2| + |S_3|."""
+    from oracle import dag as OD
+    cfg = C.CONFIGS["c1"].with_(page=16, lp=37, t=40, lc=8, n_queries=2)
+    lay = T.make_layout(cfg, ragged=True, extra_tokens=16, dag_override=lambda: W.chain(6))
+    for slot in (lay.own_len.copy(), lay.own_len - 1):
+        pos = DE.token_positions(OS.bound_segments(lay, own_len=lay.own_len), slot)
+        for qi in range(2):
+            b0 = int(lay.branch0[qi])
+            for j in range(6):
+                want = int(lay.prefix_len[qi]) + int(lay.own_len[b0:b0 + j].sum()) + int(slot[b0 + j])
+                assert pos[b0 + j] == want
+    lay = T.make_layout(cfg, ragged=True, extra_tokens=16, dag_override=lambda: W.wide(5))
+    pos = DE.token_positions(OS.bound_segments(lay), lay.own_len)
+    assert np.array_equal(pos, lay.prefix_len[lay.branch_query] + lay.own_len)
+    lay = T.make_layout(cfg.with_(n_queries=1), ragged=True, extra_tokens=16, dag_override=W.diamond)
+    o = lay.own_len
+    pos = DE.token_positions(OS.bound_segments(lay, OD.PARENTS_EQ3), o)
+    assert pos[3] == 37 + (o[1] - 8) + (o[2] - 8) + o[3]
+    pos = DE.token_positions(OS.bound_segments(lay, OD.ANCESTORS), o)
+    assert pos[3] == 37 + 8 + o[1] + o[2] + o[3]
+    assert pos[1] == 37 + 8 + o[1] and pos[0] == 37 + o[0]
+
+
+def _hf_layer(w, hidden, hq, hkv, d, inter):
+    from transformers import LlamaConfig
+    from transformers.models.llama.modeling_llama import LlamaDecoderLayer, LlamaRotaryEmbedding
+    cfg = LlamaConfig(hidden_size=hidden, intermediate_size=inter, num_attention_heads=hq,
+                      num_key_value_heads=hkv, head_dim=d, rms_norm_eps=1e-5, rope_theta=500000.0,
+                      hidden_act="silu", attention_bias=False, mlp_bias=False,
+                      max_position_embeddings=4096)
+    cfg._attn_implementation = "eager"
+    layer = LlamaDecoderLayer(cfg, 0).double().eval()
+    sd = {"input_layernorm.weight": w["w_in"], "post_attention_layernorm.weight": w["w_post"],
+          "self_attn.q_proj.weight": w["w_qkv"][:, :hq * d].T,
+          "self_attn.k_proj.weight": w["w_qkv"][:, hq * d:(hq + hkv) * d].T,
+          "self_attn.v_proj.weight": w["w_qkv"][:, (hq + hkv) * d:].T,
+          "self_attn.o_proj.weight": w["w_o"].T, "mlp.gate_proj.weight": w["w_gate"].T,
+          "mlp.up_proj.weight": w["w_up"].T, "mlp.down_proj.weight": w["w_down"].T}
+    layer.load_state_dict({k: torch.from_numpy(np.ascontiguousarray(v)) for k, v in sd.items()})
+    return layer, LlamaRotaryEmbedding(cfg).double()
+
+
+def test_chain_positions_match_hf_causal_decode():
+    """A 2-point Dependent chain is ordinary causal decode of [prefix | S_1 | S_2] (north_star;
+    reading S6/S7): HF's LlamaDecoderLayer over that sequence in fp64 gives the last token's output;
+    O7 decodes the same token as branch 2 of the chain, its K/V history in three page runs, with the
+    positions from token_positions.  Mutations of the position rule (dropping FULL(1), counting the
+    own run twice) fail the same gate."""
+    from transformers.cache_utils import DynamicCache
+    rng = np.random.default_rng(11)
+    hidden, hq, hkv, d, inter = 128, 4, 2, 32, 192
+    Lp, T1, T2, page = 21, 30, 13, 16
+    L = Lp + T1 + T2
+    w = small_model(rng, hidden, hq, hkv, d, inter)
+    w["w_qkv"] = DE.bf16(rng.standard_normal(w["w_qkv"].shape) * 0.2)   # sharp, position-sensitive attention
+    layer, rot = _hf_layer(w, hidden, hq, hkv, d, inter)
+    x = DE.bf16(rng.standard_normal((1, L, hidden)))
+    xt = torch.from_numpy(x)
+    p = torch.arange(L)[None]
+    cos, sin = rot(xt, p)
+    mask = torch.full((L, L), float("-inf"), dtype=torch.float64).triu(1)[None, None]
+    cache = DynamicCache()
+    with torch.no_grad():
+        y_hf = layer(xt, attention_mask=mask, position_ids=p, past_key_values=cache, use_cache=True,
+                     position_embeddings=(cos, sin))
+    y_hf = (y_hf[0] if isinstance(y_hf, tuple) else y_hf)[0, -1].numpy()
+    k_all = cache.layers[0].keys[0].numpy()
+    v_all = cache.layers[0].values[0].numpy()
+    ccfg = C.CONFIGS["c1"].with_(hq=hq, hkv=hkv, d=d, page=page, lp=Lp, t=max(T1, T2), lc=4, n_queries=1)
+    lay = T.make_layout(ccfg, extra_tokens=page, dag_override=lambda: W.chain(2))
+    kc = np.zeros((lay.num_pages, hkv, page, d), np.uint16)
+    vc = np.zeros_like(kc)
+    runs = [(lay.pages_of(lay.prefix_pt_off[0], Lp), 0, Lp),
+            (lay.pages_of(lay.point_pt_off[0], T1), Lp, T1),
+            (lay.pages_of(lay.point_pt_off[1], T2), Lp + T1, T2 - 1)]
+    for pages, t0, n in runs:
+        for t in range(n):
+            kc[pages[t // page], :, t % page] = DE.to_u16(DE.bf16(k_all[:, t0 + t]))
+            vc[pages[t // page], :, t % page] = DE.to_u16(DE.bf16(v_all[:, t0 + t]))
+    own = np.array([T1, T2 - 1])                       # lengths the step starts from
+    pos = DE.token_positions(OS.bound_segments(lay, own_len=own), own)
+    assert pos[1] == L - 1
+    bound = OS.bound_segments(lay, own_len=np.array([T1, T2]))   # branch 2 after its append
+    xin = np.stack([x[0, -2], x[0, -1]])
+
+    def err(pp):
+        y, _, _ = DE.decoder_layer(xin, w, kc, vc, lay, bound, own, pp, hq, hkv)
+        return np.linalg.norm(y[1] - y_hf) / np.linalg.norm(y_hf)
+
+    assert err(pos) < 1.5e-2                            # bf16 interface rounding only
+    assert err(pos - np.array([0, T1])) > 0.1          # FULL(1) dropped from the base
+    assert err(pos + own) > 0.1                         # own run counted twice
+    assert err(pos - 1) > 0.1                           # off by one
