@@ -116,7 +116,13 @@ typedef struct { int32_t pt_off, content_len, capacity; } orion_point_desc;
  * rows-on-lanes tcgen05 kernel.  ORION_PLAN_ROWS_ON_LANES forces the rows-on-lanes tcgen05 kernel
  * (<= 128 rows per item); ORION_PLAN_MMA_SYNC the legacy mma.sync m16n8k16 + cp.async kernel
  * (<= 64 rows per item).  All variants compute the same result (same plan semantics). */
-enum { ORION_PLAN_MMA_SYNC = 1, ORION_PLAN_ROWS_ON_LANES = 2, ORION_PLAN_NO_MERGE = 4, ORION_PLAN_PAIR = 8 };
+enum { ORION_PLAN_MMA_SYNC = 1, ORION_PLAN_ROWS_ON_LANES = 2, ORION_PLAN_NO_MERGE = 4, ORION_PLAN_PAIR = 8,
+       ORION_PLAN_NO_HYBRID = 16 };
+/* Hybrid decode plans (default for head_dim 128): readers are grouped into blocks of up to 128 query
+ * rows; a block's items with 65..128 rows run on the rows-on-lanes kernel (one 128-row MMA tile
+ * reads each K/V tile once for all of them), items with <= 64 rows on the swap-AB kernel -- two
+ * launches, both writing the fp16 partial format the combine reads.  ORION_PLAN_NO_HYBRID keeps
+ * every item on the swap-AB kernel (<= 64 rows per item). */
 /* ORION_PLAN_NO_MERGE: one work item per (piece, kv head, chunk, row block) -- without it, the
  * tcgen05 decode plans group rows into fixed reader blocks and merge every chunk one block reads
  * with the same reader subset into a multi-range item (one partial per row for the lot).
@@ -260,9 +266,11 @@ orion_status orion_kv_append(const orion_attn_shape* shape, int32_t n_branches,
  *  k_cache, v_cache, num_pages, page_table  as for orion_kv_append.
  *  own_len       device int32 [n_branches] (dyn segment lengths).
  *  h_plan, d_plan  the host plan and its device copy (same bytes).
- *  workspace     device, >= workspace_needed bytes from orion_expand_plan, 16-byte aligned.  The
- *                split kernels keep their work-distribution counter in it (reset by every launch,
- *                so a workspace serves one launch at a time, in stream order).
+ *  workspace     device, >= workspace_needed bytes from orion_expand_plan, 16-byte aligned, and
+ *                ZEROED before its first use (e.g. allocated with zeros).  The split kernels keep
+ *                their work-distribution counter in its last 16 bytes; every launch leaves it zero
+ *                again (the last CTA resets it, so no memset runs between launches), so a
+ *                workspace serves one launch at a time, in stream order.
  * Errors: INVALID_ARG (null/unaligned pointers, plan/shape mismatch, workspace too small),
  * UNSUPPORTED (shape), CUDA.  Page-table contents are not checked by the release library (K/V
  * tiles are read by TMA, which zero-fills a box outside the cache instead of faulting): the debug

@@ -143,6 +143,7 @@ PLAN_MMA_SYNC = 1        # ORION_PLAN_MMA_SYNC: legacy mma.sync split kernel
 PLAN_ROWS_ON_LANES = 2   # ORION_PLAN_ROWS_ON_LANES: rows-on-lanes tcgen05 split kernel
 PLAN_NO_MERGE = 4        # ORION_PLAN_NO_MERGE: one item per piece chunk (no multi-range merging)
 PLAN_PAIR = 8            # ORION_PLAN_PAIR: point-prefill items run in pairs sharing K/V tiles (opt-in)
+PLAN_NO_HYBRID = 16      # ORION_PLAN_NO_HYBRID: every decode item on the swap-AB kernel (<= 64 rows)
 
 
 def expand_plan(hq, hkv, d, page, seg_offsets, segs, own_len=None, chunk_tokens=0, num_sms=0,
@@ -323,7 +324,8 @@ class ExpansionBatch:
         self.stats = plan_stats(self.h_plan)
         dev = torch.device(device)
         self.d_plan = torch.from_numpy(self.h_plan.copy()).to(dev)
-        self.workspace = torch.empty((ws + 15) // 16 * 4, dtype=torch.float32, device=dev)
+        # zeroed once: the split kernels' work counter must start at zero (include/orion.h)
+        self.workspace = torch.zeros((ws + 15) // 16 * 4, dtype=torch.float32, device=dev)
         self.page_table = (page_table if isinstance(page_table, torch.Tensor)
                            else torch.from_numpy(np.ascontiguousarray(page_table, np.int32)).to(dev))
         self.own_pt_off = torch.from_numpy(np.ascontiguousarray(own_pt_off, np.int32)).to(dev)

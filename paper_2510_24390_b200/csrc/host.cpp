@@ -451,6 +451,10 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
   // one multi-range item.  A Dependent chain's shared history then streams once per block as one
   // accumulation (one partial per row) instead of one short item and one partial per ancestor.
   const bool merge = Lc == 0 && variant != kVariantMmaSync && !(flags & ORION_PLAN_NO_MERGE);
+  // Hybrid (swap-AB decode plans): reader blocks of up to 128 rows; a block's items with more than
+  // 64 rows run on the rows-on-lanes kernel (MMA M = 128), the others on the swap-AB kernel.
+  const bool hybrid = merge && variant == kVariantTCT && !(flags & ORION_PLAN_NO_HYBRID);
+  std::vector<char> is_big;
   if (!merge) {
     for (size_t pi = 0; pi < pieces.size(); ++pi) {
       const Piece& p = pieces[pi];
@@ -458,20 +462,18 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
       add_items(p.pt_off, p.t0, p.t1, p.dyn, 0, p.readers, (int32_t)pi);
     }
   } else {
-    const int32_t RB = std::max(1, rows_per_item / G);
+    const int32_t RB = std::max(1, (hybrid ? kRowsPerItemBig : rows_per_item) / G);
     // Blocks are counted from each query's first branch, so a query's plan does not depend on
     // what else is in the batch (a strong-scaling shard reproduces the single-GPU plan and its
     // results bitwise).  The planner has no query ids: every list starts with its query's PREFIX
-    // segment, whose page run identifies the query.
-    std::map<int32_t, int32_t> first_branch;
-    std::vector<int32_t> qkey(n_branches);
+    // segment, whose page run identifies the query; a query is a contiguous run of branches with
+    // the same PREFIX run (two queries sharing a prefix page run are told apart unless adjacent).
+    std::vector<int32_t> qkey(n_branches), qstart(n_branches);
     for (int32_t b = 0; b < n_branches; ++b) {
       qkey[b] = h_seg_offsets[b] < h_seg_offsets[b + 1] ? h_segs[h_seg_offsets[b]].pt_off : -1 - b;
-      auto f = first_branch.find(qkey[b]);
-      if (f == first_branch.end()) first_branch.emplace(qkey[b], b);
-      else f->second = std::min(f->second, b);
+      qstart[b] = (b > 0 && qkey[b] == qkey[b - 1]) ? qstart[b - 1] : b;
     }
-    auto block_of = [&](int32_t b) { return (int64_t)qkey[b] * 1000003 + (b - first_branch[qkey[b]]) / RB; };
+    auto block_of = [&](int32_t b) { return (int64_t)qstart[b] * 1000003 + (b - qstart[b]) / RB; };
     std::map<std::pair<int32_t, std::vector<int32_t>>, int32_t> key_index;
     std::vector<std::pair<int32_t, std::vector<int32_t>>> gkeys;
     std::vector<std::vector<Range>> gchunks;
@@ -484,7 +486,7 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
         std::vector<int32_t> S;
         while (i < p.readers.size() && block_of(p.readers[i]) == blk) S.push_back(p.readers[i++]);
         const int32_t rows = (int32_t)S.size() * G;
-        int32_t ch = std::max(chunk, 32 * rows);
+        int32_t ch = std::max(chunk, 32 * std::min(rows, kRowsPerItemBig));
         ch = (ch + kTileTokens - 1) / kTileTokens * kTileTokens;
         for (int32_t g = 0; g < Hkv; ++g) {
           auto key = std::make_pair(g, S);
@@ -508,6 +510,10 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
       const int32_t g = gkeys[gi].first;
       const std::vector<int32_t>& S = gkeys[gi].second;
       const int32_t rows = (int32_t)S.size() * G;
+      // one big item (65..128 rows, hybrid), or row blocks of <= rows_per_item rows (a block of
+      // G > rows_per_item rows -- one reader -- is split, never handed to a kernel whole)
+      const bool big = hybrid && rows > rows_per_item && rows <= kRowsPerItemBig;
+      const int32_t rblk = big ? rows : rows_per_item;
       const int32_t roff = (int32_t)readers.size();
       readers.insert(readers.end(), S.begin(), S.end());
       const std::vector<Range>& cs = gchunks[gi];
@@ -524,13 +530,16 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
           w.flags = kItemRanges; w.n_ranges = (int32_t)(c1 - c0);
           ranges.insert(ranges.end(), cs.begin() + c0, cs.begin() + c1);
         }
-        w.kv_head = g; w.readers_off = roff; w.row_begin = 0; w.n_rows = rows;
-        w.slot0 = n_slots; w.piece = gpiece[gi];
-        for (int32_t r = 0; r < rows; ++r)
-          row_slots[(size_t)S[r / G] * Hq + g * G + r % G].push_back(n_slots + r);
-        n_slots += rows;
-        items.push_back(w);
-        cost.push_back(tok * (2 + (rows + 15) / 16) + 256 * (int64_t)(c1 - c0));
+        w.kv_head = g; w.readers_off = roff; w.piece = gpiece[gi];
+        for (int32_t r0 = 0; r0 < rows; r0 += rblk) {
+          w.row_begin = r0; w.n_rows = std::min(rblk, rows - r0); w.slot0 = n_slots;
+          for (int32_t r = r0; r < r0 + w.n_rows; ++r)
+            row_slots[(size_t)S[r / G] * Hq + g * G + r % G].push_back(n_slots + (r - r0));
+          n_slots += w.n_rows;
+          items.push_back(w);
+          is_big.push_back(big ? 1 : 0);
+          cost.push_back(tok * (2 + (w.n_rows + 15) / 16) + 256 * (int64_t)(c1 - c0));
+        }
         c0 = c1;
       }
     }
@@ -617,11 +626,20 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
       return fail(ORION_ERR_INVALID_ARG, "row %zu (branch %zu) has no context", r, r / ((size_t)Lrows * Hq));
 
   // Longest first; row blocks of one chunk stay adjacent (same cost, stable sort) so they run
-  // together and share the chunk through L2.
+  // together and share the chunk through L2.  A hybrid plan lists its big items first.
+  is_big.resize(items.size(), 0);
   std::vector<int32_t> perm(items.size());
   for (size_t i = 0; i < perm.size(); ++i) perm[i] = (int32_t)i;
   if (Lc == 0 || !paired)
-    std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) { return cost[a] > cost[b]; });
+    std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) {
+      if (is_big[a] != is_big[b]) return is_big[a] > is_big[b];
+      return cost[a] > cost[b];
+    });
+  int32_t n_big = 0;
+  for (size_t i = 0; i < items.size(); ++i) n_big += is_big[i];
+  for (size_t i = 0; i < items.size(); ++i)
+    if (items[i].n_rows > (is_big[i] ? kRowsPerItemBig : rows_per_item))
+      return fail(ORION_ERR_INVALID_ARG, "internal: item %zu has %d rows", i, items[i].n_rows);
 
   // 4. Serialise.
   const int64_t n_rows = (int64_t)n_branches * Lrows * Hq;
@@ -645,10 +663,11 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
     h.acc_bytes = align16((int64_t)n_slots * shape->head_dim * 4);
     h.workspace_bytes = h.acc_bytes + align16((int64_t)n_slots * 8);
   }
-  if (variant != kVariantMmaSync) {   // the tcgen05 kernels' dynamic work counter (zeroed by the launcher)
+  if (variant != kVariantMmaSync) {   // the tcgen05 kernels' work counters (kept zero between launches)
     h.counter_off = h.workspace_bytes;
-    h.workspace_bytes += 16;
+    h.workspace_bytes += n_big > 0 ? 32 : 16;
   }
+  h.n_big = n_big;
   h.n_pieces = (int64_t)pieces.size();
   h.unique_tokens = unique_tokens;
   h.logical_tokens = logical_total;
@@ -679,6 +698,11 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
   }
   coff[n_rows] = o;
   if (!ranges.empty()) std::memcpy(base + h.ranges_off, ranges.data(), ranges.size() * sizeof(Range));
+  // plan id: FNV-1a over the body, so a stale or mismatched device copy can be detected
+  uint64_t id = 1469598103934665603ull;
+  for (int64_t i = h.items_off; i < h.plan_bytes; ++i) id = (id ^ (uint8_t)base[i]) * 1099511628211ull;
+  id ^= (uint64_t)h.n_items << 32 ^ (uint64_t)(uint32_t)h.n_partials;
+  reinterpret_cast<PlanHeader*>(base)->plan_id = id;
   return ORION_OK;
 }
 

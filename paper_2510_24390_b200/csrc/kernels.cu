@@ -637,8 +637,23 @@ orion_status launch_split(const PlanHeader* h, const char* dplan, const void* q,
     t.scale_log2 = h->sm_scale * kLog2e;
     t.lc = h->prefill_rows > 0 ? h->prefill_rows : 1;
     t.work_counter = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + h->counter_off);
+    t.part16 = 0;
+    t.pdl_late = 0;
     if (h->variant == kVariantTCT) {
       if (D != 128) return fail(ORION_ERR_UNSUPPORTED, "transposed split kernel needs head_dim 128");
+      if (h->n_big > 0) {
+        // hybrid plan: items [0, n_big) (65..128 rows) on the rows-on-lanes kernel, writing the
+        // fp16 partial format, then [n_big, n_items) on the swap-AB kernel with its own counter
+        TcArgs tb = t;
+        tb.n_items = h->n_big;
+        tb.part16 = 1;
+        const orion_status s1 = launch_split_tc<D>(h, tb, k, v, num_pages, st);
+        if (s1 != ORION_OK || h->n_big == h->n_items) return s1;
+        t.items += h->n_big;
+        t.n_items = h->n_items - h->n_big;
+        t.work_counter += 4;
+        t.pdl_late = 1;
+      }
       return launch_split_tct(h, t, k, v, num_pages, st);
     }
     return launch_split_tc<D>(h, t, k, v, num_pages, st);

@@ -27,6 +27,7 @@ constexpr int kRowsPerItemTC = 128;  // query rows per work item, tcgen05 kernel
 constexpr int kRowsPerItemMMA = 64;  // query rows per work item, mma.sync kernel (4 warps x m16)
 constexpr int kRowsPerItem = kRowsPerItemMMA;  // smem sizing of the mma.sync kernel
 constexpr int kRowsPerItemTCT = 64;  // query rows per work item, transposed tcgen05 kernel (MMA N)
+constexpr int kRowsPerItemBig = 128; // hybrid decode plans: rows of a big item (rows-on-lanes kernel, MMA M)
 enum : int32_t { kVariantTC = 0, kVariantMmaSync = 1, kVariantTCT = 2 };
 inline bool partials_fp16(int32_t variant) { return variant == kVariantTCT; }
 constexpr int32_t kItemCausal = 1;
@@ -50,7 +51,12 @@ struct PlanHeader {
   int32_t n_ranges;
   int32_t paired;
   int64_t streamed_tokens;  // orion_plan_stats::streamed_tokens
-  int64_t counter_off;      // tcgen05 plans: workspace byte offset of the split kernel's work counter (int32)
+  int64_t counter_off;      // tcgen05 plans: workspace byte offset of the split kernels' work counters
+                            // (16 bytes each: the first kernel's, then a hybrid plan's second one)
+  int32_t n_big;            // kVariantTCT hybrid plans: items [0, n_big) have 65..128 rows and run on the
+                            // rows-on-lanes kernel (fp16 partials); [n_big, n_items) on the swap-AB kernel
+  int32_t pad0;
+  uint64_t plan_id;         // FNV-1a of the serialised plan body: the host and device copies must match
 };        // prefill plans: items 2u, 2u+1 run as one pair unit (split_pair.cu);
                          // items[2u].t1 = number of leading ranges the two lists share
 static_assert(sizeof(PlanHeader) % 16 == 0, "header must keep 16-byte alignment");

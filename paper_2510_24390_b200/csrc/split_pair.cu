@@ -570,6 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
   }
+  if (threadIdx.x == 0) release_work_counter(a.work_counter);
 }
 
 }  // namespace tcp
@@ -583,8 +584,6 @@ orion_status launch_split_pair(const PlanHeader* h, const TcArgs& a, const CUten
     return fail(ORION_ERR_CUDA, "cudaFuncSetAttribute(split_pair): %s", cudaGetErrorString(attr_err));
   const int n_units = (h->n_items + 1) / 2;
   if (!a.work_counter) return fail(ORION_ERR_INVALID_ARG, "paired plan without a work counter");
-  const cudaError_t me = cudaMemsetAsync(a.work_counter, 0, sizeof(int32_t), st);
-  if (me != cudaSuccess) return fail(ORION_ERR_CUDA, "split_pair counter reset: %s", cudaGetErrorString(me));
   int grid = std::min<int>(n_units, num_sms > 0 ? num_sms : 148);
   if (h->max_ctas > 0) grid = std::min(grid, h->max_ctas);
   tcp::split_pair_kernel<D><<<grid, tcp::kThreads, tcp::Smem<D>::BYTES + 1024, st>>>(maps[0], maps[1], maps[2],

@@ -136,6 +136,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int n_items = a.n_items;
+  // Programmatic dependent launch: wait for the previous kernel (the KV append) first, then let
+  // the next one launch -- a hybrid plan's second split kernel relies on this order (it starts
+  // without its own wait once this kernel has triggered; split_tc.h TcArgs::pdl_late).
+  pdl_wait();
+  pdl_trigger();
 
   TRACE_DECL
   // Items are handed out by an atomic counter (zeroed by the launcher) in plan order: greedy list
@@ -386,10 +391,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         if (item_tiles(a, w) > 0) return it;
         // empty (dyn end <= t0): neutral partial (direct output: prefill rows are never empty)
         if (p == 0 && r < w.n_rows && !a.out) {
-          float* dst = a.part_acc + static_cast<size_t>(w.slot0 + r) * D;
+          if (a.part16) {
+            uint4* dst = reinterpret_cast<uint4*>(a.part_o + static_cast<size_t>(w.slot0 + r) * D);
 #pragma unroll
-          for (int c = 0; c < D; c += 4) *reinterpret_cast<float4*>(dst + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-          a.part_ml[w.slot0 + r] = make_float2(-INFINITY, 0.f);
+            for (int c = 0; c < D / 8; ++c) dst[c] = make_uint4(0, 0, 0, 0);
+            a.part_lse[w.slot0 + r] = -INFINITY;
+          } else {
+            float* dst = a.part_acc + static_cast<size_t>(w.slot0 + r) * D;
+#pragma unroll
+            for (int c = 0; c < D; c += 4) *reinterpret_cast<float4*>(dst + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+            a.part_ml[w.slot0 + r] = make_float2(-INFINITY, 0.f);
+          }
         }
       }
     };
@@ -577,6 +589,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                   pk2.x = pack_bf16(v.x * inv, v.y * inv);
                   pk2.y = pack_bf16(v.z * inv, v.w * inv);
                   *reinterpret_cast<uint2*>(a.out + orow * D + cb + c) = pk2;
+                } else if (a.part16) {   // fp16 partial format (plan_format.h): o = acc / l
+                  __half2 h0 = __floats2half2_rn(v.x * inv, v.y * inv);
+                  __half2 h1 = __floats2half2_rn(v.z * inv, v.w * inv);
+                  uint2 pk2;
+                  pk2.x = *reinterpret_cast<uint32_t*>(&h0);
+                  pk2.y = *reinterpret_cast<uint32_t*>(&h1);
+                  *reinterpret_cast<uint2*>(a.part_o + static_cast<size_t>(w.slot0 + r) * D + cb + c) = pk2;
                 } else {
                   *reinterpret_cast<float4*>(dst + cb + c) = v;
                 }
@@ -585,7 +604,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           }
         }
         if (r < w.n_rows) {
-          if (!a.out) a.part_ml[w.slot0 + r] = make_float2(M, Lr);
+          if (a.part16) a.part_lse[w.slot0 + r] = Lr > 0.f ? M + log2f(Lr) : -INFINITY;
+          else if (!a.out) a.part_ml[w.slot0 + r] = make_float2(M, Lr);
           else if (a.lse) a.lse[orow] = Lr > 0.f ? (M + log2f(Lr)) * 0.69314718055994531f : -INFINITY;
         }
         tc_fence_before();
@@ -606,6 +626,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
   }
+  if (threadIdx.x == 0) release_work_counter(a.work_counter);
 }
 
 }  // namespace tc
@@ -617,16 +638,15 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 EncodeTiledFn get_encode() {
-  static EncodeTiledFn fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  // C++11 function-local static: initialised exactly once, thread-safe.
+  static const EncodeTiledFn fn = []() -> EncodeTiledFn {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  }
+      return reinterpret_cast<EncodeTiledFn>(p);
+    return nullptr;
+  }();
   return fn;
 }
 
@@ -664,10 +684,9 @@ orion_status launch_split_tc(const PlanHeader* h, const TcArgs& a, const void* k
   int grid = std::min<int>(h->n_items, num_sms > 0 ? num_sms : 148);
   if (h->max_ctas > 0) grid = std::min(grid, h->max_ctas);
   if (!a.work_counter) return fail(ORION_ERR_INVALID_ARG, "split_tc without a work counter");
-  const cudaError_t me = cudaMemsetAsync(a.work_counter, 0, sizeof(int32_t), st);
-  if (me != cudaSuccess) return fail(ORION_ERR_CUDA, "split_tc counter reset: %s", cudaGetErrorString(me));
-  tc::split_tc_kernel<D><<<grid, tc::kThreadsTC, tc::Smem<D>::BYTES + 1024, st>>>(mk, mv, mk16, mv16, a);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(tc::split_tc_kernel<D>, dim3(grid), dim3(tc::kThreadsTC), tc::Smem<D>::BYTES + 1024, st,
+                             mk, mv, mk16, mv16, a);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ORION_ERR_CUDA, "split_tc_kernel: %s", cudaGetErrorString(e));
   return ORION_OK;
 }

@@ -30,6 +30,20 @@ cudaError_t ensure_dynamic_smem(const void* func, int bytes);
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
+// Work counter of the persistent split kernels: counter[0] hands out items (atomicAdd), counter[1]
+// counts finished CTAs.  The last CTA to finish zeroes both, so the next launch on the same
+// workspace starts from zero with no memset between the previous kernel and this one (a memset
+// node would break the programmatic-dependent-launch chain append -> split).  The workspace's
+// counter words must be zero before its first launch (include/orion.h).  Called by one thread per
+// CTA after the CTA's last access to the counter.
+__device__ __forceinline__ void release_work_counter(int32_t* counter) {
+  __threadfence();
+  if (atomicAdd(counter + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+    atomicExch(counter, 0);
+    atomicExch(counter + 1, 0);
+  }
+}
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                        Args&&... args) {
@@ -64,6 +78,11 @@ struct TcArgs {
   float* lse;             // the epilogue writes out = acc / l (bf16) and lse directly: no combine
   float scale_log2;
   int32_t* work_counter;  // items (split_tct) / pair units (split_pair) handed out by atomicAdd
+  int32_t part16;         // rows-on-lanes kernel on a hybrid plan's big items: write the fp16 partial
+                          // format (part_o = acc / l, part_lse = m + log2 l) instead of fp32
+  int32_t pdl_late;       // second kernel of a hybrid step: it may start once the first kernel has
+                          // passed its own dependency wait (the step's inputs are complete) and waits
+                          // for the first kernel's completion only before it exits
 };
 
 template <int D>

@@ -38,6 +38,7 @@
 #include "../../include/orion.h"
 #include "plan_format.h"
 #include "split_tc.h"
+#include "tc_ptx.h"
 #include "tmem_ops.h"
 
 namespace orion {
@@ -79,63 +80,29 @@ struct L {
 };
 static_assert(L::BYTES <= 232448, "shared memory budget");
 
-// ------------------------------------------------------------------------------ PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(c));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(smem_u32(b)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ int g_orion_dump[1024];   // debugging: a timed-out wait asks every role of the CTA to report
+// PTX helpers shared with the rows-on-lanes kernels (tc_ptx.h): mbarrier, TMA, tcgen05.
+using tc::smem_u32;
+using tc::mbar_init;
+using tc::mbar_arrive;
+using tc::mbar_expect_tx;
+using tc::mbar_wait;
+using tc::elect_one;
+using tc::fence_proxy_async;
+using tc::tc_fence_before;
+using tc::tc_fence_after;
+using tc::tc_commit;
+using tc::tc_wait_ld;
+using tc::tc_wait_st;
+using tc::mma_ss;
+using tc::tma_load_2d;
+using tc::cp_async16;
+using tc::ex2;
+using tc::pack_bf16;
+using tc::sw128_desc;
 
-// Blocking wait.  try_wait carries a suspend-time hint so a waiting warp sleeps instead of
-// spinning (it resumes as soon as the phase completes); a protocol bug traps after ~2 s instead of
-// hanging the GPU.
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  const uint32_t a = smem_u32(b);
-  uint32_t ok;
-  asm volatile(
-      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(ok)
-      : "r"(a), "r"(parity), "r"(20000u)
-      : "memory");
-  if (ok) return;
-  const long long t0 = clock64();
-  for (;;) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(a), "r"(parity), "r"(20000u)
-        : "memory");
-    if (ok) return;
-    if (clock64() - t0 > (4ll << 30)) {
-      printf("ORION DEADLOCK blk %d warp %d lane %d bar_off %u parity %u\n", blockIdx.x, threadIdx.x >> 5,
-             threadIdx.x & 31, a & 0xFFFF, parity);
-      atomicExch(&g_orion_dump[blockIdx.x & 1023], 1);
-      const long long t1 = clock64();
-      while (clock64() - t1 < (1ll << 30)) {}   // give the other roles time to report
-      __trap();
-    }
-  }
-}
-// Non-blocking probe of a phase (warp-uniform: lane 0 decides).
-__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(b)), "r"(parity)
-      : "memory");
-  return __shfl_sync(0xffffffffu, ok, 0) != 0;
-}
+#undef TRACE_DECL
+#undef TW
+#undef TRACE_DUMP
 #ifdef ORION_TC_TRACE
 #define TRACE_DECL unsigned long long tr_[12] = {0}; const unsigned long long tr_t0 = clock64();
 #define TRP tr_
@@ -156,50 +123,6 @@ __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
 #define STW(slot, stmt) stmt
 #endif
 
-__device__ __forceinline__ bool elect_one() {
-  uint32_t pred = 0;
-  asm volatile("{\n .reg .b32 rx;\n .reg .pred px;\n elect.sync rx|px, %1;\n @px mov.s32 %0, 1;\n}\n"
-               : "+r"(pred)
-               : "r"(0xFFFFFFFFu));
-  return pred != 0;
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
-__device__ __forceinline__ void tc_commit(uint64_t* b) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(b))
-               : "memory");
-}
-__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
-__device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
-__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
-  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-               "l"(a), "l"(b), "r"(id), "r"(acc)
-               : "memory");
-}
-__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t id, uint32_t acc) {
-  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
-               "r"(a), "l"(b), "r"(id), "r"(acc)
-               : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool ok) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0));
-}
-__device__ __forceinline__ float ex2(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
 __device__ __forceinline__ float warp_max(float v) {
   float r;
   asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;\n" : "=f"(r) : "f"(v));
@@ -216,15 +139,6 @@ __device__ __forceinline__ bool wg_any(bool v, int id) {
 }
 __device__ __forceinline__ void wg_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
 
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
-  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
-  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
-  d |= static_cast<uint64_t>(1) << 46;
-  d |= static_cast<uint64_t>(2) << 61;
-  return d;
-}
 __device__ __forceinline__ uint32_t idesc(int n, bool a_mn, bool b_mn) {   // M = 128, bf16 -> fp32
   return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
          (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
@@ -544,7 +458,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                      const __grid_constant__ CUtensorMap tmK16, const __grid_constant__ CUtensorMap tmV16,
                      const TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  if (smem_u32(smem) & 1023) __trap();               // 128B-swizzle atoms need 1 KB alignment
   const Bars bars = carve_bars(smem);
   uint64_t *k_full = bars.k_full, *k_empty = bars.k_empty, *v_full = bars.v_full, *v_empty = bars.v_empty;
   uint64_t *s_full = bars.s_full, *s_free = bars.s_free, *p_full = bars.p_full, *pv_done = bars.pv_done;
@@ -582,7 +495,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_trigger();
-  pdl_wait();                                        // KV appended / previous step's reads done
+  // KV appended / previous step's reads done.  A hybrid plan's second kernel (pdl_late) was
+  // launched only once the first had passed this wait, so it defers its own wait to the end.
+  if (!a.pdl_late) pdl_wait();
   const int n_items = a.n_items;
 
   TRACE_DECL
@@ -911,6 +826,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
   }
+  if (tid == 0) release_work_counter(a.work_counter);
+  if (a.pdl_late) pdl_wait();                        // complete only after the first kernel (combine reads both)
 }
 
 }  // namespace tct
@@ -920,16 +837,15 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 EncodeTiledFn get_encode_t() {
-  static EncodeTiledFn fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  // C++11 function-local static: initialised exactly once, thread-safe.
+  static const EncodeTiledFn fn = []() -> EncodeTiledFn {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  }
+      return reinterpret_cast<EncodeTiledFn>(p);
+    return nullptr;
+  }();
   return fn;
 }
 bool make_map_t(CUtensorMap* m, const void* base, int64_t rows, int box_rows) {
@@ -960,10 +876,10 @@ orion_status launch_split_tct(const PlanHeader* h, const TcArgs& a, const void* 
     return fail(ORION_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   int grid = std::min<int>(h->n_items, num_sms > 0 ? num_sms : 148);
   if (h->max_ctas > 0) grid = std::min(grid, h->max_ctas);
-  if (const char* g = getenv("ORION_DEBUG_GRID")) grid = std::max(1, std::min(grid, atoi(g)));   // debugging only
+#ifdef ORION_CHECK
+  if (const char* g = getenv("ORION_DEBUG_GRID")) grid = std::max(1, std::min(grid, atoi(g)));   // debug build only
+#endif
   if (!a.work_counter) return fail(ORION_ERR_INVALID_ARG, "split_tct without a work counter");
-  const cudaError_t me = cudaMemsetAsync(a.work_counter, 0, sizeof(int32_t), st);
-  if (me != cudaSuccess) return fail(ORION_ERR_CUDA, "split_tct counter reset: %s", cudaGetErrorString(me));
   cudaError_t e = launch_pdl(tct::split_tct_kernel, dim3(grid), dim3(tct::kThreads), tct::L::BYTES, st, mk, mv,
                              mk16, mv16, a);
   if (e == cudaSuccess) e = cudaGetLastError();

@@ -35,24 +35,29 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
-// Bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU.
+// Blocking wait on a phase parity.  try_wait carries a suspend-time hint, so a waiting warp sleeps
+// instead of spinning and resumes as soon as the phase completes.  Release builds wait without a
+// bound; the debug builds (ORION_WATCHDOG: `make check`, `make trace`) trap after ~2^22 polls so a
+// protocol bug shows up as a kernel error instead of a hung GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   const uint32_t a = smem_u32(b);
+#ifdef ORION_WATCHDOG
   for (uint32_t spin = 0;; ++spin) {
+#else
+  for (;;) {
+#endif
     uint32_t ok;
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(ok)
-        : "r"(a), "r"(parity)
+        : "r"(a), "r"(parity), "r"(20000u)
         : "memory");
     if (ok) return;
-#ifdef ORION_TC_TRACE
-    if (spin == (1u << 22))   // report every stuck waiter, then give the others time to report
-      printf("mbar timeout blk %d warp %d lane %d bar smem 0x%x parity %u\n", blockIdx.x, threadIdx.x >> 5,
-             threadIdx.x & 31, a, parity);
-    if (spin > (1u << 24)) __trap();
-#else
-    if (spin > (1u << 22)) __trap();
+#ifdef ORION_WATCHDOG
+    if (spin == (1u << 22))
+      printf("orion watchdog: mbarrier wait blk %d warp %d lane %d bar smem 0x%x parity %u\n", blockIdx.x,
+             threadIdx.x >> 5, threadIdx.x & 31, a, parity);
+    if (spin > (1u << 22) + (1u << 20)) __trap();
 #endif
   }
 }

@@ -101,13 +101,15 @@ def test_c4_full_size_mma_sync_sampled():
                  flags=orion.PLAN_MMA_SYNC)
 
 
+@pytest.mark.parametrize("flags", [0, orion.PLAN_NO_HYBRID])
 @pytest.mark.parametrize("policy", [0, 1])
 @pytest.mark.parametrize("name", ["c5w", "c5c"])
-def test_c5_per_gpu_share_every_branch(name, policy):
+def test_c5_per_gpu_share_every_branch(name, policy, flags):
     """c5 (BASELINE configs[4]) at one GPU's share of the 8-GPU run (8 queries x wide-64 / chain-64,
-    8K prefix, 512 branches): every branch and head."""
+    8K prefix, 512 branches): every branch and head; the default hybrid plan (>64-row items on the
+    rows-on-lanes kernel) and the swap-AB-only plan."""
     cfg, lay, ten = _full_size(name, n_queries=8, q_scale=2.0)
-    r = check_parity(cfg, lay, ten, policy)
+    r = check_parity(cfg, lay, ten, policy, flags=flags)
     print(f"{name} policy {policy}: max_abs {r['max_abs']:.2e} rel_l2 {r['rel_l2']:.2e} "
           f"worst branch {r['worst_branch_rel']:.2e}")
 
@@ -117,6 +119,30 @@ def test_c5_per_gpu_share_mma_sync_sampled(name):
     cfg, lay, ten = _full_size(name, n_queries=8, q_scale=2.0)
     check_parity(cfg, lay, ten, 0, branches=_sample(lay, 12, 5) + [63, lay.n_branches - 1],
                  flags=orion.PLAN_MMA_SYNC)
+
+
+@pytest.mark.parametrize("flags", [0, orion.PLAN_NO_HYBRID])
+@pytest.mark.parametrize("hq,hkv", [(128, 1), (96, 1), (64, 2)])
+def test_wide_head_groups(hq, hkv, flags):
+    """G = Hq / Hkv at or above the kernels' row limits: one reader's rows are split into
+    row blocks (or form one 128-row item on the rows-on-lanes kernel) -- every row written."""
+    cfg = C.CONFIGS["c1"].with_(hq=hq, hkv=hkv, d=128, page=32, lp=260, t=90, lc=16, n_queries=2,
+                                dag="mixed8")
+    lay = T.make_layout(cfg, ragged=True, extra_tokens=32)
+    ten = T.make_qkv(cfg, lay, q_scale=2.0)
+    check_parity(cfg, lay, ten, 0, chunk_tokens=128, flags=flags)
+
+
+@pytest.mark.parametrize("policy", [0, 1])
+def test_hybrid_c3_and_chain(policy):
+    """Hybrid plans (both kernels in one step) on c3 and a Dependent chain of 40 points."""
+    cfg = C.CONFIGS["c3"].with_(lp=1000)
+    lay = T.make_layout(cfg, ragged=True, extra_tokens=cfg.page)
+    check_parity(cfg, lay, T.make_qkv(cfg, lay, q_scale=2.0), policy)
+    cfg = C.CONFIGS["c5c"].with_(n_queries=2, lp=700, t=80, lc=16)
+    lay = T.make_layout(cfg, ragged=True, extra_tokens=cfg.page, dag_override=lambda: W.chain(40, 2))
+    r = check_parity(cfg, lay, T.make_qkv(cfg, lay, q_scale=2.0), policy)
+    assert r["res"]["batch"].stats["n_items"] > 0
 
 
 def test_page_permutation_bitwise_and_determinism():

@@ -167,7 +167,8 @@ HDR = np.dtype([("magic", "<i4"), ("version", "<i4"), ("n_branches", "<i4"), ("h
                 ("acc_bytes", "<i8"), ("n_pieces", "<i8"), ("unique_tokens", "<i8"),
                 ("logical_tokens", "<i8"), ("sm_scale", "<f4"), ("pad", "<i4", 3),
                 ("ranges_off", "<i8"), ("n_ranges", "<i4"), ("paired", "<i4"),
-                ("streamed_tokens", "<i8"), ("counter_off", "<i8")])
+                ("streamed_tokens", "<i8"), ("counter_off", "<i8"), ("n_big", "<i4"), ("pad0", "<i4"),
+                ("plan_id", "<u8")])
 RANGE = np.dtype([(n, "<i4") for n in ("pt_off", "t0", "t1", "dyn", "flags", "r0", "r1", "r2")])
 ITEM = np.dtype([(n, "<i4") for n in ("pt_off", "t0", "t1", "dyn", "kv_head", "readers_off",
                                       "row_begin", "n_rows", "slot0", "piece", "p0", "p1")])
@@ -182,8 +183,9 @@ def parse_plan(plan):
     return h, items, readers, coff, cslot
 
 
-def _check_plan_covers(cfg, lay, offs, segs, own_len):
-    plan, ws = orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, own_len, chunk_tokens=128)
+def _check_plan_covers(cfg, lay, offs, segs, own_len, flags=0):
+    plan, ws = orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, own_len, chunk_tokens=128,
+                                 flags=flags)
     h, items, readers, coff, cslot = parse_plan(plan)
     G = cfg.hq // cfg.hkv
     assert h["magic"] == 0x314e524f and h["n_rows"] == lay.n_branches * cfg.hq
@@ -407,6 +409,24 @@ def test_prefill_plan_errors():
     assert b"prefill" in L.orion_last_error()
 
 
+@pytest.mark.parametrize("hq,hkv", [(128, 1), (256, 2), (96, 1)])
+@pytest.mark.parametrize("flags", [0, 16])          # hybrid (default) / ORION_PLAN_NO_HYBRID
+def test_plan_splits_rows_of_wide_groups(hq, hkv, flags):
+    """G = Hq / Hkv above a kernel's row limit (64 swap-AB, 128 rows-on-lanes): one reader's rows
+    alone exceed an item, so the planner must split them into row blocks (never an item with more
+    rows than its kernel handles), and every row is still covered exactly once."""
+    cfg = C.CONFIGS["c1"].with_(hq=hq, hkv=hkv, d=128, page=16, lp=80, t=48, lc=8, n_queries=2,
+                                dag="mixed8")
+    lay = T.make_layout(cfg, ragged=True, extra_tokens=16)
+    offs, segs = _bind_layout(cfg, lay, 0)
+    h = _check_plan_covers(cfg, lay, offs, segs, lay.own_len, flags=flags)
+    plan, _ = orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, lay.own_len, flags=flags)
+    h, items, *_ = parse_plan(plan)
+    nb = int(h["n_big"])
+    assert (items["n_rows"][:nb] <= 128).all() and (items["n_rows"][nb:] <= 64).all()
+    assert (nb > 0) == (flags == 0 and hq // hkv in (96, 128))
+
+
 def test_chain_plan_merges_history_per_reader_block():
     # Dependent chain under ANCESTORS: point j reads the full runs of points 1..j-1.  With fixed
     # reader blocks, a block's shared history becomes multi-range items (kItemRanges) -- far fewer
@@ -414,12 +434,22 @@ def test_chain_plan_merges_history_per_reader_block():
     cfg = C.CONFIGS["c5c"].with_(n_queries=1, lp=512, t=96, lc=16, dag="chain64")
     lay = T.make_layout(cfg, dag_override=lambda: W.chain(48, 2))
     offs, segs = _bind_layout(cfg, lay, 0)
-    merged, _ = orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, lay.own_len)
+    merged, _ = orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, lay.own_len,
+                                  flags=orion.PLAN_NO_HYBRID)
+    hybrid, _ = orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, lay.own_len)
     plain, _ = orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, lay.own_len,
                                  flags=orion.PLAN_NO_MERGE)
     hm, im, *_ = parse_plan(merged)
+    hh, ih, *_ = parse_plan(hybrid)
     hp, ip, *_ = parse_plan(plain)
     assert (im["p0"] & 2).any() and not (ip["p0"] & 2).any()
     assert hm["n_partials"] * 2 < hp["n_partials"]            # 3x fewer at this size
-    assert hm["unique_tokens"] == hp["unique_tokens"] and hm["logical_tokens"] == hp["logical_tokens"]
+    assert hh["n_partials"] < hp["n_partials"]                # 128-row blocks: 1.8x fewer
+    for h in (hm, hh):
+        assert h["unique_tokens"] == hp["unique_tokens"] and h["logical_tokens"] == hp["logical_tokens"]
+    # hybrid: the big items (65..128 rows) come first, every other item has <= 64 rows
+    nb = int(hh["n_big"])
+    assert nb > 0 and (ih["n_rows"][:nb] > 64).all() and (ih["n_rows"][:nb] <= 128).all()
+    assert (ih["n_rows"][nb:] <= 64).all() and hm["n_big"] == 0
     _check_plan_covers(cfg, lay, offs, segs, lay.own_len)
+    _check_plan_covers(cfg, lay, offs, segs, lay.own_len, flags=orion.PLAN_NO_HYBRID)
