@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <iterator>
 #include <map>
 #include <string>
 #include <vector>
@@ -478,6 +479,17 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
     std::vector<std::pair<int32_t, std::vector<int32_t>>> gkeys;
     std::vector<std::vector<Range>> gchunks;
     std::vector<int32_t> gpiece;
+    // Hybrid plans with reader blocks of <= 32 readers: every range a block reads with more than
+    // rows_per_item rows joins ONE masked item per (block, kv head) -- its readers the union of
+    // the ranges' reader subsets, each range carrying the bitmask of the readers that read it --
+    // instead of one item per distinct subset (a Dependent chain's block would otherwise get one
+    // short item per ancestor inside the block, each paying an item's start-up and epilogue).
+    const bool masked_blocks = hybrid && RB <= 32;
+    std::map<std::pair<int32_t, int64_t>, int32_t> bkey_index;
+    std::vector<std::pair<int32_t, int64_t>> bkeys;
+    std::vector<std::vector<std::pair<Range, std::vector<int32_t>>>> bchunks;
+    std::vector<std::vector<int32_t>> bunion;
+    std::vector<int32_t> bpiece;
     for (size_t pi = 0; pi < pieces.size(); ++pi) {
       const Piece& p = pieces[pi];
       unique_tokens += p.t1 - p.t0;
@@ -488,6 +500,29 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
         const int32_t rows = (int32_t)S.size() * G;
         int32_t ch = std::max(chunk, 32 * std::min(rows, kRowsPerItemBig));
         ch = (ch + kTileTokens - 1) / kTileTokens * kTileTokens;
+        if (masked_blocks && rows > rows_per_item) {
+          for (int32_t g = 0; g < Hkv; ++g) {
+            auto key = std::make_pair(g, blk);
+            auto f = bkey_index.find(key);
+            int32_t idx;
+            if (f == bkey_index.end()) {
+              idx = (int32_t)bkeys.size();
+              bkey_index.emplace(key, idx);
+              bkeys.push_back(key);
+              bchunks.emplace_back();
+              bunion.emplace_back();
+              bpiece.push_back((int32_t)pi);
+            } else {
+              idx = f->second;
+            }
+            for (int32_t t = p.t0; t < p.t1; t += ch)
+              bchunks[idx].push_back({Range{p.pt_off, t, std::min(p.t1, t + ch), p.dyn, 0, {0, 0, 0}}, S});
+            std::vector<int32_t> u;
+            std::set_union(bunion[idx].begin(), bunion[idx].end(), S.begin(), S.end(), std::back_inserter(u));
+            bunion[idx].swap(u);
+          }
+          continue;
+        }
         for (int32_t g = 0; g < Hkv; ++g) {
           auto key = std::make_pair(g, S);
           auto f = key_index.find(key);
@@ -504,6 +539,45 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
           for (int32_t t = p.t0; t < p.t1; t += ch)
             gchunks[idx].push_back(Range{p.pt_off, t, std::min(p.t1, t + ch), p.dyn, 0, {0, 0, 0}});
         }
+      }
+    }
+    for (size_t bi = 0; bi < bkeys.size(); ++bi) {
+      const int32_t g = bkeys[bi].first;
+      const std::vector<int32_t>& U = bunion[bi];
+      const int32_t rows = (int32_t)U.size() * G;
+      if (U.size() > 32 || rows > kRowsPerItemBig)
+        return fail(ORION_ERR_INVALID_ARG, "internal: masked block of %zu readers", U.size());
+      const int32_t roff = (int32_t)readers.size();
+      readers.insert(readers.end(), U.begin(), U.end());
+      const auto& cs = bchunks[bi];
+      for (size_t c0 = 0; c0 < cs.size();) {
+        size_t c1 = c0;
+        int64_t tok = 0;
+        while (c1 < cs.size() && (c1 == c0 || tok + (cs[c1].first.t1 - cs[c1].first.t0) <= kMergeTokens))
+          tok += cs[c1].first.t1 - cs[c1].first.t0, ++c1;
+        WorkItem w{};
+        w.pt_off = (int32_t)ranges.size(); w.dyn = -1;
+        w.flags = kItemRanges; w.n_ranges = (int32_t)(c1 - c0);
+        for (size_t c = c0; c < c1; ++c) {
+          Range R = cs[c].first;
+          if (cs[c].second.size() != U.size()) {
+            uint32_t mask = 0;
+            for (int32_t b : cs[c].second)
+              mask |= 1u << (std::lower_bound(U.begin(), U.end(), b) - U.begin());
+            R.flags |= kRangeMasked;
+            R.pad_[0] = (int32_t)mask;
+          }
+          ranges.push_back(R);
+        }
+        w.kv_head = g; w.readers_off = roff; w.piece = bpiece[bi];
+        w.row_begin = 0; w.n_rows = rows; w.slot0 = n_slots;
+        for (int32_t r = 0; r < rows; ++r)
+          row_slots[(size_t)U[r / G] * Hq + g * G + r % G].push_back(n_slots + r);
+        n_slots += rows;
+        items.push_back(w);
+        is_big.push_back(1);
+        cost.push_back(tok * (2 + (rows + 15) / 16) + 256 * (int64_t)(c1 - c0));
+        c0 = c1;
       }
     }
     for (size_t gi = 0; gi < gkeys.size(); ++gi) {

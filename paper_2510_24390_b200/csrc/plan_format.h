@@ -32,6 +32,8 @@ enum : int32_t { kVariantTC = 0, kVariantMmaSync = 1, kVariantTCT = 2 };
 inline bool partials_fp16(int32_t variant) { return variant == kVariantTCT; }
 constexpr int32_t kItemCausal = 1;
 constexpr int32_t kItemRanges = 2;
+constexpr int32_t kRangeMasked = 4;   // Range only: readers_mask (pad_[0]) selects the item's readers
+                                      // (bit i: the item's i-th reader) that read this range
 constexpr int64_t kMergeTokens = 8192;   // token cap of a merged multi-range decode item
 constexpr int kTileTokens = 64;    // tokens per pipeline stage in the split kernel
 
@@ -75,7 +77,10 @@ struct WorkItem {
 
 // A token range of a multi-range item (kItemRanges: the item streams ranges[pt_off ..
 // pt_off + n_ranges) of the plan in order, as one accumulation): tokens [t0, min(t1,
-// own_len[dyn])) of the page run at pt_off; flags & kItemCausal: row i sees tokens < t0 + i + 1.
+// own_len[dyn])) of the page run at pt_off; flags & kItemCausal: row i sees tokens < t0 + i + 1;
+// flags & kRangeMasked: only rows of the readers whose bit is set in pad_[0] see the range (hybrid
+// plans' big items, rows-on-lanes kernel only: a reader block's ranges with different reader
+// subsets streamed as one accumulation; at most 32 readers per such item).
 struct Range {
   int32_t pt_off, t0, t1, dyn, flags, pad_[3];
 };

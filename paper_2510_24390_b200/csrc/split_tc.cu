@@ -426,7 +426,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       int ti = 0;                                   // tile index within the item (WG ti & 1)
       for (int rg_i = 0; rg_i < item_nranges(w); ++rg_i) {
       const RangeG g = range_geom(a, w, rg_i);
-      const int row_end = g.causal ? min(g.end, g.t0 + rpos + 1) : g.end;
+      // a masked range (hybrid big items): rows of readers outside its mask see none of it
+      const bool rmask = g.masked && !((g.mask >> ((w.row_begin + r) / (a.lc * a.group))) & 1u);
+      const int row_end = rmask ? g.t0 : (g.causal ? min(g.end, g.t0 + rpos + 1) : g.end);
       for (int t = 0; t < g.ntiles; ++t, ++j, ++ti) {
         if ((ti & 1) != p) continue;
         const int tb = g.base + t * kTok;
@@ -447,21 +449,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         // late as possible so that its latency overlaps this tile's exponentials.
         bool pv_ok = np == 0;
         const bool edge = g.causal || (tb < g.t0) || (tb + kTok > g.end);
+        const bool cmask = edge || rmask;            // this row's scores need the column mask
         uint32_t pk[32];
         if (active) {
           float mx = -INFINITY;                     // raw scores; scale > 0 commutes with max
-          if (!edge) {
-#pragma unroll
-            for (int c = 0; c < 64; ++c) mx = fmaxf(mx, __uint_as_float(sr[c]));
-          } else {
+          if (cmask) {
             const int lo_c = g.t0 - tb, hi_c = row_end - tb;   // valid columns [lo_c, hi_c)
 #pragma unroll
-            for (int c = 0; c < 64; ++c) {
-              const float v = (c >= lo_c && c < hi_c) ? __uint_as_float(sr[c]) : -INFINITY;
-              sr[c] = __float_as_uint(v);
-              mx = fmaxf(mx, v);
-            }
+            for (int c = 0; c < 64; ++c)
+              sr[c] = (c >= lo_c && c < hi_c) ? sr[c] : __float_as_uint(-INFINITY);
           }
+          mx = max_tree(sr);
           mx *= a.scale_log2;
           // Lazy rescale (exact: O_p and l_p refer to m_used).  Warp-uniform so the aligned TMEM
           // accesses are executed by the whole warp.

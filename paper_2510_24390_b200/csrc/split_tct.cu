@@ -217,12 +217,9 @@ __device__ __forceinline__ void softmax_tile(uint32_t tmem, uint32_t lane_base, 
         const float4 m4 = *reinterpret_cast<const float4*>(mrow + c4);
         const float mm[4] = {m4.x, m4.y, m4.z, m4.w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float d = fmaf(__uint_as_float(s[c4 + e]), scale_log2, -mm[e]);
-          s[c4 + e] = __float_as_uint(d);
-          dmax = fmaxf(dmax, d);
-        }
+        for (int e = 0; e < 4; ++e) s[c4 + e] = __float_as_uint(fmaf(__uint_as_float(s[c4 + e]), scale_log2, -mm[e]));
       }
+      dmax = tc::max_tree(s);
     } else {
 #pragma unroll
       for (int c = 0; c < NH; ++c) s[c] = __float_as_uint(-INFINITY);

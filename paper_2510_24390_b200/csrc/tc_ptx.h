@@ -148,6 +148,27 @@ __device__ __forceinline__ float add_bf16x2_f32(uint32_t pk, float acc) {
       : "=f"(r) : "r"(pk), "f"(acc));
   return r;
 }
+// Three-input max (sm_100 FMNMX3), and the max of N values as four independent FMNMX3 chains: a
+// softmax row max in ~N/8 dependent steps instead of N (the latency of a 64-long fmaxf chain was a
+// quarter of a tile's softmax time).  Same result as a sequential fmaxf fold (max is exact).
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+template <int N>
+__device__ __forceinline__ float max_tree(const uint32_t (&v)[N]) {
+  static_assert(N % 8 == 0, "max_tree: N multiple of 8");
+  float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
+#pragma unroll
+  for (int c = 0; c < N; c += 8) {
+    m0 = fmax3(m0, __uint_as_float(v[c]), __uint_as_float(v[c + 1]));
+    m1 = fmax3(m1, __uint_as_float(v[c + 2]), __uint_as_float(v[c + 3]));
+    m2 = fmax3(m2, __uint_as_float(v[c + 4]), __uint_as_float(v[c + 5]));
+    m3 = fmax3(m3, __uint_as_float(v[c + 6]), __uint_as_float(v[c + 7]));
+  }
+  return fmaxf(fmax3(m0, m1, m2), m3);
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -172,7 +193,8 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int m, int n, bool b_mn_major)
 // Geometry of one token range of an item: the item itself, or range r of a multi-range item
 // (kItemRanges, point-prefill plans).  Tiles sit on the 64-token grid of the range's page run.
 struct RangeG {
-  int32_t pt_off, t0, end, base, ntiles, causal;
+  int32_t pt_off, t0, end, base, ntiles, causal, masked;
+  uint32_t mask;   // kRangeMasked: bit i = the item's i-th reader reads this range
 };
 __device__ __forceinline__ int item_nranges(const WorkItem& w) {
   return (w.flags & kItemRanges) ? w.n_ranges : 1;
@@ -180,12 +202,15 @@ __device__ __forceinline__ int item_nranges(const WorkItem& w) {
 __device__ __forceinline__ RangeG range_geom(const TcArgs& a, const WorkItem& w, int r) {
   int32_t t1, dyn, fl;
   RangeG g;
+  g.mask = 0xffffffffu;
   if (w.flags & kItemRanges) {
     const Range R = a.ranges[w.pt_off + r];
     g.pt_off = R.pt_off; g.t0 = R.t0; t1 = R.t1; dyn = R.dyn; fl = R.flags;
+    if (fl & kRangeMasked) g.mask = static_cast<uint32_t>(R.pad_[0]);
   } else {
-    g.pt_off = w.pt_off; g.t0 = w.t0; t1 = w.t1; dyn = w.dyn; fl = w.flags;
+    g.pt_off = w.pt_off; g.t0 = w.t0; t1 = w.t1; dyn = w.dyn; fl = w.flags & ~kRangeMasked;
   }
+  g.masked = (fl & kRangeMasked) != 0;
   g.end = t1;
   if (dyn >= 0) g.end = min(g.end, __ldg(a.own_len + dyn));
   g.base = g.t0 & ~(kTok - 1);

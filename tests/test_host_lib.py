@@ -196,19 +196,21 @@ def _check_plan_covers(cfg, lay, offs, segs, own_len, flags=0):
     ranges = np.frombuffer(plan, RANGE, int(h["n_ranges"]), int(h["ranges_off"]))
     for it in items:
         if it["p0"] & 2:                             # multi-range item: its ranges' tokens
-            rl = [(int(r["pt_off"]), int(r["t0"]), int(r["t1"]), int(r["dyn"]))
+            rl = [(int(r["pt_off"]), int(r["t0"]), int(r["t1"]), int(r["dyn"]),
+                   int(r["r0"]) & 0xffffffff if r["flags"] & 4 else 0xffffffff)   # kRangeMasked
                   for r in ranges[it["pt_off"]:it["pt_off"] + it["p1"]]]
-            assert len(rl) >= 2
+            assert len(rl) >= 2 or rl[0][4] != 0xffffffff
         else:
-            rl = [(int(it["pt_off"]), int(it["t0"]), int(it["t1"]), int(it["dyn"]))]
-        toks = []
-        for pt, t0, t1, dyn in rl:
-            end = t1 if dyn < 0 else min(t1, own_len[dyn])
-            toks += [(pt, t) for t in range(t0, max(t0, end))]
+            rl = [(int(it["pt_off"]), int(it["t0"]), int(it["t1"]), int(it["dyn"]), 0xffffffff)]
         for r in range(it["row_begin"], it["row_begin"] + it["n_rows"]):
             b = readers[it["readers_off"] + r // G]
             hh = it["kv_head"] * G + r % G
             s = it["slot0"] + r - it["row_begin"]
+            toks = []
+            for pt, t0, t1, dyn, mask in rl:         # a masked range: only the readers in its mask
+                if (mask >> (r // G)) & 1:
+                    end = t1 if dyn < 0 else min(t1, own_len[dyn])
+                    toks += [(pt, t) for t in range(t0, max(t0, end))]
             assert s not in slot_tokens
             slot_tokens[s] = toks
             slot_row[s] = b * cfg.hq + hh

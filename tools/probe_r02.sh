@@ -4,8 +4,8 @@ NOX="--no-cpu-baseline --no-prefill --no-e2e --no-model --no-expansion --no-poin
 ORION_LIB=paper_2510_24390_b200/liborion_check.so timeout 400 python -m pytest tests/test_gpu_parity.py -x -q -k "c1 or shapes or c2 or grid or wide or hybrid" > gpurun_out/p_check.log 2>&1
 echo "check rc=$?"; tail -3 gpurun_out/p_check.log
 [ "$1" == "quick" ] && exit 0
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fuzz.py tests/test_gpu_prefill.py -x -q > gpurun_out/p_rel.log 2>&1
-echo "release rc=$?"; tail -3 gpurun_out/p_rel.log
+[ "$1" != "bench" ] && timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fuzz.py tests/test_gpu_prefill.py -x -q > gpurun_out/p_rel.log 2>&1
+[ "$1" != "bench" ] && { echo "release rc=$?"; tail -3 gpurun_out/p_rel.log; }
 for c in c5w c5c; do
   timeout 300 python bench.py --config $c --queries 8 --steps 10 --warmup 3 $NOX > gpurun_out/p_$c.json 2> gpurun_out/p_$c.err
 done
