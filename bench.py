@@ -11,16 +11,21 @@ larger than L2 — no flush needed.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl orion|reference]
 
-Multi-GPU: launched by torchrun, one rank per GPU, no collective on the data path (queries are
-independent).  --scaling weak (default): every rank expands its own full batch of
-the config (own seed); --scaling strong: the config's queries are partitioned across ranks
-(paper_2510_24390_b200/shard.py).  Rank 0 prints one JSON line with the whole-job value
-(branches of all ranks / max-over-ranks device-timed step).
+Multi-GPU: one process per GPU, no collective on the data path (queries are
+independent).  `--gpus N` under torchrun (WORLD_SIZE=N) runs this process as
+one rank; without WORLD_SIZE it launches the N ranks itself (torch.distributed.run, 127.0.0.1).
+--scaling strong (default): the config's queries are partitioned over the ranks (c4: 64/N per
+GPU, BASELINE configs[3] "queries partitioned across 2/4/8 B200"); --scaling weak: every rank
+expands its own full batch.  Rank 0 prints one JSON line: the whole-job value (branches of all
+ranks / max-over-ranks device-timed step) and every rank's own step time.  `--plan-only` runs
+the launcher, sharding, planning and reductions without a GPU (gloo): the CPU test of this path.
 `--impl reference` times the CPU oracle (the tier's reference arm) on a bounded sample.
 """
 import argparse
 import json
 import os
+import platform
+import socket
 import statistics
 import subprocess
 import sys
@@ -38,7 +43,7 @@ METRIC = "expansion tokens/sec"
 UNIT = "tokens/s"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -51,13 +56,17 @@ def parse():
                     help="KV cache layout: separate K / V pools, or K and V of a (page, kv head) adjacent")
     ap.add_argument("--no-merge", action="store_true",
                     help="plan without multi-range item merging (ORION_PLAN_NO_MERGE), for comparison")
+    ap.add_argument("--no-hybrid", action="store_true",
+                    help="every decode item on the swap-AB kernel (ORION_PLAN_NO_HYBRID), for comparison")
     ap.add_argument("--kernel", default="tc", choices=["tc", "rol", "mma"],
                     help="split kernel: tcgen05 swap-AB (default), tcgen05 rows-on-lanes (rol) or legacy mma.sync")
     ap.add_argument("--layers", type=int, default=0, help="override layer count (0 = config)")
     ap.add_argument("--queries", type=int, default=0, help="override query count (0 = config)")
-    ap.add_argument("--scaling", default="weak", choices=["strong", "weak"],
-                    help="strong: the config's queries are split across ranks; weak: every rank "
-                         "runs the full config")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong (default): the config's queries are split across ranks; weak: every "
+                         "rank runs the full config")
+    ap.add_argument("--plan-only", action="store_true",
+                    help="launch, shard, plan and reduce without a GPU (gloo; CPU test of the N>1 path)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -69,11 +78,15 @@ def parse():
                     help="skip the point-prefill attention measurement (SURVEY.md §8(f) rank 1)")
     ap.add_argument("--no-prefill", action="store_true",
                     help="skip the co-scheduled prefill measurement (SURVEY.md §8(a) a8)")
+    ap.add_argument("--no-shares", action="store_true",
+                    help="skip the per-GPU shares of the strong-scaling curve (N=1 only)")
+    ap.add_argument("--no-c5", action="store_true",
+                    help="skip the c5 stress sub-results (wide-64 / chain-64, one GPU's 8-query share)")
     ap.add_argument("--prefill-caps", default="148,132,116",
                     help="split-kernel SM caps tried with the prefill co-stream")
     ap.add_argument("--green-splits", default="116,100,84",
                     help="expansion SM counts of the green-context partitions (prefill gets the rest)")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 # ------------------------------------------------------------------------------ helpers
@@ -99,22 +112,26 @@ def context_tokens(batch):
     return int(ln.sum())
 
 
-def load_peaks():
-    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+def load_json(name):
+    p = os.path.join(ROOT, name)
     if os.path.exists(p):
         with open(p) as f:
-            d = json.load(f)
+            return json.load(f)
+    return {}
+
+
+def load_peaks():
+    d = load_json("MEASURED_PEAKS.json")
+    if "hbm_gbs" in d:
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 def load_traffic(config_name, kernel):
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if not os.path.exists(p):
-        return None
-    with open(p) as f:
-        d = json.load(f)
-    e = d.get(config_name if kernel == "tc" else f"{config_name}:{kernel}")
+    """ncu DRAM bytes per split launch of this workload (profiles/ncu_traffic.json, from one
+    `ncu --set full` capture), or None."""
+    e = load_json(os.path.join("profiles", "ncu_traffic.json")).get(
+        config_name if kernel == "tc" else f"{config_name}:{kernel}")
     return None if e is None else e.get("split_dram_bytes_per_launch")
 
 
@@ -159,15 +176,20 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def blas_threads():
+def host_cpu():
+    """(usable cores, CPU model) of this host: the cores the process may run on
+    (sched_getaffinity) and /proc/cpuinfo's model name."""
+    cores = len(os.sched_getaffinity(0))
+    model = platform.processor() or "unknown"
     try:
-        from threadpoolctl import threadpool_info
-        n = [i["num_threads"] for i in threadpool_info() if i.get("user_api") == "blas"]
-        if n:
-            return max(n)
-    except Exception:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
         pass
-    return len(os.sched_getaffinity(0))
+    return cores, model
 
 
 # ------------------------------------------------------------------------------ oracle leg
@@ -192,71 +214,93 @@ def oracle_sample(cfg, seed):
 
 
 def cpu_baseline(cfg, layers, seconds):
+    """The oracle as it stands, on this host's cores (BLAS pinned to them with threadpoolctl), on a
+    bounded sample: whole queries of the workload at one layer, extrapolated to `layers`."""
+    from threadpoolctl import threadpool_limits
+    cores, model = host_cpu()
     spent, n_br, n = 0.0, 0, 0
-    while spent < seconds or n == 0:
-        dt, br = oracle_sample(cfg, cfg.seed + 17 * n)
-        spent += dt
-        n_br += br
-        n += 1
-        if n >= 64:
-            break
+    with threadpool_limits(cores):
+        while spent < seconds or n == 0:
+            dt, br = oracle_sample(cfg, cfg.seed + 17 * n)
+            spent += dt
+            n_br += br
+            n += 1
+            if n >= 64:
+                break
     # whole-job equivalent: each sampled (query, layer) would repeat for every layer
     value = n_br / (spent * layers)
-    return {"value": value, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+    return {"value": value, "unit": UNIT, "cores": cores, "cpu_model": model, "kind": "oracle",
+            "extrapolated": True, "blas_threads": cores,
             "sample": f"{n} x (1 query of {cfg.name}: append + attention of all its branches, "
-                      f"1 layer), {spent:.1f} s CPU; scaled by {layers} layers"}
+                      f"1 layer), {spent:.1f} s CPU measured; rate extrapolated to {layers} layers"}
 
 
-def workload_str(cfg, layers):
+def workload_str(cfg, layers, world=1, scaling="strong"):
     """config.workload of both arms (the same workload; the reference arm times a sample of it)."""
-    return (f"{cfg.name}: Hq/Hkv/d={cfg.hq}/{cfg.hkv}/{cfg.d}, {cfg.n_queries} queries x {cfg.dag}, "
-            f"prefix {cfg.lp}, {cfg.t} tok/point (Lc {cfg.lc}), page {cfg.page}, {layers} layers")
+    s = (f"{cfg.name}: Hq/Hkv/d={cfg.hq}/{cfg.hkv}/{cfg.d}, {cfg.n_queries} queries x {cfg.dag}, "
+         f"prefix {cfg.lp}, {cfg.t} tok/point (Lc {cfg.lc}), page {cfg.page}, {layers} layers")
+    if world > 1:
+        s += (f"; queries partitioned over {world} GPUs" if scaling == "strong"
+              else f"; each of {world} GPUs its own {cfg.n_queries}-query batch")
+    return s
 
 
 def run_reference(args, cfg, layers):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    from threadpoolctl import threadpool_limits
+    cores, model = host_cpu()
     times, n_br = [], 0
-    for s in range(args.warmup + args.steps):
-        dt, br = oracle_sample(cfg, cfg.seed + 1000 + s)
-        if s >= args.warmup:
-            times.append(dt)
-            n_br = br
-    t_step = statistics.mean(times) * layers          # seconds per (query x all layers)
-    value = n_br / t_step
-    cores = blas_threads()
+    with threadpool_limits(cores):
+        for s in range(args.warmup + args.steps):
+            dt, br = oracle_sample(cfg, cfg.seed + 1000 + s)
+            if s >= args.warmup:
+                times.append(dt)
+                n_br = br
+    t_sample = statistics.mean(times)                  # measured seconds per step (1 query, 1 layer)
+    value = n_br / (t_sample * layers)                 # extrapolated: every layer of one query
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": t_sample * 1e3, "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference",
+            "impl": "reference", "extrapolated": True,
+            "extrapolation": f"ms_per_step is the measured time of one step's sample (1 query x 1 layer: "
+                             f"append + attention of its {n_br} branches); value = {n_br} branches / "
+                             f"(that time x {layers} layers), the config's per-query rate (queries are "
+                             f"independent)",
             "config": {"workload": workload_str(cfg, layers), "policy": "ancestors"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": f"per step 1 query of {cfg.name} (all {n_br} branches), "
-                                       f"1 layer, append + attention; the rate scaled by {layers} "
-                                       f"layers (queries are independent: the config's value is "
-                                       f"branches / (per-query time x layers))"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "cpu_model": model,
+                             "blas_threads": cores, "kind": "oracle", "extrapolated": True,
+                             "sample": f"per step 1 query of {cfg.name} (all {n_br} branches), 1 layer, "
+                                       f"append + attention, {t_sample:.2f} s measured; the rate scaled "
+                                       f"by {layers} layers"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------------------ GPU leg
-def run_orion(args, cfg, layers):
-    import torch
-    import torch.distributed as dist
+def plan_flags(args):
     import paper_2510_24390_b200 as orion
-    from paper_2510_24390_b200 import shard
+    return ({"tc": 0, "rol": orion.PLAN_ROWS_ON_LANES, "mma": orion.PLAN_MMA_SYNC}[args.kernel]
+            | (orion.PLAN_NO_MERGE if args.no_merge else 0) | (orion.PLAN_NO_HYBRID if args.no_hybrid else 0))
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
 
-    qs = shard.rank_queries(cfg.n_queries, rank, world, args.scaling)
-    lay = WT.make_layout(cfg, queries=qs, seed=shard.rank_seed(cfg.seed, rank))
+def batch_of(args, cfg, lay, dev, **kw):
+    import paper_2510_24390_b200 as orion
+    queries = [dict(n_points=int(lay.n_points[i]), edges=lay.edges[i],
+                    prefix_pt_off=int(lay.prefix_pt_off[i]), prefix_len=int(lay.prefix_len[i]))
+               for i in range(lay.n_queries)]
+    points = np.stack([lay.point_pt_off, lay.content_len, lay.point_cap], 1)
+    opts = dict(policy=args.policy, device=dev, chunk_tokens=args.chunk,
+                kv_interleaved=args.kv_layout == "interleaved", flags=plan_flags(args))
+    opts.update(kw)
+    return orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, lay.page_table,
+                                lay.own_len, **opts)
+
+
+def alloc_tensors(args, cfg, lay, layers, dev, seed):
+    """Per-layer KV pools and per-step inputs, seeded N(0,1) bf16 on the device."""
+    import torch
     B = lay.n_branches
     P, H, Hq, D = cfg.page, cfg.hkv, cfg.hq, cfg.d
     if args.kv_layout == "interleaved":          # one [pages][Hkv][2][P][d] pool per layer
@@ -270,23 +314,19 @@ def run_orion(args, cfg, layers):
     vn = torch.empty_like(kn)
     out = torch.empty_like(q)
     g = torch.Generator(device=dev)
-    g.manual_seed(cfg.seed * 7 + rank)
+    g.manual_seed(seed)
     for t in (kc, vc, q, kn, vn):
         for l in range(layers):
             t[l].normal_(generator=g)
-    queries = [dict(n_points=int(lay.n_points[i]), edges=lay.edges[i],
-                    prefix_pt_off=int(lay.prefix_pt_off[i]), prefix_len=int(lay.prefix_len[i]))
-               for i in range(lay.n_queries)]
-    points = np.stack([lay.point_pt_off, lay.content_len, lay.point_cap], 1)
-    t0 = time.perf_counter()
-    batch = orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, lay.page_table,
-                                 lay.own_len, policy=args.policy, device=dev,
-                                 chunk_tokens=args.chunk, kv_interleaved=args.kv_layout == "interleaved",
-                                 flags={"tc": 0, "rol": orion.PLAN_ROWS_ON_LANES,
-                                        "mma": orion.PLAN_MMA_SYNC}[args.kernel]
-                                       | (orion.PLAN_NO_MERGE if args.no_merge else 0))
-    plan_s = time.perf_counter() - t0
-    stream = torch.cuda.current_stream(dev)
+    return kc, vc, q, kn, vn, out
+
+
+def time_steps(batch, layers, tens, steps, warmup, stream, world=1, barrier=None):
+    """Warm up, then time `steps` steps (per layer: append REWRITE, split, combine) with CUDA events
+    on `stream`: returns (elapsed_ms, per-step ms sorted, per-launch split ms, launches)."""
+    import torch
+    import paper_2510_24390_b200 as orion
+    kc, vc, q, kn, vn, out = tens
     REW = orion.APPEND_REWRITE
 
     def step(ev=None, k=0):
@@ -299,35 +339,121 @@ def run_orion(args, cfg, layers):
                 ev[k][l][1].record(stream)
             batch.combine(out[l])
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize()
     ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(layers)] for _ in range(args.steps)]
+           for _ in range(layers)] for _ in range(steps)]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sampler = ClockSampler(local) if rank == 0 else None
-    if world > 1:
-        dist.barrier()
+    if barrier:
+        barrier()
     torch.cuda.synchronize()
     e0.record(stream)
-    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
     step_ev[0].record(stream)
-    for k in range(args.steps):
+    for k in range(steps):
         step(ev, k)
         step_ev[k + 1].record(stream)
     e1.record(stream)
     torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    step_ms = sorted(step_ev[k].elapsed_time(step_ev[k + 1]) for k in range(steps))
+    split_ms = [ev[k][l][0].elapsed_time(ev[k][l][1]) for k in range(steps) for l in range(layers)]
+    n_kernels = 3 + (1 if batch.stats.get("n_big", 0) and batch.stats["n_big"] < batch.stats["n_items"] else 0)
+    return e0.elapsed_time(e1), step_ms, split_ms, steps * layers * n_kernels, step
+
+
+def bounds_of(cfg, lay, batch, split_bytes):
+    """three bounds per split launch -- bytes / HBM, flops / tensor, exps / MUFU."""
+    peaks_all = load_json("MEASURED_PEAKS.json")
+    sm_mhz = peaks_all.get("sm_max_mhz", 1965.0)
+    ctx_tok = context_tokens(batch)
+    flops = 4.0 * cfg.d * cfg.hq * ctx_tok
+    exps = float(cfg.hq * ctx_tok)
+    return {"hbm": split_bytes / (load_peaks()[0] * 1e9) * 1e6,
+            "tensor_bf16": flops / (peaks_all.get("bf16_tflops", 2250.0) * 1e12) * 1e6,
+            "mufu_ex2": exps / (16 * 148 * sm_mhz * 1e6) * 1e6,
+            "flops": flops, "exps": exps,
+            "note": "MUFU: 16 ex2/clk/SM x 148 SMs at the max SM clock"}
+
+
+def plan_only(args, cfg, layers):
+    """The N>1 host path without a GPU: rank launch, query sharding, per-rank layouts and plans,
+    the max/sum reductions and the per-rank gather over torch.distributed (gloo), and rank 0's
+    JSON line.  Nothing is timed (value null)."""
+    import torch.distributed as dist
+    import paper_2510_24390_b200 as orion
+    from paper_2510_24390_b200 import shard
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
     if world > 1:
-        dist.barrier()
+        dist.init_process_group("gloo")
+    qs = shard.rank_queries(cfg.n_queries, rank, world, args.scaling)
+    lay = WT.make_layout(cfg, queries=qs, seed=shard.rank_seed(cfg.seed, rank))
+    t0 = time.perf_counter()
+    batch = batch_of(args, cfg, lay, "cpu")
+    plan_s = time.perf_counter() - t0
+    kv_b, q_b, _ = algorithmic_bytes(cfg, lay)
+    mine = {"rank": rank, "queries": qs, "branches": lay.n_branches, "plan_s": plan_s,
+            "items": batch.stats["n_items"], "kv_bytes_per_layer": kv_b}
+    plan_s_max, total_b = shard.reduce_timing(plan_s, float(lay.n_branches))
+    per_rank = [mine]
+    if world > 1:
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, mine)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "steps": 0,
+                          "warmup": 0, "ms_per_step": None, "higher_is_better": True,
+                          "scaling": args.scaling, "vs_baseline": None, "dtype": "bf16",
+                          "data": "synthetic", "plan_only": True,
+                          "config": {"workload": workload_str(cfg, layers, world, args.scaling),
+                                     "branches_per_step": int(total_b), "layers": layers},
+                          "plan_s_max": plan_s_max, "per_rank": per_rank,
+                          "gpu_launches": 0}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_orion(args, cfg, layers):
+    import torch
+    import torch.distributed as dist
+    import paper_2510_24390_b200 as orion
+    from paper_2510_24390_b200 import shard
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    barrier = dist.barrier if world > 1 else None
+
+    qs = shard.rank_queries(cfg.n_queries, rank, world, args.scaling)
+    lay = WT.make_layout(cfg, queries=qs, seed=shard.rank_seed(cfg.seed, rank))
+    B = lay.n_branches
+    tens = alloc_tensors(args, cfg, lay, layers, dev, cfg.seed * 7 + rank)
+    kc, vc, q, kn, vn, out = tens
+    t0 = time.perf_counter()
+    batch = batch_of(args, cfg, lay, dev)
+    plan_s = time.perf_counter() - t0
+    stream = torch.cuda.current_stream(dev)
+    sampler = ClockSampler(local) if rank == 0 else None
+    elapsed_ms, step_ms, split_ms, launches, step = time_steps(batch, layers, tens, args.steps, args.warmup,
+                                                               stream, world, barrier)
     clocks = sampler.stop() if sampler else None
-    elapsed_ms = e0.elapsed_time(e1)
-    step_ms = sorted(step_ev[k].elapsed_time(step_ev[k + 1]) for k in range(args.steps))
     pct = lambda f: step_ms[min(len(step_ms) - 1, int(round(f * (len(step_ms) - 1))))]
-    split_ms = [ev[k][l][0].elapsed_time(ev[k][l][1]) for k in range(args.steps) for l in range(layers)]
+    my_ms = elapsed_ms
     # whole-job aggregation: branches of all ranks / max step time over ranks
     elapsed_ms, total_b = shard.reduce_timing(elapsed_ms, float(B), device=dev)
     ms_step = elapsed_ms / args.steps
     value = total_b / (ms_step / 1e3)
+    per_rank = [{"rank": rank, "queries": len(qs), "branches": B, "ms_per_step": my_ms / args.steps}]
+    if world > 1:
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, {"rank": rank, "queries": len(qs), "branches": B,
+                                          "ms_per_step": my_ms / args.steps})
 
     # ---- the same step captured once as a CUDA graph and replayed (SURVEY.md §8(d) protocol)
     graph = None
@@ -364,25 +490,20 @@ def run_orion(args, cfg, layers):
         e2e = run_e2e(args, batch, layers, q, kn, vn, out, kc, vc, dev, world, total_b)
 
     kv_b, q_b, o_b = algorithmic_bytes(cfg, lay)
-    # three bounds per launch -- bytes / HBM, flops / tensor, exps / MUFU
-    ctx_tok = context_tokens(batch)
-    peaks_all = {}
-    if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")):
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            peaks_all = json.load(f)
-    sm_mhz = peaks_all.get("sm_max_mhz", 1965.0)
-    flops = 4.0 * cfg.d * cfg.hq * ctx_tok
-    exps = float(cfg.hq * ctx_tok)
-    bounds = {"hbm": (kv_b + q_b) / (load_peaks()[0] * 1e9) * 1e6,
-              "tensor_bf16": flops / (peaks_all.get("bf16_tflops", 2250.0) * 1e12) * 1e6,
-              "mufu_ex2": exps / (16 * 148 * sm_mhz * 1e6) * 1e6,
-              "flops": flops, "exps": exps,
-              "note": "MUFU: 16 ex2/clk/SM x 148 SMs at the max SM clock"}
     split_bytes = kv_b + q_b                        # K2 reads: unique KV + q
     split_avg_s = statistics.mean(split_ms) / 1e3
     peak, peak_src = load_peaks()
     achieved = split_bytes / split_avg_s / 1e9
     st = batch.stats
+    costream = None
+    if world > 1 and not args.no_prefill:           # c4 "with co-scheduled prefill stream": every rank
+        mine = run_costream(args, cfg, lay, layers, q, kn, vn, out, kc, vc, dev, B / (my_ms / args.steps / 1e3))
+        allc = [None] * world
+        dist.all_gather_object(allc, mine)
+        costream = {"per_rank": allc,
+                    "expansion_tok_s_together_cap148_total": sum(
+                        c["together"][0]["expansion_tok_s"] for c in allc if c and c.get("together")),
+                    "note": "each rank runs the co-stream experiment on its own GPU and query share"}
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -392,41 +513,51 @@ def run_orion(args, cfg, layers):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded N(0,1) bf16 q/K/V; random page permutation)",
-        "config": {"workload": workload_str(cfg, layers),
+        "config": {"workload": workload_str(cfg, layers, world, args.scaling),
                    "branches_per_step": int(total_b), "layers": layers,
                    "policy": "parents_eq3" if args.policy else "ancestors",
                    "append_mode": "rewrite (stationary snapshot)",
                    "kv_layout": args.kv_layout,
                    "l2": "no flush: per-layer KV pools, step working set "
-                         f"{layers * (kv_b + q_b + o_b) / 1e9:.1f} GB >> 126 MB L2",
-                   "parallelism": (f"{world} GPU(s), each its own {cfg.n_queries}-query batch, no collective"
-                                   if args.scaling == "weak" else
-                                   f"{cfg.n_queries} queries partitioned over {world} GPU(s), no collective")},
+                         f"{layers * (kv_b + q_b + o_b) / 1e9:.1f} GB per GPU >> 126 MB L2",
+                   "parallelism": (f"{cfg.n_queries} queries partitioned over {world} GPU(s) "
+                                   f"({cfg.n_queries // world if world <= cfg.n_queries else 0}+ per GPU), no collective"
+                                   if args.scaling == "strong" else
+                                   f"{world} GPU(s), each its own {cfg.n_queries}-query batch, no collective")},
         "roofline": {"bound": "hbm",
-                     "kernel": {"tc": "split_tct_kernel (K2, tcgen05 swap-AB)", "rol": "split_tc_kernel (K2, tcgen05 rows-on-lanes)",
-                                "mma": "split_kernel (K2, mma.sync)"}[args.kernel], "achieved": achieved, "peak": peak,
+                     "kernel": {"tc": "split_tct_kernel (K2, tcgen05 swap-AB) + split_tc_kernel on hybrid big items",
+                                "rol": "split_tc_kernel (K2, tcgen05 rows-on-lanes)",
+                                "mma": "split_kernel (K2, mma.sync)"}[args.kernel],
+                     "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": load_traffic(cfg.name, args.kernel),
                      "frac_of_nominal_8tbs": achieved / 8000.0,
-                     "bounds_us_per_launch": bounds,
+                     "bounds_us_per_launch": bounds_of(cfg, lay, batch, split_bytes),
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": split_bytes,
                      "split_ms_per_launch": split_avg_s * 1e3,
-                     "split_share_of_step": sum(split_ms) / elapsed_ms if world == 1 else None,
+                     "split_share_of_step": sum(split_ms) / my_ms,
+                     "rank": 0,
                      "step_gbs_all_kernels": layers * (kv_b + q_b + o_b) / (ms_step / 1e3) / 1e9},
-        "plan": {"items": st["n_items"], "pieces": st["n_pieces"], "partials": st["n_partials"],
+        "plan": {"items": st["n_items"], "big_items": st.get("n_big", 0), "pieces": st["n_pieces"],
+                 "partials": st["n_partials"],
                  "unique_tokens_per_kvhead": st["unique_tokens"],
                  "logical_tokens_per_kvhead": st["logical_tokens"],
                  "partial_bytes_per_layer": st["workspace_bytes"] * 2,   # written by K2 + read by K3
                  "plan_build_s": plan_s},
+        "per_rank": per_rank,
         "step_ms": {"p10": pct(0.1), "median": pct(0.5), "p90": pct(0.9), "rank0_only": world > 1},
         "cuda_graph": graph,
-        "per_layer": {"us": ms_step / layers * 1e3, "tokens_per_s": float(B) / (ms_step / layers / 1e3)},
-        "gpu_launches": args.steps * layers * 3,
+        "per_layer": {"us": ms_step / layers * 1e3, "tokens_per_s": float(total_b) / (ms_step / layers / 1e3)},
+        "gpu_launches": launches,
         "clocks": clocks,
         "e2e": e2e,
     }
+    if costream is not None:
+        line["prefill_costream"] = costream
     if world == 1:
         line["contiguous_pages"] = run_contiguous(args, cfg, lay, layers, q, kc, vc, out, dev)
+    if world == 1 and not args.no_shares and args.scaling == "strong" and cfg.n_queries >= 16:
+        line["strong_scaling_shares"] = run_shares(args, cfg, lay, layers, tens, dev, value)
     if world == 1 and not args.no_model:
         line["model_step"] = run_model_step(args, cfg, lay, layers, kc, vc, dev, value)
     if world == 1 and not args.no_expansion:
@@ -436,11 +567,75 @@ def run_orion(args, cfg, layers):
     if world == 1 and not args.no_prefill:
         line["prefill_costream"] = run_costream(args, cfg, lay, layers, q, kn, vn, out, kc, vc, dev,
                                                 value)
+    if world == 1 and not args.no_c5 and cfg.name == "c4":
+        del batch, tens, kc, vc, q, kn, vn, out
+        torch.cuda.empty_cache()
+        line["c5"] = run_c5(args, dev)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, layers, args.cpu_seconds)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_shares(args, cfg, lay, layers, tens, dev, full_value):
+    """The single-GPU points of the strong-scaling curve: the step on the first Q/N queries of the
+    batch (what one rank of an N-GPU run expands, same pools), N = 2, 4, 8.  projected_value =
+    N x its rate (ranks share nothing)."""
+    import torch
+    kc, vc, q, kn, vn, out = tens
+    res = {}
+    for n in (2, 4, 8):
+        nq = cfg.n_queries // n
+        if nq < 1:
+            continue
+        sub, br = WT.subset_layout(lay, list(range(nq)))
+        idx = torch.from_numpy(br).to(dev)
+        sub_t = (kc, vc, q.index_select(1, idx), kn.index_select(1, idx), vn.index_select(1, idx),
+                 out.index_select(1, idx))
+        batch = batch_of(args, cfg, sub, dev)
+        steps = max(3, min(args.steps, 10))
+        ms, _, split_ms, _, _ = time_steps(batch, layers, sub_t, steps, 2, torch.cuda.current_stream(dev))
+        tok_s = sub.n_branches / (ms / steps / 1e3)
+        res[f"n{n}"] = {"queries_per_gpu": nq, "branches_per_gpu": sub.n_branches,
+                        "ms_per_step": ms / steps, "tokens_per_s_per_gpu": tok_s,
+                        "split_ms_per_launch": statistics.mean(split_ms),
+                        "projected_value": n * tok_s, "projected_efficiency": n * tok_s / (n * full_value)}
+    return res
+
+
+def run_c5(args, dev):
+    """BASELINE configs[4] (the stress config): one GPU's share of the 8-GPU run, 8 queries x wide-64
+    and 8 queries x chain-64 (8K prefix, 256 tok/point, 32 layers), the default plan; tok/s, the
+    split kernels' time against the three bounds and ncu's DRAM bytes."""
+    import torch
+    res = {}
+    for name in ("c5w", "c5c"):
+        cfg = WC.CONFIGS[name].with_(n_queries=8)
+        layers = cfg.layers
+        lay = WT.make_layout(cfg, seed=cfg.seed)
+        tens = alloc_tensors(args, cfg, lay, layers, dev, cfg.seed * 7)
+        batch = batch_of(args, cfg, lay, dev)
+        steps = max(3, min(args.steps, 10))
+        ms, _, split_ms, _, _ = time_steps(batch, layers, tens, steps, 3, torch.cuda.current_stream(dev))
+        kv_b, q_b, _ = algorithmic_bytes(cfg, lay)
+        split_s = statistics.mean(split_ms) / 1e3
+        b = bounds_of(cfg, lay, batch, kv_b + q_b)
+        peak, _ = load_peaks()
+        bound_us = max(b["hbm"], b["tensor_bf16"], b["mufu_ex2"])
+        res[f"{name}_8q"] = {
+            "workload": workload_str(cfg, layers) + " (one GPU's share of 64 queries on 8 GPUs)",
+            "tokens_per_s": lay.n_branches / (ms / steps / 1e3), "ms_per_step": ms / steps,
+            "split_us_per_launch": split_s * 1e6, "split_gbs": (kv_b + q_b) / split_s / 1e9,
+            "frac_of_hbm_peak": (kv_b + q_b) / split_s / 1e9 / peak,
+            "bounds_us": {k: b[k] for k in ("hbm", "tensor_bf16", "mufu_ex2")},
+            "frac_of_max_bound": bound_us / (split_s * 1e6),
+            "ncu_dram_bytes_per_launch": load_traffic(name, args.kernel),
+            "plan": {"items": batch.stats["n_items"], "big_items": batch.stats.get("n_big", 0),
+                     "partials": batch.stats["n_partials"]}}
+        del tens, batch
+        torch.cuda.empty_cache()
+    return res
 
 
 def run_contiguous(args, cfg, lay, layers, q, kc, vc, out, dev):
@@ -965,14 +1160,32 @@ def run_e2e(args, batch, layers, q, kn, vn, out, kc, vc, dev, world, total_b):
             "note": "pinned host inputs copied H2D and out copied D2H every step, pipelined per layer"}
 
 
+def spawn_ranks(args):
+    """`--gpus N` without torchrun: launch the N ranks through torch.distributed.run (one process
+    per GPU, 127.0.0.1 rendezvous) with the same arguments; rank 0 prints the JSON line."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     args = parse()
     cfg = WC.CONFIGS[args.config]
     if args.queries:
         cfg = cfg.with_(n_queries=args.queries)
     layers = args.layers or cfg.layers
+    world_env = os.environ.get("WORLD_SIZE")
+    if args.gpus > 1 and world_env is None:
+        sys.exit(spawn_ranks(args))
+    if world_env is not None and int(world_env) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}")
     if args.impl == "reference":
         run_reference(args, cfg, layers)
+    elif args.plan_only:
+        plan_only(args, cfg, layers)
     else:
         run_orion(args, cfg, layers)
 

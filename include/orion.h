@@ -155,6 +155,7 @@ typedef struct {
   int64_t streamed_tokens;  /* K/V token rows the split kernel streams, all kv heads (capacity
                                bound): a paired prefill plan streams its pairs' shared ranges once */
   int64_t paired;           /* 1: point-prefill plan run as item pairs (ORION_PLAN_PAIR) */
+  int64_t n_big;            /* hybrid decode plan: items run on the rows-on-lanes kernel (65..128 rows) */
 } orion_plan_stats;
 
 /*

@@ -61,7 +61,7 @@ class PlanOpts(ctypes.Structure):
 class PlanStats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in ("n_items", "n_pieces", "n_partials", "n_rows",
                                                "unique_tokens", "logical_tokens", "plan_bytes",
-                                               "workspace_bytes", "streamed_tokens", "paired")]
+                                               "workspace_bytes", "streamed_tokens", "paired", "n_big")]
 
 
 SEG_DTYPE = np.dtype([("pt_off", np.int32), ("start", np.int32), ("len", np.int32), ("dyn", np.int32)])

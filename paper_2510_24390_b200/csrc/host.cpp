@@ -795,6 +795,7 @@ extern "C" orion_status orion_plan_get_stats(const void* h_plan, orion_plan_stat
   out->workspace_bytes = h->workspace_bytes;
   out->streamed_tokens = h->streamed_tokens;
   out->paired = h->paired;
+  out->n_big = h->n_big;
   return ORION_OK;
 }
 

@@ -122,3 +122,39 @@ def test_two_rank_gloo(scaling):
         else:
             assert all(s == list(range(cfg.n_queries)) for s in shards)
             assert units == world * lay.n_branches
+
+
+@pytest.mark.parametrize("scaling", ["strong", "weak"])
+def test_bench_launcher_two_ranks_plan_only(scaling):
+    """bench.py's own N>1 path on CPU: `--gpus 2` without torchrun launches the two ranks itself
+    (torch.distributed.run, 127.0.0.1, gloo under --plan-only), each shards / plans its queries, and
+    rank 0 prints one JSON line with the whole-job branch count and every rank's share."""
+    import json
+    import subprocess
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--plan-only",
+                        "--config", "c3", "--scaling", scaling], capture_output=True, text=True, env=env,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    cfg = C.CONFIGS["c3"]
+    lay = T.make_layout(cfg)
+    assert d["n_gpus"] == 2 and d["scaling"] == scaling and d["plan_only"]
+    qs = [p["queries"] for p in sorted(d["per_rank"], key=lambda p: p["rank"])]
+    if scaling == "strong":
+        assert qs == shard.partition_queries([1.0] * cfg.n_queries, 2)
+        assert d["config"]["branches_per_step"] == lay.n_branches
+    else:
+        assert qs == [list(range(cfg.n_queries))] * 2
+        assert d["config"]["branches_per_step"] == 2 * lay.n_branches
+
+
+def test_bench_rejects_inconsistent_world():
+    import subprocess
+    env = dict(os.environ, WORLD_SIZE="3", RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--plan-only"],
+                       capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode != 0 and "WORLD_SIZE=3" in r.stderr
