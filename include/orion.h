@@ -240,17 +240,19 @@ orion_status orion_plan_get_stats(const void* h_plan, orion_plan_stats* out);
  *  k_new, v_new   bf16 [n_branches][Hkv][d] (device).
  *  k_cache, v_cache  bf16 [num_pages][Hkv][P][d] (device, one layer).
  *  own_pt_off[n_branches], own_cap[n_branches]  device int32: branch page runs and capacities.
- *  page_table     device int32.
+ *  page_table     device int32;  num_pages  pages in the caches.
  *  own_len[n_branches]  device int32, in/out.  ADVANCE: write slot own_len, then own_len += 1.
- *                 REWRITE: write slot own_len - 1.  A slot outside [0, own_cap) is skipped and
- *                 own_len is left unchanged (no out-of-run write ever happens).
- * Errors: INVALID_ARG (null/unaligned pointers, bad mode), UNSUPPORTED (shape), CUDA.
+ *                 REWRITE: write slot own_len - 1.  A slot outside [0, own_cap), or a page id
+ *                 outside [0, num_pages), is skipped and own_len is left unchanged (no write
+ *                 outside the caches ever happens); the debug build (ORION_CHECK) reports such a
+ *                 page id as INVALID_ARG (it synchronises the stream).
+ * Errors: INVALID_ARG (null/unaligned pointers, bad mode, num_pages < 1), UNSUPPORTED (shape), CUDA.
  */
 orion_status orion_kv_append(const orion_attn_shape* shape, int32_t n_branches,
                              const void* k_new, const void* v_new, void* k_cache, void* v_cache,
                              const int32_t* own_pt_off, const int32_t* own_cap,
-                             const int32_t* page_table, int32_t* own_len, int32_t mode,
-                             void* stream);
+                             const int32_t* page_table, int32_t num_pages, int32_t* own_len,
+                             int32_t mode, void* stream);
 
 /*
  * orion_expand_attn — one dependency-masked, batched GQA decode-attention step (PAPER.md:337
@@ -405,15 +407,16 @@ orion_status orion_rmsnorm(int32_t n_rows, int32_t hidden, const void* a, const 
  * at position pos = pos_base[b] + slot (rotate_half pairs (i, i + d/2), inv_freq_i =
  * rope_theta^(-2i/d); slot = own_len[b] for ADVANCE, own_len[b] - 1 for REWRITE, as in
  * orion_kv_append); q goes to q_out bf16 [n_branches][Hq][d], k and v to the slot of b's own run
- * in the paged caches (skipped when the slot is outside [0, own_cap)); ADVANCE then increments
- * own_len.  pos_base[b] = the number of context tokens before b's own run (reading M2: a token's
+ * in the paged caches (skipped when the slot is outside [0, own_cap) or its page id outside
+ * [0, num_pages), as in orion_kv_append); ADVANCE then increments own_len.  pos_base[b] = the number of context tokens before b's own run (reading M2: a token's
  * position is its index in its branch's concatenated context).  shape->kv_interleaved as for the
  * attention calls.  Errors: INVALID_ARG, UNSUPPORTED, CUDA.
  */
 orion_status orion_rope_append(const orion_attn_shape* shape, int32_t n_branches, const void* qkv,
                                void* q_out, void* k_cache, void* v_cache, const int32_t* own_pt_off,
-                               const int32_t* own_cap, const int32_t* page_table, int32_t* own_len,
-                               const int32_t* pos_base, float rope_theta, int32_t mode, void* stream);
+                               const int32_t* own_cap, const int32_t* page_table, int32_t num_pages,
+                               int32_t* own_len, const int32_t* pos_base, float rope_theta,
+                               int32_t mode, void* stream);
 
 /*
  * orion_silu_mul — out = bf16(SiLU(g) * u) per row of gate_up = [g (inter) | u (inter)] (the fused

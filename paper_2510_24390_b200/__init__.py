@@ -195,8 +195,8 @@ def kv_append(hq, hkv, d, page, k_new, v_new, k_cache, v_cache, own_pt_off, own_
     _lib.check(lib().orion_kv_append(ctypes.byref(shape), int(own_len.shape[0]), k_new.data_ptr(),
                                      v_new.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(),
                                      own_pt_off.data_ptr(), own_cap.data_ptr(),
-                                     page_table.data_ptr(), own_len.data_ptr(), int(mode),
-                                     _stream_ptr(stream)))
+                                     page_table.data_ptr(), int(k_cache.shape[0]), own_len.data_ptr(),
+                                     int(mode), _stream_ptr(stream)))
 
 
 def expand_attn(hq, hkv, d, page, q, out, lse, k_cache, v_cache, page_table, own_len, h_plan,
@@ -346,8 +346,8 @@ class ExpansionBatch:
         _lib.check(lib().orion_rope_append(
             ctypes.byref(shape), self.n_branches, qkv.data_ptr(), q_out.data_ptr(), k_cache.data_ptr(),
             v_cache.data_ptr(), self.own_pt_off.data_ptr(), self.own_cap.data_ptr(),
-            self.page_table.data_ptr(), self.own_len.data_ptr(), pos_base.data_ptr(),
-            float(rope_theta), int(mode), _stream_ptr(stream)))
+            self.page_table.data_ptr(), int(k_cache.shape[0]), self.own_len.data_ptr(),
+            pos_base.data_ptr(), float(rope_theta), int(mode), _stream_ptr(stream)))
 
     def append(self, k_new, v_new, k_cache, v_cache, mode=APPEND_ADVANCE, stream=None):
         kv_append(self.hq, self.hkv, self.d, self.page, k_new, v_new, k_cache, v_cache,

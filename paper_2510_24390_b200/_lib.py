@@ -93,7 +93,7 @@ def lib():
         L.orion_expand_plan.argtypes = [P(AttnShape), i32, vp, vp, vp, P(PlanOpts), vp, sz,
                                         P(sz), P(sz)]
         L.orion_plan_get_stats.argtypes = [vp, P(PlanStats)]
-        L.orion_kv_append.argtypes = [P(AttnShape), i32, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp]
+        L.orion_kv_append.argtypes = [P(AttnShape), i32, vp, vp, vp, vp, vp, vp, vp, i32, vp, i32, vp]
         L.orion_expand_attn.argtypes = [P(AttnShape), i32, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp,
                                         vp, sz, vp]
         L.orion_expand_split.argtypes = [P(AttnShape), i32, vp, vp, vp, i32, vp, vp, vp, vp, vp,
@@ -104,7 +104,7 @@ def lib():
         L.orion_select_branches.argtypes = [i32, vp, vp, vp, i32, vp, vp, vp, i32, vp]
         L.orion_context_base.argtypes = [i32, vp, vp, vp, vp]
         L.orion_rmsnorm.argtypes = [i32, i32, vp, vp, vp, ctypes.c_float, vp, vp, vp]
-        L.orion_rope_append.argtypes = [P(AttnShape), i32, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+        L.orion_rope_append.argtypes = [P(AttnShape), i32, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp,
                                         ctypes.c_float, i32, vp]
         L.orion_silu_mul.argtypes = [i32, i32, vp, vp, vp]
         for f in ("orion_expand_split", "orion_expand_combine", "orion_dag_waves", "orion_bind_segments", "orion_expand_plan",

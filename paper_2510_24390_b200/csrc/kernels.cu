@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(128) kv_append_kernel(
     __nv_bfloat16* __restrict__ k_cache, __nv_bfloat16* __restrict__ v_cache,
     const int32_t* __restrict__ own_pt_off, const int32_t* __restrict__ own_cap,
     const int32_t* __restrict__ page_table, int32_t* __restrict__ own_len, int hkv,
-    int page_shift, int mode, int kvs) {
+    int page_shift, int mode, int kvs, int num_pages, int* err) {
   constexpr int CH = D / 8;
   __shared__ int s_pos, s_page, s_len;
   const int b = blockIdx.x;
@@ -470,7 +470,12 @@ __global__ void __launch_bounds__(128) kv_append_kernel(
     const bool ok = pos >= 0 && pos < own_cap[b];
     s_len = len;
     s_pos = pos;
-    s_page = ok ? page_table[own_pt_off[b] + (pos >> page_shift)] : -1;
+    int page = ok ? page_table[own_pt_off[b] + (pos >> page_shift)] : -1;
+    if (page >= num_pages || (ok && page < 0)) {     // outside the caches: never written
+      if (err) atomicCAS(err, 0, b + 1);
+      page = -1;
+    }
+    s_page = page;
   }
   __syncthreads();
   const int page = s_page, pos = s_pos;
@@ -583,6 +588,16 @@ orion_status check_plan_contents(const PlanHeader* h, const char* dplan, const i
                                  const int32_t* own_len, int num_pages, cudaStream_t st) {
   static const int zero[4] = {0, 0, 0, 0};
   int res[4] = {0, 0, 0, 0};
+  {   // the device plan must be a copy of this host plan (not a stale or foreign one)
+    PlanHeader dh;
+    cudaError_t ce = cudaMemcpyAsync(&dh, dplan, sizeof dh, cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+    if (ce != cudaSuccess) return fail(ORION_ERR_CUDA, "ORION_CHECK plan read-back: %s", cudaGetErrorString(ce));
+    if (dh.magic != h->magic || dh.plan_id != h->plan_id || dh.n_items != h->n_items ||
+        dh.n_partials != h->n_partials)
+      return fail(ORION_ERR_INVALID_ARG, "ORION_CHECK: d_plan is not a copy of h_plan (plan id %llx vs %llx)",
+                  (unsigned long long)dh.plan_id, (unsigned long long)h->plan_id);
+  }
   cudaError_t e = cudaMemcpyToSymbolAsync(g_check_err, zero, sizeof zero, 0, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) {
     check_plan_kernel<<<(h->n_items + 127) / 128, 128, 0, st>>>(
@@ -602,6 +617,36 @@ orion_status check_plan_contents(const PlanHeader* h, const char* dplan, const i
   return ORION_OK;
 }
 #endif
+
+}  // namespace
+
+namespace orion {
+// Append page-id check of the debug build (ORION_CHECK): the append kernels record the first
+// branch whose target page lies outside [0, num_pages) (they skip its write in every build); the
+// debug build reads the record back (synchronising) and reports INVALID_ARG.
+#ifdef ORION_CHECK
+__device__ int g_append_err;
+int* append_check_begin(cudaStream_t st) {
+  int* p = nullptr;
+  if (cudaGetSymbolAddress(reinterpret_cast<void**>(&p), g_append_err) != cudaSuccess) return nullptr;
+  cudaMemsetAsync(p, 0, sizeof(int), st);
+  return p;
+}
+orion_status append_check_end(cudaStream_t st, const char* what) {
+  int v = 0;
+  cudaError_t e = cudaMemcpyFromSymbolAsync(&v, g_append_err, sizeof v, 0, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return fail(ORION_ERR_CUDA, "ORION_CHECK %s: %s", what, cudaGetErrorString(e));
+  if (v) return fail(ORION_ERR_INVALID_ARG, "ORION_CHECK %s: branch %d's own-run page id is outside [0, num_pages)", what, v - 1);
+  return ORION_OK;
+}
+#else
+int* append_check_begin(cudaStream_t) { return nullptr; }
+orion_status append_check_end(cudaStream_t, const char*) { return ORION_OK; }
+#endif
+}  // namespace orion
+
+namespace {
 
 template <int D>
 orion_status launch_split(const PlanHeader* h, const char* dplan, const void* q, const void* k,
@@ -740,7 +785,8 @@ extern "C" orion_status orion_kv_append(const orion_attn_shape* shape, int32_t n
                                         const void* k_new, const void* v_new, void* k_cache,
                                         void* v_cache, const int32_t* own_pt_off,
                                         const int32_t* own_cap, const int32_t* page_table,
-                                        int32_t* own_len, int32_t mode, void* stream) {
+                                        int32_t num_pages, int32_t* own_len, int32_t mode,
+                                        void* stream) {
   orion_status st = check_shape_public(shape);
   if (st != ORION_OK) return st;
   if (n_branches < 0) return fail(ORION_ERR_INVALID_ARG, "n_branches < 0");
@@ -751,17 +797,19 @@ extern "C" orion_status orion_kv_append(const orion_attn_shape* shape, int32_t n
     return fail(ORION_ERR_INVALID_ARG, "null device pointer");
   if (!aligned16(k_new) || !aligned16(v_new) || !aligned16(k_cache) || !aligned16(v_cache))
     return fail(ORION_ERR_INVALID_ARG, "K/V pointers must be 16-byte aligned");
+  if (num_pages < 1) return fail(ORION_ERR_INVALID_ARG, "num_pages < 1");
   if (n_branches == 0) return ORION_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int shift = log2i(shape->page_size);
+  int* err = append_check_begin(s);
   cudaError_t e = launch_pdl(
       shape->head_dim == 128 ? kv_append_kernel<128> : kv_append_kernel<64>, dim3(n_branches), dim3(128), 0, s,
       static_cast<const __nv_bfloat16*>(k_new), static_cast<const __nv_bfloat16*>(v_new),
       static_cast<__nv_bfloat16*>(k_cache), static_cast<__nv_bfloat16*>(v_cache), own_pt_off,
-      own_cap, page_table, own_len, shape->num_kv_heads, shift, mode, 1 + shape->kv_interleaved);
+      own_cap, page_table, own_len, shape->num_kv_heads, shift, mode, 1 + shape->kv_interleaved, num_pages, err);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ORION_ERR_CUDA, "kv_append_kernel: %s", cudaGetErrorString(e));
-  return ORION_OK;
+  return append_check_end(s, "kv_append");
 }
 
 extern "C" orion_status orion_expand_split(const orion_attn_shape* shape, int32_t n_branches,
@@ -854,8 +902,8 @@ extern "C" orion_status orion_point_prefill_attn(const orion_attn_shape* shape, 
 }
 
 extern "C" const char* orion_version(void) {
-  return "orion-b200 0.3 (sm_100a; K1 append; K2 split: tcgen05.mma + TMEM + TMA swap-AB (decode, "
-         "default) | rows-on-lanes (d = 64, point prefill; K/V-sharing item pairs with ORION_PLAN_PAIR) | "
-         "mma.sync m16n8k16 (ORION_PLAN_MMA_SYNC); "
-         "K3 combine)";
+  return "orion-b200 0.4 (sm_100a; K1 append; K2 split: hybrid decode plans -- tcgen05.mma + TMEM + TMA swap-AB "
+         "for items of <= 64 rows, rows-on-lanes tcgen05 for 65..128-row (masked) block items, two PDL-chained "
+         "launches | rows-on-lanes (d = 64, point prefill; K/V-sharing item pairs with ORION_PLAN_PAIR) | "
+         "mma.sync m16n8k16 (ORION_PLAN_MMA_SYNC); K3 combine)";
 }

@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(128) rope_append_kernel(
     const int32_t* __restrict__ own_pt_off, const int32_t* __restrict__ own_cap,
     const int32_t* __restrict__ page_table, int32_t* __restrict__ own_len,
     const int32_t* __restrict__ pos_base, int hq, int hkv, int page_shift, int kvs, int mode,
-    float log2_theta) {
+    float log2_theta, int num_pages, int* err) {
   constexpr int HALF = D / 2;
   __shared__ int s_slot, s_page, s_len;
   pdl_trigger();
@@ -124,7 +124,12 @@ __global__ void __launch_bounds__(128) rope_append_kernel(
     const bool ok = slot >= 0 && slot < own_cap[b];
     s_len = len;
     s_slot = slot;
-    s_page = ok ? page_table[own_pt_off[b] + (slot >> page_shift)] : -1;
+    int page = ok ? page_table[own_pt_off[b] + (slot >> page_shift)] : -1;
+    if (page >= num_pages || (ok && page < 0)) {     // outside the caches: never written
+      if (err) atomicCAS(err, 0, b + 1);
+      page = -1;
+    }
+    s_page = page;
   }
   __syncthreads();
   const int slot = s_slot;
@@ -220,9 +225,9 @@ extern "C" orion_status orion_rmsnorm(int32_t n_rows, int32_t hidden, const void
 extern "C" orion_status orion_rope_append(const orion_attn_shape* shape, int32_t n_branches,
                                           const void* qkv, void* q_out, void* k_cache, void* v_cache,
                                           const int32_t* own_pt_off, const int32_t* own_cap,
-                                          const int32_t* page_table, int32_t* own_len,
-                                          const int32_t* pos_base, float rope_theta, int32_t mode,
-                                          void* stream) {
+                                          const int32_t* page_table, int32_t num_pages,
+                                          int32_t* own_len, const int32_t* pos_base, float rope_theta,
+                                          int32_t mode, void* stream) {
   orion_status st = check_shape_public(shape);
   if (st != ORION_OK) return st;
   if (n_branches < 0) return fail(ORION_ERR_INVALID_ARG, "n_branches < 0");
@@ -234,20 +239,22 @@ extern "C" orion_status orion_rope_append(const orion_attn_shape* shape, int32_t
   if (!al16(qkv) || !al16(q_out) || !al16(k_cache) || !al16(v_cache))
     return fail(ORION_ERR_INVALID_ARG, "rope_append: pointers must be 16-byte aligned");
   if (!(rope_theta > 1.f)) return fail(ORION_ERR_INVALID_ARG, "rope_theta must be > 1");
+  if (num_pages < 1) return fail(ORION_ERR_INVALID_ARG, "rope_append: num_pages < 1");
   if (n_branches == 0) return ORION_OK;
   int shift = 0;
   while ((1 << shift) < shape->page_size) ++shift;
   const float lt = std::log2(rope_theta);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int* err = append_check_begin(s);
   cudaError_t e = launch_pdl(
       shape->head_dim == 128 ? rope_append_kernel<128> : rope_append_kernel<64>, dim3(n_branches), dim3(128), 0, s,
       static_cast<const __nv_bfloat16*>(qkv), static_cast<__nv_bfloat16*>(q_out),
       static_cast<__nv_bfloat16*>(k_cache), static_cast<__nv_bfloat16*>(v_cache), own_pt_off, own_cap,
       page_table, own_len, pos_base, shape->num_q_heads, shape->num_kv_heads, shift,
-      1 + shape->kv_interleaved, mode, lt);
+      1 + shape->kv_interleaved, mode, lt, num_pages, err);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ORION_ERR_CUDA, "rope_append_kernel: %s", cudaGetErrorString(e));
-  return ORION_OK;
+  return append_check_end(s, "rope_append");
 }
 
 extern "C" orion_status orion_silu_mul(int32_t n_rows, int32_t inter, const void* gate_up, void* out,

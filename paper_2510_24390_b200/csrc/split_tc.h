@@ -13,6 +13,10 @@
 namespace orion {
 
 orion_status fail(orion_status code, const char* fmt, ...);
+// Debug-build (ORION_CHECK) report of an append whose own-run page id is outside [0, num_pages):
+// begin returns the device record to pass to the kernel (nullptr in release builds), end reads it.
+int* append_check_begin(cudaStream_t st);
+orion_status append_check_end(cudaStream_t st, const char* what);
 orion_status check_shape_public(const orion_attn_shape* s);
 
 // Per-device launch setup, thread-safe: the SM count of the current device, and the opt-in

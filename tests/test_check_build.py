@@ -49,6 +49,35 @@ for cfg in (C.CONFIGS["c1"], C.CONFIGS["c1"].with_(d=128, hq=8, hkv=2)):
         assert e.code == _lib.ERR_INVALID_ARG and "ORION_CHECK" in str(e) and "page id" in str(e), str(e)
     else:
         raise AssertionError("out-of-range page id not reported")
+# a device plan that is not a copy of the host plan (stale / foreign) is reported
+cfg = C.CONFIGS["c1"].with_(d=128, hq=8, hkv=2)
+lay = T.make_layout(cfg, ragged=True, extra_tokens=cfg.page)
+ten = T.make_qkv(cfg, lay)
+from tests.gpu_helpers import batch_for
+a = batch_for(cfg, lay, chunk_tokens=64)
+b = batch_for(cfg, lay, chunk_tokens=512, flags=orion.PLAN_NO_MERGE)
+dev = torch.device("cuda")
+q = ten["q"][0].to(dev); out = torch.empty_like(q)
+kc, vc = ten["k_cache"][0].to(dev), ten["v_cache"][0].to(dev)
+try:
+    orion.expand_attn(cfg.hq, cfg.hkv, cfg.d, cfg.page, q, out, None, kc, vc, a.page_table, a.own_len,
+                      a.h_plan, b.d_plan, a.workspace)
+except orion.OrionError as e:
+    assert e.code == _lib.ERR_INVALID_ARG and "d_plan" in str(e), str(e)
+else:
+    raise AssertionError("mismatched device plan not reported")
+# an append whose own-run page id lies outside the caches is reported (never written)
+bad = lay.page_table.copy()
+bad[int(lay.point_pt_off[1])] = lay.num_pages + 3
+c = batch_for(cfg, lay)
+c.page_table = torch.from_numpy(bad).to(dev)
+kn, vn = ten["k_new"][0].to(dev), ten["v_new"][0].to(dev)
+try:
+    c.append(kn, vn, kc, vc)
+except orion.OrionError as e:
+    assert e.code == _lib.ERR_INVALID_ARG and "outside [0, num_pages)" in str(e), str(e)
+else:
+    raise AssertionError("out-of-range append page not reported")
 print("CHECK_BUILD_OK")
 '''
 

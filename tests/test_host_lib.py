@@ -296,13 +296,16 @@ def test_device_entry_points_validate_without_gpu():
     import ctypes
     L = _lib.lib()
     shape = _lib.AttnShape(4, 2, 64, 16, 0.0)
-    assert L.orion_kv_append(ctypes.byref(shape), 1, None, None, None, None, None, None, None,
+    assert L.orion_kv_append(ctypes.byref(shape), 1, None, None, None, None, None, None, None, 8,
                              None, 0, None) == _lib.ERR_INVALID_ARG
     assert L.orion_expand_attn(ctypes.byref(shape), 1, None, None, None, None, None, 1, None,
                                None, None, None, None, 0, None) == _lib.ERR_INVALID_ARG
     bad = _lib.AttnShape(4, 2, 80, 16, 0.0)
-    assert L.orion_kv_append(ctypes.byref(bad), 1, None, None, None, None, None, None, None,
+    assert L.orion_kv_append(ctypes.byref(bad), 1, None, None, None, None, None, None, None, 8,
                              None, 0, None) == _lib.ERR_UNSUPPORTED
+    fake = ctypes.c_void_p(16)                       # num_pages < 1 is refused before any launch
+    assert L.orion_kv_append(ctypes.byref(shape), 1, fake, fake, fake, fake, fake, fake, fake, 0,
+                             fake, 0, None) == _lib.ERR_INVALID_ARG
 
 
 # ------------------------------------------------------------------ point-prefill plans
