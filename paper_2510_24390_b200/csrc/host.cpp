@@ -490,6 +490,7 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
     std::vector<std::vector<std::pair<Range, std::vector<int32_t>>>> bchunks;
     std::vector<std::vector<int32_t>> bunion;
     std::vector<int32_t> bpiece;
+    int64_t big_tokens = 0;                        // tokens of the masked ranges, per kv head
     for (size_t pi = 0; pi < pieces.size(); ++pi) {
       const Piece& p = pieces[pi];
       unique_tokens += p.t1 - p.t0;
@@ -515,8 +516,10 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
             } else {
               idx = f->second;
             }
-            for (int32_t t = p.t0; t < p.t1; t += ch)
-              bchunks[idx].push_back({Range{p.pt_off, t, std::min(p.t1, t + ch), p.dyn, 0, {0, 0, 0}}, S});
+            // 1024-token ranges: the granularity at which the block's ranges are grouped into items
+            for (int32_t t = p.t0; t < p.t1; t += 1024)
+              bchunks[idx].push_back({Range{p.pt_off, t, std::min(p.t1, t + 1024), p.dyn, 0, {0, 0, 0}}, S});
+            big_tokens += p.t1 - p.t0;
             std::vector<int32_t> u;
             std::set_union(bunion[idx].begin(), bunion[idx].end(), S.begin(), S.end(), std::back_inserter(u));
             bunion[idx].swap(u);
@@ -541,6 +544,10 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
         }
       }
     }
+    // Masked items are long (whole reader blocks): cap their tokens so that there are about six
+    // per SM (a few 8K-token items per SM left the busiest SM 1.5x above the mean on c5 chain-64).
+    const int64_t sms = (opts && opts->num_sms > 0) ? opts->num_sms : 148;
+    const int64_t big_cap = std::max<int64_t>(1024, std::min<int64_t>(kMergeTokens, big_tokens * Hkv / (6 * sms)));
     for (size_t bi = 0; bi < bkeys.size(); ++bi) {
       const int32_t g = bkeys[bi].first;
       const std::vector<int32_t>& U = bunion[bi];
@@ -553,7 +560,7 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
       for (size_t c0 = 0; c0 < cs.size();) {
         size_t c1 = c0;
         int64_t tok = 0;
-        while (c1 < cs.size() && (c1 == c0 || tok + (cs[c1].first.t1 - cs[c1].first.t0) <= kMergeTokens))
+        while (c1 < cs.size() && (c1 == c0 || tok + (cs[c1].first.t1 - cs[c1].first.t0) <= big_cap))
           tok += cs[c1].first.t1 - cs[c1].first.t0, ++c1;
         WorkItem w{};
         w.pt_off = (int32_t)ranges.size(); w.dyn = -1;

@@ -199,7 +199,7 @@ def _check_plan_covers(cfg, lay, offs, segs, own_len, flags=0):
             rl = [(int(r["pt_off"]), int(r["t0"]), int(r["t1"]), int(r["dyn"]),
                    int(r["r0"]) & 0xffffffff if r["flags"] & 4 else 0xffffffff)   # kRangeMasked
                   for r in ranges[it["pt_off"]:it["pt_off"] + it["p1"]]]
-            assert len(rl) >= 2 or rl[0][4] != 0xffffffff
+            assert len(rl) >= 1
         else:
             rl = [(int(it["pt_off"]), int(it["t0"]), int(it["t1"]), int(it["dyn"]), 0xffffffff)]
         for r in range(it["row_begin"], it["row_begin"] + it["n_rows"]):
