@@ -71,6 +71,10 @@ struct Smem {
 __device__ __forceinline__ uint32_t colS(uint32_t p) { return p * 64; }
 __device__ __forceinline__ uint32_t colP(uint32_t p) { return 128 + p * 32; }
 __device__ __forceinline__ uint32_t colO(uint32_t p) { return 256 + p * 128; }
+// Q of the current item as the QK MMAs' A operand in TMEM (D / 2 columns): copied from its smem
+// staging buffer once per item (tcgen05.cp, in the QK issuer's pipeline order) instead of being
+// re-read from shared memory by every tile's QK -- a third of a tile's smem operand traffic.
+constexpr uint32_t kColQ = 192;
 constexpr int kThreadsTC = 384;   // warps 0-3: TMEM alloc / idle / TMA / MMA; 4-7: WG0; 8-11: WG1
 // The TMA and MMA warps sit on SM sub-partitions 2 and 3 so that their barrier polling does not
 // steal issue slots from the softmax warps of items with <= 64 rows (TMEM lanes 0-63 are only
@@ -302,11 +306,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       const uint64_t dk = dk0 + static_cast<uint64_t>((s * L::KVB) >> 4);
       const uint32_t dS = tmem + colS(p);
       if (elect_one()) {
+        if (c.t == 0) {                             // the item's Q: smem staging buffer -> TMEM
+#pragma unroll
+          for (int ks = 0; ks < D / 16; ++ks)
+            tc_cp_128x256b(tmem + kColQ + ks * 8,
+                           dq + static_cast<uint64_t>(((ks >> 2) * L::HALF_Q + (ks & 3) * 32) >> 4));
+        }
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
           const uint64_t off = static_cast<uint64_t>(((ks >> 2) * L::HALF_KV + (ks & 3) * 32) >> 4);
-          const uint64_t offq = static_cast<uint64_t>(((ks >> 2) * L::HALF_Q + (ks & 3) * 32) >> 4);
-          mma_ss(dS, dq + offq, dk + off, ID_QK, ks > 0);
+          mma_ts(dS, tmem + kColQ + ks * 8, dk + off, ID_QK, ks > 0);
         }
         tc_commit(s_full + p);
         tc_commit(k_empty + s);

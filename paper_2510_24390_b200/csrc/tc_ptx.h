@@ -123,6 +123,13 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accum)
       : "memory");
 }
+// tcgen05.cp 128x256b: 128 rows x 32 bytes of a shared-memory matrix (described like an MMA
+// operand) into TMEM lanes 0..127, 8 columns.  Runs in the issuing thread's tcgen05 pipeline order
+// with its MMAs (an MMA issued after it reads the copied data; one issued before it has read its
+// own operands first), and tcgen05.commit tracks it.
+__device__ __forceinline__ void tc_cp_128x256b(uint32_t taddr, uint64_t s_desc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;\n" ::"r"(taddr), "l"(s_desc) : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
                                             uint64_t* bar) {
   asm volatile(

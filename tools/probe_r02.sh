@@ -10,6 +10,8 @@ for c in c5w c5c; do
   timeout 300 python bench.py --config $c --queries 8 --steps 10 --warmup 3 $NOX > gpurun_out/p_$c.json 2> gpurun_out/p_$c.err
 done
 timeout 300 python bench.py --steps 10 --warmup 3 $NOX > gpurun_out/p_c4.json 2> gpurun_out/p_c4.err
+timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-prefill --no-e2e --no-model --no-expansion --no-shares --no-c5 --layers 4 > gpurun_out/p_pp.json 2> gpurun_out/p_pp.err
+python -c "import json;d=json.loads(open('gpurun_out/p_pp.json').read().strip().splitlines()[-1]);pp=d['point_prefill'];print('prefill ms/layer', round(pp['ms_per_layer'],3), 'frac', round(pp['roofline']['frac'],3))"
 for c in c5w c5c; do
   ORION_LIB=paper_2510_24390_b200/liborion_trace.so timeout 300 python bench.py --config $c --queries 8 --layers 2 --steps 1 --warmup 0 $NOX > gpurun_out/p_trace_$c.txt 2>&1
 done
