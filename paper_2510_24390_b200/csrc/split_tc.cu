@@ -50,6 +50,20 @@ template <> struct Rings<128> { static constexpr int K = 3, V = 6; };
 template <> struct Rings<64> { static constexpr int K = 4, V = 8; };
 constexpr int kRows = 128;     // MMA M (query rows per item)
 
+constexpr int kRing = 6;          // item ring entries (warp 0 schedules after TMEM allocation)
+constexpr int kMaxRanges = 64;    // ranges whose geometry an entry carries (more: read from the plan)
+// A scheduled item with the geometry of its ranges, resolved once by the scheduler warp (one lane
+// per range: the plan's Range and the dynamic end's own_len loads overlap) and read from shared
+// memory by every role.  Walking an item's range list through dependent global loads at every
+// item and range boundary had cost each role ~1 us per range on the critical path (point-prefill
+// lists carry up to ~20 ranges, c5 chain-64 masked items ~50).
+struct ItemG {
+  int32_t it, n_ranges, ntiles, pad_;
+  WorkItem w;
+  RangeG r[kMaxRanges];
+};
+static_assert(sizeof(RangeG) == 32, "RangeG is 32 bytes");
+
 template <int D>
 struct Smem {
   static constexpr int QB = kRows * D * 2;      // one Q buffer
@@ -60,12 +74,14 @@ struct Smem {
   static constexpr int SK = Rings<D>::K, SV = Rings<D>::V;
   static constexpr int OFF_K = 2 * QB;
   static constexpr int OFF_V = OFF_K + SK * KVB;
-  static constexpr int OFF_XCH = OFF_V + SV * KVB;   // WG1 -> WG0 (m, l) per row, x2
-  static constexpr int OFF_RING = OFF_XCH + 2 * kRows * 8;   // scheduled item indices
-  static constexpr int OFF_BAR = OFF_RING + 64;
-  static constexpr int N_BAR = 2 * SK + 2 * SV + 2 + 2 + 2 + 2 + 1 + 2 + 2 * 8;
+  static constexpr int OFF_XCH = OFF_V + SV * KVB;   // both WGs' (m, l) per row, x2 (item parity)
+  static constexpr int OFF_RING = OFF_XCH + 4 * kRows * 8;   // scheduled items with their geometry
+  static constexpr int OFF_BAR = OFF_RING + kRing * static_cast<int>(sizeof(ItemG));
+  static constexpr int N_BAR = 2 * SK + 2 * SV + 2 + 2 + 2 + 2 + 1 + 2 + 2 * 8 + 2;
   static constexpr int BYTES = OFF_BAR + N_BAR * 8 + 16;
 };
+
+static_assert(Smem<128>::BYTES + 1024 <= 232448 && Smem<64>::BYTES + 1024 <= 232448, "shared memory budget");
 
 // TMEM columns: S and P double-buffered by tile parity; one O accumulator per softmax warpgroup.
 __device__ __forceinline__ uint32_t colS(uint32_t p) { return p * 64; }
@@ -80,8 +96,11 @@ constexpr int kThreadsTC = 384;   // warps 0-3: TMEM alloc / idle / TMA / MMA; 4
 // steal issue slots from the softmax warps of items with <= 64 rows (TMEM lanes 0-63 are only
 // reachable from warps 4k and 4k+1, i.e. sub-partitions 0 and 1).
 constexpr int kWarpAlloc = 0, kWarpQK = 1, kWarpTMA = 2, kWarpMMA = 3;
-constexpr int kRing = 8;          // item ring entries (warp 0 schedules after TMEM allocation)
 constexpr int kRingReaders = 11;  // producer, QK and PV warps + the 8 softmax warps
+
+__device__ __forceinline__ RangeG geo_range(const TcArgs& a, const ItemG& e, int r) {
+  return r < kMaxRanges ? e.r[r] : range_geom(a, e.w, r);
+}
 
 template <int D>
 __global__ void __launch_bounds__(kThreadsTC, 1)
@@ -106,8 +125,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   uint64_t* s_free = o_free + 1;                  // softmax WG has read S[b] into registers
   uint64_t* u_full = s_free + 2;                  // [kRing] scheduler published an item index
   uint64_t* u_empty = u_full + kRing;             // [kRing] every reader warp took it
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(u_empty + kRing);
-  volatile int32_t* ring = reinterpret_cast<volatile int32_t*>(smem + L::OFF_RING);
+  uint64_t* pv_iss = u_empty + kRing;             // [2] PV(j) of parity p issued (QK(j+2) may follow)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_iss + 2);
+  ItemG* geo = reinterpret_cast<ItemG*>(smem + L::OFF_RING);
   float2* xch = reinterpret_cast<float2*>(smem + L::OFF_XCH);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -118,10 +138,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       mbar_init(s_full + b, 1); mbar_init(p_full + b, 128); mbar_init(pv_done + b, 1);
       mbar_init(q_full + b, 128);
     }
-    mbar_init(o_free, 128);
+    mbar_init(o_free, 256);                         // both warpgroups read both O accumulators
     mbar_init(s_free + 0, 128);
     mbar_init(s_free + 1, 128);
     for (int s = 0; s < kRing; ++s) { mbar_init(u_full + s, 1); mbar_init(u_empty + s, kRingReaders); }
+    mbar_init(pv_iss + 0, 1);
+    mbar_init(pv_iss + 1, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmK)) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmV)) : "memory");
@@ -147,31 +169,46 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   pdl_trigger();
 
   TRACE_DECL
-  // Items are handed out by an atomic counter (zeroed by the launcher) in plan order: greedy list
-  // scheduling over the SMs (a static grid stride left the busiest SM 19 % above the mean on the
-  // c4 point prefill).  Warp 0 publishes the k-th item this CTA runs in ring entry k (-1: done);
-  // every other role takes every entry in order.
-  auto take = [&](uint32_t k) -> int {
-    const int s = k % kRing;
-    mbar_wait(u_full + s, (k / kRing) & 1);
-    const int it = ring[s];
+  // Items are handed out by an atomic counter in plan order: greedy list scheduling over the SMs
+  // (a static grid stride left the busiest SM 19 % above the mean on the c4 point prefill).  Warp 0
+  // publishes the k-th item this CTA runs, with its range geometry, in ring entry k % kRing (it =
+  // -1: done); every other role takes every entry in order and releases it when done with it.
+  auto take = [&](uint32_t k) -> const ItemG& {
+    mbar_wait(u_full + (k % kRing), (k / kRing) & 1);
+    return geo[k % kRing];
+  };
+  auto release = [&](uint32_t k) {
     __syncwarp();
-    if (lane == 0) mbar_arrive(u_empty + s);
-    return it;
+    if (lane == 0) mbar_arrive(u_empty + (k % kRing));
   };
   if (warp == kWarpAlloc) {
     // ------------------------------------------------------------------ scheduler
     for (uint32_t k = 0;; ++k) {
       const int s = k % kRing;
       mbar_wait(u_empty + s, ((k / kRing) & 1) ^ 1);
+      ItemG& e = geo[s];
       int it = 0;
       if (lane == 0) {
         it = atomicAdd(a.work_counter, 1);
         if (it >= n_items) it = -1;
-        ring[s] = it;
-        mbar_arrive(u_full + s);
       }
       it = __shfl_sync(0xffffffffu, it, 0);
+      if (it >= 0) {
+        const WorkItem w = a.items[it];
+        const int nr = item_nranges(w);
+        int tiles = 0;
+        for (int r = lane; r < nr; r += 32) {
+          const RangeG g = range_geom(a, w, r);
+          if (r < kMaxRanges) e.r[r] = g;
+          tiles += g.ntiles;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) tiles += __shfl_xor_sync(0xffffffffu, tiles, o);
+        if (lane == 0) { e.w = w; e.n_ranges = nr; e.ntiles = tiles; }
+      }
+      if (lane == 0) e.it = it;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(u_full + s);
       if (it < 0) break;
     }
   } else if (warp == kWarpTMA) {
@@ -184,11 +221,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const int pmask = (1 << a.page_shift) - 1;
     const int big = min(kTok, 1 << a.page_shift);          // rows of a full-tile box
     for (uint32_t ke = 0;; ++ke) {
-      const int it = take(ke);
-      if (it < 0) break;
-      const WorkItem w = a.items[it];
-      for (int rg_i = 0; rg_i < item_nranges(w); ++rg_i) {
-      const RangeG g = range_geom(a, w, rg_i);
+      const ItemG& e = take(ke);
+      if (e.it < 0) { release(ke); break; }
+      const int kv_head = e.w.kv_head;
+      for (int rg_i = 0; rg_i < e.n_ranges; ++rg_i) {
+      const RangeG g = geo_range(a, e, rg_i);
       for (int tb0 = 0; tb0 < g.ntiles; tb0 += 32) {
         // lane l describes tile tb0 + l: up to 4 boxes (row coordinate each), kind, offsets
         int brow[4] = {0, 0, 0, 0};
@@ -205,7 +242,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             if (b < nbox) {
               const int pos = pos0 + b * step;
               const int page = __ldg(a.page_table + g.pt_off + (pos >> a.page_shift));
-              brow[b] = (((page * a.hkv + w.kv_head) * a.kvs) << a.page_shift) + (pos & pmask);
+              brow[b] = (((page * a.hkv + kv_head) * a.kvs) << a.page_shift) + (pos & pmask);
             }
           }
         }
@@ -252,6 +289,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
       }
       }
+      release(ke);
     }
     TRACE_DUMP("producer");
   } else if (warp == kWarpMMA || warp == kWarpQK) {
@@ -266,15 +304,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const uint64_t dk0 = sw128_desc(smem_u32(smem + L::OFF_K), 16, 1024);
     const uint64_t dv0 = sw128_desc(smem_u32(smem + L::OFF_V), L::HALF_KV, 1024);
     struct Cur {
-      int it, t, nt;
-      uint32_t k, j, e;                             // e: ring entries taken
+      int live, t, nt;
+      uint32_t k, j, e, ent;                        // e: ring entries taken; ent: the current one
     };
     auto next_ne = [&](Cur& c) {                    // next non-empty item of the ring, or the end
       for (;;) {
-        const int it = take(c.e++);
-        if (it < 0) { c.it = n_items; c.nt = 0; return; }
-        const int nt = item_tiles(a, a.items[it]);
-        if (nt > 0) { c.it = it; c.nt = nt; return; }
+        const uint32_t ke = c.e++;
+        const ItemG& g = take(ke);
+        if (g.it < 0) { release(ke); c.live = 0; c.nt = 0; return; }
+        if (g.ntiles > 0) { c.live = 1; c.nt = g.ntiles; c.ent = ke; return; }
+        release(ke);
       }
     };
     auto start = [&](Cur& c) {
@@ -284,6 +323,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     auto advance = [&](Cur& c) {
       ++c.j;
       if (++c.t == c.nt) {
+        release(c.ent);
         next_ne(c);
         c.t = 0; ++c.k;
       }
@@ -301,6 +341,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       const int s = j % SK;
       TW(2, mbar_wait(k_full + s, (j / SK) & 1));
       if (nq[p] > 0) TW(3, mbar_wait(s_free + p, (nq[p] - 1) & 1));   // S[p] read out
+      // QK(j) enters the in-order tensor pipe after PV(j-2): the PV a warpgroup waits for before
+      // it may store its next P never queues behind the next tiles' QKs.
+      if (nq[p] > 0) TW(4, mbar_wait(pv_iss + p, (nq[p] - 1) & 1));
       tc_fence_after();
       const uint64_t dq = dq0 + static_cast<uint64_t>(((c.k & 1) * L::QB) >> 4);
       const uint64_t dk = dk0 + static_cast<uint64_t>((s * L::KVB) >> 4);
@@ -344,6 +387,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
         tc_commit(pv_done + p);
         tc_commit(v_empty + s);
+        mbar_arrive(pv_iss + p);
       }
       __syncwarp();
       ++nv[p];
@@ -357,9 +401,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     Cur c;
     start(c);
     if (warp == kWarpQK) {
-      while (c.it < n_items) { issue_qk(c); advance(c); }
+      while (c.live) { issue_qk(c); advance(c); }
     } else {
-      while (c.it < n_items) { issue_pv(c); advance(c); }
+      while (c.live) { issue_pv(c); advance(c); }
     }
     TRACE_DUMP("mma");
   } else if (warp >= 4) {
@@ -370,9 +414,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const int p = (warp - 4) >> 2;
     const int r = tid - 128 - p * 128;             // query row == TMEM lane
     const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    auto load_q = [&](int k_item, int it) {        // WG0 only
-      if (it >= 0) {
-        const WorkItem w = a.items[it];
+    auto load_q = [&](int k_item, int ent) {       // WG0 only; ent: the item's ring entry or -1
+      if (ent >= 0) {
+        const WorkItem& w = geo[ent % kRing].w;
         const bool ok = r < w.n_rows;
         const __nv_bfloat16* src = a.q;
         if (ok) {   // row -> (reader b, content position i, q head h): plan_format.h
@@ -392,12 +436,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
     uint32_t ke = 0;                                // ring entries taken by this warp
-    auto next_item = [&]() -> int {                 // next non-empty item, or -1
+    auto next_item = [&]() -> int {                 // the next non-empty item's ring entry (held), or -1
       for (;;) {
-        const int it = take(ke++);
-        if (it < 0) return -1;
-        const WorkItem w = a.items[it];
-        if (item_tiles(a, w) > 0) return it;
+        const uint32_t kk = ke++;
+        const ItemG& g = take(kk);
+        if (g.it < 0) { release(kk); return -1; }
+        if (g.ntiles > 0) return static_cast<int>(kk);
+        const WorkItem& w = g.w;
         // empty (dyn end <= t0): neutral partial (direct output: prefill rows are never empty)
         if (p == 0 && r < w.n_rows && !a.out) {
           if (a.part16) {
@@ -412,6 +457,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             a.part_ml[w.slot0 + r] = make_float2(-INFINITY, 0.f);
           }
         }
+        release(kk);
       }
     };
     int cur = next_item(), pf = -1;
@@ -425,7 +471,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     }
     uint32_t j = 0, k = 0, np = 0;                  // np: this warpgroup's tiles so far
     while (cur >= 0) {
-      const WorkItem w = a.items[cur];
+      const ItemG& cg = geo[cur % kRing];
+      const WorkItem w = cg.w;
       const bool active = (warp & 3) * 32 < w.n_rows;   // warp-uniform
       // point prefill: this row's content position i; in the causal own range it sees [t0, t0 + i]
       const int rpos = ((w.row_begin + r) % (a.lc * a.group)) / a.group;
@@ -433,8 +480,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       float l_run = 0.f;                            // this row's sum of the bf16 P it published
       bool had = false;
       int ti = 0;                                   // tile index within the item (WG ti & 1)
-      for (int rg_i = 0; rg_i < item_nranges(w); ++rg_i) {
-      const RangeG g = range_geom(a, w, rg_i);
+      for (int rg_i = 0; rg_i < cg.n_ranges; ++rg_i) {
+      const RangeG g = geo_range(a, cg, rg_i);
       // a masked range (hybrid big items): rows of readers outside its mask see none of it
       const bool rmask = g.masked && !((g.mask >> ((w.row_begin + r) / (a.lc * a.group))) & 1u);
       const int row_end = rmask ? g.t0 : (g.causal ? min(g.end, g.t0 + rpos + 1) : g.end);
@@ -542,6 +589,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         ++np;
       }
       }
+#ifdef ORION_TC_TRACE
+      const unsigned long long tep0 = clock64();
+#endif
       if (p == 0) {                  // next item's Q was gathered one item ahead: publish it
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         fence_proxy_async();
@@ -552,19 +602,21 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         TW(8, mbar_wait(pv_done + p, (np - 1) & 1));      // last PV of this WG complete
         tc_fence_after();
       }
-      if (p == 1) {
-        xch[(k & 1) * kRows + r] = make_float2(had ? m_used : -INFINITY, l_run);
-        TW(9, asm volatile("bar.sync 1, 256;\n" ::: "memory"));
-        cur = next_item();
-      } else {
-        TW(9, asm volatile("bar.sync 1, 256;\n" ::: "memory"));
-        const float2 o1 = xch[(k & 1) * kRows + r];
+      // Both warpgroups publish their (m, l), then each merges O_0 and O_1 over its half of the
+      // head dimension (warpgroup p: columns [p D/2, (p + 1) D/2)), so the readout and its
+      // scattered row stores take half as long and run on both warpgroups at once.
+      xch[((k & 1) * 2 + p) * kRows + r] = make_float2(had ? m_used : -INFINITY, l_run);
+      TW(9, asm volatile("bar.sync 1, 256;\n" ::: "memory"));
+      {
+        const float2 o0 = xch[((k & 1) * 2 + 0) * kRows + r];
+        const float2 o1 = xch[((k & 1) * 2 + 1) * kRows + r];
+        const bool had0 = __any_sync(0xffffffffu, o0.x > -INFINITY);   // WG0 owned a tile
         const bool had1 = __any_sync(0xffffffffu, o1.x > -INFINITY);   // WG1 owned a tile
-        const float M = fmaxf(m_used, o1.x);
+        const float M = fmaxf(o0.x, o1.x);
         const float Mb = M == -INFINITY ? 0.f : M;
-        const float a0 = had ? ex2(m_used - Mb) : 0.f;
+        const float a0 = had0 ? ex2(o0.x - Mb) : 0.f;
         const float a1 = had1 ? ex2(o1.x - Mb) : 0.f;
-        const float l0 = had ? l_run : 0.f, l1 = had1 ? o1.y : 0.f;
+        const float l0 = had0 ? o0.y : 0.f, l1 = had1 ? o1.y : 0.f;
         // Direct output (point-prefill plans: the item holds every token of its rows, so this is
         // the row's only partial): out = acc / l in bf16 and lse, no combine pass.
         const float Lr = a0 * l0 + a1 * l1;
@@ -578,19 +630,19 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         float* dst = a.part_acc + static_cast<size_t>(w.slot0 + r) * D;
         if (active) {
 #pragma unroll 1
-          for (int cb = 0; cb < D; cb += 16) {
+          for (int cb = p * (D / 2); cb < (p + 1) * (D / 2); cb += 16) {
             uint32_t o[16], q1[16];
-            if (had) { tmem_ld32x16(tmem + lane_base + colO(0) + cb, o); }
+            if (had0) { tmem_ld32x16(tmem + lane_base + colO(0) + cb, o); }
             if (had1) { tmem_ld32x16(tmem + lane_base + colO(1) + cb, q1); }
             tc_wait_ld();
             if (r < w.n_rows) {
 #pragma unroll
               for (int c = 0; c < 16; c += 4) {
                 float4 v;
-                v.x = (had ? a0 * __uint_as_float(o[c]) : 0.f) + (had1 ? a1 * __uint_as_float(q1[c]) : 0.f);
-                v.y = (had ? a0 * __uint_as_float(o[c + 1]) : 0.f) + (had1 ? a1 * __uint_as_float(q1[c + 1]) : 0.f);
-                v.z = (had ? a0 * __uint_as_float(o[c + 2]) : 0.f) + (had1 ? a1 * __uint_as_float(q1[c + 2]) : 0.f);
-                v.w = (had ? a0 * __uint_as_float(o[c + 3]) : 0.f) + (had1 ? a1 * __uint_as_float(q1[c + 3]) : 0.f);
+                v.x = (had0 ? a0 * __uint_as_float(o[c]) : 0.f) + (had1 ? a1 * __uint_as_float(q1[c]) : 0.f);
+                v.y = (had0 ? a0 * __uint_as_float(o[c + 1]) : 0.f) + (had1 ? a1 * __uint_as_float(q1[c + 1]) : 0.f);
+                v.z = (had0 ? a0 * __uint_as_float(o[c + 2]) : 0.f) + (had1 ? a1 * __uint_as_float(q1[c + 2]) : 0.f);
+                v.w = (had0 ? a0 * __uint_as_float(o[c + 3]) : 0.f) + (had1 ? a1 * __uint_as_float(q1[c + 3]) : 0.f);
                 if (a.out) {
                   uint2 pk2;
                   pk2.x = pack_bf16(v.x * inv, v.y * inv);
@@ -610,18 +662,27 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             }
           }
         }
-        if (r < w.n_rows) {
+        if (p == 0 && r < w.n_rows) {
           if (a.part16) a.part_lse[w.slot0 + r] = Lr > 0.f ? M + log2f(Lr) : -INFINITY;
           else if (!a.out) a.part_ml[w.slot0 + r] = make_float2(M, Lr);
           else if (a.lse) a.lse[orow] = Lr > 0.f ? (M + log2f(Lr)) * 0.69314718055994531f : -INFINITY;
         }
         tc_fence_before();
         mbar_arrive(o_free);
+      }
+      release(static_cast<uint32_t>(cur));
+      if (p == 1) {
+        cur = next_item();
+      } else {
         const int nx = pf;
         pf = pf >= 0 ? next_item() : -1;
         load_q(k, pf);               // Q buffer (k & 1) is free: every QK of item k completed
         cur = nx;
       }
+#ifdef ORION_TC_TRACE
+      tr_[4] += clock64() - tep0;
+      tr_[5] += 1;
+#endif
       ++k;
     }
     if (p == 0) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
