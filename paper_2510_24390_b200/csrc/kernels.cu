@@ -26,6 +26,7 @@
 
 #include "../../include/orion.h"
 #include "plan_format.h"
+#include "merge16.h"
 #include "split_tc.h"
 
 namespace orion {
@@ -369,86 +370,11 @@ __global__ void __launch_bounds__(kCombThreads) combine16_kernel(const int32_t* 
                                                                  const float* __restrict__ part_lse,
                                                                  __nv_bfloat16* __restrict__ out,
                                                                  float* __restrict__ lse, int n_rows) {
-  constexpr int E = D / kCombLanes;  // elements per lane (8 or 16)
-  constexpr int U = E / 8;           // 16-B loads per lane per partial
   const int row = blockIdx.x * kCombRowsPerBlock + (threadIdx.x / kCombLanes);
-  const int sub = threadIdx.x & (kCombLanes - 1);
-  const unsigned full = 0xffffffffu;
   pdl_trigger();
   pdl_wait();
-  const bool valid = row < n_rows;
-  const int e0 = valid ? __ldg(comb_off + row) : 0;
-  const int n = valid ? __ldg(comb_off + row + 1) - e0 : 0;
-  int nmax = n;  // the warp walks chunks uniformly (shuffles need every lane)
-#pragma unroll
-  for (int o = 16; o >= kCombLanes; o >>= 1) nmax = max(nmax, __shfl_xor_sync(full, nmax, o));
-  // Pass 1: M = max lse2 of the row; chunk 0's slot / lse stay in registers.
-  const int slot0 = sub < n ? __ldg(comb_slot + e0 + sub) : 0;
-  const float lse0 = sub < n ? __ldg(part_lse + slot0) : -INFINITY;
-  float M = lse0;
-  for (int c = kCombLanes; c < nmax; c += kCombLanes)
-    if (c + sub < n) M = fmaxf(M, __ldg(part_lse + __ldg(comb_slot + e0 + c + sub)));
-#pragma unroll
-  for (int o = kCombLanes / 2; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(full, M, o, kCombLanes));
-  const float base = M == -INFINITY ? 0.f : M;
-  float acc[E];
-#pragma unroll
-  for (int i = 0; i < E; ++i) acc[i] = 0.f;
-  float L = 0.f;
-  // Pass 2: weights and the weighted sum of o, chunk by chunk, 4 partials per batch.
-  for (int c = 0; c < nmax; c += kCombLanes) {
-    int slot_l = slot0;
-    float lse_l = lse0;
-    if (c > 0) {
-      slot_l = c + sub < n ? __ldg(comb_slot + e0 + c + sub) : 0;
-      lse_l = c + sub < n ? __ldg(part_lse + slot_l) : -INFINITY;
-    }
-    const float w_l = c + sub < n ? fast_exp2(lse_l - base) : 0.f;
-    const int cn = min(nmax - c, kCombLanes);
-    for (int j0 = 0; j0 < cn; j0 += 4) {
-      uint4 x[4][U];
-      float wt[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int s = __shfl_sync(full, slot_l, (j0 + j) & (kCombLanes - 1), kCombLanes);
-        wt[j] = __shfl_sync(full, w_l, (j0 + j) & (kCombLanes - 1), kCombLanes);
-        if (c + j0 + j < n) {
-          const uint4* src = reinterpret_cast<const uint4*>(part_o + static_cast<size_t>(s) * D + sub * E);
-#pragma unroll
-          for (int u = 0; u < U; ++u) x[j][u] = __ldg(src + u);
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (c + j0 + j < n) {
-          L += wt[j];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const __half2* h2 = reinterpret_cast<const __half2*>(&x[j][u]);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float2 f = __half22float2(h2[i]);
-              acc[u * 8 + 2 * i] += wt[j] * f.x;
-              acc[u * 8 + 2 * i + 1] += wt[j] * f.y;
-            }
-          }
-        }
-      }
-    }
-  }
-  if (!valid) return;
-  const float inv = L > 0.f ? 1.f / L : 0.f;
-  uint4* o = reinterpret_cast<uint4*>(out + static_cast<size_t>(row) * D + sub * E);
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    uint4 pk;
-    pk.x = pack_bf16(acc[u * 8 + 0] * inv, acc[u * 8 + 1] * inv);
-    pk.y = pack_bf16(acc[u * 8 + 2] * inv, acc[u * 8 + 3] * inv);
-    pk.z = pack_bf16(acc[u * 8 + 4] * inv, acc[u * 8 + 5] * inv);
-    pk.w = pack_bf16(acc[u * 8 + 6] * inv, acc[u * 8 + 7] * inv);
-    o[u] = pk;
-  }
-  if (lse && sub == 0) lse[row] = L > 0.f ? (M + log2f(L)) * kLn2 : -INFINITY;
+  merge_row16<D>(comb_off, comb_slot, part_o, part_lse, out, lse, row < n_rows ? row : 0, row < n_rows,
+                 threadIdx.x & (kCombLanes - 1));
 }
 
 // ------------------------------------------------------------------------------ K1 append
@@ -862,9 +788,8 @@ extern "C" orion_status orion_expand_attn(const orion_attn_shape* shape, int32_t
   if (h_plan && static_cast<const PlanHeader*>(h_plan)->magic == kPlanMagic &&
       static_cast<const PlanHeader*>(h_plan)->prefill_rows > 0)
     return fail(ORION_ERR_INVALID_ARG, "a point-prefill plan needs orion_point_prefill_attn");
-  orion_status st = orion_expand_split(shape, n_branches, q, k_cache, v_cache, num_pages,
-                                       page_table, own_len, h_plan, d_plan, workspace,
-                                       workspace_bytes, stream);
+  orion_status st = orion_expand_split(shape, n_branches, q, k_cache, v_cache, num_pages, page_table, own_len,
+                                       h_plan, d_plan, workspace, workspace_bytes, stream);
   if (st != ORION_OK) return st;
   return orion_expand_combine(shape, n_branches, out, lse, h_plan, d_plan, workspace,
                               workspace_bytes, stream);

@@ -1,0 +1,113 @@
+// merge16.h — the LSE merge of one output row's fp16 partials (K3), shared by the combine kernel
+// (kernels.cu) and the split kernels if the merge is ever fused into them.
+// Product-side only.
+//
+// A row's partials i (plan_format.h fp16 format: o_i = acc_i / l_i, lse2_i = m_i + log2 l_i) are
+// listed in plan order by the combine CSR (comb_off / comb_slot):
+//   out = sum_i 2^(lse2_i - M) o_i / sum_i 2^(lse2_i - M),  lse = (M + log2 sum) ln 2,  M = max lse2_i.
+// One row per group of 8 consecutive lanes; every lane of the warp calls it (the shuffles use the
+// full mask; a group without a row passes valid = false).  Lane `sub` of the group owns D/8
+// consecutive elements (one or two 16-B loads per partial).  Lane j of a row's group holds the slot
+// and lse of partials j, j+8, ... in turn, so the dependent chain comb_off -> comb_slot -> part_lse
+// -> part_o is walked once per chunk of 8 partials and the o loads of 4 partials issue together.
+// The weighted sum runs in the fixed plan order: a row's result does not depend on which kernel or
+// CTA merges it (the combine kernel and the split kernel's merge phase agree bitwise).  Loads use
+// ld.global.cg: in the merge phase the partials were written by other CTAs of the same kernel, so
+// the incoherent read-only path must not serve them.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+namespace orion {
+
+constexpr int kMergeLanes = 8;
+
+template <int D>
+__device__ __forceinline__ void merge_row16(const int32_t* __restrict__ comb_off, const int32_t* __restrict__ comb_slot,
+                                            const __half* part_o, const float* part_lse,
+                                            __nv_bfloat16* __restrict__ out, float* __restrict__ lse, int row,
+                                            bool valid, int sub) {
+  constexpr int E = D / kMergeLanes;  // elements per lane (8 or 16)
+  constexpr int U = E / 8;            // 16-B loads per lane per partial
+  const unsigned full = 0xffffffffu;
+  const int e0 = valid ? __ldcg(comb_off + row) : 0;
+  const int n = valid ? __ldcg(comb_off + row + 1) - e0 : 0;
+  int nmax = n;  // the warp walks chunks uniformly (shuffles need every lane)
+#pragma unroll
+  for (int o = 16; o >= kMergeLanes; o >>= 1) nmax = max(nmax, __shfl_xor_sync(full, nmax, o));
+  // Pass 1: M = max lse2 of the row; chunk 0's slot / lse stay in registers.
+  const int slot0 = sub < n ? __ldcg(comb_slot + e0 + sub) : 0;
+  const float lse0 = sub < n ? __ldcg(part_lse + slot0) : -INFINITY;
+  float M = lse0;
+  for (int c = kMergeLanes; c < nmax; c += kMergeLanes)
+    if (c + sub < n) M = fmaxf(M, __ldcg(part_lse + __ldcg(comb_slot + e0 + c + sub)));
+#pragma unroll
+  for (int o = kMergeLanes / 2; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(full, M, o, kMergeLanes));
+  const float base = M == -INFINITY ? 0.f : M;
+  float acc[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) acc[i] = 0.f;
+  float L = 0.f;
+  // Pass 2: weights and the weighted sum of o, chunk by chunk, 4 partials per batch.
+  for (int c = 0; c < nmax; c += kMergeLanes) {
+    int slot_l = slot0;
+    float lse_l = lse0;
+    if (c > 0) {
+      slot_l = c + sub < n ? __ldcg(comb_slot + e0 + c + sub) : 0;
+      lse_l = c + sub < n ? __ldcg(part_lse + slot_l) : -INFINITY;
+    }
+    float w_l = 0.f;
+    if (c + sub < n) asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(w_l) : "f"(lse_l - base));
+    const int cn = min(nmax - c, kMergeLanes);
+    for (int j0 = 0; j0 < cn; j0 += 4) {
+      uint4 x[4][U];
+      float wt[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int s = __shfl_sync(full, slot_l, (j0 + j) & (kMergeLanes - 1), kMergeLanes);
+        wt[j] = __shfl_sync(full, w_l, (j0 + j) & (kMergeLanes - 1), kMergeLanes);
+        if (c + j0 + j < n) {
+          const uint4* src = reinterpret_cast<const uint4*>(part_o + static_cast<size_t>(s) * D + sub * E);
+#pragma unroll
+          for (int u = 0; u < U; ++u) x[j][u] = __ldcg(src + u);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (c + j0 + j < n) {
+          L += wt[j];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const __half2* h2 = reinterpret_cast<const __half2*>(&x[j][u]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float2 f = __half22float2(h2[i]);
+              acc[u * 8 + 2 * i] += wt[j] * f.x;
+              acc[u * 8 + 2 * i + 1] += wt[j] * f.y;
+            }
+          }
+        }
+      }
+    }
+  }
+  if (!valid) return;
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  uint4* o = reinterpret_cast<uint4*>(out + static_cast<size_t>(row) * D + sub * E);
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    uint4 pk;
+    __nv_bfloat162 b0 = __floats2bfloat162_rn(acc[u * 8 + 0] * inv, acc[u * 8 + 1] * inv);
+    __nv_bfloat162 b1 = __floats2bfloat162_rn(acc[u * 8 + 2] * inv, acc[u * 8 + 3] * inv);
+    __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[u * 8 + 4] * inv, acc[u * 8 + 5] * inv);
+    __nv_bfloat162 b3 = __floats2bfloat162_rn(acc[u * 8 + 6] * inv, acc[u * 8 + 7] * inv);
+    pk.x = *reinterpret_cast<uint32_t*>(&b0);
+    pk.y = *reinterpret_cast<uint32_t*>(&b1);
+    pk.z = *reinterpret_cast<uint32_t*>(&b2);
+    pk.w = *reinterpret_cast<uint32_t*>(&b3);
+    o[u] = pk;
+  }
+  if (lse && sub == 0) lse[row] = L > 0.f ? (M + log2f(L)) * 0.6931471805599453f : -INFINITY;
+}
+
+}  // namespace orion
