@@ -490,7 +490,7 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
     std::vector<std::vector<std::pair<Range, std::vector<int32_t>>>> bchunks;
     std::vector<std::vector<int32_t>> bunion;
     std::vector<int32_t> bpiece;
-    int64_t big_tokens = 0;                        // tokens of the masked ranges, per kv head
+    int64_t big_tokens = 0;                        // tokens of the masked ranges, summed over kv heads
     for (size_t pi = 0; pi < pieces.size(); ++pi) {
       const Piece& p = pieces[pi];
       unique_tokens += p.t1 - p.t0;
@@ -544,10 +544,18 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
         }
       }
     }
-    // Masked items are long (whole reader blocks): cap their tokens so that there are about six
-    // per SM (a few 8K-token items per SM left the busiest SM 1.5x above the mean on c5 chain-64).
+    // Masked items are long (whole reader blocks).  When the swap-AB part of the step is small
+    // (c5 chain-64: 0.25 of the big part's tokens), cap them to ~4 per SM (4K-8K tokens): 2-3
+    // 8K-token items per SM had left the busiest SM 1.4x above the mean.  When it is large (c5
+    // wide-64: the points' own runs, as many tokens as the prefix), keep them long: fewer items
+    // than SMs leave SMs on which the swap-AB kernel starts at once, beside the first kernel.
     const int64_t sms = (opts && opts->num_sms > 0) ? opts->num_sms : 148;
-    const int64_t big_cap = std::max<int64_t>(1024, std::min<int64_t>(kMergeTokens, big_tokens * Hkv / (6 * sms)));
+    int64_t small_tokens = 0;
+    for (const auto& cs : gchunks)
+      for (const Range& R : cs) small_tokens += R.t1 - R.t0;
+    const int64_t big_cap = 2 * small_tokens >= big_tokens
+                                ? kMergeTokens
+                                : std::max<int64_t>(4096, std::min<int64_t>(kMergeTokens, big_tokens / (4 * sms)));
     for (size_t bi = 0; bi < bkeys.size(); ++bi) {
       const int32_t g = bkeys[bi].first;
       const std::vector<int32_t>& U = bunion[bi];

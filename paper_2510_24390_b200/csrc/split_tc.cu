@@ -51,6 +51,7 @@ template <> struct Rings<64> { static constexpr int K = 4, V = 8; };
 constexpr int kRows = 128;     // MMA M (query rows per item)
 
 constexpr int kRing = 6;          // item ring entries (warp 0 schedules after TMEM allocation)
+constexpr int kAhead = 3;         // items fetched ahead of the oldest unfinished one
 constexpr int kMaxRanges = 64;    // ranges whose geometry an entry carries (more: read from the plan)
 // A scheduled item with the geometry of its ranges, resolved once by the scheduler warp (one lane
 // per range: the plan's Range and the dynamic end's own_len loads overlap) and read from shared
@@ -186,6 +187,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     for (uint32_t k = 0;; ++k) {
       const int s = k % kRing;
       mbar_wait(u_empty + s, ((k / kRing) & 1) ^ 1);
+      // Take item k from the global counter only once item k - kAhead is done: a CTA holding
+      // several fetched but unstarted items at the end of the plan leaves other SMs idle (with the
+      // ring's full depth of look-ahead the busiest SM ran 1.4x the mean on c5 chain-64).
+      if (k >= static_cast<uint32_t>(kAhead))
+        mbar_wait(u_empty + ((k - kAhead) % kRing), ((k - kAhead) / kRing) & 1);
       ItemG& e = geo[s];
       int it = 0;
       if (lane == 0) {
@@ -687,6 +693,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     }
     if (p == 0) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     if ((warp & 3) < 2) TRACE_DUMP("softmax");
+#ifdef ORION_TC_TRACE
+    if (warp == 4 && lane == 0)   // per-CTA balance: total cycles, tiles, items of warpgroup 0
+      printf("CTA %d tot %llu tiles %u items %u\n", blockIdx.x, clock64() - tr_t0, np, k);
+#endif
   }
   tc_fence_before();
   __syncthreads();

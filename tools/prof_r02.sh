@@ -6,6 +6,7 @@ C4="python bench.py $NOX"
 C5W="python bench.py --config c5w --queries 8 $NOX"
 C5C="python bench.py --config c5c --queries 8 $NOX"
 C4S="python bench.py --queries 8 $NOX"
+PP="python tools/prefill_probe.py 16"
 M="--clock-control none"
 $C4 > gpurun_out/plain_c4.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum $M -c 300 --csv --log-file gpurun_out/launches_c4.csv $C4 > gpurun_out/ncu_l1.log 2>&1 && \
@@ -22,4 +23,7 @@ echo "c5c rc=$?"
 $C4S > gpurun_out/plain_c4s.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum $M -c 300 --csv --log-file gpurun_out/launches_c4_8q.csv $C4S > gpurun_out/ncu_l4.log 2>&1
 echo "c4 8q rc=$?"
+$PP > gpurun_out/plain_pp.log 2>&1 && \
+  ncu --set full $M --import-source on -k regex:split_tc -s 2 -c 1 -o gpurun_out/prof_prefill $PP > gpurun_out/ncu_f5.log 2>&1
+echo "prefill rc=$?"
 ls -la gpurun_out/*.ncu-rep
