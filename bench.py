@@ -578,6 +578,8 @@ def run_orion(args, cfg, layers):
         line["model_step"] = run_model_step(args, cfg, lay, layers, kc, vc, dev, value)
     if world == 1 and not args.no_expansion:
         line["expansion_run"] = run_expansion(args, cfg, lay, layers, q, kn, vn, kc, vc, dev)
+        if cfg.name == "c4":
+            line["expansion_run_c2"] = run_expansion_small(args, dev)
     if world == 1 and not args.no_point_prefill:
         line["point_prefill"] = run_point_prefill(args, cfg, lay, layers, kc, vc, dev)
     if world == 1 and not args.no_prefill:
@@ -767,13 +769,15 @@ def expansion_decode_bytes(cfg, lay, ex, schedule, layers):
     return total
 
 
-def run_expansion(args, cfg, lay, layers, q, kn, vn, kc, vc, dev):
+def run_expansion(args, cfg, lay, layers, q, kn, vn, kc, vc, dev, graph=True):
     """§8(f) rank 2: a whole expansion of the config's queries (Alg. 1 l.9-22 with
     continuous batching, reading D1): rounds of orion_expansion_round; each round prefills the
     points that became ready (orion_point_prefill_attn, every layer) and decodes one token of the
     running set through all layers (append + split + combine); plans are rebuilt only when the
-    running set changes.  Every point generates T - Lc tokens.  Device-timed end to end (host
-    scheduling, plan rebuilds and the per-set input gathers inside the timed region)."""
+    running set changes.  Every point generates T - Lc tokens.  graph=True replays each decode
+    round from a CUDA graph captured once per running set (Expansion.decode).  Device-timed end
+    to end (host scheduling, plan rebuilds, graph captures and the per-set input gathers inside
+    the timed region)."""
     import torch
     from paper_2510_24390_b200.expansion import Expansion
     queries = [dict(n_points=int(lay.n_points[i]), edges=lay.edges[i],
@@ -812,7 +816,7 @@ def run_expansion(args, cfg, lay, layers, q, kn, vn, kc, vc, dev):
                 subs = [t.index_select(1, idx) for t in (q, kn, vn)]
                 subs.append(torch.empty_like(subs[0]))
                 cur = dec.copy()
-            ex.decode(dec, subs[0], subs[1], subs[2], kc[:layers], vc[:layers], subs[3])
+            ex.decode(dec, subs[0], subs[1], subs[2], kc[:layers], vc[:layers], subs[3], graph=graph)
             dec_sum += len(dec)
             schedule.append(dec)
         rounds += 1
@@ -829,7 +833,8 @@ def run_expansion(args, cfg, lay, layers, q, kn, vn, kc, vc, dev):
             "metric": "expansion tokens/sec (whole expansion)", "value": gen / (ms / 1e3), "unit": "tokens/s",
             "generated_tokens": gen, "rounds": rounds, "rounds_with_prefill": pre_rounds,
             "mean_running_set": dec_sum / max(1, rounds), "max_branches": B,
-            "plan_rebuilds": ex.rebuilds, "ms": ms, "wall_ms": wall * 1e3,
+            "plan_rebuilds": ex.rebuilds, "decode_graph": graph, "graph_captures": ex.captures,
+            "ms": ms, "wall_ms": wall * 1e3, "us_per_round": ms * 1e3 / max(1, rounds),
             "roofline": {"bound": "hbm", "algorithmic_bytes": kv_bytes, "achieved": kv_bytes / (ms / 1e3) / 1e9,
                          "peak": peak, "unit": "GB/s", "frac": kv_bytes / (ms / 1e3) / 1e9 / peak,
                          "peak_source": peak_src,
@@ -839,6 +844,25 @@ def run_expansion(args, cfg, lay, layers, q, kn, vn, kc, vc, dev):
                                  "8(d)); prefill rounds, appends and plan rebuilds count as time only"},
             "note": "device-timed (events) around the whole loop; host scheduling and plan "
                     "rebuilds inside; compare the snapshot value where every point decodes at once"}
+
+
+def run_expansion_small(args, dev):
+    """The latency-bound end of §8(f) rank 2: a whole expansion of BASELINE configs[1] (c2: one
+    query, 8 points, 2K prefix, 256 tok/point, 32 layers), each decode round launched eagerly
+    (3 launches per layer from the host) and replayed from a per-running-set CUDA graph."""
+    import torch
+    cfg = WC.CONFIGS["c2"]
+    lay = WT.make_layout(cfg, seed=cfg.seed)
+    kc, vc, q, kn, vn, _ = alloc_tensors(args, cfg, lay, cfg.layers, dev, cfg.seed * 7)
+    res = {}
+    for graph in (False, True):
+        run_expansion(args, cfg, lay, cfg.layers, q, kn, vn, kc, vc, dev, graph=graph)   # warm-up
+        r = run_expansion(args, cfg, lay, cfg.layers, q, kn, vn, kc, vc, dev, graph=graph)
+        res["graph" if graph else "eager"] = r
+    res["graph_speedup"] = res["graph"]["value"] / res["eager"]["value"]
+    del kc, vc, q, kn, vn
+    torch.cuda.empty_cache()
+    return res
 
 
 def run_point_prefill(args, cfg, lay, layers, kc, vc, dev):

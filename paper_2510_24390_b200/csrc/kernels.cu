@@ -27,6 +27,7 @@
 #include "../../include/orion.h"
 #include "plan_format.h"
 #include "merge16.h"
+#include "nvtx_range.h"
 #include "split_tc.h"
 
 namespace orion {
@@ -713,6 +714,7 @@ extern "C" orion_status orion_kv_append(const orion_attn_shape* shape, int32_t n
                                         const int32_t* own_cap, const int32_t* page_table,
                                         int32_t num_pages, int32_t* own_len, int32_t mode,
                                         void* stream) {
+  const orion::NvtxRange nvtx_range("orion_kv_append");
   orion_status st = check_shape_public(shape);
   if (st != ORION_OK) return st;
   if (n_branches < 0) return fail(ORION_ERR_INVALID_ARG, "n_branches < 0");
@@ -745,6 +747,7 @@ extern "C" orion_status orion_expand_split(const orion_attn_shape* shape, int32_
                                            const void* h_plan, const void* d_plan,
                                            void* workspace, size_t workspace_bytes,
                                            void* stream) {
+  const orion::NvtxRange nvtx_range("orion_expand_split");
   const PlanHeader* h = nullptr;
   orion_status st = check_attn(shape, n_branches, h_plan, d_plan, workspace, workspace_bytes, &h);
   if (st != ORION_OK) return st;
@@ -766,6 +769,7 @@ extern "C" orion_status orion_expand_combine(const orion_attn_shape* shape, int3
                                              void* out, float* lse, const void* h_plan,
                                              const void* d_plan, const void* workspace,
                                              size_t workspace_bytes, void* stream) {
+  const orion::NvtxRange nvtx_range("orion_expand_combine");
   const PlanHeader* h = nullptr;
   orion_status st = check_attn(shape, n_branches, h_plan, d_plan, workspace, workspace_bytes, &h);
   if (st != ORION_OK) return st;
@@ -784,6 +788,7 @@ extern "C" orion_status orion_expand_attn(const orion_attn_shape* shape, int32_t
                                           const int32_t* own_len, const void* h_plan,
                                           const void* d_plan, void* workspace,
                                           size_t workspace_bytes, void* stream) {
+  const orion::NvtxRange nvtx_range("orion_expand_attn");
   if (!out) return fail(ORION_ERR_INVALID_ARG, "null out");
   if (h_plan && static_cast<const PlanHeader*>(h_plan)->magic == kPlanMagic &&
       static_cast<const PlanHeader*>(h_plan)->prefill_rows > 0)
@@ -802,6 +807,7 @@ extern "C" orion_status orion_point_prefill_attn(const orion_attn_shape* shape, 
                                                  const int32_t* own_len, const void* h_plan,
                                                  const void* d_plan, void* workspace,
                                                  size_t workspace_bytes, void* stream) {
+  const orion::NvtxRange nvtx_range("orion_point_prefill_attn");
   if (!out) return fail(ORION_ERR_INVALID_ARG, "null out");
   if (!h_plan || static_cast<const PlanHeader*>(h_plan)->magic != kPlanMagic ||
       static_cast<const PlanHeader*>(h_plan)->prefill_rows <= 0)

@@ -11,6 +11,7 @@
 #include <cmath>
 
 #include "../../include/orion.h"
+#include "nvtx_range.h"
 #include "split_tc.h"
 
 namespace orion {
@@ -204,6 +205,7 @@ using namespace orion;
 extern "C" orion_status orion_rmsnorm(int32_t n_rows, int32_t hidden, const void* a, const void* b,
                                       const void* weight, float eps, void* out, void* residual_out,
                                       void* stream) {
+  const orion::NvtxRange nvtx_range("orion_rmsnorm");
   if (n_rows < 0 || hidden < 8 || hidden % 8 || hidden > 8192)
     return fail(ORION_ERR_UNSUPPORTED, "rmsnorm: hidden %d must be a multiple of 8 in [8, 8192]", hidden);
   if (!a || (out && !weight) || (!out && !residual_out))
@@ -228,6 +230,7 @@ extern "C" orion_status orion_rope_append(const orion_attn_shape* shape, int32_t
                                           const int32_t* page_table, int32_t num_pages,
                                           int32_t* own_len, const int32_t* pos_base, float rope_theta,
                                           int32_t mode, void* stream) {
+  const orion::NvtxRange nvtx_range("orion_rope_append");
   orion_status st = check_shape_public(shape);
   if (st != ORION_OK) return st;
   if (n_branches < 0) return fail(ORION_ERR_INVALID_ARG, "n_branches < 0");
@@ -259,6 +262,7 @@ extern "C" orion_status orion_rope_append(const orion_attn_shape* shape, int32_t
 
 extern "C" orion_status orion_silu_mul(int32_t n_rows, int32_t inter, const void* gate_up, void* out,
                                        void* stream) {
+  const orion::NvtxRange nvtx_range("orion_silu_mul");
   if (n_rows < 0 || inter < 8 || inter % 8) return fail(ORION_ERR_UNSUPPORTED, "silu_mul: inter %d", inter);
   if (!gate_up || !out) return fail(ORION_ERR_INVALID_ARG, "silu_mul: null pointer");
   if (!al16(gate_up) || !al16(out)) return fail(ORION_ERR_INVALID_ARG, "silu_mul: pointers must be 16-byte aligned");

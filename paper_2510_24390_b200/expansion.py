@@ -10,6 +10,12 @@ to decode.  The round then
 Plans are built by the native planner over `orion_select_branches`' segment lists, and only when
 the running set changes (points join after their Pre, leave after their last token); between
 changes the decode state (own_len) lives on the device and is advanced by the append kernel.
+With `graph=True` a decode round (every layer's append + split + combine launches, PDL edges
+included) is captured once per running set into a CUDA graph and replayed each round: the host
+then does one graph launch per round instead of 3-4 launches per layer, so a latency-bound
+expansion (few branches, short contexts) is no longer bound by host launch rate.  The release
+library's launch path is capture-safe (no synchronising call; the ORION_CHECK build's read-backs
+are not, so the debug library must run eagerly).
 This module is orchestration only: no arithmetic on the data happens here.
 """
 import numpy as np
@@ -58,6 +64,8 @@ class Expansion:
         self.dec_set = None
         self.dec_batch = None
         self.rebuilds = 0
+        self.graph = None               # (key, torch.cuda.CUDAGraph) of the current running set
+        self.captures = 0
 
     # -- schedule ------------------------------------------------------------------------------
     def next_round(self):
@@ -85,16 +93,40 @@ class Expansion:
             batch.attend(q_pre[l], out[l], k_caches[l], v_caches[l], stream=stream)
         return batch
 
-    def decode(self, dec, q, k_new, v_new, k_caches, v_caches, out, lse=None, stream=None):
+    def decode(self, dec, q, k_new, v_new, k_caches, v_caches, out, lse=None, stream=None, graph=False):
         """One decode token of the running set `dec` through all layers: q/k_new/v_new/out
-        [layers][len(dec), ...] in the order of `dec`.  Rebuilds the plan if the set changed."""
+        [layers][len(dec), ...] in the order of `dec`.  Rebuilds the plan if the set changed.
+        graph=True: replay the round's CUDA graph, captured when the set or a tensor changes."""
         if self.dec_set is None or len(self.dec_set) != len(dec) or not np.array_equal(self.dec_set, dec):
             self.dec_batch = self._batch(dec)
             self.dec_set = np.array(dec, np.int32)
             self.rebuilds += 1
-        for l in range(len(k_caches)):
-            mode = APPEND_ADVANCE if l == 0 else APPEND_REWRITE
-            self.dec_batch.step(q[l], k_new[l], v_new[l], k_caches[l], v_caches[l], out[l],
-                                None if lse is None else lse[l], mode=mode, stream=stream)
+            self.graph = None
+
+        def launches(s):
+            for l in range(len(k_caches)):
+                mode = APPEND_ADVANCE if l == 0 else APPEND_REWRITE
+                self.dec_batch.step(q[l], k_new[l], v_new[l], k_caches[l], v_caches[l], out[l],
+                                    None if lse is None else lse[l], mode=mode, stream=s)
+
+        if graph:
+            import torch
+            ts = [t for ls in (q, k_new, v_new, k_caches, v_caches, out, lse or []) for t in ls]
+            key = (self.rebuilds, tuple(t.data_ptr() for t in ts))
+            if self.graph is None or self.graph[0] != key:
+                g = torch.cuda.CUDAGraph()
+                cs = torch.cuda.Stream(device=self.device)
+                cs.wait_stream(torch.cuda.current_stream(self.device) if stream is None else stream)
+                with torch.cuda.graph(g, stream=cs, capture_error_mode="thread_local"):
+                    launches(cs)
+                self.graph = (key, g)
+                self.captures += 1
+            if stream is None:
+                self.graph[1].replay()
+            else:
+                with torch.cuda.stream(stream):
+                    self.graph[1].replay()
+        else:
+            launches(stream)
         self.own_len[dec] += 1
         return self.dec_batch

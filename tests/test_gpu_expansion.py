@@ -84,3 +84,59 @@ def test_whole_expansion_matches_oracles(dagf, policy):
     assert rnd == len(want)
     assert np.array_equal(u16(kc.cpu()), k_ref) and np.array_equal(u16(vc.cpu()), v_ref)
     assert (ex.own_len == cfg.lc + tokens).all()
+
+
+@pytest.mark.parametrize("dagf,policy", [(W.mixed8, 0), (W.fig4, 1)])
+def test_graph_replay_equals_eager(dagf, policy):
+    """Decode rounds replayed from a CUDA graph (captured once per running set) give bitwise the
+    eager launches' outputs and caches, over a whole ragged expansion of 2 layers; the round's
+    input tensors keep their addresses and are refilled in place each round."""
+    cfg = C.CONFIGS["c1"].with_(n_queries=2, lp=96, t=21, lc=8, page=16, d=128, hq=8, hkv=2)
+    lay = T.make_layout(cfg, dag_override=dagf)
+    ten = T.make_qkv(cfg, lay)
+    dev = torch.device("cuda")
+    tokens = np.full(lay.n_branches, cfg.t - cfg.lc, np.int32)
+    tokens[1::3] = 3
+    queries = [dict(n_points=int(lay.n_points[i]), edges=lay.edges[i],
+                    prefix_pt_off=int(lay.prefix_pt_off[i]), prefix_len=int(lay.prefix_len[i]))
+               for i in range(lay.n_queries)]
+    points = np.stack([lay.point_pt_off, lay.content_len, lay.point_cap], 1)
+    L, B = 2, lay.n_branches
+    arms = []
+    for _ in range(2):
+        ex = Expansion(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, lay.page_table, cfg.lc,
+                       tokens, policy=policy, device=dev)
+        kc = [ten["k_cache"][0].to(dev).contiguous() for _ in range(L)]
+        vc = [ten["v_cache"][0].to(dev).contiguous() for _ in range(L)]
+        bufs = {n: [torch.empty((B, h, cfg.d), dtype=torch.bfloat16, device=dev) for _ in range(L)]
+                for n, h in (("q", cfg.hq), ("k", cfg.hkv), ("v", cfg.hkv), ("o", cfg.hq))}
+        arms.append((ex, kc, vc, bufs))
+    rnd = 0
+    while True:
+        rounds = [a[0].next_round() for a in arms]
+        pre, dec = rounds[0]
+        assert all(np.array_equal(r[0], pre) and np.array_equal(r[1], dec) for r in rounds)
+        if len(pre) == 0 and len(dec) == 0:
+            break
+        outs = []
+        for gi, (ex, kc, vc, bufs) in enumerate(arms):
+            if len(pre):
+                qp = T.bf16_randn_u16((len(pre), cfg.lc, cfg.hq, cfg.d), 1000 + rnd, "cpu").to(dev)
+                op = torch.empty_like(qp)
+                ex.prefill(pre, [qp] * L, kc, vc, [op] * L)
+            if len(dec):
+                n = len(dec)
+                for l in range(L):
+                    for nm, h, sd in (("q", cfg.hq, 2000), ("k", cfg.hkv, 3000), ("v", cfg.hkv, 4000)):
+                        bufs[nm][l][:n].copy_(T.bf16_randn_u16((n, h, cfg.d), sd + 10 * rnd + l, "cpu").to(dev))
+                view = lambda nm: [t[:n] for t in bufs[nm]]
+                ex.decode(dec, view("q"), view("k"), view("v"), kc, vc, view("o"), graph=gi == 1)
+                outs.append(torch.stack([t[:n] for t in bufs["o"]]).cpu())
+        if len(dec):
+            assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16)), f"round {rnd}"
+        rnd += 1
+    torch.cuda.synchronize()
+    for l in range(L):
+        assert torch.equal(arms[0][1][l].view(torch.int16), arms[1][1][l].view(torch.int16))
+        assert torch.equal(arms[0][2][l].view(torch.int16), arms[1][2][l].view(torch.int16))
+    assert arms[1][0].captures == arms[1][0].rebuilds >= 2

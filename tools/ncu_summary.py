@@ -16,7 +16,10 @@ WANT = [("gpu__time_duration.sum", "dur"), ("dram__bytes_read.sum", "dram_rd"), 
         ("sm__cycles_active.avg", "cyc_avg"), ("sm__cycles_active.max", "cyc_max"),
         ("launch__registers_per_thread", "regs"), ("sm__cycles_elapsed.avg.per_second", "clk")]
 rep = sys.argv[1]
-out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+if rep.endswith(".csv"):  # an already exported raw page
+    out = open(rep).read()
+else:
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr, units = rows[0], rows[1]
 idx = {h: i for i, h in enumerate(hdr)}
