@@ -491,6 +491,28 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
     std::vector<std::vector<int32_t>> bunion;
     std::vector<int32_t> bpiece;
     int64_t big_tokens = 0;                        // tokens of the masked ranges, summed over kv heads
+    const int64_t sms = (opts && opts->num_sms > 0) ? opts->num_sms : 148;
+    // Small steps (a latency-bound running set: c2's 1-8 branches) would get fewer items than
+    // SMs from the chunk and merge lengths tuned for partial traffic; there the chunk and merge
+    // caps shrink so the step still spreads over about 2 items per SM (tile granularity), when
+    // that needs items shorter than kSmallStepTokens (c4's 8-query share, 2.6K tokens per item at
+    // 2 per SM, measured slower with the cap: its partials outweigh the spread).  This
+    // makes a small batch's chunking depend on the batch's total work; with an explicit
+    // chunk_tokens the planner keeps the fixed chunking (a query's items then never depend on
+    // the rest of the batch).
+    int64_t work = 0;                              // streamed tokens x reader blocks x kv heads
+    for (const Piece& p : pieces) {
+      int64_t nblk = 0, last = -1;
+      for (int32_t b : p.readers)
+        if (block_of(b) != last) last = block_of(b), ++nblk;
+      work += (int64_t)(p.t1 - p.t0) * nblk * Hkv;
+    }
+    const int64_t fill = (work + 2 * sms - 1) / (2 * sms);
+    const bool adapt = !(opts && opts->chunk_tokens > 0);   // an explicit chunk length is kept
+    const int32_t small_cap = adapt && fill < kSmallStepTokens ? (int32_t)std::max<int64_t>(kTileTokens, (fill + kTileTokens - 1) / kTileTokens * kTileTokens)
+                                                  : INT32_MAX;
+    const int64_t merge_cap = std::min<int64_t>(kMergeTokens, small_cap);
+    static_assert(kSmallStepTokens <= kMergeTokens, "the small-step cap only ever shortens items");
     for (size_t pi = 0; pi < pieces.size(); ++pi) {
       const Piece& p = pieces[pi];
       unique_tokens += p.t1 - p.t0;
@@ -500,7 +522,7 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
         while (i < p.readers.size() && block_of(p.readers[i]) == blk) S.push_back(p.readers[i++]);
         const int32_t rows = (int32_t)S.size() * G;
         int32_t ch = std::max(chunk, 32 * std::min(rows, kRowsPerItemBig));
-        ch = (ch + kTileTokens - 1) / kTileTokens * kTileTokens;
+        ch = std::min((ch + kTileTokens - 1) / kTileTokens * kTileTokens, small_cap);
         if (masked_blocks && rows > rows_per_item) {
           for (int32_t g = 0; g < Hkv; ++g) {
             auto key = std::make_pair(g, blk);
@@ -549,7 +571,6 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
     // 8K-token items per SM had left the busiest SM 1.4x above the mean.  When it is large (c5
     // wide-64: the points' own runs, as many tokens as the prefix), keep them long: fewer items
     // than SMs leave SMs on which the swap-AB kernel starts at once, beside the first kernel.
-    const int64_t sms = (opts && opts->num_sms > 0) ? opts->num_sms : 148;
     int64_t small_tokens = 0;
     for (const auto& cs : gchunks)
       for (const Range& R : cs) small_tokens += R.t1 - R.t0;
@@ -609,7 +630,7 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
       for (size_t c0 = 0; c0 < cs.size();) {
         size_t c1 = c0;
         int64_t tok = 0;
-        while (c1 < cs.size() && (c1 == c0 || tok + (cs[c1].t1 - cs[c1].t0) <= kMergeTokens))
+        while (c1 < cs.size() && (c1 == c0 || tok + (cs[c1].t1 - cs[c1].t0) <= merge_cap))
           tok += cs[c1].t1 - cs[c1].t0, ++c1;
         WorkItem w{};
         if (c1 - c0 == 1) {
@@ -719,11 +740,28 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
   is_big.resize(items.size(), 0);
   std::vector<int32_t> perm(items.size());
   for (size_t i = 0; i < perm.size(); ++i) perm[i] = (int32_t)i;
-  if (Lc == 0 || !paired)
+  if (Lc == 0)
     std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) {
       if (is_big[a] != is_big[b]) return is_big[a] > is_big[b];
       return cost[a] > cost[b];
     });
+  else if (!paired) {
+    // Prefill: the items of one prefix group (kv head x the query's leading range) run together,
+    // so the group's prefix streams from DRAM about once and the rest of its readers hit L2;
+    // groups in generation order (kv head major), longest first inside a group.
+    std::vector<int64_t> gkey(items.size());
+    for (size_t i = 0; i < items.size(); ++i) {
+      const Range& r0 = ranges[items[i].pt_off];
+      gkey[i] = ((int64_t)items[i].kv_head << 40) | ((int64_t)(uint32_t)r0.pt_off << 8);
+    }
+    std::map<int64_t, int32_t> gorder;
+    for (size_t i = 0; i < items.size(); ++i) gorder.emplace(gkey[i], (int32_t)gorder.size());
+    std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) {
+      const int32_t ga = gorder[gkey[a]], gb = gorder[gkey[b]];
+      if (ga != gb) return ga < gb;
+      return cost[a] > cost[b];
+    });
+  }
   int32_t n_big = 0;
   for (size_t i = 0; i < items.size(); ++i) n_big += is_big[i];
   for (size_t i = 0; i < items.size(); ++i)

@@ -193,13 +193,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       if (k >= static_cast<uint32_t>(kAhead))
         mbar_wait(u_empty + ((k - kAhead) % kRing), ((k - kAhead) / kRing) & 1);
       ItemG& e = geo[s];
-      int it = 0;
-      if (lane == 0) {
-        it = atomicAdd(a.work_counter, 1);
-        if (it >= n_items) it = -1;
-      }
-      it = __shfl_sync(0xffffffffu, it, 0);
-      if (it >= 0) {
+      int it;
+      for (;;) {
+        it = 0;
+        if (lane == 0) {
+          it = atomicAdd(a.work_counter, 1);
+          if (it >= n_items) it = -1;
+        }
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (it < 0) break;
         const WorkItem w = a.items[it];
         const int nr = item_nranges(w);
         int tiles = 0;
@@ -210,7 +212,28 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) tiles += __shfl_xor_sync(0xffffffffu, tiles, o);
-        if (lane == 0) { e.w = w; e.n_ranges = nr; e.ntiles = tiles; }
+        if (tiles > 0 || a.out) {
+          if (lane == 0) { e.w = w; e.n_ranges = nr; e.ntiles = tiles; }
+          break;
+        }
+        // An empty item (its dynamic ranges end at or before t0 at the current lengths) never
+        // enters the ring: this warp writes its neutral partials and takes the next item.  (In the
+        // ring it could deadlock the look-ahead: a warpgroup holding item k while it skips empty
+        // entries towards its prefetch would wait for entry k + kAhead, which waits for item k.)
+        for (int i = lane; i < w.n_rows * (D / 8); i += 32) {
+          const int row = i / (D / 8), c = i % (D / 8);
+          if (a.part16) {
+            reinterpret_cast<uint4*>(a.part_o + static_cast<size_t>(w.slot0 + row) * D)[c] = make_uint4(0, 0, 0, 0);
+          } else {
+            float4* dst = reinterpret_cast<float4*>(a.part_acc + static_cast<size_t>(w.slot0 + row) * D) + 2 * c;
+            dst[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+            dst[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          if (c == 0) {
+            if (a.part16) a.part_lse[w.slot0 + row] = -INFINITY;
+            else a.part_ml[w.slot0 + row] = make_float2(-INFINITY, 0.f);
+          }
+        }
       }
       if (lane == 0) e.it = it;
       __syncwarp();
@@ -442,27 +465,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
     uint32_t ke = 0;                                // ring entries taken by this warp
-    auto next_item = [&]() -> int {                 // the next non-empty item's ring entry (held), or -1
+    auto next_item = [&]() -> int {                 // the next item's ring entry (held), or -1
       for (;;) {
         const uint32_t kk = ke++;
         const ItemG& g = take(kk);
         if (g.it < 0) { release(kk); return -1; }
         if (g.ntiles > 0) return static_cast<int>(kk);
-        const WorkItem& w = g.w;
-        // empty (dyn end <= t0): neutral partial (direct output: prefill rows are never empty)
-        if (p == 0 && r < w.n_rows && !a.out) {
-          if (a.part16) {
-            uint4* dst = reinterpret_cast<uint4*>(a.part_o + static_cast<size_t>(w.slot0 + r) * D);
-#pragma unroll
-            for (int c = 0; c < D / 8; ++c) dst[c] = make_uint4(0, 0, 0, 0);
-            a.part_lse[w.slot0 + r] = -INFINITY;
-          } else {
-            float* dst = a.part_acc + static_cast<size_t>(w.slot0 + r) * D;
-#pragma unroll
-            for (int c = 0; c < D; c += 4) *reinterpret_cast<float4*>(dst + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-            a.part_ml[w.slot0 + r] = make_float2(-INFINITY, 0.f);
-          }
-        }
+        // ntiles == 0 reaches the ring only in a direct-output (prefill) plan, whose items are
+        // never empty (the own causal range has Lc >= 1 tokens); decode plans' empty items are
+        // resolved by the scheduler warp
         release(kk);
       }
     };

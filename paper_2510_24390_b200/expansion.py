@@ -114,11 +114,18 @@ class Expansion:
             ts = [t for ls in (q, k_new, v_new, k_caches, v_caches, out, lse or []) for t in ls]
             key = (self.rebuilds, tuple(t.data_ptr() for t in ts))
             if self.graph is None or self.graph[0] != key:
+                # capture_begin/end directly: the torch.cuda.graph context also synchronises,
+                # runs the garbage collector and empties the allocator cache (~0.1 s a capture);
+                # the launches allocate nothing
                 g = torch.cuda.CUDAGraph()
                 cs = torch.cuda.Stream(device=self.device)
                 cs.wait_stream(torch.cuda.current_stream(self.device) if stream is None else stream)
-                with torch.cuda.graph(g, stream=cs, capture_error_mode="thread_local"):
-                    launches(cs)
+                with torch.cuda.stream(cs):
+                    g.capture_begin(capture_error_mode="thread_local")
+                    try:
+                        launches(cs)
+                    finally:
+                        g.capture_end()
                 self.graph = (key, g)
                 self.captures += 1
             if stream is None:

@@ -167,12 +167,14 @@ def test_page_permutation_bitwise_and_determinism():
 @pytest.mark.parametrize("world", [2, 3])
 def test_strong_shards_bitwise(world):
     """SURVEY.md §8(e) bitwise check: each rank's sub-batch (shard.rank_queries, strong mode) gives
-    exactly the single-GPU outputs of its queries -- queries share no work, so nothing can differ."""
+    exactly the single-GPU outputs of its queries -- queries share no work, so nothing can differ.
+    With fixed chunking (explicit chunk_tokens): the planner's small-step split adapts the chunk
+    length to a batch's total work, which a shard changes."""
     from paper_2510_24390_b200 import shard
     cfg = C.CONFIGS["c3"].with_(lp=1024, t=200)
     lay = T.make_layout(cfg, ragged=True, extra_tokens=cfg.page)
     ten = T.make_qkv(cfg, lay)
-    full = run_step(cfg, lay, ten)
+    full = run_step(cfg, lay, ten, chunk_tokens=512)
     for rank in range(world):
         qs = shard.rank_queries(cfg.n_queries, rank, world, "strong")
         sub, br = T.subset_layout(lay, qs)
@@ -180,7 +182,7 @@ def test_strong_shards_bitwise(world):
         ten_r = dict(ten)
         for key in ("q", "k_new", "v_new"):
             ten_r[key] = ten[key][:, idx]
-        got = run_step(cfg, sub, ten_r)
+        got = run_step(cfg, sub, ten_r, chunk_tokens=512)
         assert torch.equal(got["out"], full["out"][idx.cuda()])
         assert torch.equal(got["lse"], full["lse"][idx.cuda()])
 
@@ -257,7 +259,8 @@ def test_interleaved_kv_layout(cfgname, flags):
 def test_grid_size_does_not_change_results(flags):
     # Items are handed out by an atomic counter (any CTA may run any item); each item's arithmetic
     # and its partial slots are fixed by the plan, so a 3-CTA grid (the ring wraps many times) and
-    # the full grid must give the same bytes.
+    # the full grid must give the same bytes.  Fixed chunking: the planner's small-step split
+    # would otherwise size the chunks for the SM count.
     cfg = C.CONFIGS["c2"].with_(layers=1)
     lay = T.make_layout(cfg, ragged=True)
     ten = T.make_qkv(cfg, lay)
@@ -269,7 +272,7 @@ def test_grid_size_does_not_change_results(flags):
                    for i in range(lay.n_queries)]
         points = np.stack([lay.point_pt_off, lay.content_len, lay.point_cap], 1)
         batch = orion.ExpansionBatch(cfg.hq, cfg.hkv, cfg.d, cfg.page, queries, points, lay.page_table,
-                                     lay.own_len, device=dev, flags=flags, num_sms=num_sms)
+                                     lay.own_len, device=dev, flags=flags, num_sms=num_sms, chunk_tokens=512)
         q = ten["q"][0].to(dev).contiguous()
         out = torch.empty_like(q)
         lse = torch.empty(q.shape[:2], dtype=torch.float32, device=dev)
@@ -277,3 +280,16 @@ def test_grid_size_does_not_change_results(flags):
         torch.cuda.synchronize()
         outs.append((out.cpu(), lse.cpu()))
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("flags", [0, orion.PLAN_ROWS_ON_LANES])
+@pytest.mark.parametrize("chunk", [0, 64])
+def test_empty_items(flags, chunk):
+    """Own runs chunked past their current length give items that are empty at run time (their
+    dynamic ranges end before t0): c2 with 448 extra capacity tokens per point, the small-step
+    split (chunk 0) or explicit 64-token chunks.  Both kernels write neutral partials for them
+    (the rows-on-lanes kernel in its scheduler warp, outside the item ring) and match the oracle."""
+    cfg = C.CONFIGS["c2"]
+    lay = T.make_layout(cfg, ragged=True, extra_tokens=7 * cfg.page)
+    ten = T.make_qkv(cfg, lay)
+    check_parity(cfg, lay, ten, chunk_tokens=chunk, flags=flags)

@@ -183,9 +183,9 @@ def parse_plan(plan):
     return h, items, readers, coff, cslot
 
 
-def _check_plan_covers(cfg, lay, offs, segs, own_len, flags=0):
-    plan, ws = orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, own_len, chunk_tokens=128,
-                                 flags=flags)
+def _check_plan_covers(cfg, lay, offs, segs, own_len, flags=0, chunk_tokens=128):
+    plan, ws = orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, own_len,
+                                 chunk_tokens=chunk_tokens, flags=flags)
     h, items, readers, coff, cslot = parse_plan(plan)
     G = cfg.hq // cfg.hkv
     assert h["magic"] == 0x314e524f and h["n_rows"] == lay.n_branches * cfg.hq
@@ -439,11 +439,13 @@ def test_chain_plan_merges_history_per_reader_block():
     cfg = C.CONFIGS["c5c"].with_(n_queries=1, lp=512, t=96, lc=16, dag="chain64")
     lay = T.make_layout(cfg, dag_override=lambda: W.chain(48, 2))
     offs, segs = _bind_layout(cfg, lay, 0)
+    # fixed 512-token chunking (an explicit chunk_tokens turns off the small-step split)
     merged, _ = orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, lay.own_len,
-                                  flags=orion.PLAN_NO_HYBRID)
-    hybrid, _ = orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, lay.own_len)
+                                  flags=orion.PLAN_NO_HYBRID, chunk_tokens=512)
+    hybrid, _ = orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, lay.own_len,
+                                  chunk_tokens=512)
     plain, _ = orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, lay.own_len,
-                                 flags=orion.PLAN_NO_MERGE)
+                                 flags=orion.PLAN_NO_MERGE, chunk_tokens=512)
     hm, im, *_ = parse_plan(merged)
     hh, ih, *_ = parse_plan(hybrid)
     hp, ip, *_ = parse_plan(plain)
@@ -458,3 +460,24 @@ def test_chain_plan_merges_history_per_reader_block():
     assert (ih["n_rows"][nb:] <= 64).all() and hm["n_big"] == 0
     _check_plan_covers(cfg, lay, offs, segs, lay.own_len)
     _check_plan_covers(cfg, lay, offs, segs, lay.own_len, flags=orion.PLAN_NO_HYBRID)
+
+
+@pytest.mark.parametrize("nb", [1, 2, 8])
+def test_small_step_spreads_over_the_sms(nb):
+    """A latency-bound running set (c2: 1-8 branches of one query) is cut into about two items
+    per SM (chunks of >= one 64-token tile) instead of a few 8K-token merged items; an explicit
+    chunk_tokens keeps the fixed chunking; coverage holds either way."""
+    cfg = C.CONFIGS["c2"]
+    lay = T.make_layout(cfg)
+    offs, segs = _bind_layout(cfg, lay, 0)
+    sel = np.arange(nb, dtype=np.int32)
+    so, sg = orion.select_branches(offs, segs, lay.own_len, sel)
+    own = np.ascontiguousarray(lay.own_len[sel], np.int32)
+    adaptive, _ = orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, so, sg, own, num_sms=148)
+    fixed, _ = orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, so, sg, own, num_sms=148, chunk_tokens=512)
+    ha, ia, *_ = parse_plan(adaptive)
+    hf, if_, *_ = parse_plan(fixed)
+    assert ha["unique_tokens"] == hf["unique_tokens"] and ha["logical_tokens"] == hf["logical_tokens"]
+    assert hf["n_items"] < 148 <= ha["n_items"] <= 4 * 148
+    from types import SimpleNamespace
+    _check_plan_covers(cfg, SimpleNamespace(n_branches=nb), so, sg, own, chunk_tokens=0)
