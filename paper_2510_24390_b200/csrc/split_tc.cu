@@ -78,7 +78,8 @@ struct Smem {
   static constexpr int OFF_XCH = OFF_V + SV * KVB;   // both WGs' (m, l) per row, x2 (item parity)
   static constexpr int OFF_RING = OFF_XCH + 4 * kRows * 8;   // scheduled items with their geometry
   static constexpr int OFF_BAR = OFF_RING + kRing * static_cast<int>(sizeof(ItemG));
-  static constexpr int N_BAR = 2 * SK + 2 * SV + 2 + 2 + 2 + 2 + 1 + 2 + 2 * 8 + 2;
+  // k/v full+empty; s_full, p_full, pv_done, q_full; o_free; s_free; u_full + u_empty
+  static constexpr int N_BAR = 2 * SK + 2 * SV + 2 + 2 + 2 + 2 + 1 + 2 + 2 * kRing;
   static constexpr int BYTES = OFF_BAR + N_BAR * 8 + 16;
 };
 
@@ -126,8 +127,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   uint64_t* s_free = o_free + 1;                  // softmax WG has read S[b] into registers
   uint64_t* u_full = s_free + 2;                  // [kRing] scheduler published an item index
   uint64_t* u_empty = u_full + kRing;             // [kRing] every reader warp took it
-  uint64_t* pv_iss = u_empty + kRing;             // [2] PV(j) of parity p issued (QK(j+2) may follow)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_iss + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(u_empty + kRing);
   ItemG* geo = reinterpret_cast<ItemG*>(smem + L::OFF_RING);
   float2* xch = reinterpret_cast<float2*>(smem + L::OFF_XCH);
 
@@ -143,8 +143,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     mbar_init(s_free + 0, 128);
     mbar_init(s_free + 1, 128);
     for (int s = 0; s < kRing; ++s) { mbar_init(u_full + s, 1); mbar_init(u_empty + s, kRingReaders); }
-    mbar_init(pv_iss + 0, 1);
-    mbar_init(pv_iss + 1, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmK)) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmV)) : "memory");
@@ -359,8 +357,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     };
     // Tile t of an item goes to softmax warpgroup t & 1 (item-relative, so an item's arithmetic does
     // not depend on which CTA runs it or what ran before: results are deterministic under the
-    // atomic item hand-out); n*[p] count warpgroup p's tiles for its barrier phases.
-    uint32_t nq[2] = {0, 0}, nv[2] = {0, 0};
+    // atomic item hand-out); nq_p / nv_p count warpgroup p's tiles for its barrier phases
+    // (scalars, not arrays indexed by the runtime parity: those would live in local memory)
+    uint32_t nq0 = 0, nq1 = 0, nv0 = 0, nv1 = 0;
     auto issue_qk = [&](const Cur& c) {
       const uint32_t j = c.j;
       const uint32_t p = c.t & 1;
@@ -369,10 +368,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       }
       const int s = j % SK;
       TW(2, mbar_wait(k_full + s, (j / SK) & 1));
-      if (nq[p] > 0) TW(3, mbar_wait(s_free + p, (nq[p] - 1) & 1));   // S[p] read out
-      // QK(j) enters the in-order tensor pipe after PV(j-2): the PV a warpgroup waits for before
-      // it may store its next P never queues behind the next tiles' QKs.
-      if (nq[p] > 0) TW(4, mbar_wait(pv_iss + p, (nq[p] - 1) & 1));
+      const uint32_t nqp = p ? nq1 : nq0;
+      if (nqp > 0) TW(3, mbar_wait(s_free + p, (nqp - 1) & 1));   // S[p] read out
+      // QK(j) is issued as soon as S(j-2) is read out, ahead of PV(j-2): S(j) is then ready when
+      // the warpgroup finishes tile j-2, and PV(j-2) still completes long before the warpgroup
+      // stores P(j) (after tile j's exponentials).
       tc_fence_after();
       const uint64_t dq = dq0 + static_cast<uint64_t>(((c.k & 1) * L::QB) >> 4);
       const uint64_t dk = dk0 + static_cast<uint64_t>((s * L::KVB) >> 4);
@@ -393,14 +393,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         tc_commit(k_empty + s);
       }
       __syncwarp();
-      ++nq[p];
+      if (p) ++nq1; else ++nq0;
     };
     auto issue_pv = [&](const Cur& c) {
       const uint32_t j = c.j;
       const uint32_t p = c.t & 1;
       const int s = j % SV;
       TW(6, mbar_wait(v_full + s, (j / SV) & 1));
-      TW(4, mbar_wait(p_full + p, nv[p] & 1));
+      TW(4, mbar_wait(p_full + p, (p ? nv1 : nv0) & 1));
       if (c.t == 0 && c.k > 0) TW(5, mbar_wait(o_free, (c.k - 1) & 1));   // previous item's O read
       tc_fence_after();
       const uint64_t dv = dv0 + static_cast<uint64_t>((s * L::KVB) >> 4);
@@ -416,10 +416,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
         tc_commit(pv_done + p);
         tc_commit(v_empty + s);
-        mbar_arrive(pv_iss + p);
       }
       __syncwarp();
-      ++nv[p];
+      if (p) ++nv1; else ++nv0;
     };
     // Two issuers (tcgen05.commit tracks the issuing thread's own MMAs): warp 1 issues every
     // S(j) = Q K(j)^T as soon as K(j) landed and softmax warpgroup j&1 has read S(j-2) out
@@ -487,6 +486,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       load_q(1, pf);
     }
     uint32_t j = 0, k = 0, np = 0;                  // np: this warpgroup's tiles so far
+    // The two warpgroups take turns at the exponentials (named barriers 2: WG0's turn, 3: WG1's):
+    // one warpgroup's ex2 phase saturates the SM's MUFU on its own, so running them one after the
+    // other overlaps each warpgroup's S read-out, P store and barrier waits with the other's
+    // exponentials instead of both doing them at once.  Turns follow the item's tile order
+    // (tile t: warpgroup t & 1); an item with an odd tile count ends with a pass by WG1, so every
+    // item hands the turn back to WG0.  WG1 gives WG0 the first turn; WG0 takes the last token.
+    if (p == 1) asm volatile("bar.arrive 2, 256;\n" ::: "memory");
     while (cur >= 0) {
       const ItemG& cg = geo[cur % kRing];
       const WorkItem w = cg.w;
@@ -524,6 +530,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         const bool edge = g.causal || (tb < g.t0) || (tb + kTok > g.end);
         const bool cmask = edge || rmask;            // this row's scores need the column mask
         uint32_t pk[32];
+#ifdef ORION_TC_TRACE
+        unsigned long long tm0 = clock64();
+#endif
         if (active) {
           float mx = -INFINITY;                     // raw scores; scale > 0 commutes with max
           if (cmask) {
@@ -537,6 +546,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           // Lazy rescale (exact: O_p and l_p refer to m_used).  Warp-uniform so the aligned TMEM
           // accesses are executed by the whole warp.
           const bool mine = mx > m_used + 8.f;
+#ifdef ORION_TC_TRACE
+          tr_[5] += clock64() - tm0; tm0 = clock64();
+#endif
           if (__any_sync(0xffffffffu, mine)) {
             const float alpha = mine ? ex2(m_used - mx) : 1.f;   // 0 when m_used == -inf
             if (had) {
@@ -556,6 +568,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             if (mine) m_used = mx;
             l_run *= alpha;
           }
+        }
+        TW(10, asm volatile("bar.sync %0, 256;\n" ::"r"(2 + p) : "memory"));   // my turn at the exponentials
+#ifdef ORION_TC_TRACE
+        tr_[8] += clock64() - tm0;
+        const unsigned long long tx0 = clock64();
+#endif
+        if (active) {
           const float mb = m_used == -INFINITY ? 0.f : m_used;
           float la[4] = {0.f, 0.f, 0.f, 0.f};   // 4 chains: the mixed adds are dependent
 #pragma unroll
@@ -570,6 +589,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #pragma unroll
           for (int c = 0; c < 32; ++c) pk[c] = 0u;
         }
+#ifdef ORION_TC_TRACE
+        tr_[11] += clock64() - tx0;
+#endif
+        asm volatile("bar.arrive %0, 256;\n" ::"r"(3 - p) : "memory");   // the other warpgroup's turn
 #ifdef ORION_TC_TRACE
         tr_[1] += clock64() - ts0; ts0 = clock64();
 #endif
@@ -606,6 +629,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         ++np;
       }
       }
+      if (p == 1 && (cg.ntiles & 1)) {   // odd tile count: WG1 passes its turn
+        asm volatile("bar.sync 3, 256;\n" ::: "memory");
+        asm volatile("bar.arrive 2, 256;\n" ::: "memory");
+      }
 #ifdef ORION_TC_TRACE
       const unsigned long long tep0 = clock64();
 #endif
@@ -616,7 +643,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       }
       // ---- epilogue
       if (had) {
-        TW(8, mbar_wait(pv_done + p, (np - 1) & 1));      // last PV of this WG complete
+        mbar_wait(pv_done + p, (np - 1) & 1);      // last PV of this WG complete
         tc_fence_after();
       }
       // Both warpgroups publish their (m, l), then each merges O_0 and O_1 over its half of the
@@ -645,6 +672,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           orow = (static_cast<size_t>(b) * a.lc + (rr % rpr) / a.group) * a.hq + w.kv_head * a.group + rr % a.group;
         }
         float* dst = a.part_acc + static_cast<size_t>(w.slot0 + r) * D;
+        // 16-bit results (bf16 out, fp16 partials) are staged in item k's Q buffer -- free since
+        // its Q went to TMEM -- as 128 rows x D/8 16-byte chunks (chunk c of row r at c ^ (r % (D/8)):
+        // conflict-free row writes and chunk reads), then copied out with 16-byte row-contiguous
+        // stores instead of one scattered 8-byte store per thread and 4 columns.
+        const bool staged = a.out || a.part16;
+        uint8_t* const ob = smem + L::OFF_Q + (k & 1) * L::QB;
         if (active) {
 #pragma unroll 1
           for (int cb = p * (D / 2); cb < (p + 1) * (D / 2); cb += 16) {
@@ -660,18 +693,19 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                 v.y = (had0 ? a0 * __uint_as_float(o[c + 1]) : 0.f) + (had1 ? a1 * __uint_as_float(q1[c + 1]) : 0.f);
                 v.z = (had0 ? a0 * __uint_as_float(o[c + 2]) : 0.f) + (had1 ? a1 * __uint_as_float(q1[c + 2]) : 0.f);
                 v.w = (had0 ? a0 * __uint_as_float(o[c + 3]) : 0.f) + (had1 ? a1 * __uint_as_float(q1[c + 3]) : 0.f);
-                if (a.out) {
+                if (staged) {
                   uint2 pk2;
-                  pk2.x = pack_bf16(v.x * inv, v.y * inv);
-                  pk2.y = pack_bf16(v.z * inv, v.w * inv);
-                  *reinterpret_cast<uint2*>(a.out + orow * D + cb + c) = pk2;
-                } else if (a.part16) {   // fp16 partial format (plan_format.h): o = acc / l
-                  __half2 h0 = __floats2half2_rn(v.x * inv, v.y * inv);
-                  __half2 h1 = __floats2half2_rn(v.z * inv, v.w * inv);
-                  uint2 pk2;
-                  pk2.x = *reinterpret_cast<uint32_t*>(&h0);
-                  pk2.y = *reinterpret_cast<uint32_t*>(&h1);
-                  *reinterpret_cast<uint2*>(a.part_o + static_cast<size_t>(w.slot0 + r) * D + cb + c) = pk2;
+                  if (a.out) {
+                    pk2.x = pack_bf16(v.x * inv, v.y * inv);
+                    pk2.y = pack_bf16(v.z * inv, v.w * inv);
+                  } else {                 // fp16 partial format (plan_format.h): o = acc / l
+                    __half2 h0 = __floats2half2_rn(v.x * inv, v.y * inv);
+                    __half2 h1 = __floats2half2_rn(v.z * inv, v.w * inv);
+                    pk2.x = *reinterpret_cast<uint32_t*>(&h0);
+                    pk2.y = *reinterpret_cast<uint32_t*>(&h1);
+                  }
+                  const int col = cb + c, ch = col >> 3;
+                  *reinterpret_cast<uint2*>(ob + r * (D * 2) + ((ch ^ (r & (D / 8 - 1))) << 4) + ((col & 4) << 1)) = pk2;
                 } else {
                   *reinterpret_cast<float4*>(dst + cb + c) = v;
                 }
@@ -686,6 +720,26 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
         tc_fence_before();
         mbar_arrive(o_free);
+        if (staged) {
+          asm volatile("bar.sync 1, 256;\n" ::: "memory");   // the item's rows are staged
+          constexpr int CPR = D / 8;                            // 16-byte chunks per row
+          const int t = tid - 128;
+          for (int idx = t; idx < w.n_rows * CPR; idx += 256) {
+            const int row = idx / CPR, ch = idx % CPR;
+            const uint4 val = *reinterpret_cast<const uint4*>(ob + row * (D * 2) + ((ch ^ (row & (CPR - 1))) << 4));
+            __nv_bfloat16* gdst;
+            if (a.out) {
+              const int rr = w.row_begin + row, rpr = a.lc * a.group;
+              const int b = __ldg(a.readers + w.readers_off + rr / rpr);
+              gdst = a.out + ((static_cast<size_t>(b) * a.lc + (rr % rpr) / a.group) * a.hq +
+                              w.kv_head * a.group + rr % a.group) * D;
+            } else {
+              gdst = reinterpret_cast<__nv_bfloat16*>(a.part_o + static_cast<size_t>(w.slot0 + row) * D);
+            }
+            reinterpret_cast<uint4*>(gdst)[ch] = val;
+          }
+          asm volatile("bar.sync 1, 256;\n" ::: "memory");   // buffer read out: WG0 refills it with Q
+        }
       }
       release(static_cast<uint32_t>(cur));
       if (p == 1) {
@@ -698,11 +752,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       }
 #ifdef ORION_TC_TRACE
       tr_[4] += clock64() - tep0;
-      tr_[5] += 1;
 #endif
       ++k;
     }
     if (p == 0) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    if (p == 0) asm volatile("bar.sync 2, 256;\n" ::: "memory");   // the token WG1 passed last
     if ((warp & 3) < 2) TRACE_DUMP("softmax");
 #ifdef ORION_TC_TRACE
     if (warp == 4 && lane == 0)   // per-CTA balance: total cycles, tiles, items of warpgroup 0

@@ -74,9 +74,9 @@ __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
 #define TRACE_DECL unsigned long long tr_[12] = {0}; const unsigned long long tr_t0 = clock64();
 #define TW(slot, stmt) do { const unsigned long long t_ = clock64(); stmt; tr_[slot] += clock64() - t_; } while (0)
 #define TRACE_DUMP(role) do { if (blockIdx.x < 2 && (threadIdx.x & 31) == 0) printf( \
-    "TRACE blk %d warp %2d %-8s tot %llu | %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu\n", blockIdx.x, \
+    "TRACE blk %d warp %2d %-8s tot %llu | %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu %llu\n", blockIdx.x, \
     threadIdx.x >> 5, role, clock64() - tr_t0, tr_[0], tr_[1], tr_[2], tr_[3], tr_[4], tr_[5], tr_[6], tr_[7], \
-    tr_[8], tr_[9]); } while (0)
+    tr_[8], tr_[9], tr_[10], tr_[11]); } while (0)
 #else
 #define TRACE_DECL
 #define TW(slot, stmt) stmt
