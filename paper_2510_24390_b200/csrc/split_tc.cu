@@ -619,7 +619,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             }
           }
         }
-        fence_proxy_async();
+        if (edge) fence_proxy_async();   // the zeroed V rows (generic writes) before the PV reads them
         tc_fence_before();
         mbar_arrive(p_full + p);
 #ifdef ORION_TC_TRACE
