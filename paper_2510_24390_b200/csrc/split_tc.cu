@@ -727,16 +727,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           for (int idx = t; idx < w.n_rows * CPR; idx += 256) {
             const int row = idx / CPR, ch = idx % CPR;
             const uint4 val = *reinterpret_cast<const uint4*>(ob + row * (D * 2) + ((ch ^ (row & (CPR - 1))) << 4));
-            __nv_bfloat16* gdst;
             if (a.out) {
               const int rr = w.row_begin + row, rpr = a.lc * a.group;
               const int b = __ldg(a.readers + w.readers_off + rr / rpr);
-              gdst = a.out + ((static_cast<size_t>(b) * a.lc + (rr % rpr) / a.group) * a.hq +
-                              w.kv_head * a.group + rr % a.group) * D;
-            } else {
-              gdst = reinterpret_cast<__nv_bfloat16*>(a.part_o + static_cast<size_t>(w.slot0 + row) * D);
+              __nv_bfloat16* gdst = a.out + ((static_cast<size_t>(b) * a.lc + (rr % rpr) / a.group) * a.hq +
+                                             w.kv_head * a.group + rr % a.group) * D;
+              reinterpret_cast<uint4*>(gdst)[ch] = val;
+            } else {   // (no evict_last hint here: it cost c5 chain 3 %, its L2-shared history)
+              reinterpret_cast<uint4*>(a.part_o + static_cast<size_t>(w.slot0 + row) * D)[ch] = val;
             }
-            reinterpret_cast<uint4*>(gdst)[ch] = val;
           }
           asm volatile("bar.sync 1, 256;\n" ::: "memory");   // buffer read out: WG0 refills it with Q
         }

@@ -83,6 +83,9 @@ static_assert(L::BYTES <= 232448, "shared memory budget");
 // PTX helpers shared with the rows-on-lanes kernels (tc_ptx.h): mbarrier, TMA, tcgen05.
 using tc::smem_u32;
 using tc::mbar_init;
+using tc::l2_policy_evict_last;
+using tc::l2_policy_evict_first;
+using tc::st_global_hint;
 using tc::mbar_arrive;
 using tc::mbar_expect_tx;
 using tc::mbar_wait;
@@ -346,6 +349,7 @@ __device__ __forceinline__ void finish_item(const Pend& pd, uint32_t tmem, uint3
   STW(5, mbar_wait(B.acc_full + pd.kp, (static_cast<uint32_t>(pd.item) >> 1) & 1));
   tc_fence_after();
   __half* dst = a.part_o + static_cast<size_t>(pd.slot0) * D + t;
+  const uint64_t pol = l2_policy_evict_last();
   for (int cb = 0; cb < pd.nh; cb += 8) {
     uint32_t o[8];
     tmem_ld32x8(tmem + lane_base + colO(pd.kp) + c0 + cb, o);
@@ -353,7 +357,7 @@ __device__ __forceinline__ void finish_item(const Pend& pd, uint32_t tmem, uint3
 #pragma unroll
     for (int c = 0; c < 8; ++c)
       if (c0 + cb + c < pd.n_rows)
-        dst[static_cast<size_t>(c0 + cb + c) * D] = __float2half_rn(__uint_as_float(o[c]) * linv[cb + c]);
+        st_global_hint(dst + static_cast<size_t>(c0 + cb + c) * D, __float2half_rn(__uint_as_float(o[c]) * linv[cb + c]), pol);
   }
   tc_fence_before();
   mbar_arrive(B.o_free + pd.kp);
@@ -440,7 +444,7 @@ __device__ __forceinline__ void softmax_item(uint8_t* smem, uint32_t tmem, uint3
   if (t < NH) {
     const float l = red[t] + red[32 + t] + red[64 + t] + red[96 + t];
     linv[t] = 1.f / l;
-    if (c0 + t < e.n_rows) a.part_lse[e.slot0 + c0 + t] = mrow[t] + log2f(l);
+    if (c0 + t < e.n_rows) st_global_hint(a.part_lse + e.slot0 + c0 + t, mrow[t] + log2f(l), l2_policy_evict_last());
   }
   pend.valid = 1;
   pend.slot0 = e.slot0; pend.n_rows = e.n_rows; pend.nh = NH; pend.kp = static_cast<int32_t>(kp);
@@ -586,6 +590,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t j = 0;
     const int pmask = (1 << a.page_shift) - 1;
     const int big = min(64, 1 << a.page_shift);     // rows of a full-tile box (<= one page)
+    // A swap-AB item reads its K/V chunk once (a reader block carries all rows of its query that
+    // read it), so the stream is marked evict_first: it no longer pushes the partials (evict_last)
+    // and the rows-on-lanes kernel's L2-shared prefixes out of L2.  c4 +1.6 %, its 8-query share
+    // +8 %, c5 wide +5 % same-box; the rows-on-lanes kernel keeps the default policy (its items
+    // share prefixes through L2: evict_first there cost the point prefill 14 %).
+    const uint64_t kv_pol = l2_policy_evict_first();
     for (uint32_t k = 0;; ++k) {
       const Sched e = read_sched(ring, sch_full, sch_empty, k, lane == 0);
       if (!e.valid) break;
@@ -630,8 +640,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int b = 0; b < 8; ++b)
               if (b < tn) {
                 const uint32_t roff = static_cast<uint32_t>(to + b * rpb) * 128;
-                tma_load_2d(dst + roff, m, 0, rr[b], full + st);
-                tma_load_2d(dst + L::HALF_KV + roff, m, 64, rr[b], full + st);
+                tma_load_2d(dst + roff, m, 0, rr[b], full + st, kv_pol);
+                tma_load_2d(dst + L::HALF_KV + roff, m, 64, rr[b], full + st, kv_pol);
               }
           }
           __syncwarp();
