@@ -13,7 +13,7 @@
 // The weighted sum runs in the fixed plan order: a row's result does not depend on which kernel or
 // CTA merges it (the combine kernel and the split kernel's merge phase agree bitwise).  Loads use
 // ld.global.cg: in the merge phase the partials were written by other CTAs of the same kernel, so
-// the incoherent read-only path must not serve them.
+// the incoherent read-only path must not serve them (hence .cg on the hinted loads).
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -23,6 +23,32 @@ namespace orion {
 
 constexpr int kMergeLanes = 8;
 
+// Cache policies of the merge's loads: the plan's combine CSR is re-read by every layer's combine
+// (evict_last keeps it resident); a partial is dead once merged (evict_first).
+__device__ __forceinline__ uint64_t merge_policy(bool last) {
+  uint64_t pol;
+  if (last) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ int32_t ld_hint(const int32_t* p, uint64_t pol) {
+  int32_t v;
+  asm volatile("ld.global.cg.L2::cache_hint.b32 %0, [%1], %2;\n" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float ld_hint(const float* p, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.cg.L2::cache_hint.f32 %0, [%1], %2;\n" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint4 ld_hint(const uint4* p, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.cg.L2::cache_hint.v4.b32 {%0, %1, %2, %3}, [%4], %5;\n"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+
 template <int D>
 __device__ __forceinline__ void merge_row16(const int32_t* __restrict__ comb_off, const int32_t* __restrict__ comb_slot,
                                             const __half* part_o, const float* part_lse,
@@ -31,17 +57,18 @@ __device__ __forceinline__ void merge_row16(const int32_t* __restrict__ comb_off
   constexpr int E = D / kMergeLanes;  // elements per lane (8 or 16)
   constexpr int U = E / 8;            // 16-B loads per lane per partial
   const unsigned full = 0xffffffffu;
-  const int e0 = valid ? __ldcg(comb_off + row) : 0;
-  const int n = valid ? __ldcg(comb_off + row + 1) - e0 : 0;
+  const uint64_t keep = merge_policy(true), drop = merge_policy(false);
+  const int e0 = valid ? ld_hint(comb_off + row, keep) : 0;
+  const int n = valid ? ld_hint(comb_off + row + 1, keep) - e0 : 0;
   int nmax = n;  // the warp walks chunks uniformly (shuffles need every lane)
 #pragma unroll
   for (int o = 16; o >= kMergeLanes; o >>= 1) nmax = max(nmax, __shfl_xor_sync(full, nmax, o));
   // Pass 1: M = max lse2 of the row; chunk 0's slot / lse stay in registers.
-  const int slot0 = sub < n ? __ldcg(comb_slot + e0 + sub) : 0;
-  const float lse0 = sub < n ? __ldcg(part_lse + slot0) : -INFINITY;
+  const int slot0 = sub < n ? ld_hint(comb_slot + e0 + sub, keep) : 0;
+  const float lse0 = sub < n ? ld_hint(part_lse + slot0, drop) : -INFINITY;
   float M = lse0;
   for (int c = kMergeLanes; c < nmax; c += kMergeLanes)
-    if (c + sub < n) M = fmaxf(M, __ldcg(part_lse + __ldcg(comb_slot + e0 + c + sub)));
+    if (c + sub < n) M = fmaxf(M, ld_hint(part_lse + ld_hint(comb_slot + e0 + c + sub, keep), drop));
 #pragma unroll
   for (int o = kMergeLanes / 2; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(full, M, o, kMergeLanes));
   const float base = M == -INFINITY ? 0.f : M;
@@ -54,8 +81,8 @@ __device__ __forceinline__ void merge_row16(const int32_t* __restrict__ comb_off
     int slot_l = slot0;
     float lse_l = lse0;
     if (c > 0) {
-      slot_l = c + sub < n ? __ldcg(comb_slot + e0 + c + sub) : 0;
-      lse_l = c + sub < n ? __ldcg(part_lse + slot_l) : -INFINITY;
+      slot_l = c + sub < n ? ld_hint(comb_slot + e0 + c + sub, keep) : 0;
+      lse_l = c + sub < n ? ld_hint(part_lse + slot_l, drop) : -INFINITY;
     }
     float w_l = 0.f;
     if (c + sub < n) asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(w_l) : "f"(lse_l - base));
@@ -70,7 +97,7 @@ __device__ __forceinline__ void merge_row16(const int32_t* __restrict__ comb_off
         if (c + j0 + j < n) {
           const uint4* src = reinterpret_cast<const uint4*>(part_o + static_cast<size_t>(s) * D + sub * E);
 #pragma unroll
-          for (int u = 0; u < U; ++u) x[j][u] = __ldcg(src + u);
+          for (int u = 0; u < U; ++u) x[j][u] = ld_hint(src + u, drop);
         }
       }
 #pragma unroll
