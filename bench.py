@@ -56,6 +56,9 @@ def parse(argv=None):
                     help="KV cache layout: separate K / V pools, or K and V of a (page, kv head) adjacent")
     ap.add_argument("--no-merge", action="store_true",
                     help="plan without multi-range item merging (ORION_PLAN_NO_MERGE), for comparison")
+    ap.add_argument("--unfused", action="store_true",
+                    help="time the step as orion_kv_append + orion_expand_attn instead of orion_expand_step "
+                         "(the append fused into the split launch), for A/B")
     ap.add_argument("--no-hybrid", action="store_true",
                     help="every decode item on the swap-AB kernel (ORION_PLAN_NO_HYBRID), for comparison")
     ap.add_argument("--kernel", default="tc", choices=["tc", "rol", "mma"],
@@ -321,13 +324,18 @@ def alloc_tensors(args, cfg, lay, layers, dev, seed):
     return kc, vc, q, kn, vn, out
 
 
+FUSED = True    # region A through orion_expand_step (--unfused: the three calls, for A/B)
+
+
 def time_steps(batch, layers, tens, steps, warmup, stream, world=1, barrier=None):
     """Warm up, then two timed regions of `steps` steps each (per layer: append REWRITE, split,
     combine), CUDA events on `stream`:
-      A (the headline): events only at step boundaries -- an event recorded between two kernels
-        breaks their programmatic-dependent-launch edge (≈ 2 % of the c4 step), so none is;
-      B (the kernel timing): the same steps with events around every split launch, for the split
-        kernel's average launch duration (the roofline) and its share of B's step time.
+      A (the headline): per layer one orion_expand_step (the append runs inside the split launch
+        where the plan allows), events only at step boundaries -- an event recorded between two
+        kernels breaks their programmatic-dependent-launch edge (≈ 2 % of the c4 step), so none is;
+      B (the kernel timing): the same steps as three calls (append, split, combine) with events
+        around every split launch, for the split kernel's average launch duration (the roofline)
+        and its share of B's step time.
     Returns (elapsed_ms A, per-step ms A sorted, per-launch split ms B, elapsed_ms B, launches, step)."""
     import torch
     import paper_2510_24390_b200 as orion
@@ -335,13 +343,21 @@ def time_steps(batch, layers, tens, steps, warmup, stream, world=1, barrier=None
     REW = orion.APPEND_REWRITE
 
     def step(ev=None, k=0):
+        if ev is None and FUSED:   # the public call: orion_expand_step (append in the split launch)
+            for l in range(layers):
+                batch.step(q[l], kn[l], vn[l], kc[l], vc[l], out[l], mode=REW)
+            return
+        if ev is None:
+            for l in range(layers):
+                batch.append(kn[l], vn[l], kc[l], vc[l], mode=REW)
+                batch.split(q[l], kc[l], vc[l])
+                batch.combine(out[l])
+            return
         for l in range(layers):
             batch.append(kn[l], vn[l], kc[l], vc[l], mode=REW)
-            if ev is not None:
-                ev[k][l][0].record(stream)
+            ev[k][l][0].record(stream)
             batch.split(q[l], kc[l], vc[l])
-            if ev is not None:
-                ev[k][l][1].record(stream)
+            ev[k][l][1].record(stream)
             batch.combine(out[l])
 
     for _ in range(warmup):
@@ -371,7 +387,10 @@ def time_steps(batch, layers, tens, steps, warmup, stream, world=1, barrier=None
     b1.record(stream)
     torch.cuda.synchronize()
     split_ms = [ev[k][l][0].elapsed_time(ev[k][l][1]) for k in range(steps) for l in range(layers)]
-    n_kernels = 3 + (1 if batch.stats.get("n_big", 0) and batch.stats["n_big"] < batch.stats["n_items"] else 0)
+    nb = batch.stats.get("n_big", 0)
+    # region A's launches per layer: orion_step_launches (2 when orion_expand_step fuses the
+    # append into the split launch, else append + split kernel(s) + combine)
+    n_kernels = batch.step_launches() if FUSED else 3 + (1 if 0 < nb < batch.stats["n_items"] else 0)
     return elapsed_a, step_ms, split_ms, b0.elapsed_time(b1), steps * layers * n_kernels, step
 
 
@@ -490,7 +509,7 @@ def run_orion(args, cfg, layers):
         torch.cuda.synchronize()
         gms, _ = shard.reduce_timing(g0.elapsed_time(g1), 0.0, device=dev)
         graph = {"ms_per_step": gms / args.steps, "tokens_per_s": total_b / (gms / args.steps / 1e3),
-                 "note": f"one step ({layers} layers x append/split/combine) captured once, replayed {args.steps}x"}
+                 "note": f"one step ({layers} layers x orion_expand_step) captured once, replayed {args.steps}x"}
         del cg
     except Exception as exc:                             # capture unsupported here: say so
         graph = {"unavailable": f"{type(exc).__name__}: {exc}"}
@@ -1212,7 +1231,9 @@ def spawn_ranks(args):
 
 
 def main():
+    global FUSED
     args = parse()
+    FUSED = not args.unfused
     cfg = WC.CONFIGS[args.config]
     if args.queries:
         cfg = cfg.with_(n_queries=args.queries)

@@ -14,6 +14,8 @@
  *   orion_expand_plan    cut the bound segments into shared pieces (maximal token ranges with
  *                        a fixed reader set) and emit the device work plan.
  *   orion_kv_append      write each branch's new-token K/V into its own pages (device).
+ *   orion_expand_step    orion_kv_append + orion_expand_attn in one call (device; the append
+ *                        fused into the split launch where the plan allows).
  *   orion_expand_attn    dependency-masked batched GQA decode attention over the paged bf16
  *                        cache; each shared piece is read from HBM once per (query, kv head)
  *                        group (device; split kernel + combine kernel).
@@ -271,7 +273,7 @@ orion_status orion_kv_append(const orion_attn_shape* shape, int32_t n_branches,
  *  h_plan, d_plan  the host plan and its device copy (same bytes).
  *  workspace     device, >= workspace_needed bytes from orion_expand_plan, 16-byte aligned, and
  *                ZEROED before its first use (e.g. allocated with zeros).  The split kernels keep
- *                their work-distribution counter in its last 16 bytes; every launch leaves it zero
+ *                their work-distribution counters in its last 256 bytes; every launch leaves them zero
  *                again (the last CTA resets it, so no memset runs between launches), so a
  *                workspace serves one launch at a time, in stream order.
  * Errors: INVALID_ARG (null/unaligned pointers, plan/shape mismatch, workspace too small),
@@ -287,6 +289,40 @@ orion_status orion_expand_attn(const orion_attn_shape* shape, int32_t n_branches
                                int32_t num_pages, const int32_t* page_table,
                                const int32_t* own_len, const void* h_plan, const void* d_plan,
                                void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * orion_expand_step — one whole expansion decode step for one layer: orion_kv_append of every
+ * branch's new token followed by orion_expand_attn over the same plan (Alg. 1 l.16;
+ * SURVEY.md §8(a) a5 + a6 + a7).  Results are those of the two calls in order (outputs bitwise
+ * equal; tests/test_gpu_parity.py::test_expand_step_equals_append_then_attn).
+ * Device; enqueued on `stream`.  With the release library, a plan on the default swap-AB kernel
+ * without rows-on-lanes items (no `n_big`; every plan whose query groups have <= 64 rows) and a
+ * short step (<= 2048 streamed tokens per SM: latency-bound running sets), the append runs inside
+ * the split launch: every CTA appends its share of the branches first and releases a per-branch
+ * flag, and a range growing with branch b waits for b's flag only, so the step is two launches
+ * (split, combine) instead of three.  Otherwise (longer steps, where the separate append overlaps
+ * the split's prologue; hybrid plans; head_dim 64; the debug build) it runs the two calls.
+ * own_len must stay below 2^20.
+ *  q, out, lse, k_cache, v_cache, num_pages, page_table, h_plan, d_plan, workspace,
+ *  workspace_bytes   as for orion_expand_attn;
+ *  k_new, v_new, own_pt_off, own_cap, own_len, mode   as for orion_kv_append (own_len in/out).
+ * Errors: the union of the two calls' errors.
+ */
+orion_status orion_expand_step(const orion_attn_shape* shape, int32_t n_branches, const void* q,
+                               const void* k_new, const void* v_new, void* out, float* lse,
+                               void* k_cache, void* v_cache, int32_t num_pages,
+                               const int32_t* page_table, const int32_t* own_pt_off,
+                               const int32_t* own_cap, int32_t* own_len, int32_t mode,
+                               const void* h_plan, const void* d_plan, void* workspace,
+                               size_t workspace_bytes, void* stream);
+
+/*
+ * orion_step_launches — host: the number of kernels one orion_expand_step (or, for a point-prefill
+ * plan, one orion_point_prefill_attn) enqueues with this plan on the current device: 2 when the
+ * append is fused into the split launch, else 3 (4 for a hybrid plan with both split kernels).
+ * Errors: INVALID_ARG (null pointer, not a plan).
+ */
+orion_status orion_step_launches(const void* h_plan, int32_t* launches);
 
 /*
  * orion_point_prefill_attn — the attention of the Pre stage (Alg. 1 l.12 / l.19, Eq. (2);

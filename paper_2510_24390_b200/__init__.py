@@ -6,6 +6,7 @@ Python surface of the C ABI in include/orion.h (same names, argument marshalling
     bind_segments(queries, points, offs, refs)   -> bound segments                   (host)
     expand_plan(shape, offs, segs, own_len)      -> device work plan                 (host)
     kv_append(...)                               -> K1 on the current CUDA stream    (device)
+    expand_step(...)                             -> K1 + K2 + K3 (K1 fused into K2 where possible)
     expand_attn(...)                             -> K2 + K3 on the current stream    (device)
 
 `ExpansionBatch` strings them together for a set of in-flight queries: it builds the plan once
@@ -21,7 +22,7 @@ from ._lib import (OrionError, POLICY_ANCESTORS, POLICY_PARENTS_EQ3, APPEND_ADVA
                    APPEND_REWRITE, SEG_PREFIX, SEG_CONTENT, SEG_FULL, SEG_OUTPUT, SEG_OWN,
                    EDGE_NULL, EDGE_CONTEXTUAL, EDGE_DEPENDENT, SEG_DTYPE, SEGREF_DTYPE, lib)
 
-__all__ = ["dag_waves", "bind_segments", "expand_plan", "context_base", "plan_stats", "kv_append", "expand_attn",
+__all__ = ["dag_waves", "bind_segments", "expand_plan", "context_base", "plan_stats", "kv_append", "expand_attn", "expand_step",
            "expand_split", "expand_combine",
            "ExpansionBatch", "OrionError", "version", "POLICY_ANCESTORS", "POLICY_PARENTS_EQ3",
            "APPEND_ADVANCE", "APPEND_REWRITE"]
@@ -212,6 +213,22 @@ def expand_attn(hq, hkv, d, page, q, out, lse, k_cache, v_cache, page_table, own
         _stream_ptr(stream)))
 
 
+def expand_step(hq, hkv, d, page, q, k_new, v_new, out, lse, k_cache, v_cache, page_table, own_pt_off,
+                own_cap, own_len, h_plan, d_plan, workspace, mode=APPEND_ADVANCE, stream=None, sm_scale=0.0,
+                kv_interleaved=False):
+    """orion_expand_step (append + attention of one layer; the append fused into the split launch
+    where the plan allows) on `stream` (default: torch's current stream)."""
+    _require_cuda(q, k_new, v_new, out, lse, k_cache, v_cache, page_table, own_pt_off, own_cap, own_len,
+                  d_plan, workspace)
+    shape = _shape(hq, hkv, d, page, sm_scale, kv_interleaved)
+    _lib.check(lib().orion_expand_step(
+        ctypes.byref(shape), int(q.shape[0]), q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(), out.data_ptr(),
+        None if lse is None else lse.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(), int(k_cache.shape[0]),
+        page_table.data_ptr(), own_pt_off.data_ptr(), own_cap.data_ptr(), own_len.data_ptr(), int(mode),
+        _lib.ptr(h_plan), d_plan.data_ptr(), workspace.data_ptr(), workspace.numel() * workspace.element_size(),
+        _stream_ptr(stream)))
+
+
 def point_prefill_attn(hq, hkv, d, page, q, out, lse, k_cache, v_cache, page_table, own_len, h_plan,
                        d_plan, workspace, stream=None, sm_scale=0.0, kv_interleaved=False):
     """orion_point_prefill_attn: q/out bf16 [B, Lc, Hq, d], lse fp32 [B, Lc, Hq] (nullable)."""
@@ -349,6 +366,12 @@ class ExpansionBatch:
             self.page_table.data_ptr(), int(k_cache.shape[0]), self.own_len.data_ptr(),
             pos_base.data_ptr(), float(rope_theta), int(mode), _stream_ptr(stream)))
 
+    def step_launches(self):
+        """orion_step_launches: kernels one step() enqueues with this plan on the current device."""
+        n = np.zeros(1, np.int32)
+        _lib.check(lib().orion_step_launches(_lib.ptr(self.h_plan), _lib.ptr(n)))
+        return int(n[0])
+
     def append(self, k_new, v_new, k_cache, v_cache, mode=APPEND_ADVANCE, stream=None):
         kv_append(self.hq, self.hkv, self.d, self.page, k_new, v_new, k_cache, v_cache,
                   self.own_pt_off, self.own_cap, self.page_table, self.own_len, mode, stream,
@@ -373,7 +396,14 @@ class ExpansionBatch:
                        self.kv_interleaved)
 
     def step(self, q, k_new, v_new, k_cache, v_cache, out, lse=None, mode=APPEND_ADVANCE,
-             stream=None):
-        """One expansion decode step for one layer: K1 append, then K2 split + K3 combine."""
+             stream=None, fused=True):
+        """One expansion decode step for one layer: K1 append, then K2 split + K3 combine --
+        orion_expand_step (the append inside the split launch where the plan allows), or with
+        fused=False the two calls."""
+        if fused and not self.prefill_rows:
+            expand_step(self.hq, self.hkv, self.d, self.page, q, k_new, v_new, out, lse, k_cache, v_cache,
+                        self.page_table, self.own_pt_off, self.own_cap, self.own_len, self.h_plan, self.d_plan,
+                        self.workspace, mode, stream, self.sm_scale, self.kv_interleaved)
+            return
         self.append(k_new, v_new, k_cache, v_cache, mode, stream)
         self.attend(q, out, k_cache, v_cache, lse, stream)

@@ -18,7 +18,7 @@ SEG_PREFIX, SEG_CONTENT, SEG_FULL, SEG_OUTPUT, SEG_OWN = range(5)
 APPEND_ADVANCE, APPEND_REWRITE = 0, 1
 
 EXPORTED_SYMBOLS = ("orion_dag_waves", "orion_bind_segments", "orion_expand_plan",
-                    "orion_plan_get_stats", "orion_kv_append", "orion_expand_attn",
+                    "orion_plan_get_stats", "orion_kv_append", "orion_expand_attn", "orion_expand_step", "orion_step_launches",
                     "orion_expand_split", "orion_expand_combine", "orion_point_prefill_attn",
                     "orion_expansion_round", "orion_select_branches", "orion_context_base", "orion_rmsnorm",
                     "orion_rope_append", "orion_silu_mul", "orion_last_error", "orion_version")
@@ -100,6 +100,9 @@ def lib():
                                          sz, vp]
         L.orion_expand_combine.argtypes = [P(AttnShape), i32, vp, vp, vp, vp, vp, sz, vp]
         L.orion_point_prefill_attn.argtypes = L.orion_expand_attn.argtypes
+        L.orion_step_launches.argtypes = [vp, vp]
+        L.orion_expand_step.argtypes = [P(AttnShape), i32, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp, i32,
+                                        vp, vp, vp, sz, vp]
         L.orion_expansion_round.argtypes = [i32, vp, vp, vp, i32, vp, vp, vp, vp, i32, vp, vp, vp, vp]
         L.orion_select_branches.argtypes = [i32, vp, vp, vp, i32, vp, vp, vp, i32, vp]
         L.orion_context_base.argtypes = [i32, vp, vp, vp, vp]
@@ -109,7 +112,7 @@ def lib():
         L.orion_silu_mul.argtypes = [i32, i32, vp, vp, vp]
         for f in ("orion_expand_split", "orion_expand_combine", "orion_dag_waves", "orion_bind_segments", "orion_expand_plan",
                   "orion_plan_get_stats", "orion_kv_append", "orion_expand_attn", "orion_point_prefill_attn",
-                  "orion_expansion_round", "orion_select_branches", "orion_context_base", "orion_rmsnorm",
+                  "orion_expand_step", "orion_step_launches", "orion_expansion_round", "orion_select_branches", "orion_context_base", "orion_rmsnorm",
                   "orion_rope_append", "orion_silu_mul"):
             getattr(L, f).restype = ctypes.c_int32
         L.orion_last_error.restype = ctypes.c_char_p

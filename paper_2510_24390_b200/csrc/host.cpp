@@ -792,7 +792,8 @@ extern "C" orion_status orion_expand_plan(const orion_attn_shape* shape, int32_t
   }
   if (variant != kVariantMmaSync) {   // the tcgen05 kernels' work counters (kept zero between launches)
     h.counter_off = h.workspace_bytes;
-    h.workspace_bytes += n_big > 0 ? 32 : 16;
+    // work counters, the fused append's epoch and one append flag per branch (orion_expand_step)
+    h.workspace_bytes += kCounterBytes + align16((int64_t)n_branches * 4);
   }
   h.n_big = n_big;
   h.n_pieces = (int64_t)pieces.size();

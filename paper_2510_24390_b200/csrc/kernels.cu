@@ -579,7 +579,7 @@ template <int D>
 orion_status launch_split(const PlanHeader* h, const char* dplan, const void* q, const void* k,
                           const void* v, int32_t num_pages, const int32_t* page_table,
                           const int32_t* own_len, void* ws, cudaStream_t st, int kvs, void* out = nullptr,
-                          float* lse = nullptr) {
+                          float* lse = nullptr, const FusedAppend* app = nullptr) {
 #ifdef ORION_CHECK
   {
     const orion_status cs = check_plan_contents(h, dplan, page_table, own_len, num_pages, st);
@@ -611,6 +611,14 @@ orion_status launch_split(const PlanHeader* h, const char* dplan, const void* q,
     t.work_counter = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + h->counter_off);
     t.part16 = 0;
     t.pdl_late = 0;
+    t.app = FusedAppend{};
+    if (app) {   // only on the swap-AB kernel of a plan without big items (orion_expand_step)
+      if (h->variant != kVariantTCT || h->n_big > 0) return fail(ORION_ERR_UNSUPPORTED, "fused append on a hybrid plan");
+      t.app = *app;
+      t.app.epoch = t.work_counter + kAppendEpochWord;
+      t.app.flags = t.work_counter + kCounterBytes / 4;
+      t.app.enabled = 1;
+    }
     if (h->variant == kVariantTCT) {
       if (D != 128) return fail(ORION_ERR_UNSUPPORTED, "transposed split kernel needs head_dim 128");
       if (h->n_big > 0) {
@@ -798,6 +806,83 @@ extern "C" orion_status orion_expand_attn(const orion_attn_shape* shape, int32_t
   if (st != ORION_OK) return st;
   return orion_expand_combine(shape, n_branches, out, lse, h_plan, d_plan, workspace,
                               workspace_bytes, stream);
+}
+
+namespace {
+constexpr int64_t kFuseTokensPerSm = 2048;
+bool step_fuses(const PlanHeader* h) {
+#ifdef ORION_CHECK
+  return false;
+#else
+  return h->variant == kVariantTCT && h->n_big == 0 && h->head_dim == 128 &&
+         h->streamed_tokens <= kFuseTokensPerSm * current_device_sms();
+#endif
+}
+}  // namespace
+
+extern "C" orion_status orion_step_launches(const void* h_plan, int32_t* launches) {
+  if (!h_plan || !launches) return fail(ORION_ERR_INVALID_ARG, "null pointer");
+  const PlanHeader* h = static_cast<const PlanHeader*>(h_plan);
+  if (h->magic != kPlanMagic || h->version != kPlanVersion) return fail(ORION_ERR_INVALID_ARG, "not an orion plan");
+  if (h->prefill_rows > 0) { *launches = 1; return ORION_OK; }   // point prefill: the split kernel only
+  if (step_fuses(h)) { *launches = 2; return ORION_OK; }
+  const bool hybrid2 = h->variant == kVariantTCT && h->n_big > 0 && h->n_big < h->n_items;
+  *launches = 3 + (hybrid2 ? 1 : 0);
+  return ORION_OK;
+}
+
+extern "C" orion_status orion_expand_step(const orion_attn_shape* shape, int32_t n_branches,
+                                          const void* q, const void* k_new, const void* v_new, void* out,
+                                          float* lse, void* k_cache, void* v_cache, int32_t num_pages,
+                                          const int32_t* page_table, const int32_t* own_pt_off,
+                                          const int32_t* own_cap, int32_t* own_len, int32_t mode,
+                                          const void* h_plan, const void* d_plan, void* workspace,
+                                          size_t workspace_bytes, void* stream) {
+  const orion::NvtxRange nvtx_range("orion_expand_step");
+  const PlanHeader* h = nullptr;
+  orion_status st = check_attn(shape, n_branches, h_plan, d_plan, workspace, workspace_bytes, &h);
+  if (st != ORION_OK) return st;
+  if (h->prefill_rows > 0) return fail(ORION_ERR_INVALID_ARG, "a point-prefill plan needs orion_point_prefill_attn");
+  // K1 fused into the swap-AB split launch when the plan has no rows-on-lanes items and the step
+  // is short (<= kFuseTokensPerSm streamed tokens per SM: there the saved launch and kernel
+  // boundary dominate -- c4 with 2 queries 20.4k -> 26.8k tok/s -- while on longer steps the
+  // separate append kernel, overlapping the split's prologue through PDL, measured 1-2 % faster:
+  // c4 with 8 and 64 queries).  The release library only (the debug build checks every append and
+  // plan separately).  Otherwise the two calls it stands for, with the same results.
+  bool fuse = step_fuses(h) && shape->head_dim == 128;
+  if (!fuse) {
+    st = orion_kv_append(shape, n_branches, k_new, v_new, k_cache, v_cache, own_pt_off, own_cap, page_table,
+                         num_pages, own_len, mode, stream);
+    if (st != ORION_OK) return st;
+    return orion_expand_attn(shape, n_branches, q, out, lse, k_cache, v_cache, num_pages, page_table, own_len,
+                             h_plan, d_plan, workspace, workspace_bytes, stream);
+  }
+  if (mode != ORION_APPEND_ADVANCE && mode != ORION_APPEND_REWRITE)
+    return fail(ORION_ERR_INVALID_ARG, "bad append mode %d", mode);
+  if (!q || !out || !k_new || !v_new || !k_cache || !v_cache || !page_table || !own_pt_off || !own_cap || !own_len)
+    return fail(ORION_ERR_INVALID_ARG, "null pointer");
+  if (!aligned16(q) || !aligned16(out) || !aligned16(k_new) || !aligned16(v_new) || !aligned16(k_cache) ||
+      !aligned16(v_cache))
+    return fail(ORION_ERR_INVALID_ARG, "device pointers must be 16-byte aligned");
+  if (num_pages < 1) return fail(ORION_ERR_INVALID_ARG, "num_pages < 1");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const char* dp = static_cast<const char*>(d_plan);
+  FusedAppend ap{};
+  ap.k_new = static_cast<const __nv_bfloat16*>(k_new);
+  ap.v_new = static_cast<const __nv_bfloat16*>(v_new);
+  ap.k_cache = static_cast<__nv_bfloat16*>(k_cache);
+  ap.v_cache = static_cast<__nv_bfloat16*>(v_cache);
+  ap.own_pt_off = own_pt_off;
+  ap.own_cap = own_cap;
+  ap.own_len = own_len;
+  ap.err = nullptr;
+  ap.n_branches = n_branches;
+  ap.mode = mode;
+  ap.num_pages = num_pages;
+  st = launch_split<128>(h, dp, q, k_cache, v_cache, num_pages, page_table, own_len, workspace, s,
+                         1 + shape->kv_interleaved, nullptr, nullptr, &ap);
+  if (st != ORION_OK) return st;
+  return launch_combine<128>(h, dp, out, lse, workspace, s);
 }
 
 extern "C" orion_status orion_point_prefill_attn(const orion_attn_shape* shape, int32_t n_branches,

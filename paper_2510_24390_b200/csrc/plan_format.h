@@ -35,6 +35,11 @@ constexpr int32_t kItemRanges = 2;
 constexpr int32_t kRangeMasked = 4;   // Range only: readers_mask (pad_[0]) selects the item's readers
                                       // (bit i: the item's i-th reader) that read this range
 constexpr int64_t kMergeTokens = 8192;   // token cap of a merged multi-range decode item
+// Workspace tail of the tcgen05 kernels' counters: words 0-1 (item counter, done count) of the
+// first split kernel, words 4-5 of a hybrid plan's second; the fused append's launch epoch at word
+// kAppendEpochWord (its own cache line), then one append flag per branch (kCounterBytes on).
+constexpr int64_t kCounterBytes = 256;
+constexpr int kAppendEpochWord = 32;
 constexpr int64_t kSmallStepTokens = 1024;   // small-step split: below this many tokens per item at 2 items per SM
 constexpr int kTileTokens = 64;    // tokens per pipeline stage in the split kernel
 

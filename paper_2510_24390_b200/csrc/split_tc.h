@@ -47,6 +47,16 @@ __device__ __forceinline__ void release_work_counter(int32_t* counter) {
     atomicExch(counter + 1, 0);
   }
 }
+// The fused append's launch epoch (FusedAppend): advanced by the last CTA of a fused launch, so
+// the next fused launch's CTAs all read epoch + 1 as their flag value.
+__device__ __forceinline__ void release_work_counter(int32_t* counter, bool advance_epoch) {
+  __threadfence();
+  if (atomicAdd(counter + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+    atomicExch(counter, 0);
+    atomicExch(counter + 1, 0);
+    if (advance_epoch) atomicAdd(counter + kAppendEpochWord, 1);
+  }
+}
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
@@ -63,6 +73,27 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
+
+// K1 fused into the swap-AB split kernel (orion_expand_step on a plan without big items): every
+// CTA first appends the new K/V rows of its share of the branches and releases each branch's flag
+// (flags[b] = this launch's epoch + 1); a range growing with branch b reads own_len[b] only once
+// flags[b] carries that value (acquire; the appended rows reach its TMA loads through proxy
+// fences).  No grid-wide barrier: an item waits only for the branches it reads.  The epoch sits in
+// work counter word kAppendEpochWord, the flags after the counters (plan_format.h).
+// enabled = 0: no append in the kernel.
+struct FusedAppend {
+  const __nv_bfloat16* k_new;
+  const __nv_bfloat16* v_new;
+  __nv_bfloat16* k_cache;
+  __nv_bfloat16* v_cache;
+  const int32_t* own_pt_off;
+  const int32_t* own_cap;
+  int32_t* own_len;       // the array TcArgs::own_len points to
+  int32_t* epoch;         // work counter word kAppendEpochWord
+  int32_t* flags;         // [n_branches]
+  int32_t* err;           // debug build: first branch whose target page is out of range
+  int32_t n_branches, mode, num_pages, enabled;
+};
 
 struct TcArgs {
   const WorkItem* items;
@@ -84,6 +115,7 @@ struct TcArgs {
   int32_t* work_counter;  // items (split_tct) / pair units (split_pair) handed out by atomicAdd
   int32_t part16;         // rows-on-lanes kernel on a hybrid plan's big items: write the fp16 partial
                           // format (part_o = acc / l, part_lse = m + log2 l) instead of fp32
+  FusedAppend app;
   int32_t pdl_late;       // second kernel of a hybrid step: it may start once the first kernel has
                           // passed its own dependency wait (the step's inputs are complete) and waits
                           // for the first kernel's completion only before it exits

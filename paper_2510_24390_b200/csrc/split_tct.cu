@@ -149,7 +149,7 @@ __device__ __forceinline__ uint32_t idesc(int n, bool a_mn, bool b_mn) {   // M 
 
 // Geometry of range r of an item (the item itself unless kItemRanges).
 struct RangeT {
-  int32_t pt_off, t0, end, base, ntiles;
+  int32_t pt_off, t0, end, base, ntiles, dyn;
 };
 // (a, b) += (lo, hi) of a packed bf16x2 word, each in fp32: bit-identical to unpacking and adding
 // (bf16 -> f32 is exact), in two instructions (add.rn.f32.bf16 -> FHADD.BF16 with a half selector).
@@ -159,7 +159,22 @@ __device__ __forceinline__ void add_bf16x2_f32x2(uint32_t pk, float& a, float& b
       : "+f"(a), "+f"(b) : "r"(pk));
 }
 __device__ __forceinline__ int item_nranges(const WorkItem& w) { return (w.flags & kItemRanges) ? w.n_ranges : 1; }
-__device__ __forceinline__ RangeT range_of(const TcArgs& a, const WorkItem& w, int r) {
+// Fused append: branch d's flag word carries (epoch + 1) << 20 | own_len once its append is done
+// (12 epoch bits suffice: every fused launch rewrites every branch's flag; own_len < 2^20);
+// the range reads its length from the flag (one acquire load: no separate own_len load), after
+// which the appended K/V rows may be read.  Lane 0 spins; the warp follows.
+__device__ __forceinline__ int appended_len(const TcArgs& a, int d, uint32_t seq) {
+  int v = 0;
+  if ((threadIdx.x & 31) == 0) {
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(a.app.flags + d) : "memory");
+      if ((static_cast<uint32_t>(v) >> 20) == (seq & 0xfffu)) break;
+      __nanosleep(64);
+    }
+  }
+  return __shfl_sync(0xffffffffu, v, 0) & 0xfffff;
+}
+__device__ __forceinline__ RangeT range_of(const TcArgs& a, const WorkItem& w, int r, uint32_t seq) {
   RangeT g;
   int32_t t1, dyn;
   if (w.flags & kItemRanges) {
@@ -169,7 +184,14 @@ __device__ __forceinline__ RangeT range_of(const TcArgs& a, const WorkItem& w, i
     g.pt_off = w.pt_off; g.t0 = w.t0; t1 = w.t1; dyn = w.dyn;
   }
   g.end = t1;
-  if (dyn >= 0) g.end = min(g.end, __ldg(a.own_len + dyn));
+  g.dyn = dyn;
+  if (dyn >= 0) {
+    if (a.app.enabled) {
+      g.end = min(g.end, appended_len(a, dyn, seq));   // written in this launch
+    } else {
+      g.end = min(g.end, __ldg(a.own_len + dyn));
+    }
+  }
   g.base = g.t0 & ~(kTok - 1);
   g.ntiles = g.end > g.t0 ? (g.end - g.base + kTok - 1) / kTok : 0;
   return g;
@@ -294,6 +316,51 @@ __device__ __forceinline__ void softmax_tile(uint32_t tmem, uint32_t lane_base, 
 // One entry per token range: an item is one range, or (kItemRanges) a list of ranges streamed as
 // one accumulation.  `item` numbers the CTA's non-empty items (Q / O^T double-buffer parity);
 // `first` / `last` mark an item's first and last non-empty range.
+// K1 inside the split launch (FusedAppend), before the CTA's roles start: warp w appends the
+// new-token K/V rows of branches blockIdx.x + (w + 12 i) gridDim.x exactly as kv_append_kernel
+// does (ADVANCE: slot own_len, then own_len + 1; REWRITE: slot own_len - 1; no write ever leaves
+// the caches) and releases the branch's flag.  One warp per branch keeps the dependent
+// own_len -> page -> copy chains of a CTA's branches in parallel; no grid-wide barrier follows
+// (a count of CTAs done, polled by every item with a growing range, measured 4 % slower on c4's
+// 8-query share than the separate append kernel).
+constexpr int kAppendWarps = kThreads / 32;
+__device__ __forceinline__ void fused_append(const TcArgs& a, int sw, int lane) {
+  constexpr int CH = D / 8;
+  const FusedAppend& ap = a.app;
+  const uint32_t seq = static_cast<uint32_t>(__ldcg(ap.epoch)) + 1u;
+  for (int b = blockIdx.x + sw * gridDim.x; b < ap.n_branches; b += kAppendWarps * gridDim.x) {
+    const int len = __ldcg(ap.own_len + b);
+    const int pos = ap.mode == ORION_APPEND_REWRITE ? len - 1 : len;
+    const bool ok = pos >= 0 && pos < __ldg(ap.own_cap + b);
+    int page = ok ? __ldg(a.page_table + __ldg(ap.own_pt_off + b) + (pos >> a.page_shift)) : -1;
+    if (page >= ap.num_pages || (ok && page < 0)) {
+      if (ap.err && lane == 0) atomicCAS(ap.err, 0, b + 1);
+      page = -1;
+    }
+    if (page >= 0) {
+      const size_t row = static_cast<size_t>(pos & ((1 << a.page_shift) - 1)) * D;
+      for (int i = lane; i < a.hkv * CH; i += 32) {
+        const int g = i / CH, c = i % CH;
+        const size_t dst = (((static_cast<size_t>(page) * a.hkv + g) * a.kvs) << a.page_shift) * D + row + c * 8;
+        const size_t src = (static_cast<size_t>(b) * a.hkv + g) * D + c * 8;
+        *reinterpret_cast<uint4*>(ap.k_cache + dst) = *reinterpret_cast<const uint4*>(ap.k_new + src);
+        *reinterpret_cast<uint4*>(ap.v_cache + dst) = *reinterpret_cast<const uint4*>(ap.v_new + src);
+      }
+    }
+    // ADVANCE moves own_len only when the slot was written (as kv_append_kernel)
+    const int nlen = (page >= 0 && ap.mode == ORION_APPEND_ADVANCE) ? len + 1 : len;
+    __syncwarp();                                   // the warp's row copies issued
+    if (lane == 0) {
+      if (nlen != len) ap.own_len[b] = nlen;
+      asm volatile("fence.proxy.async.global;\n" ::: "memory");   // generic K/V writes vs TMA reads
+      __threadfence();
+      asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(ap.flags + b),
+                   "r"(static_cast<int>((seq & 0xfffu) << 20) | (nlen & 0xfffff))
+                   : "memory");
+    }
+  }
+}
+
 struct Sched {
   int32_t valid, it, pt_off, t0, end, base, ntiles, npad, kv_head, n_rows, slot0, item, first, last, pad[2];
 };
@@ -499,6 +566,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // KV appended / previous step's reads done.  A hybrid plan's second kernel (pdl_late) was
   // launched only once the first had passed this wait, so it defers its own wait to the end.
   if (!a.pdl_late) pdl_wait();
+  if (a.app.enabled) fused_append(a, warp, lane);
   const int n_items = a.n_items;
 
   TRACE_DECL
@@ -506,6 +574,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------------ scheduler + Q gather
     uint32_t k = 0;                                 // ring entries published (one per range)
     uint32_t iq = 0;                                // non-empty items of this CTA
+    // fused append: this launch's flag epoch (every CTA reads the value the previous fused
+    // launch's last CTA left)
+    const uint32_t seq = a.app.enabled ? static_cast<uint32_t>(__ldcg(a.app.epoch)) + 1u : 0u;
     // Items are handed out by an atomic counter (zeroed by the launcher) in the planner's
     // longest-first order: greedy LPT over the SMs.  A static stride left the busiest SM ~5 %
     // above the mean (ncu sm__cycles_active max / avg on c4).
@@ -517,12 +588,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const WorkItem w = a.items[it];
       const int nr = item_nranges(w);
       int rfirst = -1, rlast = -1;
-      RangeT g0 = range_of(a, w, 0);
+      RangeT g0 = range_of(a, w, 0, seq);
       if (nr == 1) {                                 // the common single-range item: one lookup
         if (g0.ntiles > 0) rfirst = rlast = 0;
       } else {
         for (int r = 0; r < nr; ++r)
-          if (range_of(a, w, r).ntiles > 0) { if (rfirst < 0) rfirst = r; rlast = r; }
+          if (range_of(a, w, r, seq).ntiles > 0) { if (rfirst < 0) rfirst = r; rlast = r; }
       }
       if (rfirst < 0) {                              // every range empty (dyn end <= t0): neutral partial
         for (int i = lane; i < w.n_rows * D / 8; i += 32)
@@ -531,7 +602,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         continue;
       }
       for (int r = rfirst; r <= rlast; ++r) {
-        const RangeT g = nr == 1 ? g0 : range_of(a, w, r);
+        const RangeT g = nr == 1 ? g0 : range_of(a, w, r, seq);
         if (g.ntiles == 0) continue;
         TW(0, mbar_wait(sch_empty + (k % kSched), ((k / kSched) & 1) ^ 1));
         if (lane == 0) {
@@ -539,6 +610,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           e.valid = 1; e.it = it; e.pt_off = g.pt_off; e.t0 = g.t0; e.end = g.end; e.base = g.base;
           e.ntiles = g.ntiles; e.npad = npad_of(w.n_rows); e.kv_head = w.kv_head; e.n_rows = w.n_rows;
           e.slot0 = w.slot0; e.item = static_cast<int32_t>(iq); e.first = r == rfirst; e.last = r == rlast;
+          e.pad[0] = g.dyn >= 0 && a.app.enabled;   // may hold rows appended in this launch
           ring[k % kSched] = e;
           mbar_arrive(sch_full + (k % kSched));
         }
@@ -596,8 +668,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     // +8 %, c5 wide +5 % same-box; the rows-on-lanes kernel keeps the default policy (its items
     // share prefixes through L2: evict_first there cost the point prefill 14 %).
     const uint64_t kv_pol = l2_policy_evict_first();
+    bool fenced = false;
     for (uint32_t k = 0;; ++k) {
       const Sched e = read_sched(ring, sch_full, sch_empty, k, lane == 0);
+      if (e.valid && e.pad[0] && !fenced) {   // rows other CTAs appended (generic writes) -> TMA reads
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        fenced = true;
+      }
       if (!e.valid) break;
       for (int tb0 = 0; tb0 < e.ntiles; tb0 += 32) {
         int brow[8];
@@ -833,7 +910,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
   }
-  if (tid == 0) release_work_counter(a.work_counter);
+  if (tid == 0) release_work_counter(a.work_counter, a.app.enabled != 0);
   if (a.pdl_late) pdl_wait();                        // complete only after the first kernel (combine reads both)
 }
 

@@ -27,7 +27,7 @@ def batch_for(cfg, lay, policy=0, chunk_tokens=0, device="cuda", flags=0, interl
 
 
 def run_step(cfg, lay, ten, policy=0, mode=orion.APPEND_ADVANCE, chunk_tokens=0, layer=0, flags=0,
-             interleaved=False):
+             interleaved=False, fused=True):
     """Returns dict(out, lse, k_cache, v_cache, own_len) from the GPU after one step.  interleaved:
     the caches live in one [pages][Hkv][2][P][d] array (K/V views of it are passed)."""
     dev = torch.device("cuda")
@@ -43,7 +43,7 @@ def run_step(cfg, lay, ten, policy=0, mode=orion.APPEND_ADVANCE, chunk_tokens=0,
     vn = ten["v_new"][layer].to(dev).contiguous()
     out = torch.empty_like(q)
     lse = torch.empty(q.shape[:2], dtype=torch.float32, device=dev)
-    batch.step(q, kn, vn, kc, vc, out, lse, mode=mode)
+    batch.step(q, kn, vn, kc, vc, out, lse, mode=mode, fused=fused)
     torch.cuda.synchronize()
     return dict(out=out, lse=lse, k_cache=kc, v_cache=vc, own_len=batch.own_len.cpu().numpy(),
                 batch=batch)

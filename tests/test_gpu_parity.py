@@ -293,3 +293,24 @@ def test_empty_items(flags, chunk):
     lay = T.make_layout(cfg, ragged=True, extra_tokens=7 * cfg.page)
     ten = T.make_qkv(cfg, lay)
     check_parity(cfg, lay, ten, chunk_tokens=chunk, flags=flags)
+
+
+@pytest.mark.parametrize("cfgname,mode,extra", [("c2", orion.APPEND_ADVANCE, {}), ("c2", orion.APPEND_REWRITE, {}),
+                                                ("c3", orion.APPEND_ADVANCE, {"n_queries": 4}),
+                                                ("c4", orion.APPEND_ADVANCE, {"n_queries": 2}),
+                                                ("c5c", orion.APPEND_ADVANCE, {"n_queries": 1})])
+def test_expand_step_equals_append_then_attn(cfgname, mode, extra):
+    """orion_expand_step (the append inside the swap-AB split launch; on c5's hybrid plan the two
+    calls) gives bitwise the outputs, lse, caches and lengths of orion_kv_append followed by
+    orion_expand_attn.  Ragged own runs with spare capacity, so appended rows land in partially
+    filled pages that the same launch's items read."""
+    cfg = C.CONFIGS[cfgname].with_(**extra)
+    lay = T.make_layout(cfg, ragged=True, extra_tokens=cfg.page)
+    ten = T.make_qkv(cfg, lay)
+    a = run_step(cfg, lay, ten, mode=mode, fused=True)
+    b = run_step(cfg, lay, ten, mode=mode, fused=False)
+    assert np.array_equal(a["own_len"], b["own_len"])
+    for key in ("out", "lse", "k_cache", "v_cache"):
+        x, y = a[key], b[key]
+        assert torch.equal(x.view(torch.int16) if x.dtype == torch.bfloat16 else x,
+                           y.view(torch.int16) if y.dtype == torch.bfloat16 else y), key
