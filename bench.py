@@ -566,6 +566,9 @@ def run_orion(args, cfg, layers):
                      "algorithmic_bytes_per_launch": split_bytes,
                      "split_ms_per_launch": split_avg_s * 1e3,
                      "split_share_of_step": sum(split_ms) / elapsed_b,
+                     # the same split launches against the headline step (region A, no inner events):
+                     # what the rest of a layer (append, combine, launch edges) costs the headline
+                     "split_share_of_headline_step": split_avg_s * 1e3 * layers / ms_step,
                      "timing_note": "value / ms_per_step: timed region A, events only at step boundaries; "
                                     "split_ms_per_launch: region B, the same steps with events around every "
                                     "split launch (those events cost ~2 % of the step: they break the "
