@@ -481,3 +481,31 @@ def test_small_step_spreads_over_the_sms(nb):
     assert hf["n_items"] < 148 <= ha["n_items"] <= 4 * 148
     from types import SimpleNamespace
     _check_plan_covers(cfg, SimpleNamespace(n_branches=nb), so, sg, own, chunk_tokens=0)
+
+
+def test_step_launches():
+    """orion_step_launches: 2 kernels per orion_expand_step on a short step of the swap-AB kernel
+    (the append fused into the split launch), 3 on a long one (c4's 64 queries: the separate
+    append overlaps the split's prologue), 4 on a hybrid plan with both split kernels, 1 for a
+    point-prefill plan.  Host only (148 SMs without a GPU)."""
+    from paper_2510_24390_b200 import _lib
+
+    def launches(plan):
+        n = np.zeros(1, np.int32)
+        _lib.check(orion.lib().orion_step_launches(_lib.ptr(plan), _lib.ptr(n)))
+        return int(n[0])
+
+    def plan_of(cfgname, nq, **kw):
+        cfg = C.CONFIGS[cfgname].with_(n_queries=nq)
+        lay = T.make_layout(cfg)
+        offs, segs = _bind_layout(cfg, lay, 0)
+        return orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, lay.own_len, **kw)[0], cfg
+
+    assert launches(plan_of("c4", 2)[0]) == 2
+    assert launches(plan_of("c4", 64)[0]) == 3
+    hyb, _ = plan_of("c5c", 1)
+    assert orion.plan_stats(hyb)["n_big"] > 0 and launches(hyb) == 4
+    pre, cfg = plan_of("c2", 1, prefill_rows=C.CONFIGS["c2"].lc)
+    assert launches(pre) == 1
+    with pytest.raises(orion.OrionError):
+        launches(np.zeros(256, np.uint8))
