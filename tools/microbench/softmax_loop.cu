@@ -1,0 +1,79 @@
+// The rows-on-lanes kernel's exponential loop in isolation: one warp per SM sub-partition (4 per
+// SM, as one softmax warpgroup holding the turn), 64 scores per thread per "tile", variants:
+//   0 full loop: FFMA + ex2 + bf16x2 pack + 2 mixed bf16 adds per pair (as split_tc.cu)
+//   1 no row sums (FFMA + ex2 + pack)
+//   2 no pack (FFMA + ex2, fp32 sums)
+//   3 ex2 only (the MUFU floor)
+// Cycles per 64-score tile per warp.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ float ex2f(float x) { float y; asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ float add_bf16x2_f32(uint32_t pk, float acc) {
+  float r;
+  asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %1;\n\tadd.rn.f32.bf16 %0, lo, %2;\n\t"
+      "add.rn.f32.bf16 %0, hi, %0;\n\t}" : "=f"(r) : "r"(pk), "f"(acc));
+  return r;
+}
+
+template <int V>
+__global__ void k(const float* in, uint32_t* out, long long* cyc, int tiles) {
+  float sr[64];
+#pragma unroll
+  for (int c = 0; c < 64; ++c) sr[c] = in[(threadIdx.x * 64 + c) & 1023];
+  const float scale = 0.127f, mb = 1.5f;
+  float l = 0.f;
+  uint32_t acc = 0;
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int t = 0; t < tiles; ++t) {
+    uint32_t pk[32];
+    float la[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      float a, b;
+      if (V == 3) { a = ex2f(sr[2 * c]); b = ex2f(sr[2 * c + 1]); }
+      else { a = ex2f(fmaf(sr[2 * c], scale, -mb)); b = ex2f(fmaf(sr[2 * c + 1], scale, -mb)); }
+      if (V == 0 || V == 1) pk[c] = pack_bf16(a, b);
+      else pk[c] = __float_as_uint(a) ^ __float_as_uint(b);
+      if (V == 0) la[c & 3] = add_bf16x2_f32(pk[c], la[c & 3]);
+      if (V == 2) la[c & 3] += a + b;
+    }
+    l += (la[0] + la[1]) + (la[2] + la[3]);
+#pragma unroll
+    for (int c = 0; c < 32; ++c) acc ^= pk[c];
+#pragma unroll
+    for (int c = 0; c < 64; ++c) sr[c] = __uint_as_float(__float_as_uint(sr[c]) ^ (t & 1));   // new scores
+  }
+  const long long t1 = clock64();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc ^ __float_as_uint(l);
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+template <int V>
+void run(const char* name, int warps) {
+  float* in; uint32_t* out; long long* cyc;
+  cudaMalloc(&in, 4096); cudaMemset(in, 0, 4096);
+  cudaMalloc(&out, 148 * 1024 * 4); cudaMalloc(&cyc, 148 * 8);
+  const int tiles = 2000;
+  k<V><<<148, warps * 32>>>(in, out, cyc, tiles);
+  k<V><<<148, warps * 32>>>(in, out, cyc, tiles);
+  cudaDeviceSynchronize();
+  long long c; cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+  printf("%-28s warps/SM %d: %.0f cycles per 64-score tile per warp\n", name, warps, (double)c / tiles);
+  cudaFree(in); cudaFree(out); cudaFree(cyc);
+}
+
+int main() {
+  for (int w : {4, 8}) {
+    run<0>("ffma+ex2+pack+bf16 sums", w); run<1>("ffma+ex2+pack", w);
+    run<2>("ffma+ex2+fp32 sums", w); run<3>("ex2 only", w);
+  }
+  return 0;
+}
