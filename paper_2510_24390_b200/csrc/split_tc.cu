@@ -486,6 +486,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       load_q(1, pf);
     }
     uint32_t j = 0, k = 0, np = 0;                  // np: this warpgroup's tiles so far
+#ifdef ORION_TC_TIMELINE
+    // dev only (-DORION_TC_TIMELINE): CTA 0's first 48 turns per warpgroup, printed at the end
+    long long tl_r[48], tl_e[48];
+#endif
     // The two warpgroups take turns at the exponentials (named barriers 2: WG0's turn, 3: WG1's):
     // one warpgroup's ex2 phase saturates the SM's MUFU on its own, so running them one after the
     // other overlaps each warpgroup's S read-out, P store and barrier waits with the other's
@@ -569,6 +573,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             l_run *= alpha;
           }
         }
+#ifdef ORION_TC_TIMELINE
+        const long long tl_ready = clock64();
+#endif
         TW(10, asm volatile("bar.sync %0, 256;\n" ::"r"(2 + p) : "memory"));   // my turn at the exponentials
 #ifdef ORION_TC_TRACE
         tr_[8] += clock64() - tm0;
@@ -591,6 +598,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
 #ifdef ORION_TC_TRACE
         tr_[11] += clock64() - tx0;
+#endif
+#ifdef ORION_TC_TIMELINE
+        if (np < 48) { tl_r[np] = tl_ready; tl_e[np] = clock64(); }   // ready for / end of the turn
 #endif
         asm volatile("bar.arrive %0, 256;\n" ::"r"(3 - p) : "memory");   // the other warpgroup's turn
 #ifdef ORION_TC_TRACE
@@ -757,6 +767,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     if (p == 0) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     if (p == 0) asm volatile("bar.sync 2, 256;\n" ::: "memory");   // the token WG1 passed last
     if ((warp & 3) < 2) TRACE_DUMP("softmax");
+#ifdef ORION_TC_TIMELINE
+    if (blockIdx.x == 0 && (warp & 3) == 0 && lane == 0)
+      for (uint32_t i = 0; i < min(np, 48u); ++i) printf("TL p=%d np=%u ready=%lld end=%lld\n", p, i, tl_r[i], tl_e[i]);
+#endif
 #ifdef ORION_TC_TRACE
     if (warp == 4 && lane == 0)   // per-CTA balance: total cycles, tiles, items of warpgroup 0
       printf("CTA %d tot %llu tiles %u items %u\n", blockIdx.x, clock64() - tr_t0, np, k);
