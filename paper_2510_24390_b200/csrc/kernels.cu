@@ -918,7 +918,7 @@ extern "C" orion_status orion_point_prefill_attn(const orion_attn_shape* shape, 
 }
 
 extern "C" const char* orion_version(void) {
-  return "orion-b200 0.4 (sm_100a; K1 append; K2 split: hybrid decode plans -- tcgen05.mma + TMEM + TMA swap-AB "
+  return "orion-b200 0.5 (sm_100a; K1 append (fused into the split launch on short steps: orion_expand_step); K2 split: hybrid decode plans -- tcgen05.mma + TMEM + TMA swap-AB "
          "for items of <= 64 rows, rows-on-lanes tcgen05 for 65..128-row (masked) block items, two PDL-chained "
          "launches | rows-on-lanes (d = 64, point prefill; K/V-sharing item pairs with ORION_PLAN_PAIR) | "
          "mma.sync m16n8k16 (ORION_PLAN_MMA_SYNC); K3 combine)";
