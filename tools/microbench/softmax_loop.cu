@@ -4,10 +4,13 @@
 //   1 no row sums (FFMA + ex2 + pack)
 //   2 no pack (FFMA + ex2, fp32 sums)
 //   3 ex2 only (the MUFU floor)
+//   4 packed: FFMA -> f16x2 pack -> ex2.approx.f16x2 -> f32 -> bf16x2 pack + bf16 sums
+//   5 packed ex2.f16x2 only
 // Cycles per 64-score tile per warp.
 #include <cstdio>
 #include <cstdint>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ float ex2f(float x) { float y; asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
@@ -38,11 +41,24 @@ __global__ void k(const float* in, uint32_t* out, long long* cyc, int tiles) {
 #pragma unroll
     for (int c = 0; c < 32; ++c) {
       float a, b;
-      if (V == 3) { a = ex2f(sr[2 * c]); b = ex2f(sr[2 * c + 1]); }
+      if (V == 4 || V == 5) {
+        uint32_t h;
+        if (V == 4) {
+          const float x0 = fmaf(sr[2 * c], scale, -mb), x1 = fmaf(sr[2 * c + 1], scale, -mb);
+          asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(x1), "f"(x0));
+        } else {
+          h = __float_as_uint(sr[2 * c]);
+        }
+        asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(h));
+        if (V == 5) { pk[c] = h; continue; }
+        __half2 hh = *reinterpret_cast<__half2*>(&h);
+        const float2 f = __half22float2(hh);
+        a = f.x; b = f.y;
+      } else if (V == 3) { a = ex2f(sr[2 * c]); b = ex2f(sr[2 * c + 1]); }
       else { a = ex2f(fmaf(sr[2 * c], scale, -mb)); b = ex2f(fmaf(sr[2 * c + 1], scale, -mb)); }
-      if (V == 0 || V == 1) pk[c] = pack_bf16(a, b);
+      if (V == 0 || V == 1 || V == 4) pk[c] = pack_bf16(a, b);
       else pk[c] = __float_as_uint(a) ^ __float_as_uint(b);
-      if (V == 0) la[c & 3] = add_bf16x2_f32(pk[c], la[c & 3]);
+      if (V == 0 || V == 4) la[c & 3] = add_bf16x2_f32(pk[c], la[c & 3]);
       if (V == 2) la[c & 3] += a + b;
     }
     l += (la[0] + la[1]) + (la[2] + la[3]);
@@ -74,6 +90,7 @@ int main() {
   for (int w : {4, 8}) {
     run<0>("ffma+ex2+pack+bf16 sums", w); run<1>("ffma+ex2+pack", w);
     run<2>("ffma+ex2+fp32 sums", w); run<3>("ex2 only", w);
+    run<4>("packed f16x2 full loop", w); run<5>("packed ex2.f16x2 only", w);
   }
   return 0;
 }
