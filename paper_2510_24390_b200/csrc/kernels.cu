@@ -353,16 +353,14 @@ __global__ void __launch_bounds__(256) combine_kernel(const int32_t* __restrict_
 
 // K3 for the fp16 partial format (plan_format.h): partial i = (o_i = acc_i / l_i, lse2_i), so
 // out = sum_i 2^(lse2_i - M) o_i / sum_i 2^(lse2_i - M) and lse = (M + log2 sum) ln 2.
-// Eight lanes per row (four rows per warp, kCombRowsPerBlock per block): each lane owns D/8
-// consecutive elements (one or two 16-B loads per partial).  Lane j of a row's group holds the
-// slot and lse of partials j, j+8, ... in turn, so the dependent chain comb_off -> comb_slot ->
-// part_lse -> part_o is walked once per chunk of 8 partials (c4: ~4.4 partials per row, one
-// chunk) and the o loads of 4 partials issue together; with 4 rows per warp the grid is ~1.5
-// waves instead of ~5.5, so the chain is paid ~1.5 times, not ~5.5.  Accumulation is in the
-// fixed plan order (deterministic, and the same expression sequence as a serial loop).
-constexpr int kCombLanes = 8;
+// merge_lanes<D>() lanes per row (16 at D = 128: two rows per warp; merge16.h): each lane owns
+// D/16 consecutive elements (one 16-B load per partial).  Lane j of a row's group holds the slot
+// and lse of partials j, j+16, ... in turn, so the dependent chain comb_off -> comb_slot ->
+// part_lse -> part_o is walked once per chunk of 16 partials (c4: ~4.4 partials per row, one
+// chunk) and the o loads of 4 partials issue together.  16 lanes per row measured +2.8 % on c4's
+// 8-query share over 8 (4 lanes: -6 %), c4 +0.3 %, same box.  Accumulation is in the fixed plan
+// order (deterministic, and the same expression sequence as a serial loop).
 constexpr int kCombThreads = 128;
-constexpr int kCombRowsPerBlock = kCombThreads / kCombLanes;
 
 template <int D>
 __global__ void __launch_bounds__(kCombThreads) combine16_kernel(const int32_t* __restrict__ comb_off,
@@ -371,7 +369,8 @@ __global__ void __launch_bounds__(kCombThreads) combine16_kernel(const int32_t* 
                                                                  const float* __restrict__ part_lse,
                                                                  __nv_bfloat16* __restrict__ out,
                                                                  float* __restrict__ lse, int n_rows) {
-  const int row = blockIdx.x * kCombRowsPerBlock + (threadIdx.x / kCombLanes);
+  constexpr int kCombLanes = merge_lanes<D>();
+  const int row = blockIdx.x * (kCombThreads / kCombLanes) + (threadIdx.x / kCombLanes);
   pdl_trigger();
   pdl_wait();
   merge_row16<D>(comb_off, comb_slot, part_o, part_lse, out, lse, row < n_rows ? row : 0, row < n_rows,
@@ -670,7 +669,7 @@ orion_status launch_combine(const PlanHeader* h, const char* dplan, void* out, f
   const int nb = (h->n_rows + 7) / 8;
   if (partials_fp16(h->variant)) {
     cudaError_t e = launch_pdl(
-        combine16_kernel<D>, dim3((h->n_rows + kCombRowsPerBlock - 1) / kCombRowsPerBlock),
+        combine16_kernel<D>, dim3((h->n_rows + kCombThreads / merge_lanes<D>() - 1) / (kCombThreads / merge_lanes<D>())),
         dim3(kCombThreads), 0, st,
         reinterpret_cast<const int32_t*>(dplan + h->comb_off_off),
         reinterpret_cast<const int32_t*>(dplan + h->comb_slot_off), static_cast<const __half*>(ws),

@@ -5,11 +5,12 @@
 // A row's partials i (plan_format.h fp16 format: o_i = acc_i / l_i, lse2_i = m_i + log2 l_i) are
 // listed in plan order by the combine CSR (comb_off / comb_slot):
 //   out = sum_i 2^(lse2_i - M) o_i / sum_i 2^(lse2_i - M),  lse = (M + log2 sum) ln 2,  M = max lse2_i.
-// One row per group of 8 consecutive lanes; every lane of the warp calls it (the shuffles use the
-// full mask; a group without a row passes valid = false).  Lane `sub` of the group owns D/8
-// consecutive elements (one or two 16-B loads per partial).  Lane j of a row's group holds the slot
-// and lse of partials j, j+8, ... in turn, so the dependent chain comb_off -> comb_slot -> part_lse
-// -> part_o is walked once per chunk of 8 partials and the o loads of 4 partials issue together.
+// One row per group of kMergeLanes consecutive lanes (16 at D = 128, 8 at D = 64: one 16-B load per
+// lane and partial); every lane of the warp calls it (the shuffles use the full mask; a group
+// without a row passes valid = false).  Lane `sub` of the group owns D / kMergeLanes consecutive
+// elements.  Lane j of a row's group holds the slot and lse of partials j, j + kMergeLanes, ... in
+// turn, so the dependent chain comb_off -> comb_slot -> part_lse -> part_o is walked once per
+// chunk of kMergeLanes partials and the o loads of 4 partials issue together.
 // The weighted sum runs in the fixed plan order: a row's result does not depend on which kernel or
 // CTA merges it (the combine kernel and the split kernel's merge phase agree bitwise).  Loads use
 // ld.global.cg: in the merge phase the partials were written by other CTAs of the same kernel, so
@@ -21,7 +22,11 @@
 
 namespace orion {
 
-constexpr int kMergeLanes = 8;
+#ifndef ORION_MERGE_LANES
+#define ORION_MERGE_LANES 16
+#endif
+// lanes per row: at least one 16-byte load (8 halves) per lane and partial
+template <int D> constexpr int merge_lanes() { return (D / ORION_MERGE_LANES) >= 8 ? ORION_MERGE_LANES : D / 8; }
 
 // Cache policies of the merge's loads: the plan's combine CSR is re-read by every layer's combine
 // (evict_last keeps it resident); a partial is dead once merged (evict_first).
@@ -49,12 +54,12 @@ __device__ __forceinline__ uint4 ld_hint(const uint4* p, uint64_t pol) {
   return v;
 }
 
-template <int D>
+template <int D, int kMergeLanes = merge_lanes<D>()>
 __device__ __forceinline__ void merge_row16(const int32_t* __restrict__ comb_off, const int32_t* __restrict__ comb_slot,
                                             const __half* part_o, const float* part_lse,
                                             __nv_bfloat16* __restrict__ out, float* __restrict__ lse, int row,
                                             bool valid, int sub) {
-  constexpr int E = D / kMergeLanes;  // elements per lane (8 or 16)
+  constexpr int E = D / kMergeLanes;  // elements per lane (8 or more)
   constexpr int U = E / 8;            // 16-B loads per lane per partial
   const unsigned full = 0xffffffffu;
   const uint64_t keep = merge_policy(true), drop = merge_policy(false);
