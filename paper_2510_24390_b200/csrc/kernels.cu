@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const int32_t* __restrict_
 // and lse of partials j, j+16, ... in turn, so the dependent chain comb_off -> comb_slot ->
 // part_lse -> part_o is walked once per chunk of 16 partials (c4: ~4.4 partials per row, one
 // chunk) and the o loads of 4 partials issue together.  16 lanes per row measured +2.8 % on c4's
-// 8-query share over 8 (4 lanes: -6 %), c4 +0.3 %, same box.  Accumulation is in the fixed plan
+// 8-query share over 8 (4 lanes: -6 %; 32 lanes with 8-byte loads: +0.2 % more), c4 +0.3 %.  Accumulation is in the fixed plan
 // order (deterministic, and the same expression sequence as a serial loop).
 constexpr int kCombThreads = 128;
 

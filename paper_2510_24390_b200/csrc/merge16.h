@@ -20,13 +20,15 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace orion {
 
 #ifndef ORION_MERGE_LANES
 #define ORION_MERGE_LANES 16
 #endif
 // lanes per row: at least one 16-byte load (8 halves) per lane and partial
-template <int D> constexpr int merge_lanes() { return (D / ORION_MERGE_LANES) >= 8 ? ORION_MERGE_LANES : D / 8; }
+template <int D> constexpr int merge_lanes() { return (D / ORION_MERGE_LANES) >= 4 ? ORION_MERGE_LANES : D / 4; }
 
 // Cache policies of the merge's loads: the plan's combine CSR is re-read by every layer's combine
 // (evict_last keeps it resident); a partial is dead once merged (evict_first).
@@ -46,6 +48,11 @@ __device__ __forceinline__ float ld_hint(const float* p, uint64_t pol) {
   asm volatile("ld.global.cg.L2::cache_hint.f32 %0, [%1], %2;\n" : "=f"(v) : "l"(p), "l"(pol));
   return v;
 }
+__device__ __forceinline__ uint2 ld_hint(const uint2* p, uint64_t pol) {
+  uint2 v;
+  asm volatile("ld.global.cg.L2::cache_hint.v2.b32 {%0, %1}, [%2], %3;\n" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
 __device__ __forceinline__ uint4 ld_hint(const uint4* p, uint64_t pol) {
   uint4 v;
   asm volatile("ld.global.cg.L2::cache_hint.v4.b32 {%0, %1, %2, %3}, [%4], %5;\n"
@@ -59,8 +66,10 @@ __device__ __forceinline__ void merge_row16(const int32_t* __restrict__ comb_off
                                             const __half* part_o, const float* part_lse,
                                             __nv_bfloat16* __restrict__ out, float* __restrict__ lse, int row,
                                             bool valid, int sub) {
-  constexpr int E = D / kMergeLanes;  // elements per lane (8 or more)
-  constexpr int U = E / 8;            // 16-B loads per lane per partial
+  constexpr int E = D / kMergeLanes;  // elements per lane (4 or more)
+  constexpr int EV = E >= 8 ? 8 : 4;  // halves per vector load: 16 B, or 8 B at 4 elements per lane
+  constexpr int U = E / EV;           // vector loads per lane per partial
+  using Vec = typename std::conditional<(EV == 8), uint4, uint2>::type;
   const unsigned full = 0xffffffffu;
   const uint64_t keep = merge_policy(true), drop = merge_policy(false);
   const int e0 = valid ? ld_hint(comb_off + row, keep) : 0;
@@ -93,14 +102,14 @@ __device__ __forceinline__ void merge_row16(const int32_t* __restrict__ comb_off
     if (c + sub < n) asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(w_l) : "f"(lse_l - base));
     const int cn = min(nmax - c, kMergeLanes);
     for (int j0 = 0; j0 < cn; j0 += 4) {
-      uint4 x[4][U];
+      Vec x[4][U];
       float wt[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int s = __shfl_sync(full, slot_l, (j0 + j) & (kMergeLanes - 1), kMergeLanes);
         wt[j] = __shfl_sync(full, w_l, (j0 + j) & (kMergeLanes - 1), kMergeLanes);
         if (c + j0 + j < n) {
-          const uint4* src = reinterpret_cast<const uint4*>(part_o + static_cast<size_t>(s) * D + sub * E);
+          const Vec* src = reinterpret_cast<const Vec*>(part_o + static_cast<size_t>(s) * D + sub * E);
 #pragma unroll
           for (int u = 0; u < U; ++u) x[j][u] = ld_hint(src + u, drop);
         }
@@ -113,10 +122,10 @@ __device__ __forceinline__ void merge_row16(const int32_t* __restrict__ comb_off
           for (int u = 0; u < U; ++u) {
             const __half2* h2 = reinterpret_cast<const __half2*>(&x[j][u]);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
+            for (int i = 0; i < EV / 2; ++i) {
               const float2 f = __half22float2(h2[i]);
-              acc[u * 8 + 2 * i] += wt[j] * f.x;
-              acc[u * 8 + 2 * i + 1] += wt[j] * f.y;
+              acc[u * EV + 2 * i] += wt[j] * f.x;
+              acc[u * EV + 2 * i + 1] += wt[j] * f.y;
             }
           }
         }
@@ -125,19 +134,19 @@ __device__ __forceinline__ void merge_row16(const int32_t* __restrict__ comb_off
   }
   if (!valid) return;
   const float inv = L > 0.f ? 1.f / L : 0.f;
-  uint4* o = reinterpret_cast<uint4*>(out + static_cast<size_t>(row) * D + sub * E);
+  uint32_t* o = reinterpret_cast<uint32_t*>(out + static_cast<size_t>(row) * D + sub * E);
+  uint32_t pk[E / 2];
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    uint4 pk;
-    __nv_bfloat162 b0 = __floats2bfloat162_rn(acc[u * 8 + 0] * inv, acc[u * 8 + 1] * inv);
-    __nv_bfloat162 b1 = __floats2bfloat162_rn(acc[u * 8 + 2] * inv, acc[u * 8 + 3] * inv);
-    __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[u * 8 + 4] * inv, acc[u * 8 + 5] * inv);
-    __nv_bfloat162 b3 = __floats2bfloat162_rn(acc[u * 8 + 6] * inv, acc[u * 8 + 7] * inv);
-    pk.x = *reinterpret_cast<uint32_t*>(&b0);
-    pk.y = *reinterpret_cast<uint32_t*>(&b1);
-    pk.z = *reinterpret_cast<uint32_t*>(&b2);
-    pk.w = *reinterpret_cast<uint32_t*>(&b3);
-    o[u] = pk;
+  for (int i = 0; i < E / 2; ++i) {
+    __nv_bfloat162 b = __floats2bfloat162_rn(acc[2 * i] * inv, acc[2 * i + 1] * inv);
+    pk[i] = *reinterpret_cast<uint32_t*>(&b);
+  }
+  if constexpr (EV == 8) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      reinterpret_cast<uint4*>(o)[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+  } else {
+    *reinterpret_cast<uint2*>(o) = make_uint2(pk[0], pk[1]);
   }
   if (lse && sub == 0) lse[row] = L > 0.f ? (M + log2f(L)) * 0.6931471805599453f : -INFINITY;
 }
