@@ -360,7 +360,10 @@ __global__ void __launch_bounds__(256) combine_kernel(const int32_t* __restrict_
 // chunk) and the o loads of 4 partials issue together.  16 lanes per row measured +2.8 % on c4's
 // 8-query share over 8 (4 lanes: -6 %; 32 lanes with 8-byte loads: +0.2 % more), c4 +0.3 %.  Accumulation is in the fixed plan
 // order (deterministic, and the same expression sequence as a serial loop).
-constexpr int kCombThreads = 128;
+#ifndef ORION_COMB_THREADS
+#define ORION_COMB_THREADS 128
+#endif
+constexpr int kCombThreads = ORION_COMB_THREADS;
 
 template <int D>
 __global__ void __launch_bounds__(kCombThreads) combine16_kernel(const int32_t* __restrict__ comb_off,
