@@ -362,7 +362,9 @@ __device__ __forceinline__ void fused_append(const TcArgs& a, int sw, int lane) 
 }
 
 struct Sched {
-  int32_t valid, it, pt_off, t0, end, base, ntiles, npad, kv_head, n_rows, slot0, item, first, last, pad[2];
+  int32_t valid, it, pt_off, t0, end, base, ntiles, npad, kv_head, n_rows, slot0, item, first, last;
+  int32_t appended;   // the range may hold rows the fused append wrote in this launch
+  int32_t pad;
 };
 constexpr int kSched = 8;
 constexpr uint32_t kSchedConsumers = 1 + 1 + 1 + 128 + 128;   // K-TMA, V-TMA, MMA lanes, WG0, WG1
@@ -610,7 +612,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           e.valid = 1; e.it = it; e.pt_off = g.pt_off; e.t0 = g.t0; e.end = g.end; e.base = g.base;
           e.ntiles = g.ntiles; e.npad = npad_of(w.n_rows); e.kv_head = w.kv_head; e.n_rows = w.n_rows;
           e.slot0 = w.slot0; e.item = static_cast<int32_t>(iq); e.first = r == rfirst; e.last = r == rlast;
-          e.pad[0] = g.dyn >= 0 && a.app.enabled;   // may hold rows appended in this launch
+          e.appended = g.dyn >= 0 && a.app.enabled;
           ring[k % kSched] = e;
           mbar_arrive(sch_full + (k % kSched));
         }
@@ -671,7 +673,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     bool fenced = false;
     for (uint32_t k = 0;; ++k) {
       const Sched e = read_sched(ring, sch_full, sch_empty, k, lane == 0);
-      if (e.valid && e.pad[0] && !fenced) {   // rows other CTAs appended (generic writes) -> TMA reads
+      if (e.valid && e.appended && !fenced) {   // rows other CTAs appended (generic writes) -> TMA reads
         asm volatile("fence.proxy.async.global;\n" ::: "memory");
         fenced = true;
       }
