@@ -14,8 +14,8 @@
  *   orion_expand_plan    cut the bound segments into shared pieces (maximal token ranges with
  *                        a fixed reader set) and emit the device work plan.
  *   orion_kv_append      write each branch's new-token K/V into its own pages (device).
- *   orion_expand_step    orion_kv_append + orion_expand_attn in one call (device; the append
- *                        fused into the split launch where the plan allows).
+ *   orion_expand_step    orion_kv_append + orion_expand_attn in one call (device; on short
+ *                        steps one launch: append, split and combine in the split kernel).
  *   orion_expand_attn    dependency-masked batched GQA decode attention over the paged bf16
  *                        cache; each shared piece is read from HBM once per (query, kv head)
  *                        group (device; split kernel + combine kernel).
@@ -297,10 +297,10 @@ orion_status orion_expand_attn(const orion_attn_shape* shape, int32_t n_branches
  * equal; tests/test_gpu_parity.py::test_expand_step_equals_append_then_attn).
  * Device; enqueued on `stream`.  With the release library, a plan on the default swap-AB kernel
  * without rows-on-lanes items (no `n_big`; every plan whose query groups have <= 64 rows) and a
- * short step (<= 2048 streamed tokens per SM: latency-bound running sets), the append runs inside
- * the split launch: every CTA appends its share of the branches first and releases a per-branch
- * flag, and a range growing with branch b waits for b's flag only, so the step is two launches
- * (split, combine) instead of three.  Otherwise (longer steps, where the separate append overlaps
+ * short step (<= 2048 streamed tokens per SM: latency-bound running sets), the whole step is ONE
+ * launch of the split kernel: every CTA appends its share of the branches first and releases a
+ * per-branch flag (a range growing with branch b waits for b's flag only), and after a grid
+ * barrier the CTAs merge the rows' partials themselves (the combine's arithmetic, bitwise).  Otherwise (longer steps, where the separate append overlaps
  * the split's prologue; hybrid plans; head_dim 64; the debug build) it runs the two calls.
  * own_len must stay below 2^20.
  *  q, out, lse, k_cache, v_cache, num_pages, page_table, h_plan, d_plan, workspace,
@@ -318,8 +318,9 @@ orion_status orion_expand_step(const orion_attn_shape* shape, int32_t n_branches
 
 /*
  * orion_step_launches — host: the number of kernels one orion_expand_step (or, for a point-prefill
- * plan, one orion_point_prefill_attn) enqueues with this plan on the current device: 2 when the
- * append is fused into the split launch, else 3 (4 for a hybrid plan with both split kernels).
+ * plan, one orion_point_prefill_attn) enqueues with this plan on the current device: 1 when the
+ * append and the combine are fused into the split launch, else 3 (4 for a hybrid plan with both
+ * split kernels).
  * Errors: INVALID_ARG (null pointer, not a plan).
  */
 orion_status orion_step_launches(const void* h_plan, int32_t* launches);

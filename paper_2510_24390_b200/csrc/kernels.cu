@@ -827,7 +827,7 @@ extern "C" orion_status orion_step_launches(const void* h_plan, int32_t* launche
   const PlanHeader* h = static_cast<const PlanHeader*>(h_plan);
   if (h->magic != kPlanMagic || h->version != kPlanVersion) return fail(ORION_ERR_INVALID_ARG, "not an orion plan");
   if (h->prefill_rows > 0) { *launches = 1; return ORION_OK; }   // point prefill: the split kernel only
-  if (step_fuses(h)) { *launches = 2; return ORION_OK; }
+  if (step_fuses(h)) { *launches = 1; return ORION_OK; }
   const bool hybrid2 = h->variant == kVariantTCT && h->n_big > 0 && h->n_big < h->n_items;
   *launches = 3 + (hybrid2 ? 1 : 0);
   return ORION_OK;
@@ -881,10 +881,14 @@ extern "C" orion_status orion_expand_step(const orion_attn_shape* shape, int32_t
   ap.n_branches = n_branches;
   ap.mode = mode;
   ap.num_pages = num_pages;
-  st = launch_split<128>(h, dp, q, k_cache, v_cache, num_pages, page_table, own_len, workspace, s,
-                         1 + shape->kv_interleaved, nullptr, nullptr, &ap);
-  if (st != ORION_OK) return st;
-  return launch_combine<128>(h, dp, out, lse, workspace, s);
+  ap.merge = 1;                                     // K3 as the split launch's last phase
+  ap.n_rows = h->n_rows;
+  ap.comb_off = reinterpret_cast<const int32_t*>(dp + h->comb_off_off);
+  ap.comb_slot = reinterpret_cast<const int32_t*>(dp + h->comb_slot_off);
+  ap.out = static_cast<__nv_bfloat16*>(out);
+  ap.lse = lse;
+  return launch_split<128>(h, dp, q, k_cache, v_cache, num_pages, page_table, own_len, workspace, s,
+                           1 + shape->kv_interleaved, nullptr, nullptr, &ap);
 }
 
 extern "C" orion_status orion_point_prefill_attn(const orion_attn_shape* shape, int32_t n_branches,

@@ -40,6 +40,7 @@ constexpr int64_t kMergeTokens = 8192;   // token cap of a merged multi-range de
 // kAppendEpochWord (its own cache line), then one append flag per branch (kCounterBytes on).
 constexpr int64_t kCounterBytes = 256;
 constexpr int kAppendEpochWord = 32;
+constexpr int kBarCountWord = 40, kBarGenWord = 48;   // the fused merge's grid barrier
 constexpr int64_t kSmallStepTokens = 1024;   // small-step split: below this many tokens per item at 2 items per SM
 constexpr int kTileTokens = 64;    // tokens per pipeline stage in the split kernel
 

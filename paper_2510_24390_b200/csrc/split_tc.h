@@ -93,6 +93,14 @@ struct FusedAppend {
   int32_t* flags;         // [n_branches]
   int32_t* err;           // debug build: first branch whose target page is out of range
   int32_t n_branches, mode, num_pages, enabled;
+  // K3 as the same launch's last phase (merge = 1): after a grid barrier (sense reversal on work
+  // counter words kBarCountWord / kBarGenWord) every CTA merges a share of the rows' fp16
+  // partials (merge16.h) into out / lse, so a short step is one launch.
+  int32_t merge, n_rows;
+  const int32_t* comb_off;
+  const int32_t* comb_slot;
+  __nv_bfloat16* out;
+  float* lse;
 };
 
 struct TcArgs {

@@ -36,6 +36,7 @@
 #include <cstdio>
 
 #include "../../include/orion.h"
+#include "merge16.h"
 #include "plan_format.h"
 #include "split_tc.h"
 #include "tc_ptx.h"
@@ -911,6 +912,39 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kWarpAlloc) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+  }
+  if (a.app.merge) {
+    // K3 in this launch (fused short step): every CTA's partials written -> grid barrier (all CTAs
+    // are resident: grid <= SMs, one CTA per SM) -> each warp merges rows of the combine CSR, two
+    // rows per warp, exactly as combine16_kernel does (same function, same order: bitwise equal).
+    int32_t* bar_count = a.work_counter + kBarCountWord;
+    int32_t* bar_gen = a.work_counter + kBarGenWord;
+    if (tid == 0) {
+      const int gen0 = *reinterpret_cast<volatile int32_t*>(bar_gen);
+      __threadfence();                              // this CTA's partials (after the __syncthreads above)
+      if (atomicAdd(bar_count, 1) == static_cast<int>(gridDim.x) - 1) {
+        *reinterpret_cast<volatile int32_t*>(bar_count) = 0;
+        __threadfence();
+        atomicAdd(bar_gen, 1);
+      } else {
+        int g;
+        do {
+          __nanosleep(64);
+          asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(g) : "l"(bar_gen) : "memory");
+        } while (g == gen0);
+      }
+    }
+    __syncthreads();
+    constexpr int kL = merge_lanes<D>();
+    constexpr int kRowsPerWarp = 32 / kL;
+    const int nw = kThreads / 32;
+    for (int base = (static_cast<int>(blockIdx.x) * nw + warp) * kRowsPerWarp; base < a.app.n_rows;
+         base += static_cast<int>(gridDim.x) * nw * kRowsPerWarp) {
+      const int row = base + lane / kL;
+      const bool valid = row < a.app.n_rows;
+      merge_row16<D>(a.app.comb_off, a.app.comb_slot, a.part_o, a.part_lse, a.app.out, a.app.lse, valid ? row : 0,
+                     valid, lane & (kL - 1));
+    }
   }
   if (tid == 0) release_work_counter(a.work_counter, a.app.enabled != 0);
   if (a.pdl_late) pdl_wait();                        // complete only after the first kernel (combine reads both)

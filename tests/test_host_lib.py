@@ -484,8 +484,8 @@ def test_small_step_spreads_over_the_sms(nb):
 
 
 def test_step_launches():
-    """orion_step_launches: 2 kernels per orion_expand_step on a short step of the swap-AB kernel
-    (the append fused into the split launch), 3 on a long one (c4's 64 queries: the separate
+    """orion_step_launches: 1 kernel per orion_expand_step on a short step of the swap-AB kernel
+    (the append and the combine fused into the split launch), 3 on a long one (c4's 64 queries: the separate
     append overlaps the split's prologue), 4 on a hybrid plan with both split kernels, 1 for a
     point-prefill plan.  Host only (148 SMs without a GPU)."""
     from paper_2510_24390_b200 import _lib
@@ -501,7 +501,7 @@ def test_step_launches():
         offs, segs = _bind_layout(cfg, lay, 0)
         return orion.expand_plan(cfg.hq, cfg.hkv, cfg.d, cfg.page, offs, segs, lay.own_len, **kw)[0], cfg
 
-    assert launches(plan_of("c4", 2)[0]) == 2
+    assert launches(plan_of("c4", 2)[0]) == 1
     assert launches(plan_of("c4", 64)[0]) == 3
     hyb, _ = plan_of("c5c", 1)
     assert orion.plan_stats(hyb)["n_big"] > 0 and launches(hyb) == 4
