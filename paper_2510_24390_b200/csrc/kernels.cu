@@ -811,7 +811,10 @@ extern "C" orion_status orion_expand_attn(const orion_attn_shape* shape, int32_t
 }
 
 namespace {
-constexpr int64_t kFuseTokensPerSm = 2048;
+#ifndef ORION_FUSE_TOKENS_PER_SM
+#define ORION_FUSE_TOKENS_PER_SM 2048
+#endif
+constexpr int64_t kFuseTokensPerSm = ORION_FUSE_TOKENS_PER_SM;
 bool step_fuses(const PlanHeader* h) {
 #ifdef ORION_CHECK
   return false;
