@@ -295,9 +295,10 @@ orion_status orion_expand_attn(const orion_attn_shape* shape, int32_t n_branches
  * branch's new token followed by orion_expand_attn over the same plan (Alg. 1 l.16;
  * SURVEY.md §8(a) a5 + a6 + a7).  Results are those of the two calls in order (outputs bitwise
  * equal; tests/test_gpu_parity.py::test_expand_step_equals_append_then_attn).
- * Device; enqueued on `stream`.  With the release library, a plan on the default swap-AB kernel
- * without rows-on-lanes items (no `n_big`; every plan whose query groups have <= 64 rows) and a
- * short step (<= 2048 streamed tokens per SM: latency-bound running sets), the whole step is ONE
+ * Device; enqueued on `stream`.  With the release library, a stream of the whole device's context
+ * (not a green-context partition: the fused launch's CTAs wait on each other, so all of them must
+ * be resident at once), a plan on the default swap-AB kernel without rows-on-lanes items (no
+ * `n_big`; every plan whose query groups have <= 64 rows) and a short step (<= 2048 streamed tokens per SM: latency-bound running sets), the whole step is ONE
  * launch of the split kernel: every CTA appends its share of the branches first and releases a
  * per-branch flag (a range growing with branch b waits for b's flag only), and after a grid
  * barrier the CTAs merge the rows' partials themselves (the combine's arithmetic, bitwise).  Otherwise (longer steps, where the separate append overlaps
@@ -318,9 +319,9 @@ orion_status orion_expand_step(const orion_attn_shape* shape, int32_t n_branches
 
 /*
  * orion_step_launches — host: the number of kernels one orion_expand_step (or, for a point-prefill
- * plan, one orion_point_prefill_attn) enqueues with this plan on the current device: 1 when the
- * append and the combine are fused into the split launch, else 3 (4 for a hybrid plan with both
- * split kernels).
+ * plan, one orion_point_prefill_attn) enqueues with this plan on a stream of the current
+ * device's context: 1 when the append and the combine are fused into the split launch, else 3 (4
+ * for a hybrid plan with both split kernels).
  * Errors: INVALID_ARG (null pointer, not a plan).
  */
 orion_status orion_step_launches(const void* h_plan, int32_t* launches);

@@ -440,6 +440,44 @@ int current_device_sms() {
   return n;
 }
 
+// SMs available to the context that owns `stream`, or -1 for a green-context stream (a partition:
+// fewer SMs than the device) or when the driver cannot say.  Cached per context.
+int stream_context_sms(cudaStream_t stream) {
+  // the entry point's default version (12.5+) is cuStreamGetCtx_v2: (stream, context, green context)
+  typedef CUresult (*StreamGetCtxFn)(CUstream, CUcontext*, CUgreenCtx*);
+  typedef CUresult (*CtxGetDevResourceFn)(CUcontext, CUdevResource*, CUdevResourceType);
+  static const StreamGetCtxFn get_ctx = []() -> StreamGetCtxFn {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    return cudaGetDriverEntryPointByVersion("cuStreamGetCtx", &p, 12050, cudaEnableDefault, &q) == cudaSuccess &&
+                   q == cudaDriverEntryPointSuccess
+               ? reinterpret_cast<StreamGetCtxFn>(p)
+               : nullptr;
+  }();
+  static const CtxGetDevResourceFn get_res = []() -> CtxGetDevResourceFn {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    return cudaGetDriverEntryPointByVersion("cuCtxGetDevResource", &p, 12040, cudaEnableDefault, &q) == cudaSuccess &&
+                   q == cudaDriverEntryPointSuccess
+               ? reinterpret_cast<CtxGetDevResourceFn>(p)
+               : nullptr;
+  }();
+  static std::map<CUcontext, int> cache;
+  if (!get_ctx || !get_res) return -1;
+  CUcontext ctx = nullptr;
+  CUgreenCtx gctx = nullptr;
+  if (get_ctx(reinterpret_cast<CUstream>(stream), &ctx, &gctx) != CUDA_SUCCESS || !ctx) return -1;
+  if (gctx) return -1;   // a green-context stream: pctx is the primary context, not the partition
+  std::lock_guard<std::mutex> lk(g_setup_mu);
+  auto f = cache.find(ctx);
+  if (f != cache.end()) return f->second;
+  CUdevResource r;
+  int n = -1;
+  if (get_res(ctx, &r, CU_DEV_RESOURCE_TYPE_SM) == CUDA_SUCCESS) n = static_cast<int>(r.sm.smCount);
+  cache[ctx] = n;
+  return n;
+}
+
 cudaError_t ensure_dynamic_smem(const void* func, int bytes) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -854,7 +892,11 @@ extern "C" orion_status orion_expand_step(const orion_attn_shape* shape, int32_t
   // separate append kernel, overlapping the split's prologue through PDL, measured 1-2 % faster:
   // c4 with 8 and 64 queries).  The release library only (the debug build checks every append and
   // plan separately).  Otherwise the two calls it stands for, with the same results.
-  bool fuse = step_fuses(h) && shape->head_dim == 128;
+  // The fused launch's CTAs wait on each other (append flags, the merge's grid barrier), so every
+  // CTA must be resident at once: only on a stream of the whole device's context (a green-context
+  // partition -- fewer SMs -- or a driver that cannot say runs the two calls).
+  bool fuse = step_fuses(h) && shape->head_dim == 128 &&
+              stream_context_sms(static_cast<cudaStream_t>(stream)) == current_device_sms();
   if (!fuse) {
     st = orion_kv_append(shape, n_branches, k_new, v_new, k_cache, v_cache, own_pt_off, own_cap, page_table,
                          num_pages, own_len, mode, stream);
@@ -890,8 +932,9 @@ extern "C" orion_status orion_expand_step(const orion_attn_shape* shape, int32_t
   ap.comb_slot = reinterpret_cast<const int32_t*>(dp + h->comb_slot_off);
   ap.out = static_cast<__nv_bfloat16*>(out);
   ap.lse = lse;
-  return launch_split<128>(h, dp, q, k_cache, v_cache, num_pages, page_table, own_len, workspace, s,
-                           1 + shape->kv_interleaved, nullptr, nullptr, &ap);
+  st = launch_split<128>(h, dp, q, k_cache, v_cache, num_pages, page_table, own_len, workspace, s,
+                         1 + shape->kv_interleaved, nullptr, nullptr, &ap);
+  return st;
 }
 
 extern "C" orion_status orion_point_prefill_attn(const orion_attn_shape* shape, int32_t n_branches,

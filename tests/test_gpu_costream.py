@@ -134,3 +134,28 @@ def test_release_append_skips_out_of_range_page():
         assert np.array_equal(got[pg, :, lay.own_len[b] % cfg.page], u16(ten["k_new"][0])[b])
     diff = np.argwhere((got != before).any(axis=-1))
     assert len(diff) == (lay.n_branches - 1) * cfg.hkv
+
+
+def test_fused_step_on_a_partition_smaller_than_its_grid():
+    """orion_expand_step on a short step fuses append, split and combine into one cooperative
+    launch (its CTAs wait on each other).  A plan built for the whole GPU (148 CTAs) stepped on a
+    16-SM green-context partition cannot have every CTA resident: the cooperative launch is
+    refused and the call runs append + attention instead -- same results, no hang."""
+    try:
+        from paper_2510_24390_b200.partition import SmPartition
+        part = SmPartition(16)
+    except Exception as exc:                          # no green contexts on this driver / image
+        pytest.skip(f"green contexts unavailable: {type(exc).__name__}: {exc}")
+    try:
+        cfg, lay, ten, dt, ref, ref_lse, own, k2, v2 = _setup()
+        batch = batch_for(cfg, lay)                   # planned for the whole device
+        assert batch.step_launches() == 1             # a short step: fused when it fits
+        out = torch.empty_like(dt["q"])
+        lse = torch.empty(dt["q"].shape[:2], dtype=torch.float32, device=dt["q"].device)
+        part.sync_before()
+        batch.step(dt["q"], dt["k_new"], dt["v_new"], dt["k_cache"], dt["v_cache"], out, lse,
+                   stream=part.first)
+        part.synchronize()
+        _check(out, lse, batch, dt["k_cache"], dt["v_cache"], ref, ref_lse, own, k2, v2)
+    finally:
+        part.close()
